@@ -1,0 +1,224 @@
+/*
+ * loopscout_b200.h — C-ABI of the B200 batched schedule-cost engine.
+ *
+ * This is the drop-in boundary for the reference's batched cost-evaluation
+ * path (Tuna / `loopscout`, /root/reference/pkg/src/loopscout).  The
+ * reference evaluates one candidate schedule at a time in Python:
+ *
+ *   evaluate_population            ls/es.py:96-116   (batched seam)
+ *     apply_schedule               ls/ir.py:454-474
+ *     emit_mock_asm                ls/ir.py:557-659
+ *     extract_features             ls/cost.py:132-152
+ *     score                        ls/cost.py:155-161
+ *   rank / cmd_rank sort           ls/cost.py:164-168, ls/cli.py:124-126
+ *
+ * Here a *task* (one loop-nest program + one schedule template + one
+ * architecture) is created once, and candidates arrive as packed 32-byte
+ * records.  Every entry point takes plain pointers and sizes; device
+ * pointers are CUDA global-memory pointers owned by the caller, `stream` is a
+ * cudaStream_t passed as void*.  Functions return 0 on success or a negative
+ * LS_E_* code; ls_last_error() returns the thread-local message.
+ *
+ * Ownership: the library never frees caller buffers; an ls_task is owned by
+ * the library, immutable after ls_task_create (except the unroll table, which
+ * only grows), and may be used concurrently from distinct streams.
+ */
+#ifndef LOOPSCOUT_B200_H
+#define LOOPSCOUT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LS_ABI_VERSION 1
+
+/* ---- capacity limits of the descriptor (host-side; checked on create) ---- */
+#define LS_MAX_TENSORS 8
+#define LS_MAX_RANK 6
+#define LS_MAX_TERMS 8     /* terms per index expression of the base program */
+#define LS_MAX_NODES 64    /* nodes (loops + accesses) of the base program    */
+#define LS_MAX_VARS 32     /* loop variables incl. names created by tiling    */
+#define LS_MAX_XFORMS 32   /* transforms in one schedule template            */
+#define LS_MAX_PARAMS 8    /* uint16 parameter slots per record               */
+#define LS_MAX_ORDER 16    /* loops permuted by one Reorder (nibble-packed)   */
+#define LS_MAX_CHAIN 16    /* loops in a transformed perfect chain            */
+#define LS_NFEAT_CPU 5     /* CPU_FEATURES, ls/cost.py:24                     */
+#define LS_NFEAT_GPU 7     /* GPU_FEATURES, ls/cost.py:25-26                  */
+
+/* ---- enums ---- */
+enum { LS_FAMILY_CPU = 0, LS_FAMILY_GPU = 1 };                  /* ArchSpec.family */
+enum { LS_TARGET_X86 = 0, LS_TARGET_AARCH64 = 1, LS_TARGET_PTX = 2 }; /* ls/ir.py:554 */
+/* reg_effects only distinguishes "x86-att" from everything else (ls/ilp.py:98-103) */
+enum { LS_DIALECT_X86_ATT = 0, LS_DIALECT_DEST_FIRST = 1 };
+enum { LS_NODE_LOOP = 0, LS_NODE_ACCESS = 1 };
+enum {                                                          /* ls/ir.py:276-303 */
+  LS_XF_TILE = 0,
+  LS_XF_REORDER = 1,
+  LS_XF_UNROLL = 2,
+  LS_XF_VECTORIZE = 3,
+  LS_XF_PARALLEL = 4
+};
+/* The instruction shapes the mock emitter produces (ls/ir.py:584-658). */
+enum {
+  LS_I_INIT = 0,   /* counter init: movq $0 / mov x,#0 / mov.u32 r,0 */
+  LS_I_LOAD = 1,   /* vector load                                     */
+  LS_I_FMA = 2,    /* fused multiply-add into accumulator             */
+  LS_I_STORE = 3,  /* vector store                                    */
+  LS_I_ADD = 4,    /* counter increment                               */
+  LS_I_CMP = 5,    /* cmpq / cmp / setp                               */
+  LS_I_BRANCH = 6, /* jne / b.ne / @p bra                             */
+  LS_I_RET = 7,
+  LS_I_COUNT = 8
+};
+
+/* ---- error codes (return values) ---- */
+enum {
+  LS_E_OK = 0,
+  LS_E_ARG = -1,         /* bad argument / descriptor */
+  LS_E_CUDA = -2,        /* CUDA runtime error        */
+  LS_E_UNSUPPORTED = -3, /* task outside the device class */
+  LS_E_NOMEM = -4
+};
+
+/* ---- per-candidate status (mirrors the reference's exceptions) ---- */
+enum {
+  LS_OK = 0,
+  LS_ST_NO_LOOP = 1,         /* ProgramError "no loop named"      ls/ir.py:151       */
+  LS_ST_TILE_RANGE = 2,      /* tile factor out of range          ls/ir.py:363-364   */
+  LS_ST_VEC_DIVIDE = 3,      /* vectorize width does not divide   ls/ir.py:465-468   */
+  LS_ST_VEC_ZERO = 4,        /* vectorize width 0: ZeroDivisionError, ls/ir.py:465   */
+  LS_ST_REORDER_MISSING = 5, /* reorder: missing loops            ls/ir.py:416-417   */
+  LS_ST_REORDER_CHAIN = 6,   /* reorder: not a perfect nest chain ls/ir.py:398-399   */
+  LS_ST_BAD_FEATURE = 7,     /* CostModelError non-finite/negative ls/cost.py:43-45  */
+  LS_ST_UNSUPPORTED = 16,    /* transformed tree outside the device class            */
+  LS_ST_UNROLL_TABLE = 17,   /* unroll product not prepared (ls_task_prepare_unroll) */
+  LS_ST_OVERFLOW = 18        /* intermediate exceeded the device integer range       */
+};
+
+/* ---- task descriptor: the per-task parameter table ---- */
+typedef struct {
+  int32_t var;  /* variable id */
+  int32_t coef; /* nonzero coefficient */
+} ls_term;
+
+typedef struct {
+  int32_t n_terms;
+  int32_t konst;
+  ls_term terms[LS_MAX_TERMS]; /* sorted by var_rank (AffineExpr order, ls/ir.py:53) */
+} ls_expr;
+
+typedef struct {
+  int32_t kind;   /* LS_NODE_LOOP / LS_NODE_ACCESS */
+  int32_t parent; /* node index of the parent loop, -1 for the program body; nodes are in preorder */
+  /* loop fields (ls/ir.py:108-116) */
+  int32_t var, extent, step, parallel, unrolled, vector_width; /* vector_width 0 = None */
+  /* access fields (ls/ir.py:101-105) */
+  int32_t tensor, is_store;
+  ls_expr idx[LS_MAX_RANK];
+} ls_node;
+
+typedef struct {
+  int32_t rank;
+  int32_t elem_bytes;
+  int32_t shared; /* scope == "shared" */
+  int32_t dims[LS_MAX_RANK];
+} ls_tensor;
+
+typedef struct {
+  int32_t kind;       /* LS_XF_* */
+  int32_t var;        /* target loop variable id (-1: name never exists -> LS_ST_NO_LOOP) */
+  int32_t new_var;    /* TILE/VECTORIZE: id of the inner loop variable created */
+  int32_t param;      /* TILE/VECTORIZE: record param slot of the factor/width, -1 = use value */
+  int32_t value;      /* constant factor/width when param < 0 */
+  int32_t enable_bit; /* -1 = always applied, else bit index of ls_record.flags */
+  int32_t n_order;    /* REORDER: number of names in the order */
+  int32_t perm_shift; /* REORDER: first nibble of this order in ls_record.perm */
+  int32_t order[LS_MAX_ORDER]; /* REORDER: candidate var ids; nibble j picks the var at position j */
+} ls_xform;
+
+typedef struct {
+  int32_t abi_version; /* LS_ABI_VERSION */
+  int32_t family, target, dialect;
+  int32_t n_tensors;
+  ls_tensor tensors[LS_MAX_TENSORS];
+  int32_t n_nodes;
+  ls_node nodes[LS_MAX_NODES];
+  int32_t n_vars;
+  int32_t var_rank[LS_MAX_VARS]; /* rank of each var name in Python string order */
+  int32_t tid_var;               /* id of the var literally named "tid", -1 if none */
+  int32_t n_xforms;
+  ls_xform xforms[LS_MAX_XFORMS];
+  double coef[LS_NFEAT_GPU];   /* coefficients in feature order (ls/cost.py:155-161) */
+  int64_t cache_capacity;      /* CacheSpec.capacity_elements (ls/cost.py:97) */
+  int32_t issue_width;         /* SchedSpec.issue_width */
+  int32_t lat[LS_I_COUNT];     /* SchedSpec.latency_of for each emitted shape */
+  int32_t klass[LS_I_COUNT];   /* latency-class id per shape (same id <=> same class string) */
+  int32_t unit_cap[LS_I_COUNT];/* per class id: SchedSpec.units cap, 0 = uncapped */
+  double ptx_cost[LS_I_COUNT]; /* GpuSpec.instr_cost per shape root (default 1) */
+  double sm_underuse;          /* per-task constant, ls/ptx.py:238-241 */
+  double warp_slack;           /* per-task constant, ls/ptx.py:253-256 */
+  int32_t banks, warp_size;    /* GpuSpec.banks / warp_size (32 / 32) */
+} ls_task_desc;
+
+/* ---- packed candidate record (32 bytes, 16-byte aligned) ---- */
+typedef struct {
+  uint16_t param[LS_MAX_PARAMS]; /* tile factors / vector widths by template slot */
+  uint64_t perm;                 /* nibble-packed reorder permutations */
+  uint32_t flags;                /* enable bits of optional transforms */
+  uint32_t tag;                  /* reserved, must be 0 */
+} ls_record;
+
+typedef struct ls_task ls_task;
+
+/* ---- entry points ---- */
+const char* ls_last_error(void);
+int ls_abi_version(void);
+
+/* Validate and upload a task.  Replaces the per-candidate re-derivation of
+ * load_arch (ls/cost.py:81-129), the emitter's fixed block shapes
+ * (ls/ir.py:614-658) and schedule_block of those blocks (ls/ilp.py:158-204),
+ * which are computed once here instead of once per candidate. */
+int ls_task_create(const ls_task_desc* desc, int device, ls_task** out);
+int ls_task_destroy(ls_task* task);
+int ls_task_num_features(const ls_task* task);
+/* Precompute block-cycle entries for innermost-unroll products `u_values`
+ * (candidates needing an unprepared product report LS_ST_UNROLL_TABLE). */
+int ls_task_prepare_unroll(ls_task* task, const int64_t* u_values, int32_t n);
+
+/* Score n records.  Replaces evaluate_population + apply_schedule +
+ * emit_mock_asm + extract_features + score (ls/es.py:96-116,
+ * ls/cost.py:132-161).  Any output pointer may be NULL.  d_features is
+ * n x ls_task_num_features row-major float64. */
+int ls_score(ls_task* task, const ls_record* d_records, int64_t n, double* d_scores,
+             double* d_features, int32_t* d_status, void* stream);
+
+/* Score n records and return the k best by (score, base_index + i),
+ * ascending, fused in one pass (cmd_rank sort, ls/cli.py:124-126; rank,
+ * ls/cost.py:164-168).  Failed candidates are excluded.  Unfilled slots
+ * carry score +inf and index -1.  *d_n_valid (nullable) receives the number
+ * of successfully scored candidates. */
+int ls_score_topk(ls_task* task, const ls_record* d_records, int64_t n, int64_t base_index,
+                  int32_t k, double* d_top_scores, int64_t* d_top_index, int64_t* d_n_valid,
+                  void* stream);
+
+/* Merge n_lists sorted top-k lists (k_in entries each, contiguous) into the
+ * k_out best by (score, index).  Used after an NCCL all-gather of per-GPU
+ * lists; no reference equivalent (the reference is single-process). */
+int ls_topk_merge(const double* d_scores, const int64_t* d_index, int32_t n_lists, int32_t k_in,
+                  int32_t k_out, double* d_out_scores, int64_t* d_out_index, void* stream);
+
+/* Host-buffer variant of ls_score_topk: records in host memory (pinned or
+ * pageable), results written to host memory; the library stages the
+ * host->device copies in chunks overlapped with scoring.  Synchronous. */
+int ls_score_topk_host(ls_task* task, const ls_record* h_records, int64_t n, int64_t base_index,
+                       int32_t k, double* h_top_scores, int64_t* h_top_index, int64_t* h_n_valid,
+                       void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LOOPSCOUT_B200_H */

@@ -1,0 +1,157 @@
+"""Synthetic workloads of BASELINE.json's configs.
+
+Programs are built as canonical program JSON (parse_program) and schedule
+spaces as space dicts (space_axes).  Candidate lists are drawn with numpy
+seeds as per-axis choice indices, so a batch is a pure function of
+(config, n, seed) and the same indices give the reference's own schedules
+through ``SpaceTemplate.schedule_of``.
+"""
+
+from __future__ import annotations
+
+import itertools
+import json
+
+import numpy as np
+
+from .ir import parse_program
+
+
+def _acc(t, kind, idx):
+    return {"access": {"tensor": t, "kind": kind, "idx": list(idx)}}
+
+
+def _nest(loops, body):
+    for var, ext in reversed(loops):
+        body = [{"loop": {"var": var, "extent": ext, "body": body}}]
+    return body
+
+
+def divisors(n: int) -> list:
+    return [d for d in range(1, n + 1) if n % d == 0]
+
+
+def matmul_json(m: int, n: int | None = None, k: int | None = None) -> dict:
+    """C[i,j] += A[i,k] * B[k,j] over i<m, j<n, k<k (tests/helpers.py:47-56 shape)."""
+    n = m if n is None else n
+    k = m if k is None else k
+    return {"tensors": [{"name": "A", "dims": [m, k]}, {"name": "B", "dims": [k, n]},
+                        {"name": "C", "dims": [m, n]}],
+            "body": _nest([("i", m), ("j", n), ("k", k)],
+                          [_acc("A", "load", ["i", "k"]), _acc("B", "load", ["k", "j"]),
+                           _acc("C", "load", ["i", "j"]), _acc("C", "store", ["i", "j"])])}
+
+
+def batch_matmul_json(b: int, m: int, n: int, k: int) -> dict:
+    return {"tensors": [{"name": "A", "dims": [b, m, k]}, {"name": "B", "dims": [b, k, n]},
+                        {"name": "C", "dims": [b, m, n]}],
+            "body": _nest([("b", b), ("i", m), ("j", n), ("k", k)],
+                          [_acc("A", "load", ["b", "i", "k"]), _acc("B", "load", ["b", "k", "j"]),
+                           _acc("C", "load", ["b", "i", "j"]), _acc("C", "store", ["b", "i", "j"])])}
+
+
+def conv2d_json(n=1, oc=64, oh=56, ow=56, ic=64, kh=3, kw=3, stride=1) -> dict:
+    """NCHW conv2d on a pre-padded input: O[n,oc,oh,ow] += I[n,ic,s*oh+kh,s*ow+kw] * W[oc,ic,kh,kw]."""
+    s = "" if stride == 1 else f"{stride}*"
+    ih, iw = stride * (oh - 1) + kh, stride * (ow - 1) + kw
+    return {"tensors": [{"name": "I", "dims": [n, ic, ih, iw]}, {"name": "W", "dims": [oc, ic, kh, kw]},
+                        {"name": "O", "dims": [n, oc, oh, ow]}],
+            "body": _nest([("n", n), ("oc", oc), ("oh", oh), ("ow", ow), ("ic", ic), ("kh", kh), ("kw", kw)],
+                          [_acc("I", "load", ["n", "ic", f"{s}oh + kh", f"{s}ow + kw"]),
+                           _acc("W", "load", ["oc", "ic", "kh", "kw"]),
+                           _acc("O", "load", ["n", "oc", "oh", "ow"]),
+                           _acc("O", "store", ["n", "oc", "oh", "ow"])])}
+
+
+def program(spec: dict):
+    return parse_program(json.dumps(spec))
+
+
+def tiled_chain(loop_order: list, tiled: list) -> list:
+    """Loop names of the chain after tiling `tiled` loops in sorted order (each `v` -> v, v_i)."""
+    out = []
+    for v in loop_order:
+        out.append(v)
+        if v in tiled:
+            out.append(v + "_i")
+    return out
+
+
+def random_perms(names: list, count: int, seed: int) -> list:
+    rng = np.random.default_rng(seed)
+    seen, out = set(), []
+    while len(out) < count:
+        p = tuple(names[i] for i in rng.permutation(len(names)))
+        if p not in seen:
+            seen.add(p)
+            out.append(list(p))
+    return out
+
+
+def gemm_space(n: int = 1024) -> dict:
+    """Config 1: tile i/j/k by any divisor + any of the 720 chain orders."""
+    chain = tiled_chain(["i", "j", "k"], ["i", "j", "k"])
+    return {"tile": {v: divisors(n) for v in "ijk"},
+            "reorder": [list(p) for p in itertools.permutations(chain)]}
+
+
+def conv_space(reorders: int = 512, seed: int = 1, shape: dict | None = None) -> dict:
+    """Config 2: tile ic/oc/oh/ow by divisors + `reorders` random 11-loop chain orders."""
+    sh = dict(n=1, oc=64, oh=56, ow=56, ic=64, kh=3, kw=3)
+    sh.update(shape or {})
+    chain = tiled_chain(["n", "oc", "oh", "ow", "ic", "kh", "kw"], ["ic", "oc", "oh", "ow"])
+    return {"tile": {"ic": divisors(sh["ic"]), "oc": divisors(sh["oc"]),
+                     "oh": divisors(sh["oh"]), "ow": divisors(sh["ow"])},
+            "reorder": random_perms(chain, reorders, seed)}
+
+
+def distinct_indices(sizes, n: int, seed: int) -> np.ndarray:
+    """n distinct points of a mixed-radix space (rows of per-axis choice indices)."""
+    sizes = np.asarray(sizes, np.int64)
+    total = int(np.prod(sizes))
+    if n > total:
+        raise ValueError(f"space has {total} points, asked for {n}")
+    rng = np.random.default_rng(seed)
+    flat = rng.choice(total, size=n, replace=False) if total <= (1 << 27) else \
+        _feistel_sample(total, n, seed)
+    out = np.empty((n, len(sizes)), np.int64)
+    for a in range(len(sizes) - 1, -1, -1):
+        out[:, a] = flat % sizes[a]
+        flat = flat // sizes[a]
+    return out
+
+
+def _feistel_sample(total: int, n: int, seed: int) -> np.ndarray:
+    """Distinct values in [0,total) from a keyed bijection of [0, 2^b) by cycle walking."""
+    bits = max(2, int(total - 1).bit_length())
+    bits += bits & 1
+    half = bits // 2
+    mask = (1 << half) - 1
+    keys = np.random.default_rng(seed).integers(1, 1 << 31, size=4, dtype=np.int64)
+
+    def perm(x):
+        l, r = x >> half, x & mask
+        for k in keys:
+            f = ((r * 0x9E3779B1 + k) ^ (r >> 3)) & mask
+            l, r = r, l ^ f
+        return (l << half) | r
+
+    out = np.empty(0, np.int64)
+    x = np.arange(0, n, dtype=np.int64)
+    cursor = n
+    while len(out) < n:
+        y = perm(x)
+        while True:
+            bad = y >= total
+            if not bad.any():
+                break
+            y[bad] = perm(y[bad])
+        out = np.concatenate([out, y])
+        if len(out) < n:
+            x = np.arange(cursor, cursor + (n - len(out)), dtype=np.int64)
+            cursor += len(x)
+    return out[:n]
+
+
+KERNEL_LAUNCH = {"grid_blocks": 160, "threads_per_block": 256, "registers_per_thread": 32,
+                 "shared_mem_per_block": 4096}
