@@ -188,6 +188,13 @@ int ls_task_num_features(const ls_task* task);
  * (candidates needing an unprepared product report LS_ST_UNROLL_TABLE). */
 int ls_task_prepare_unroll(ls_task* task, const int64_t* u_values, int32_t n);
 
+/* Distinct innermost-unroll products U needed by the structurally supported
+ * records (device pass), sorted, at most `cap`; feed them to
+ * ls_task_prepare_unroll before scoring.  Only needed when the template or
+ * program marks loops `unroll`. */
+int ls_collect_unroll(ls_task* task, const ls_record* d_records, int64_t n, int64_t* h_values,
+                      int32_t cap, int32_t* h_count, void* stream);
+
 /* Score n records.  Replaces evaluate_population + apply_schedule +
  * emit_mock_asm + extract_features + score (ls/es.py:96-116,
  * ls/cost.py:132-161).  Any output pointer may be NULL.  d_features is

@@ -1,0 +1,1341 @@
+// loopscout_b200 engine: batched static cost evaluation of candidate loop-nest
+// schedules on sm_100a, behind the C-ABI of include/loopscout_b200.h.
+//
+// One thread evaluates one candidate end to end (record decode -> transform
+// application -> footprint/movement model -> instruction counts -> block
+// cycles -> linear score); a block-level streaming top-k is fused into the
+// same pass.  The reference pipeline this replaces, per candidate
+// (ls/ = /root/reference/pkg/src/loopscout):
+//   apply_schedule ls/ir.py:454-474, emit_mock_asm ls/ir.py:557-659,
+//   parse_asm/loop_map/count_simd ls/asm.py:110-337, CacheModel ls/cache.py:133-259,
+//   schedule_block/ilp_feature ls/ilp.py:158-271, PTX features ls/ptx.py:90-327,
+//   extract_features/score ls/cost.py:132-161, rank ls/cost.py:164-168.
+// The text pipeline is replaced by its structure: for a perfect loop chain the
+// emitted blocks, their trip weights and their schedules are closed-form in
+// the transformed chain (DESIGN.md §3 derives each term).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/loopscout_b200.h"
+
+namespace lsb {
+void fixed_block_cycles(const ls_task_desc& d, int64_t* c_init, int64_t* c_latch, int64_t* c_ret);
+int64_t body_block_cycles(const ls_task_desc& d, const std::vector<int>& load_t,
+                          const std::vector<int>& store_t, int64_t U, bool with_latch);
+}  // namespace lsb
+
+// ---------------------------------------------------------------------------
+// error reporting
+// ---------------------------------------------------------------------------
+static thread_local std::string g_err;
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+#define CUDA_TRY(x)                                                                        \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess) return fail(LS_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// device task table (staged into shared memory by every block)
+// ---------------------------------------------------------------------------
+constexpr int MAXACC = 16;
+constexpr int MAXRANK = LS_MAX_RANK;
+constexpr int MAXT = LS_MAX_TENSORS;
+constexpr int MAXTERM = 384;
+constexpr int MAXCH = LS_MAX_CHAIN;
+
+struct DTerm {
+  int32_t coef;
+  uint32_t req;  // enable bits that must be set for the term to exist
+  int32_t var;
+};
+
+struct DExpr {
+  int32_t konst;
+  int16_t t0;  // first term in DTask::term
+  int16_t nt;
+};
+
+struct DXform {
+  int8_t kind, var, new_var, param;
+  int8_t enable_bit, n_order, perm_shift, pad;
+  int32_t value;
+  int8_t order[LS_MAX_ORDER];
+};
+
+struct DUnroll {
+  int64_t u, c_inner, c_all;
+};
+
+struct __align__(16) DTask {
+  // base chain
+  int32_t n_base;
+  int32_t n_xf;
+  int32_t n_acc, n_tensors;
+  int32_t L, S;  // loads / stores of the innermost body
+  int32_t family;
+  int32_t costs_integral;
+  int32_t tid_var;
+  int32_t n_u;
+  int32_t banks, warp_size;
+  int64_t cap;
+  int64_t c_init, c_latch, c_ret;
+  double coef[LS_NFEAT_GPU];
+  double ptx_cost[LS_I_COUNT];
+  int64_t ptx_icost[LS_I_COUNT];
+  double sm_underuse, warp_slack;
+  const DUnroll* u_tab;
+  int32_t base_ext[MAXCH], base_step[MAXCH], base_vw[MAXCH];
+  int8_t base_var[MAXCH];
+  uint8_t base_flags[MAXCH];  // bit0 parallel, bit1 unrolled
+  DXform xf[LS_MAX_XFORMS];
+  // accesses of the innermost body, program order
+  uint8_t acc_tensor[MAXACC], acc_store[MAXACC];
+  DExpr expr[MAXACC][MAXRANK];
+  // tensors in first-appearance order among the accesses (CacheModel merge order)
+  uint8_t t_rank[MAXT], t_nu[MAXT], t_uacc[MAXT][MAXACC], t_eb[MAXT], t_shared[MAXT];
+  int32_t t_nacc[MAXT];
+  int32_t t_count0[MAXT][MAXRANK];
+  int64_t t_F0[MAXT];
+  int64_t t_stride[MAXT][MAXRANK];
+  int32_t n_terms;
+  DTerm term[MAXTERM];
+};
+
+struct ls_task {
+  ls_task_desc desc;
+  int device;
+  DTask host;           // host copy (u_tab points to the current device table)
+  DTask* d_task;        // current device copy
+  std::vector<DUnroll> utab;
+  std::vector<void*> retired;  // previous device copies / tables, freed on destroy
+  std::vector<int> load_t, store_t;
+  std::mutex mu;
+  int num_sms;
+};
+
+// ---------------------------------------------------------------------------
+// device helpers
+// ---------------------------------------------------------------------------
+struct SI {
+  int32_t lo, hi, stride, count;
+  int32_t exact;
+};
+
+__device__ __forceinline__ uint32_t gcd_u32(uint32_t a, uint32_t b) {
+  if (a == 0) return b;
+  if (b == 0) return a;
+  int sh = __ffs(a | b) - 1;
+  a >>= __ffs(a) - 1;
+  do {
+    b >>= __ffs(b) - 1;
+    if (a > b) {
+      uint32_t t = a;
+      a = b;
+      b = t;
+    }
+    b -= a;
+  } while (b);
+  return a << sh;
+}
+
+// _si_sum (ls/cache.py:46-62)
+__device__ __forceinline__ SI si_sum(SI a, SI b) {
+  if (a.count == 1) {
+    b.lo += a.lo;
+    b.hi += a.lo;
+    return b;
+  }
+  if (b.count == 1) {
+    a.lo += b.lo;
+    a.hi += b.lo;
+    return a;
+  }
+  int32_t lo = a.lo + b.lo, hi = a.hi + b.hi;
+  if (a.exact && b.exact) {
+    SI fine = a.stride <= b.stride ? a : b;
+    SI coarse = a.stride <= b.stride ? b : a;
+    if (coarse.stride % fine.stride == 0 && (int64_t)coarse.stride <= (int64_t)fine.stride * fine.count) {
+      SI r;
+      r.lo = lo;
+      r.hi = hi;
+      r.stride = fine.stride;
+      r.count = (hi - lo) / fine.stride + 1;
+      r.exact = 1;
+      return r;
+    }
+  }
+  int32_t g = (int32_t)gcd_u32((uint32_t)a.stride, (uint32_t)b.stride);
+  int64_t est = g ? (hi - lo) / g + 1 : 1;
+  int64_t prod = (int64_t)a.count * b.count;
+  SI r;
+  r.lo = lo;
+  r.hi = hi;
+  r.stride = g;
+  r.count = (int32_t)(est < prod ? est : prod);
+  r.exact = 0;
+  return r;
+}
+
+// _si_union (ls/cache.py:65-77)
+__device__ __forceinline__ SI si_union(SI a, SI b) {
+  if (a.lo == b.lo && a.hi == b.hi && a.stride == b.stride && a.count == b.count && a.exact == b.exact)
+    return a;
+  int32_t lo = min(a.lo, b.lo), hi = max(a.hi, b.hi);
+  if (a.exact && b.exact && a.stride == b.stride && a.stride > 0 && (a.lo - b.lo) % a.stride == 0) {
+    if (a.lo <= b.hi + a.stride && b.lo <= a.hi + a.stride) {
+      SI r;
+      r.lo = lo;
+      r.hi = hi;
+      r.stride = a.stride;
+      r.count = (hi - lo) / a.stride + 1;
+      r.exact = 1;
+      return r;
+    }
+  }
+  uint32_t dl = (uint32_t)abs(a.lo - b.lo);
+  int32_t g = (int32_t)gcd_u32(gcd_u32((uint32_t)a.stride, (uint32_t)b.stride), dl);
+  int64_t est = g ? (hi - lo) / g + 1 : 1;
+  int64_t sum = (int64_t)a.count + b.count;
+  SI r;
+  r.lo = lo;
+  r.hi = hi;
+  r.stride = g;
+  r.count = (int32_t)(est < sum ? est : sum);
+  r.exact = 0;
+  return r;
+}
+
+struct Cand {
+  int32_t ext[LS_MAX_VARS], step[LS_MAX_VARS], vw[LS_MAX_VARS];
+  int8_t pos[LS_MAX_VARS];
+  uint8_t flg[LS_MAX_VARS];
+  int8_t chain[MAXCH];
+  int n;
+  uint32_t exists;
+  uint32_t flags;
+};
+
+__device__ __forceinline__ bool present(const DTerm& t, uint32_t flags) { return (t.req & ~flags) == 0; }
+
+// expr_range (ls/cache.py:80-96): terms in name order, vars at chain
+// positions >= p expanded, others held at 0
+__device__ __forceinline__ SI expr_range(const DTask& T, const DExpr& e, const Cand& c, int p) {
+  SI acc;
+  acc.lo = acc.hi = e.konst;
+  acc.stride = 0;
+  acc.count = 1;
+  acc.exact = 1;
+  for (int k = 0; k < e.nt; ++k) {
+    const DTerm& t = T.term[e.t0 + k];
+    if (!present(t, c.flags)) continue;
+    int u = t.var;
+    if (c.pos[u] < p) continue;
+    int32_t E = c.ext[u];
+    if (E == 1) continue;
+    int32_t d = t.coef * c.step[u];
+    SI s;
+    if (d > 0) {
+      s.lo = 0;
+      s.hi = d * (E - 1);
+      s.stride = d;
+    } else {
+      s.lo = d * (E - 1);
+      s.hi = 0;
+      s.stride = -d;
+    }
+    s.count = E;
+    s.exact = 1;
+    acc = si_sum(acc, s);
+  }
+  return acc;
+}
+
+// tensor_footprint of one dimension (ls/cache.py:117-130)
+__device__ __forceinline__ int32_t dim_count(const DTask& T, const Cand& c, int t, int d, int p) {
+  SI u = expr_range(T, T.expr[T.t_uacc[t][0]][d], c, p);
+  for (int a = 1; a < T.t_nu[t]; ++a) u = si_union(u, expr_range(T, T.expr[T.t_uacc[t][a]][d], c, p));
+  return u.count;
+}
+
+__device__ __forceinline__ int64_t unroll_lookup(const DTask& T, int64_t U, bool inner, bool* ok) {
+  int lo = 0, hi = T.n_u - 1;
+  while (lo <= hi) {
+    int mid = (lo + hi) >> 1;
+    int64_t u = __ldg(&T.u_tab[mid].u);
+    if (u == U) {
+      *ok = true;
+      return inner ? __ldg(&T.u_tab[mid].c_inner) : __ldg(&T.u_tab[mid].c_all);
+    }
+    if (u < U)
+      lo = mid + 1;
+    else
+      hi = mid - 1;
+  }
+  *ok = false;
+  return 0;
+}
+
+// Apply the record's transforms to the base chain (ls/ir.py:361-474).
+__device__ int apply_transforms(const DTask& T, const ls_record& r, Cand& c) {
+  c.n = T.n_base;
+  c.exists = 0;
+  c.flags = r.flags;
+#pragma unroll 1
+  for (int v = 0; v < LS_MAX_VARS; ++v) c.pos[v] = -1;
+#pragma unroll 1
+  for (int p = 0; p < T.n_base; ++p) {
+    int v = T.base_var[p];
+    c.chain[p] = (int8_t)v;
+    c.pos[v] = (int8_t)p;
+    c.ext[v] = T.base_ext[p];
+    c.step[v] = T.base_step[p];
+    c.vw[v] = T.base_vw[p];
+    c.flg[v] = T.base_flags[p];
+    c.exists |= 1u << v;
+  }
+#pragma unroll 1
+  for (int x = 0; x < T.n_xf; ++x) {
+    const DXform& xf = T.xf[x];
+    if (xf.enable_bit >= 0 && !((r.flags >> xf.enable_bit) & 1u)) continue;
+    const int v = xf.var;
+    switch (xf.kind) {
+      case LS_XF_TILE:
+      case LS_XF_VECTORIZE: {
+        if (v < 0 || !((c.exists >> v) & 1u)) return LS_ST_NO_LOOP;
+        int32_t F = xf.param >= 0 ? (int32_t)r.param[xf.param] : xf.value;
+        if (xf.kind == LS_XF_VECTORIZE) {
+          if (F == 0) return LS_ST_VEC_ZERO;
+          if (c.ext[v] % F != 0) return LS_ST_VEC_DIVIDE;
+        }
+        if (F < 1 || F > c.ext[v]) return LS_ST_TILE_RANGE;
+        if (c.n >= MAXCH) return LS_ST_OVERFLOW;
+        const int u = xf.new_var;
+        const int p = c.pos[v];
+        for (int q = c.n; q > p + 1; --q) {
+          c.chain[q] = c.chain[q - 1];
+          c.pos[c.chain[q]] = (int8_t)q;
+        }
+        c.chain[p + 1] = (int8_t)u;
+        c.pos[u] = (int8_t)(p + 1);
+        c.n++;
+        c.ext[u] = F;
+        c.step[u] = c.step[v];
+        c.vw[u] = xf.kind == LS_XF_VECTORIZE ? F : 0;
+        c.flg[u] = 0;
+        c.exists |= 1u << u;
+        c.ext[v] = (c.ext[v] + F - 1) / F;
+        c.step[v] *= F;
+        c.vw[v] = 0;
+        break;
+      }
+      case LS_XF_REORDER: {
+        const int m = xf.n_order;
+        if (m < 2) break;
+        int8_t vars[LS_MAX_ORDER];
+        uint32_t seen = 0;
+        int pmin = MAXCH, pmax = -1;
+        for (int j = 0; j < m; ++j) {
+          int nib = (int)((r.perm >> (4 * (xf.perm_shift + j))) & 0xF);
+          int w = nib < m ? xf.order[nib] : -1;
+          if (w < 0 || !((c.exists >> w) & 1u)) return LS_ST_NO_LOOP;
+          vars[j] = (int8_t)w;
+        }
+        for (int j = 0; j < m; ++j) {
+          uint32_t bit = 1u << vars[j];
+          if (seen & bit) return LS_ST_REORDER_MISSING;
+          seen |= bit;
+          pmin = min(pmin, (int)c.pos[vars[j]]);
+          pmax = max(pmax, (int)c.pos[vars[j]]);
+        }
+        if (pmax - pmin != m - 1) return LS_ST_REORDER_CHAIN;
+        for (int j = 0; j < m; ++j) {
+          c.chain[pmin + j] = vars[j];
+          c.pos[vars[j]] = (int8_t)(pmin + j);
+        }
+        break;
+      }
+      case LS_XF_UNROLL:
+      case LS_XF_PARALLEL:
+        if (v < 0 || !((c.exists >> v) & 1u)) return LS_ST_NO_LOOP;
+        c.flg[v] |= xf.kind == LS_XF_UNROLL ? 2 : 1;
+        break;
+      default:
+        return LS_ST_UNSUPPORTED;
+    }
+  }
+  return LS_OK;
+}
+
+// Branching (non-inlined) loops and the innermost replication factor U.
+// Returns false if an unrolled loop sits above a branching loop (its sub-chain
+// would be emitted several times: the general-tree case).
+__device__ __forceinline__ bool chain_shape(const Cand& c, int8_t* cpos, int* k_out, int64_t* U_out) {
+  int k = 0, last = -1;
+  for (int p = 0; p < c.n; ++p) {
+    int v = c.chain[p];
+    if (!c.vw[v] && !(c.flg[v] & 2)) {
+      cpos[k++] = (int8_t)p;
+      last = p;
+    }
+  }
+  int64_t U = 1;
+  for (int p = 0; p < c.n; ++p) {
+    int v = c.chain[p];
+    if (c.vw[v] || !(c.flg[v] & 2)) continue;
+    if (p < last) return false;
+    U *= c.ext[v];
+  }
+  *k_out = k;
+  *U_out = U;
+  return true;
+}
+
+__device__ __forceinline__ double rn_mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double rn_add(double a, double b) { return __dadd_rn(a, b); }
+
+// bank_conflict_factor (ls/ptx.py:264-307) of innermost access a
+__device__ int64_t bank_factor(const DTask& T, const Cand& c, int a) {
+  const int t = T.acc_tensor[a];
+  const int rank = T.t_rank[t];
+  int tid = -1;
+  uint32_t used = 0;
+  for (int d = 0; d < rank; ++d) {
+    const DExpr& e = T.expr[a][d];
+    for (int k = 0; k < e.nt; ++k)
+      if (present(T.term[e.t0 + k], c.flags)) used |= 1u << T.term[e.t0 + k].var;
+  }
+  if (T.tid_var >= 0 && ((used >> T.tid_var) & 1u)) {
+    tid = T.tid_var;
+  } else {
+    for (int p = 0; p < c.n; ++p) {
+      int v = c.chain[p];
+      if ((c.flg[v] & 1) && ((used >> v) & 1u)) tid = v;
+    }
+  }
+  if (tid < 0) return 1;  // every lane hits one word
+  int lanes = min(T.warp_size, c.ext[tid]);
+  int64_t A = 0, B = 0;
+  for (int d = 0; d < rank; ++d) {
+    const DExpr& e = T.expr[a][d];
+    int64_t ct = 0;
+    for (int k = 0; k < e.nt; ++k) {
+      const DTerm& tm = T.term[e.t0 + k];
+      if (present(tm, c.flags) && tm.var == tid) ct += tm.coef;
+    }
+    A += (int64_t)e.konst * T.t_stride[t][d];
+    B += ct * T.t_stride[t][d];
+  }
+  // words are monotone in the lane id, so equal words are adjacent
+  uint8_t cnt[64];
+  for (int b = 0; b < T.banks && b < 64; ++b) cnt[b] = 0;
+  int64_t prev = 0, best = 0;
+  for (int l = 0; l < lanes; ++l) {
+    int64_t num = (A + B * l) * T.t_eb[t];
+    int64_t w = num >= 0 ? num / 4 : -((-num + 3) / 4);
+    if (l == 0 || w != prev) {
+      int64_t b = w % T.banks;
+      if (b < 0) b += T.banks;
+      int nc = ++cnt[b];
+      best = max(best, (int64_t)nc);
+    }
+    prev = w;
+  }
+  return best;
+}
+
+// extract_features + score for one candidate.  Returns the status.
+__device__ int eval_candidate(const DTask& T, const ls_record& r, double* f, double* score) {
+  Cand c;
+  int st = apply_transforms(T, r, c);
+  if (st) return st;
+  int8_t cpos[MAXCH];
+  int k;
+  int64_t U;
+  if (!chain_shape(c, cpos, &k, &U)) return LS_ST_UNSUPPORTED;
+
+  // ---- movement model over the chain, innermost first (CacheModel._visit_loop)
+  int32_t cnt[MAXT][MAXRANK];
+  uint32_t dmask[MAXT][MAXRANK];
+  uint32_t tmask[MAXT];
+  int64_t Fb[MAXT], dm[MAXT];
+  uint32_t reuse = 0;
+  const int nT = T.n_tensors;
+  for (int t = 0; t < nT; ++t) {
+    tmask[t] = 0;
+    for (int d = 0; d < T.t_rank[t]; ++d) {
+      uint32_t m = 0;
+      for (int a = 0; a < T.t_nu[t]; ++a) {
+        const DExpr& e = T.expr[T.t_uacc[t][a]][d];
+        for (int q = 0; q < e.nt; ++q)
+          if (present(T.term[e.t0 + q], c.flags)) m |= 1u << T.term[e.t0 + q].var;
+      }
+      dmask[t][d] = m;
+      tmask[t] |= m;
+      cnt[t][d] = T.t_count0[t][d];
+    }
+    Fb[t] = T.t_F0[t];
+    dm[t] = T.t_nacc[t];
+    reuse |= 1u << t;
+  }
+  const int64_t cap = T.cap;
+  for (int p = c.n - 1; p >= 0; --p) {
+    const int v = c.chain[p];
+    const int64_t E = c.ext[v];
+    int64_t single = 0;
+    for (int t = 0; t < nT; ++t) single += Fb[t];
+    for (int t = 0; t < nT; ++t) {
+      const bool uses = (tmask[t] >> v) & 1u;
+      int64_t Ff = Fb[t];
+      if (uses) {
+        Ff = 1;
+        for (int d = 0; d < T.t_rank[t]; ++d) {
+          if ((dmask[t][d] >> v) & 1u) cnt[t][d] = dim_count(T, c, t, d, p);
+          Ff *= cnt[t][d];
+        }
+      }
+      bool ru = (reuse >> t) & 1u;
+      if (single > cap && !uses) ru = false;
+      const int64_t per = (single <= cap || ru) ? Ff : dm[t] * E;
+      if (Ff > cap) ru = false;
+      dm[t] = per;
+      reuse = ru ? (reuse | (1u << t)) : (reuse & ~(1u << t));
+      Fb[t] = Ff;
+    }
+  }
+  int64_t dmov = 0;
+  for (int t = 0; t < nT; ++t) dmov += dm[t];
+
+  const int64_t L = T.L, S = T.S;
+  int nf;
+  if (T.family == LS_FAMILY_CPU) {
+    // counts over matched loop blocks and block cycles (ls/asm.py:250-337, ls/ilp.py:262-271)
+    int64_t ilp, nld = 0, nst = 0;
+    bool ok;
+    if (k == 0) {
+      ilp = unroll_lookup(T, U, false, &ok);
+      if (!ok) return LS_ST_UNROLL_TABLE;
+    } else {
+      int64_t W = 1;
+      ilp = T.c_init + (int64_t)(k - 1) * T.c_latch + T.c_ret;
+      for (int j = 0; j + 1 < k; ++j) {
+        W *= c.ext[c.chain[cpos[j]]];
+        ilp += T.c_init * W;
+      }
+      W *= c.ext[c.chain[cpos[k - 1]]];
+      int64_t ci = unroll_lookup(T, U, true, &ok);
+      if (!ok) return LS_ST_UNROLL_TABLE;
+      ilp += ci * W;
+      nld = L * U * W;
+      nst = S * U * W;
+    }
+    f[0] = (double)nst;  // n_fma == n_vstore: one fma per store
+    f[1] = (double)nld;
+    f[2] = (double)nst;
+    f[3] = (double)dmov;
+    f[4] = (double)ilp;
+    nf = LS_NFEAT_CPU;
+  } else {
+    // PTX trips: a counter register repeats every 8 depths (ls/ir.py:627), so a
+    // loop with a branching loop 8 deeper in its region has no trip (ls/ptx.py:163-169)
+    int64_t Wp[MAXCH + 1];
+    Wp[0] = 1;
+    for (int j = 0; j < k; ++j) Wp[j + 1] = Wp[j] * (j + 8 <= k - 1 ? 1 : c.ext[c.chain[cpos[j]]]);
+    const int64_t Wi = Wp[k];
+    double work;
+    if (T.costs_integral) {
+      const int64_t* ic = T.ptx_icost;
+      int64_t w = ic[LS_I_RET];
+      for (int j = 0; j < k; ++j)
+        w += ic[LS_I_INIT] * Wp[j] + (ic[LS_I_ADD] + ic[LS_I_CMP] + ic[LS_I_BRANCH]) * Wp[j + 1];
+      w += Wi * U * (L * ic[LS_I_LOAD] + S * (ic[LS_I_FMA] + ic[LS_I_STORE]));
+      work = (double)w;
+    } else {  // line-order float accumulation, as thread_cycles does (ls/ptx.py:225-235)
+      const double* pc = T.ptx_cost;
+      work = 0.0;
+      for (int j = 0; j < k; ++j) work = rn_add(work, rn_mul(pc[LS_I_INIT], (double)Wp[j]));
+      const double wi = (double)Wi;
+      for (int64_t u = 0; u < U; ++u) {
+        for (int a = 0; a < L; ++a) work = rn_add(work, rn_mul(pc[LS_I_LOAD], wi));
+        for (int a = 0; a < S; ++a) {
+          work = rn_add(work, rn_mul(pc[LS_I_FMA], wi));
+          work = rn_add(work, rn_mul(pc[LS_I_STORE], wi));
+        }
+      }
+      for (int j = k - 1; j >= 0; --j) {
+        const double wj = (double)Wp[j + 1];
+        work = rn_add(work, rn_mul(pc[LS_I_ADD], wj));
+        work = rn_add(work, rn_mul(pc[LS_I_CMP], wj));
+        work = rn_add(work, rn_mul(pc[LS_I_BRANCH], wj));
+      }
+      work = rn_add(work, pc[LS_I_RET]);
+    }
+    // shared-memory ops (ls/ptx.py:310-327): volume counts vector loops once
+    double smem = 0.0;
+    for (int a = 0; a < T.n_acc; ++a) {
+      if (!T.t_shared[T.acc_tensor[a]]) continue;
+      int64_t vol = 1;
+      for (int p = 0; p < c.n; ++p) vol *= c.vw[c.chain[p]] ? 1 : c.ext[c.chain[p]];
+      smem = rn_add(smem, (double)(vol * bank_factor(T, c, a)));
+    }
+    f[0] = work;
+    f[1] = T.sm_underuse;
+    f[2] = T.warp_slack;
+    f[3] = smem;
+    f[4] = (double)(S * U * Wi);
+    f[5] = (double)(L * U * Wi);
+    f[6] = (double)(S * U * Wi);
+    nf = LS_NFEAT_GPU;
+  }
+  double total = 0.0;
+  for (int q = 0; q < nf; ++q) {
+    if (!(f[q] >= 0.0) || isinf(f[q])) return LS_ST_BAD_FEATURE;
+    total = rn_add(total, rn_mul(T.coef[q], f[q]));
+  }
+  *score = total;
+  return LS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// kernels
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void stage_task(DTask& s, const DTask* __restrict__ g) {
+  const int4* src = reinterpret_cast<const int4*>(g);
+  int4* dst = reinterpret_cast<int4*>(&s);
+  for (int i = threadIdx.x; i < (int)(sizeof(DTask) / 16); i += blockDim.x) dst[i] = __ldg(&src[i]);
+  __syncthreads();
+}
+
+__device__ __forceinline__ ls_record load_record(const ls_record* __restrict__ recs, int64_t i) {
+  const int4* p = reinterpret_cast<const int4*>(recs + i);
+  int4 a = __ldg(p), b = __ldg(p + 1);
+  ls_record r;
+  memcpy(&r, &a, 16);
+  memcpy(reinterpret_cast<char*>(&r) + 16, &b, 16);
+  return r;
+}
+
+__global__ void __launch_bounds__(256) score_kernel(const DTask* __restrict__ gtask,
+                                                    const ls_record* __restrict__ recs, int64_t n,
+                                                    double* __restrict__ scores,
+                                                    double* __restrict__ feats,
+                                                    int32_t* __restrict__ status) {
+  __shared__ DTask T;
+  stage_task(T, gtask);
+  const int nf = T.family == LS_FAMILY_CPU ? LS_NFEAT_CPU : LS_NFEAT_GPU;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    ls_record r = load_record(recs, i);
+    double f[LS_NFEAT_GPU];
+    double s = 0.0;
+    int st = eval_candidate(T, r, f, &s);
+    if (st) s = __longlong_as_double(0x7ff8000000000000ll);
+    if (scores) scores[i] = s;
+    if (status) status[i] = st;
+    if (feats)
+      for (int q = 0; q < nf; ++q) feats[i * nf + q] = st ? __longlong_as_double(0x7ff8000000000000ll) : f[q];
+  }
+}
+
+// ---- streaming top-k on (score, index) ------------------------------------
+struct Key {
+  unsigned long long s;
+  long long i;
+};
+constexpr unsigned long long KEY_INF_S = ~0ull;
+constexpr long long KEY_INF_I = LLONG_MAX;
+
+__device__ __forceinline__ bool kless(const Key& a, const Key& b) {
+  return a.s < b.s || (a.s == b.s && a.i < b.i);
+}
+__device__ __forceinline__ unsigned long long order_bits(double x) {
+  unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double from_order_bits(unsigned long long o) {
+  unsigned long long b = (o >> 63) ? (o & 0x7fffffffffffffffull) : ~o;
+  return __longlong_as_double((long long)b);
+}
+
+constexpr int TK_BUF = 2048;
+constexpr int TK_MAXK = 1024;
+
+struct TopkState {
+  Key buf[TK_BUF];
+  Key thr;
+  int cnt;
+};
+
+// Sort buf[0..cnt) (padded to TK_BUF with +inf) and keep the k smallest.
+__device__ void topk_compact(TopkState& S, int k) {
+  const int cnt = S.cnt;
+  for (int i = cnt + threadIdx.x; i < TK_BUF; i += blockDim.x) {
+    S.buf[i].s = KEY_INF_S;
+    S.buf[i].i = KEY_INF_I;
+  }
+  __syncthreads();
+  for (int size = 2; size <= TK_BUF; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = threadIdx.x; t < TK_BUF / 2; t += blockDim.x) {
+        int lo = 2 * t - (t & (stride - 1));
+        int hi = lo + stride;
+        bool up = (lo & size) == 0;
+        Key a = S.buf[lo], b = S.buf[hi];
+        if (kless(b, a) == up) {
+          S.buf[lo] = b;
+          S.buf[hi] = a;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (threadIdx.x == 0) {
+    int keep = cnt < k ? cnt : k;
+    S.cnt = keep;
+    if (keep == k) S.thr = S.buf[k - 1];
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void topk_init(TopkState& S) {
+  if (threadIdx.x == 0) {
+    S.cnt = 0;
+    S.thr.s = KEY_INF_S;
+    S.thr.i = KEY_INF_I;
+  }
+  __syncthreads();
+}
+
+// One round: every thread offers at most one key; compacts when the buffer
+// could overflow on the next round.
+__device__ __forceinline__ void topk_offer(TopkState& S, bool has, const Key& key, int k) {
+  if (has && kless(key, S.thr)) {
+    int slot = atomicAdd(&S.cnt, 1);
+    S.buf[slot] = key;
+  }
+  __syncthreads();
+  const int c = S.cnt;
+  __syncthreads();
+  if (c > TK_BUF - (int)blockDim.x) topk_compact(S, k);
+}
+
+__global__ void __launch_bounds__(256) score_topk_kernel(const DTask* __restrict__ gtask,
+                                                         const ls_record* __restrict__ recs,
+                                                         int64_t n, int64_t base_index, int k,
+                                                         Key* __restrict__ block_out,
+                                                         unsigned long long* __restrict__ n_valid) {
+  __shared__ DTask T;
+  __shared__ TopkState S;
+  stage_task(T, gtask);
+  topk_init(S);
+  unsigned int valid = 0;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    bool has = false;
+    Key key;
+    if (i < n) {
+      ls_record r = load_record(recs, i);
+      double f[LS_NFEAT_GPU];
+      double s;
+      if (eval_candidate(T, r, f, &s) == LS_OK) {
+        has = true;
+        key.s = order_bits(s);
+        key.i = base_index + i;
+        ++valid;
+      }
+    }
+    topk_offer(S, has, key, k);
+  }
+  topk_compact(S, k);
+  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    Key o;
+    if (j < S.cnt) {
+      o = S.buf[j];
+    } else {
+      o.s = KEY_INF_S;
+      o.i = KEY_INF_I;
+    }
+    block_out[(int64_t)blockIdx.x * k + j] = o;
+  }
+  // warp-reduce the valid counts, one atomic per warp
+  for (int off = 16; off > 0; off >>= 1) valid += __shfl_down_sync(0xffffffffu, valid, off);
+  if ((threadIdx.x & 31) == 0 && valid) atomicAdd(n_valid, (unsigned long long)valid);
+}
+
+// Merge m keys (any order, +inf padded) into the k best, written as (score, index).
+__global__ void __launch_bounds__(1024) merge_keys_kernel(const Key* __restrict__ in, int64_t m, int k,
+                                                          double* __restrict__ out_s,
+                                                          int64_t* __restrict__ out_i) {
+  __shared__ TopkState S;
+  topk_init(S);
+  for (int64_t base = 0; base < m; base += blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    bool has = false;
+    Key key;
+    if (i < m) {
+      key = in[i];
+      has = !(key.s == KEY_INF_S && key.i == KEY_INF_I);
+    }
+    topk_offer(S, has, key, k);
+  }
+  topk_compact(S, k);
+  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    if (j < S.cnt) {
+      out_s[j] = from_order_bits(S.buf[j].s);
+      out_i[j] = S.buf[j].i;
+    } else {
+      out_s[j] = __longlong_as_double(0x7ff0000000000000ll);
+      out_i[j] = -1;
+    }
+  }
+}
+
+__global__ void lists_to_keys_kernel(const double* __restrict__ s, const int64_t* __restrict__ idx, int64_t m,
+                                     Key* __restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  Key k;
+  if (idx[i] < 0) {
+    k.s = KEY_INF_S;
+    k.i = KEY_INF_I;
+  } else {
+    k.s = order_bits(s[i]);
+    k.i = idx[i];
+  }
+  out[i] = k;
+}
+
+// U of every structurally supported candidate, into an open-addressing set.
+__global__ void __launch_bounds__(256) collect_unroll_kernel(const DTask* __restrict__ gtask,
+                                                             const ls_record* __restrict__ recs, int64_t n,
+                                                             unsigned long long* __restrict__ set, int cap) {
+  __shared__ DTask T;
+  stage_task(T, gtask);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    ls_record r = load_record(recs, i);
+    Cand c;
+    if (apply_transforms(T, r, c)) continue;
+    int8_t cpos[MAXCH];
+    int k;
+    int64_t U;
+    if (!chain_shape(c, cpos, &k, &U)) continue;
+    unsigned long long key = (unsigned long long)U;
+    unsigned int h = (unsigned int)((key * 0x9E3779B97F4A7C15ull) >> 40) % (unsigned)cap;
+    for (int probe = 0; probe < cap; ++probe) {
+      unsigned long long prev = atomicCAS(&set[h], 0ull, key);
+      if (prev == 0ull || prev == key) break;
+      h = (h + 1) % (unsigned)cap;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host: task construction
+// ---------------------------------------------------------------------------
+namespace {
+
+struct HTerm {
+  int var;
+  int64_t coef;
+  uint32_t req;
+};
+
+int build_task(const ls_task_desc& d, DTask& T, std::vector<int>& load_t, std::vector<int>& store_t) {
+  memset(&T, 0, sizeof(T));
+  if (d.abi_version != LS_ABI_VERSION) return fail(LS_E_ARG, "abi_version mismatch");
+  if (d.n_nodes <= 0 || d.n_nodes > LS_MAX_NODES || d.n_tensors < 1 || d.n_tensors > LS_MAX_TENSORS ||
+      d.n_vars < 1 || d.n_vars > LS_MAX_VARS || d.n_xforms < 0 || d.n_xforms > LS_MAX_XFORMS)
+    return fail(LS_E_ARG, "descriptor counts out of range");
+  if (!((d.family == LS_FAMILY_CPU && (d.target == LS_TARGET_X86 || d.target == LS_TARGET_AARCH64)) ||
+        (d.family == LS_FAMILY_GPU && d.target == LS_TARGET_PTX)))
+    return fail(LS_E_UNSUPPORTED, "family/target combination not supported");
+  // ---- perfect chain: loops 0..L-1 each the only child of the previous, accesses under the last
+  int nl = 0;
+  while (nl < d.n_nodes && d.nodes[nl].kind == LS_NODE_LOOP) {
+    if (d.nodes[nl].parent != nl - 1) return fail(LS_E_UNSUPPORTED, "program is not a perfect loop chain");
+    ++nl;
+  }
+  if (nl == 0 || nl > MAXCH) return fail(LS_E_UNSUPPORTED, "program is not a perfect loop chain of <= 16 loops");
+  const int na = d.n_nodes - nl;
+  if (na < 1 || na > MAXACC) return fail(LS_E_UNSUPPORTED, "innermost body must hold 1..16 accesses");
+  for (int i = nl; i < d.n_nodes; ++i)
+    if (d.nodes[i].kind != LS_NODE_ACCESS || d.nodes[i].parent != nl - 1)
+      return fail(LS_E_UNSUPPORTED, "program is not a perfect loop chain (accesses outside the innermost loop)");
+  int ntile = 0;
+  for (int x = 0; x < d.n_xforms; ++x)
+    if (d.xforms[x].kind == LS_XF_TILE || d.xforms[x].kind == LS_XF_VECTORIZE) ++ntile;
+  if (nl + ntile > MAXCH) return fail(LS_E_UNSUPPORTED, "transformed chain could exceed 16 loops");
+
+  T.n_base = nl;
+  std::vector<int64_t> span(LS_MAX_VARS, 0);  // bound on step*(extent) of each var's base loop
+  std::vector<int> base_of(LS_MAX_VARS, -1);
+  for (int p = 0; p < nl; ++p) {
+    const ls_node& n = d.nodes[p];
+    if (n.var < 0 || n.var >= d.n_vars || n.extent < 1 || n.step < 1 || n.extent >= (1 << 30) ||
+        n.step >= (1 << 30))
+      return fail(LS_E_ARG, "bad loop node");
+    T.base_var[p] = (int8_t)n.var;
+    T.base_ext[p] = n.extent;
+    T.base_step[p] = n.step;
+    T.base_vw[p] = n.vector_width;
+    T.base_flags[p] = (uint8_t)((n.parallel ? 1 : 0) | (n.unrolled ? 2 : 0));
+    span[n.var] = (int64_t)n.step * n.extent;
+    base_of[n.var] = p;
+  }
+  // transforms
+  T.n_xf = d.n_xforms;
+  for (int x = 0; x < d.n_xforms; ++x) {
+    const ls_xform& s = d.xforms[x];
+    DXform& o = T.xf[x];
+    if (s.var >= d.n_vars || s.new_var >= d.n_vars || s.param >= LS_MAX_PARAMS || s.enable_bit >= 32 ||
+        s.n_order < 0 || s.n_order > LS_MAX_ORDER || s.perm_shift < 0 || s.perm_shift + s.n_order > 16)
+      return fail(LS_E_ARG, "bad transform slot");
+    if ((s.kind == LS_XF_TILE || s.kind == LS_XF_VECTORIZE) && s.new_var < 0)
+      return fail(LS_E_ARG, "tile without new_var");
+    o.kind = (int8_t)s.kind;
+    o.var = (int8_t)s.var;
+    o.new_var = (int8_t)s.new_var;
+    o.param = (int8_t)s.param;
+    o.value = s.value;
+    o.enable_bit = (int8_t)s.enable_bit;
+    o.n_order = (int8_t)s.n_order;
+    o.perm_shift = (int8_t)s.perm_shift;
+    for (int j = 0; j < s.n_order; ++j) o.order[j] = (int8_t)s.order[j];
+  }
+  // ---- symbolic expression rewrite: final term lists with enable requirements
+  // (_rewrite_exprs ls/ir.py:350-358 applied for every Tile/Vectorize of the template)
+  std::vector<uint32_t> creq(LS_MAX_VARS, 0);  // enable bits under which each var exists
+  std::vector<std::vector<std::vector<HTerm>>> ex(na);
+  for (int a = 0; a < na; ++a) {
+    const ls_node& n = d.nodes[nl + a];
+    if (n.tensor < 0 || n.tensor >= d.n_tensors) return fail(LS_E_ARG, "bad tensor index");
+    const int rank = d.tensors[n.tensor].rank;
+    if (rank < 1 || rank > MAXRANK) return fail(LS_E_ARG, "bad rank");
+    ex[a].resize(rank);
+    for (int k = 0; k < rank; ++k)
+      for (int t = 0; t < n.idx[k].n_terms; ++t)
+        ex[a][k].push_back({n.idx[k].terms[t].var, n.idx[k].terms[t].coef, 0u});
+  }
+  for (int x = 0; x < d.n_xforms; ++x) {
+    const ls_xform& s = d.xforms[x];
+    if (s.kind != LS_XF_TILE && s.kind != LS_XF_VECTORIZE) continue;
+    if (s.var < 0) continue;
+    uint32_t bit = s.enable_bit >= 0 ? (1u << s.enable_bit) : 0u;
+    creq[s.new_var] = creq[s.var] | bit;
+    span[s.new_var] = span[s.var];
+    for (auto& acc : ex)
+      for (auto& e : acc) {
+        std::vector<HTerm> add;
+        for (auto& t : e)
+          if (t.var == s.var) add.push_back({s.new_var, t.coef, t.req | bit});
+        for (auto& t : add) e.push_back(t);
+      }
+  }
+  // sort terms by name rank, check ranges, flatten
+  int nt = 0;
+  for (int a = 0; a < na; ++a) {
+    const ls_node& n = d.nodes[nl + a];
+    T.acc_tensor[a] = (uint8_t)n.tensor;
+    T.acc_store[a] = (uint8_t)n.is_store;
+    for (size_t k = 0; k < ex[a].size(); ++k) {
+      auto& e = ex[a][k];
+      std::stable_sort(e.begin(), e.end(),
+                       [&](const HTerm& x, const HTerm& y) { return d.var_rank[x.var] < d.var_rank[y.var]; });
+      // |value| <= |konst| + sum |coef| * step * (extent - 1); tiling keeps step*extent
+      // below 2x its previous value, so 2^(tiles+1) bounds every candidate
+      int64_t bound = std::llabs((int64_t)n.idx[k].konst);
+      for (auto& t : e) bound += std::llabs(t.coef) * span[t.var] * (2ll << ntile);
+      if (bound >= (1ll << 30)) return fail(LS_E_UNSUPPORTED, "index range exceeds the device int32 model");
+      if (nt + (int)e.size() > MAXTERM) return fail(LS_E_UNSUPPORTED, "too many index terms");
+      T.expr[a][k].konst = n.idx[k].konst;
+      T.expr[a][k].t0 = (int16_t)nt;
+      T.expr[a][k].nt = (int16_t)e.size();
+      for (auto& t : e) T.term[nt++] = {(int32_t)t.coef, t.req, t.var};
+    }
+  }
+  T.n_terms = nt;
+  T.n_acc = na;
+  // ---- tensors in first-appearance order, deduplicated consecutive accesses
+  std::vector<int> order;
+  for (int a = 0; a < na; ++a)
+    if (std::find(order.begin(), order.end(), (int)T.acc_tensor[a]) == order.end()) order.push_back(T.acc_tensor[a]);
+  T.n_tensors = (int)order.size();
+  int L = 0, S = 0;
+  for (int a = 0; a < na; ++a) {
+    if (T.acc_store[a]) {
+      ++S;
+      store_t.push_back(T.acc_tensor[a]);
+    } else {
+      ++L;
+      load_t.push_back(T.acc_tensor[a]);
+    }
+  }
+  T.L = L;
+  T.S = S;
+  // remap acc_tensor to merge order index, keeping declaration data
+  std::vector<int> decl_of(order.size());
+  for (size_t i = 0; i < order.size(); ++i) decl_of[i] = order[i];
+  for (int a = 0; a < na; ++a)
+    T.acc_tensor[a] = (uint8_t)(std::find(order.begin(), order.end(), (int)T.acc_tensor[a]) - order.begin());
+  for (int t = 0; t < T.n_tensors; ++t) {
+    const ls_tensor& td = d.tensors[decl_of[t]];
+    T.t_rank[t] = (uint8_t)td.rank;
+    T.t_eb[t] = (uint8_t)td.elem_bytes;
+    T.t_shared[t] = (uint8_t)(td.shared != 0);
+    int64_t stride = 1;
+    for (int k = td.rank - 1; k >= 0; --k) {
+      T.t_stride[t][k] = stride;
+      stride *= td.dims[k];
+    }
+    int nu = 0, last = -1;
+    for (int a = 0; a < na; ++a) {
+      if (T.acc_tensor[a] != t) continue;
+      T.t_nacc[t]++;
+      bool same = last >= 0;
+      for (int k = 0; same && k < td.rank; ++k) {
+        const ls_expr& x = d.nodes[nl + a].idx[k];
+        const ls_expr& y = d.nodes[nl + last].idx[k];
+        same = x.konst == y.konst && x.n_terms == y.n_terms &&
+               memcmp(x.terms, y.terms, sizeof(ls_term) * x.n_terms) == 0;
+      }
+      if (!same) T.t_uacc[t][nu++] = (uint8_t)a;
+      last = a;
+    }
+    T.t_nu[t] = (uint8_t)nu;
+    // nothing expanded: union of the accesses' constant points (ls/cache.py:80-96)
+    int64_t F = 1;
+    for (int k = 0; k < td.rank; ++k) {
+      int64_t lo = 0, hi = 0, str = 0, cnt = 1;
+      bool exact = true;
+      for (int q = 0; q < nu; ++q) {
+        int64_t v = T.expr[T.t_uacc[t][q]][k].konst;
+        if (q == 0) {
+          lo = hi = v;
+          str = 0;
+          cnt = 1;
+          exact = true;
+          continue;
+        }
+        // _si_union(acc, point(v))
+        if (lo == v && hi == v && str == 0 && cnt == 1 && exact) continue;
+        int64_t nlo = std::min(lo, v), nhi = std::max(hi, v);
+        int64_t g = std::abs(lo - v);
+        auto gcd = [](int64_t a, int64_t b) {
+          while (b) {
+            int64_t t2 = a % b;
+            a = b;
+            b = t2;
+          }
+          return a;
+        };
+        g = gcd(gcd(str, 0), g);
+        int64_t est = g ? (nhi - nlo) / g + 1 : 1;
+        cnt = std::min(est, cnt + 1);
+        lo = nlo;
+        hi = nhi;
+        str = g;
+        exact = false;
+      }
+      T.t_count0[t][k] = (int32_t)cnt;
+      F *= cnt;
+    }
+    T.t_F0[t] = F;
+  }
+  // ---- arch
+  T.family = d.family;
+  T.cap = d.cache_capacity;
+  for (int q = 0; q < LS_NFEAT_GPU; ++q) T.coef[q] = d.coef[q];
+  T.costs_integral = 1;
+  for (int q = 0; q < LS_I_COUNT; ++q) {
+    T.ptx_cost[q] = d.ptx_cost[q];
+    double c = d.ptx_cost[q];
+    if (c != std::floor(c) || std::fabs(c) > 1e12) T.costs_integral = 0;
+    T.ptx_icost[q] = (int64_t)c;
+  }
+  T.sm_underuse = d.sm_underuse;
+  T.warp_slack = d.warp_slack;
+  T.tid_var = d.tid_var;
+  T.banks = d.banks > 0 ? d.banks : 32;
+  T.warp_size = d.warp_size > 0 ? d.warp_size : 32;
+  if (T.banks > 64) return fail(LS_E_UNSUPPORTED, "more than 64 banks");
+  if (d.family == LS_FAMILY_CPU) {
+    if (d.issue_width < 1) return fail(LS_E_ARG, "issue_width < 1");
+    for (int q = 0; q < LS_I_COUNT; ++q)
+      if (d.klass[q] < 0 || d.klass[q] >= LS_I_COUNT) return fail(LS_E_ARG, "bad class id");
+    lsb::fixed_block_cycles(d, &T.c_init, &T.c_latch, &T.c_ret);
+  }
+  return LS_E_OK;
+}
+
+int upload(ls_task* t) {
+  DTask* dnew = nullptr;
+  DUnroll* dtab = nullptr;
+  CUDA_TRY(cudaMalloc(&dtab, sizeof(DUnroll) * std::max<size_t>(1, t->utab.size())));
+  CUDA_TRY(cudaMemcpy(dtab, t->utab.data(), sizeof(DUnroll) * t->utab.size(), cudaMemcpyHostToDevice));
+  t->host.u_tab = dtab;
+  t->host.n_u = (int32_t)t->utab.size();
+  CUDA_TRY(cudaMalloc(&dnew, sizeof(DTask)));
+  CUDA_TRY(cudaMemcpy(dnew, &t->host, sizeof(DTask), cudaMemcpyHostToDevice));
+  if (t->d_task) t->retired.push_back(t->d_task);
+  t->retired.push_back(dtab);
+  t->d_task = dnew;
+  return LS_E_OK;
+}
+
+int add_unroll(ls_task* t, const int64_t* us, int n) {
+  bool changed = false;
+  for (int i = 0; i < n; ++i) {
+    int64_t U = us[i];
+    if (U < 1 || U > 4096) continue;
+    bool have = false;
+    for (auto& e : t->utab) have |= e.u == U;
+    if (have) continue;
+    DUnroll e;
+    e.u = U;
+    if (t->desc.family == LS_FAMILY_CPU) {
+      e.c_inner = lsb::body_block_cycles(t->desc, t->load_t, t->store_t, U, true);
+      e.c_all = lsb::body_block_cycles(t->desc, t->load_t, t->store_t, U, false);
+    } else {
+      e.c_inner = e.c_all = 0;
+    }
+    t->utab.push_back(e);
+    changed = true;
+  }
+  if (!changed && t->d_task) return LS_E_OK;
+  std::sort(t->utab.begin(), t->utab.end(), [](const DUnroll& a, const DUnroll& b) { return a.u < b.u; });
+  return upload(t);
+}
+
+int grid_for(const ls_task* t, int64_t n, int threads, int per_sm) {
+  int64_t want = (n + threads - 1) / threads;
+  int64_t cap = (int64_t)t->num_sms * per_sm;
+  return (int)std::max<int64_t>(1, std::min(want, cap));
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C-ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+const char* ls_last_error(void) { return g_err.c_str(); }
+int ls_abi_version(void) { return LS_ABI_VERSION; }
+
+int ls_task_create(const ls_task_desc* desc, int device, ls_task** out) {
+  if (!desc || !out) return fail(LS_E_ARG, "null argument");
+  *out = nullptr;
+  CUDA_TRY(cudaSetDevice(device));
+  ls_task* t = new ls_task();
+  t->desc = *desc;
+  t->device = device;
+  t->d_task = nullptr;
+  int rc = build_task(*desc, t->host, t->load_t, t->store_t);
+  if (rc) {
+    delete t;
+    return rc;
+  }
+  cudaDeviceGetAttribute(&t->num_sms, cudaDevAttrMultiProcessorCount, device);
+  int64_t one = 1;
+  rc = add_unroll(t, &one, 1);
+  if (rc) {
+    delete t;
+    return rc;
+  }
+  *out = t;
+  return LS_E_OK;
+}
+
+int ls_task_destroy(ls_task* t) {
+  if (!t) return LS_E_OK;
+  cudaSetDevice(t->device);
+  cudaDeviceSynchronize();
+  for (void* p : t->retired) cudaFree(p);
+  if (t->d_task) cudaFree(t->d_task);
+  delete t;
+  return LS_E_OK;
+}
+
+int ls_task_num_features(const ls_task* t) {
+  return t ? (t->desc.family == LS_FAMILY_CPU ? LS_NFEAT_CPU : LS_NFEAT_GPU) : LS_E_ARG;
+}
+
+int ls_task_prepare_unroll(ls_task* t, const int64_t* u, int32_t n) {
+  if (!t || (n && !u)) return fail(LS_E_ARG, "null argument");
+  std::lock_guard<std::mutex> g(t->mu);
+  CUDA_TRY(cudaSetDevice(t->device));
+  return add_unroll(t, u, n);
+}
+
+int ls_collect_unroll(ls_task* t, const ls_record* d_records, int64_t n, int64_t* h_values, int32_t cap,
+                      int32_t* h_count, void* stream) {
+  if (!t || !h_values || !h_count || cap < 1) return fail(LS_E_ARG, "bad argument");
+  CUDA_TRY(cudaSetDevice(t->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const int slots = 4096;
+  unsigned long long* set = nullptr;
+  CUDA_TRY(cudaMallocAsync(&set, sizeof(unsigned long long) * slots, s));
+  CUDA_TRY(cudaMemsetAsync(set, 0, sizeof(unsigned long long) * slots, s));
+  if (n > 0) {
+    collect_unroll_kernel<<<grid_for(t, n, 256, 4), 256, 0, s>>>(t->d_task, d_records, n, set, slots);
+    CUDA_TRY(cudaGetLastError());
+  }
+  std::vector<unsigned long long> h(slots);
+  CUDA_TRY(cudaMemcpyAsync(h.data(), set, sizeof(unsigned long long) * slots, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaFreeAsync(set, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  int c = 0;
+  for (auto v : h)
+    if (v && c < cap) h_values[c++] = (int64_t)v;
+  std::sort(h_values, h_values + c);
+  *h_count = c;
+  return LS_E_OK;
+}
+
+int ls_score(ls_task* t, const ls_record* d_records, int64_t n, double* d_scores, double* d_features,
+             int32_t* d_status, void* stream) {
+  if (!t || n < 0 || (n && !d_records)) return fail(LS_E_ARG, "bad argument");
+  if (n == 0) return LS_E_OK;
+  CUDA_TRY(cudaSetDevice(t->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  score_kernel<<<grid_for(t, n, 256, 8), 256, 0, s>>>(t->d_task, d_records, n, d_scores, d_features, d_status);
+  CUDA_TRY(cudaGetLastError());
+  return LS_E_OK;
+}
+
+static int topk_device(ls_task* t, const ls_record* d_records, int64_t n, int64_t base_index, int32_t k,
+                       double* d_top_scores, int64_t* d_top_index, unsigned long long* d_valid, cudaStream_t s) {
+  const int grid = grid_for(t, n, 256, 2);
+  Key* ws = nullptr;
+  CUDA_TRY(cudaMallocAsync(&ws, sizeof(Key) * (size_t)grid * k, s));
+  if (n > 0) {
+    score_topk_kernel<<<grid, 256, 0, s>>>(t->d_task, d_records, n, base_index, k, ws, d_valid);
+    CUDA_TRY(cudaGetLastError());
+    merge_keys_kernel<<<1, 1024, 0, s>>>(ws, (int64_t)grid * k, k, d_top_scores, d_top_index);
+  } else {
+    merge_keys_kernel<<<1, 1024, 0, s>>>(ws, 0, k, d_top_scores, d_top_index);
+  }
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaFreeAsync(ws, s));
+  return LS_E_OK;
+}
+
+int ls_score_topk(ls_task* t, const ls_record* d_records, int64_t n, int64_t base_index, int32_t k,
+                  double* d_top_scores, int64_t* d_top_index, int64_t* d_n_valid, void* stream) {
+  if (!t || n < 0 || (n && !d_records) || !d_top_scores || !d_top_index) return fail(LS_E_ARG, "bad argument");
+  if (k < 1 || k > TK_MAXK) return fail(LS_E_ARG, "k must be in 1..1024");
+  CUDA_TRY(cudaSetDevice(t->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned long long* valid = reinterpret_cast<unsigned long long*>(d_n_valid);
+  unsigned long long* tmp = nullptr;
+  if (!valid) {
+    CUDA_TRY(cudaMallocAsync(&tmp, sizeof(unsigned long long), s));
+    valid = tmp;
+  }
+  CUDA_TRY(cudaMemsetAsync(valid, 0, sizeof(unsigned long long), s));
+  int rc = topk_device(t, d_records, n, base_index, k, d_top_scores, d_top_index, valid, s);
+  if (tmp) cudaFreeAsync(tmp, s);
+  return rc;
+}
+
+int ls_topk_merge(const double* d_scores, const int64_t* d_index, int32_t n_lists, int32_t k_in, int32_t k_out,
+                  double* d_out_scores, int64_t* d_out_index, void* stream) {
+  if (!d_scores || !d_index || n_lists < 0 || k_in < 0 || k_out < 1 || k_out > TK_MAXK || !d_out_scores ||
+      !d_out_index)
+    return fail(LS_E_ARG, "bad argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t m = (int64_t)n_lists * k_in;
+  Key* keys = nullptr;
+  CUDA_TRY(cudaMallocAsync(&keys, sizeof(Key) * std::max<int64_t>(1, m), s));
+  if (m > 0) {
+    lists_to_keys_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(d_scores, d_index, m, keys);
+    CUDA_TRY(cudaGetLastError());
+  }
+  merge_keys_kernel<<<1, 1024, 0, s>>>(keys, m, k_out, d_out_scores, d_out_index);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaFreeAsync(keys, s));
+  return LS_E_OK;
+}
+
+int ls_score_topk_host(ls_task* t, const ls_record* h_records, int64_t n, int64_t base_index, int32_t k,
+                       double* h_top_scores, int64_t* h_top_index, int64_t* h_n_valid, void* stream) {
+  if (!t || n < 0 || (n && !h_records) || !h_top_scores || !h_top_index) return fail(LS_E_ARG, "bad argument");
+  if (k < 1 || k > TK_MAXK) return fail(LS_E_ARG, "k must be in 1..1024");
+  CUDA_TRY(cudaSetDevice(t->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t CH = 1 << 20;  // records per chunk (32 MiB)
+  const int64_t nch = std::max<int64_t>(1, (n + CH - 1) / CH);
+  cudaStream_t cp;
+  CUDA_TRY(cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking));
+  cudaEvent_t ev_start, ready[2], freed[2];
+  CUDA_TRY(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
+  for (int b = 0; b < 2; ++b) {
+    CUDA_TRY(cudaEventCreateWithFlags(&ready[b], cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&freed[b], cudaEventDisableTiming));
+  }
+  ls_record* buf[2] = {nullptr, nullptr};
+  double* ls = nullptr;
+  int64_t* li = nullptr;
+  unsigned long long* valid = nullptr;
+  double* out_s = nullptr;
+  int64_t* out_i = nullptr;
+  int rc = LS_E_OK;
+  CUDA_TRY(cudaEventRecord(ev_start, s));
+  CUDA_TRY(cudaStreamWaitEvent(cp, ev_start, 0));
+  for (int b = 0; b < 2; ++b) CUDA_TRY(cudaMallocAsync(&buf[b], sizeof(ls_record) * std::min(CH, std::max<int64_t>(n, 1)), s));
+  CUDA_TRY(cudaMallocAsync(&ls, sizeof(double) * nch * k, s));
+  CUDA_TRY(cudaMallocAsync(&li, sizeof(int64_t) * nch * k, s));
+  CUDA_TRY(cudaMallocAsync(&valid, sizeof(unsigned long long), s));
+  CUDA_TRY(cudaMallocAsync(&out_s, sizeof(double) * k, s));
+  CUDA_TRY(cudaMallocAsync(&out_i, sizeof(int64_t) * k, s));
+  CUDA_TRY(cudaMemsetAsync(valid, 0, sizeof(unsigned long long), s));
+  CUDA_TRY(cudaEventRecord(ev_start, s));
+  CUDA_TRY(cudaStreamWaitEvent(cp, ev_start, 0));
+  for (int64_t c = 0; c < nch && rc == LS_E_OK; ++c) {
+    const int b = (int)(c & 1);
+    const int64_t off = c * CH, m = std::min(CH, n - off);
+    if (c >= 2) CUDA_TRY(cudaStreamWaitEvent(cp, freed[b], 0));
+    if (m > 0) CUDA_TRY(cudaMemcpyAsync(buf[b], h_records + off, sizeof(ls_record) * m, cudaMemcpyHostToDevice, cp));
+    CUDA_TRY(cudaEventRecord(ready[b], cp));
+    CUDA_TRY(cudaStreamWaitEvent(s, ready[b], 0));
+    rc = topk_device(t, buf[b], std::max<int64_t>(m, 0), base_index + off, k, ls + c * k, li + c * k, valid, s);
+    CUDA_TRY(cudaEventRecord(freed[b], s));
+  }
+  if (rc == LS_E_OK) {
+    rc = ls_topk_merge(ls, li, (int32_t)nch, k, k, out_s, out_i, s);
+  }
+  CUDA_TRY(cudaMemcpyAsync(h_top_scores, out_s, sizeof(double) * k, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(h_top_index, out_i, sizeof(int64_t) * k, cudaMemcpyDeviceToHost, s));
+  unsigned long long hv = 0;
+  CUDA_TRY(cudaMemcpyAsync(&hv, valid, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  for (int b = 0; b < 2; ++b) cudaFreeAsync(buf[b], s);
+  cudaFreeAsync(ls, s);
+  cudaFreeAsync(li, s);
+  cudaFreeAsync(valid, s);
+  cudaFreeAsync(out_s, s);
+  cudaFreeAsync(out_i, s);
+  CUDA_TRY(cudaStreamSynchronize(s));
+  CUDA_TRY(cudaStreamSynchronize(cp));
+  cudaStreamDestroy(cp);
+  cudaEventDestroy(ev_start);
+  for (int b = 0; b < 2; ++b) {
+    cudaEventDestroy(ready[b]);
+    cudaEventDestroy(freed[b]);
+  }
+  if (h_n_valid) *h_n_valid = (int64_t)hv;
+  return rc;
+}
+
+}  // extern "C"

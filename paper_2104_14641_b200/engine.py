@@ -1,0 +1,171 @@
+"""ctypes binding of libloopscout_b200.so (the C-ABI in include/loopscout_b200.h).
+
+Device buffers are torch CUDA tensors (PyTorch is plumbing here: allocation,
+streams, copies); all compute is in the library's sm_100a kernels.  There is
+no CPU fallback: if the library or a GPU is missing, every entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+import numpy as np
+
+from . import abi
+
+PKG = Path(__file__).resolve().parent
+LIB_PATH = PKG / "libloopscout_b200.so"
+
+
+class EngineError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise EngineError(f"{LIB_PATH.name} is not built; run __graft_entry__.build() "
+                          "(there is no CPU fallback)")
+    L = C.CDLL(str(LIB_PATH))
+    vp, i64, i32 = C.c_void_p, C.c_int64, C.c_int32
+    L.ls_last_error.restype = C.c_char_p
+    L.ls_task_create.argtypes = [vp, C.c_int, C.POINTER(vp)]
+    L.ls_task_destroy.argtypes = [vp]
+    L.ls_task_num_features.argtypes = [vp]
+    L.ls_task_prepare_unroll.argtypes = [vp, vp, i32]
+    L.ls_collect_unroll.argtypes = [vp, vp, i64, vp, i32, vp, vp]
+    L.ls_score.argtypes = [vp, vp, i64, vp, vp, vp, vp]
+    L.ls_score_topk.argtypes = [vp, vp, i64, i64, i32, vp, vp, vp, vp]
+    L.ls_topk_merge.argtypes = [vp, vp, i32, i32, i32, vp, vp, vp]
+    L.ls_score_topk_host.argtypes = [vp, vp, i64, i64, i32, vp, vp, vp, vp]
+    if L.ls_abi_version() != abi.ABI_VERSION:
+        raise EngineError("libloopscout_b200 ABI version mismatch")
+    _lib = L
+    return L
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        raise EngineError(f"{what} failed ({rc}): {lib().ls_last_error().decode()}")
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise EngineError("no CUDA device visible (there is no CPU fallback)")
+    return torch
+
+
+def _stream(torch, stream):
+    return (stream or torch.cuda.current_stream()).cuda_stream
+
+
+def _dptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def to_device_records(records: np.ndarray, device=0):
+    """Upload packed records as a CUDA uint8 tensor of shape (n, 32)."""
+    torch = _torch()
+    raw = np.ascontiguousarray(records).view(np.uint8).reshape(-1, abi.RECORD_DTYPE.itemsize)
+    return torch.from_numpy(raw).to(f"cuda:{device}", non_blocking=False)
+
+
+class Task:
+    """A device task: one program + schedule template + arch (+ launch)."""
+
+    def __init__(self, desc: abi.TaskDesc, device: int = 0):
+        _torch()
+        self.device = device
+        self.desc = desc
+        self.family = desc.family
+        self.nfeat = abi.NFEAT_CPU if desc.family == 0 else abi.NFEAT_GPU
+        h = C.c_void_p()
+        _check(lib().ls_task_create(C.addressof(desc), device, C.byref(h)), "ls_task_create")
+        self._h = h
+        self.has_unroll = any(desc.xforms[i].kind == abi.XF_UNROLL for i in range(desc.n_xforms)) or \
+            any(desc.nodes[i].kind == abi.NODE_LOOP and desc.nodes[i].unrolled for i in range(desc.n_nodes))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().ls_task_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+    # -- unroll table ---------------------------------------------------------------
+    def prepare_unroll_for(self, d_records, stream=None):
+        """Collect the innermost-unroll products these records need and precompute them."""
+        if not self.has_unroll:
+            return
+        torch = _torch()
+        n = d_records.shape[0]
+        vals = np.zeros(4096, np.int64)
+        cnt = np.zeros(1, np.int32)
+        _check(lib().ls_collect_unroll(self._h, _dptr(d_records), n, vals.ctypes.data, len(vals),
+                                       cnt.ctypes.data, _stream(torch, stream)), "ls_collect_unroll")
+        u = vals[:cnt[0]].copy()
+        if len(u):
+            _check(lib().ls_task_prepare_unroll(self._h, u.ctypes.data, len(u)), "ls_task_prepare_unroll")
+
+    # -- scoring --------------------------------------------------------------------
+    def score(self, d_records, features: bool = True, stream=None):
+        """(scores f64[n], features f64[n,F] | None, status i32[n]) as CUDA tensors."""
+        torch = _torch()
+        n = d_records.shape[0]
+        dev = d_records.device
+        scores = torch.empty(n, dtype=torch.float64, device=dev)
+        feats = torch.empty((n, self.nfeat), dtype=torch.float64, device=dev) if features else None
+        status = torch.empty(n, dtype=torch.int32, device=dev)
+        _check(lib().ls_score(self._h, _dptr(d_records), n, _dptr(scores), _dptr(feats), _dptr(status),
+                              _stream(torch, stream)), "ls_score")
+        return scores, feats, status
+
+    def score_topk(self, d_records, k: int, base_index: int = 0, stream=None, out=None):
+        """k best (score, global index) ascending + number of valid candidates (CUDA tensors)."""
+        torch = _torch()
+        dev = d_records.device
+        if out is None:
+            out = (torch.empty(k, dtype=torch.float64, device=dev),
+                   torch.empty(k, dtype=torch.int64, device=dev),
+                   torch.zeros(1, dtype=torch.int64, device=dev))
+        s, i, nv = out
+        _check(lib().ls_score_topk(self._h, _dptr(d_records), d_records.shape[0], int(base_index), int(k),
+                                   _dptr(s), _dptr(i), _dptr(nv), _stream(torch, stream)), "ls_score_topk")
+        return s, i, nv
+
+    def score_topk_host(self, h_records, k: int, base_index: int = 0, stream=None):
+        """Host records in, host top-k out (H2D staged and overlapped inside the library)."""
+        torch = _torch()
+        if isinstance(h_records, np.ndarray):
+            ptr, n = h_records.ctypes.data, len(h_records)
+        else:  # pinned torch uint8 tensor (n, 32)
+            ptr, n = h_records.data_ptr(), h_records.shape[0]
+        s = np.empty(k, np.float64)
+        i = np.empty(k, np.int64)
+        nv = np.zeros(1, np.int64)
+        with torch.cuda.device(self.device):
+            _check(lib().ls_score_topk_host(self._h, ptr, n, int(base_index), int(k), s.ctypes.data,
+                                            i.ctypes.data, nv.ctypes.data, _stream(torch, stream)),
+                   "ls_score_topk_host")
+        return s, i, int(nv[0])
+
+
+def topk_merge(scores, index, n_lists: int, k_in: int, k_out: int, stream=None):
+    """Merge n_lists sorted (score, index) lists of k_in each into the k_out best (CUDA tensors)."""
+    torch = _torch()
+    out_s = torch.empty(k_out, dtype=torch.float64, device=scores.device)
+    out_i = torch.empty(k_out, dtype=torch.int64, device=scores.device)
+    _check(lib().ls_topk_merge(_dptr(scores), _dptr(index), int(n_lists), int(k_in), int(k_out),
+                               _dptr(out_s), _dptr(out_i), _stream(torch, stream)), "ls_topk_merge")
+    return out_s, out_i

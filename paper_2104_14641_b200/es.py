@@ -1,0 +1,218 @@
+"""Evolution-strategies search with device-scored populations.
+
+API and trajectory of the reference's ``optimize`` (ls/es.py:119-204): same
+EsParams, same centroid start, same SeedSequence/PCG64 noise per generation,
+same round-half-even decode, same rank-shaped update, same memo of distinct
+schedules keyed by their JSON, same incumbent tie-break (score, JSON key).
+What changes is the evaluation: each generation's *new distinct* schedules
+are packed into records and scored in one device launch instead of one
+Python call chain per candidate.  Scores are bit-identical to the reference,
+so the theta trajectory, trace and evaluated table are too.
+"""
+
+from __future__ import annotations
+
+import json
+from concurrent.futures import ThreadPoolExecutor
+from dataclasses import dataclass
+
+import numpy as np
+
+from .engine import Task, to_device_records
+from .ir import Schedule, space_axes
+from .pack import SpaceTemplate
+from .arch import CPU_FEATURES, GPU_FEATURES, FeatureVector
+
+
+class SearchError(RuntimeError):
+    pass
+
+
+@dataclass(frozen=True)
+class EsParams:
+    alpha: float = 0.05
+    sigma: float = 0.3
+    population: int = 32
+    iterations: int = 100
+    seed: int = 0
+    rank_normalize: bool = True
+
+    def __post_init__(self):
+        if self.alpha <= 0 or self.sigma <= 0:
+            raise ValueError("alpha and sigma must be positive")
+        if self.population < 2:
+            raise ValueError("population must be >= 2")
+        if self.iterations < 1:
+            raise ValueError("iterations must be >= 1")
+
+
+@dataclass(frozen=True)
+class ThetaEncoding:
+    axes: tuple
+
+    @property
+    def dim(self) -> int:
+        return len(self.axes)
+
+    def initial(self) -> np.ndarray:
+        return np.array([(len(ax.choices) - 1) / 2.0 for ax in self.axes])
+
+    def indices(self, thetas: np.ndarray) -> np.ndarray:
+        sizes = np.array([len(ax.choices) for ax in self.axes], np.int64)
+        return np.clip(np.rint(np.asarray(thetas, np.float64)), 0, sizes - 1).astype(np.int64)
+
+    def decode(self, theta) -> Schedule:
+        out = []
+        for i, ax in zip(self.indices(np.asarray(theta).reshape(1, -1))[0], self.axes):
+            out.extend(ax.choices[int(i)])
+        return Schedule(tuple(out))
+
+
+def shape_fitness(values: np.ndarray) -> np.ndarray:
+    """Centered ranks on [-0.5, 0.5] (ls/es.py:65-71)."""
+    n = len(values)
+    if n == 1 or np.ptp(values) == 0:
+        return np.zeros(n)
+    order = np.argsort(np.argsort(values, kind="stable"), kind="stable")
+    return order / (n - 1) - 0.5
+
+
+def es_update(theta: np.ndarray, params: EsParams, values: np.ndarray, noise: np.ndarray,
+              diagnostics: "list | None" = None) -> np.ndarray:
+    """theta + alpha/(n*sigma) * sum(F_i * eps_i) with the reference's NaN handling (ls/es.py:74-93)."""
+    values = np.asarray(values, dtype=float)
+    bad = ~np.isfinite(values)
+    if bad.any():
+        if diagnostics is not None:
+            diagnostics.append(f"{int(bad.sum())} non-finite objective values replaced by population minimum")
+        fill = values[~bad].min() if (~bad).any() else 0.0
+        values = np.where(bad, fill, values)
+    weights = shape_fitness(values) if params.rank_normalize else values
+    return theta + (params.alpha / (params.population * params.sigma)) * (weights @ noise)
+
+
+def es_step(theta, params: EsParams, objective, rng=None, noise=None, diagnostics=None):
+    """Generic host ES step over a Python objective (ls/es.py:74-93)."""
+    theta = np.asarray(theta, dtype=float)
+    if rng is None:
+        rng = np.random.default_rng(params.seed)
+    if noise is None:
+        noise = rng.standard_normal((params.population, theta.shape[0]))
+    values = np.array([objective(theta + params.sigma * eps) for eps in noise], dtype=float)
+    return es_update(theta, params, values, noise, diagnostics)
+
+
+def evaluate_population(thetas, objective, jobs=None, errors=None) -> list:
+    """Order-preserving evaluation of a Python objective (ls/es.py:96-116).
+
+    Generic callables cannot run on the device; the batched device path is
+    cost.score_batch / optimize below.
+    """
+    def safe(item):
+        i, th = item
+        try:
+            return objective(th)
+        except Exception as e:  # noqa: BLE001 - recorded like the reference
+            if errors is not None:
+                errors.append((i, e))
+            return None
+
+    items = list(enumerate(thetas))
+    if jobs is not None and jobs <= 1:
+        return [safe(it) for it in items]
+    with ThreadPoolExecutor(max_workers=jobs) as pool:
+        return list(pool.map(safe, items))
+
+
+@dataclass
+class OptimizeResult:
+    best_schedule: Schedule
+    best_score: float
+    best_features: FeatureVector
+    trace: list
+    evaluated: dict
+    evaluations: int
+    diagnostics: list
+
+
+class _DeviceObjective:
+    """Memoised device scoring of space points (the evaluate_schedule cache, ls/es.py:139-160)."""
+
+    def __init__(self, program, space, arch, launch, device):
+        import torch
+        self.torch = torch
+        self.st = SpaceTemplate(program, space)
+        self.task = Task(self.st.template.desc(arch, launch), device)
+        self.device = device
+        self.names = CPU_FEATURES if arch.family == "cpu" else GPU_FEATURES
+        self.sizes = self.st.sizes
+        self.cache: dict = {}   # flat point index -> (key, score, features)
+        self.by_key: dict = {}  # json key -> (score, features)
+
+    def flat(self, idx: np.ndarray) -> np.ndarray:
+        f = np.zeros(len(idx), np.int64)
+        for a, n in enumerate(self.sizes):
+            f = f * int(n) + idx[:, a]
+        return f
+
+    def evaluate(self, idx: np.ndarray, where: str) -> np.ndarray:
+        """Scores of rows of choice indices; new distinct points go to the device in one batch."""
+        flat = self.flat(idx)
+        uniq, first = np.unique(flat, return_index=True)
+        order = np.argsort(first, kind="stable")  # first-appearance order, like a serial loop
+        uniq, first = uniq[order], first[order]
+        is_new = np.array([int(u) not in self.cache for u in uniq], bool)
+        new = [int(u) for u in uniq[is_new]]
+        if new:
+            rows = idx[first[is_new]]
+            recs = self.st.records_from_indices(rows)
+            d_rec = to_device_records(recs, self.device)
+            self.task.prepare_unroll_for(d_rec)
+            s, f, st = self.task.score(d_rec, features=True)
+            s, f, st = s.cpu().numpy(), f.cpu().numpy(), st.cpu().numpy()
+            for j, u in enumerate(new):
+                key = json.dumps(self.st.schedule_of(rows[j]).to_json())
+                if st[j]:
+                    raise SearchError(f"{where}: candidate {key} failed: status {int(st[j])}")
+                self.cache[u] = (key, float(s[j]), f[j])
+                self.by_key[key] = (float(s[j]), f[j])
+        return np.array([self.cache[int(u)][1] for u in flat])
+
+
+def optimize(program, space: dict, arch, params: EsParams, jobs=None, launch=None,
+             device: int = 0) -> OptimizeResult:
+    """ES search for the lowest-scoring schedule (ls/es.py:130-204), device-scored."""
+    axes = tuple(space_axes(program, space))
+    if not axes:
+        raise SearchError("empty schedule space")
+    enc = ThetaEncoding(axes)
+    obj = _DeviceObjective(program, space, arch, launch, device)
+    diagnostics: list = []
+    theta = enc.initial()
+    trace: list = []
+    children = np.random.SeedSequence(params.seed).spawn(params.iterations)
+    obj.evaluate(enc.indices(theta.reshape(1, -1)), "start")
+    single = all(len(ax.choices) == 1 for ax in axes)
+    best = lambda: min(obj.by_key, key=lambda k: (obj.by_key[k][0], k))  # noqa: E731
+    for t in range(params.iterations):
+        if single:
+            break
+        rng = np.random.default_rng(children[t])
+        noise = rng.standard_normal((params.population, enc.dim))
+        pts = theta + params.sigma * noise
+        scores = obj.evaluate(enc.indices(pts), f"iteration {t}")
+        theta = es_update(theta, params, -scores, noise, diagnostics)
+        trace.append(obj.by_key[best()][0])
+    bk = best()
+    if not trace:
+        trace = [obj.by_key[bk][0]]
+    bs, bf = obj.by_key[bk]
+    return OptimizeResult(
+        best_schedule=Schedule.from_json(json.loads(bk)),
+        best_score=bs,
+        best_features=FeatureVector(tuple(zip(obj.names, map(float, bf)))),
+        trace=trace,
+        evaluated={k: v[0] for k, v in obj.by_key.items()},
+        evaluations=len(obj.by_key),
+        diagnostics=diagnostics,
+    )

@@ -105,15 +105,15 @@ def conv_space(reorders: int = 512, seed: int = 1, shape: dict | None = None) ->
             "reorder": random_perms(chain, reorders, seed)}
 
 
-def distinct_indices(sizes, n: int, seed: int) -> np.ndarray:
-    """n distinct points of a mixed-radix space (rows of per-axis choice indices)."""
+def distinct_indices(sizes, n: int, seed: int, start: int = 0) -> np.ndarray:
+    """Rows start..start+n-1 of a seeded enumeration of distinct points of a
+    mixed-radix space (per-axis choice indices).  Disjoint `start` ranges give
+    disjoint points, so shards can be generated independently."""
     sizes = np.asarray(sizes, np.int64)
     total = int(np.prod(sizes))
-    if n > total:
-        raise ValueError(f"space has {total} points, asked for {n}")
-    rng = np.random.default_rng(seed)
-    flat = rng.choice(total, size=n, replace=False) if total <= (1 << 27) else \
-        _feistel_sample(total, n, seed)
+    if start + n > total:
+        raise ValueError(f"space has {total} points, asked for rows up to {start + n}")
+    flat = _feistel(total, np.arange(start, start + n, dtype=np.int64), seed)
     out = np.empty((n, len(sizes)), np.int64)
     for a in range(len(sizes) - 1, -1, -1):
         out[:, a] = flat % sizes[a]
@@ -121,36 +121,27 @@ def distinct_indices(sizes, n: int, seed: int) -> np.ndarray:
     return out
 
 
-def _feistel_sample(total: int, n: int, seed: int) -> np.ndarray:
-    """Distinct values in [0,total) from a keyed bijection of [0, 2^b) by cycle walking."""
+def _feistel(total: int, x: np.ndarray, seed: int) -> np.ndarray:
+    """A keyed bijection of [0, total) (balanced Feistel on 2^b, cycle-walked)."""
     bits = max(2, int(total - 1).bit_length())
     bits += bits & 1
     half = bits // 2
-    mask = (1 << half) - 1
+    mask = np.int64((1 << half) - 1)
     keys = np.random.default_rng(seed).integers(1, 1 << 31, size=4, dtype=np.int64)
 
-    def perm(x):
-        l, r = x >> half, x & mask
+    def perm(v):
+        l, r = v >> half, v & mask
         for k in keys:
-            f = ((r * 0x9E3779B1 + k) ^ (r >> 3)) & mask
+            f = ((r * np.int64(0x9E3779B1) + k) ^ (r >> 3)) & mask
             l, r = r, l ^ f
         return (l << half) | r
 
-    out = np.empty(0, np.int64)
-    x = np.arange(0, n, dtype=np.int64)
-    cursor = n
-    while len(out) < n:
-        y = perm(x)
-        while True:
-            bad = y >= total
-            if not bad.any():
-                break
-            y[bad] = perm(y[bad])
-        out = np.concatenate([out, y])
-        if len(out) < n:
-            x = np.arange(cursor, cursor + (n - len(out)), dtype=np.int64)
-            cursor += len(x)
-    return out[:n]
+    y = perm(x)
+    while True:
+        bad = y >= total
+        if not bad.any():
+            return y
+        y[bad] = perm(y[bad])
 
 
 KERNEL_LAUNCH = {"grid_blocks": 160, "threads_per_block": 256, "registers_per_thread": 32,
