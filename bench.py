@@ -220,6 +220,10 @@ def b200_arm(args):
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     kern = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(dev) as clk:
+        t_soak = time.perf_counter()  # keep the GPU loaded while nvidia-smi starts sampling
+        while time.perf_counter() - t_soak < 1.5:
+            step()
+            torch.cuda.synchronize()
         for j in range(args.steps):
             flush.zero_()
             torch.cuda.synchronize()

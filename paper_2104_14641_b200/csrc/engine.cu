@@ -50,46 +50,52 @@ static int fail(int code, const std::string& msg) {
 // ---------------------------------------------------------------------------
 // device task table (staged into shared memory by every block)
 // ---------------------------------------------------------------------------
+constexpr int TPB = 256;          // threads per block of the scoring kernels
+constexpr int NSLOT = 16;         // loop-variable slots that can exist (a chain has <= 16 loops)
 constexpr int MAXACC = 16;
 constexpr int MAXRANK = LS_MAX_RANK;
 constexpr int MAXT = LS_MAX_TENSORS;
+constexpr int MAXD = MAXT * MAXRANK;  // dimension slots of the generic layout
+constexpr int MAXDV = 8;              // distinct loop variables per tensor dimension
 constexpr int MAXTERM = 384;
 constexpr int MAXCH = LS_MAX_CHAIN;
+constexpr int MAXSTAGE = 64;
+constexpr uint8_t NOSLOT = 0xFF;
 
 struct DTerm {
   int32_t coef;
   uint32_t req;  // enable bits that must be set for the term to exist
-  int32_t var;
+  int32_t slot;
 };
 
 struct DExpr {
   int32_t konst;
-  int16_t t0;  // first term in DTask::term
+  int16_t t0;  // first term in DTask::term (terms sorted by variable name)
   int16_t nt;
 };
 
 struct DXform {
-  int8_t kind, var, new_var, param;
+  int8_t kind;
+  uint8_t slot, new_slot;  // NOSLOT: the name never exists
+  int8_t param;
   int8_t enable_bit, n_order, perm_shift, pad;
   int32_t value;
-  int8_t order[LS_MAX_ORDER];
+  uint8_t order[LS_MAX_ORDER];
 };
 
 struct DUnroll {
   int64_t u, c_inner, c_all;
 };
 
+// loop flags in the per-candidate state
+constexpr uint8_t F_PAR = 1, F_UNR = 2, F_VEC = 4;
+
 struct __align__(16) DTask {
-  // base chain
-  int32_t n_base;
-  int32_t n_xf;
-  int32_t n_acc, n_tensors;
+  int32_t n_base, n_xf, n_acc, n_tensors;
   int32_t L, S;  // loads / stores of the innermost body
-  int32_t family;
-  int32_t costs_integral;
-  int32_t tid_var;
-  int32_t n_u;
-  int32_t banks, warp_size;
+  int32_t family, costs_integral, tid_slot, n_u;
+  int32_t banks, warp_size, layout_rm, n_stage;
+  int32_t has_shared, pad0;
   int64_t cap;
   int64_t c_init, c_latch, c_ret;
   double coef[LS_NFEAT_GPU];
@@ -97,9 +103,8 @@ struct __align__(16) DTask {
   int64_t ptx_icost[LS_I_COUNT];
   double sm_underuse, warp_slack;
   const DUnroll* u_tab;
-  int32_t base_ext[MAXCH], base_step[MAXCH], base_vw[MAXCH];
-  int8_t base_var[MAXCH];
-  uint8_t base_flags[MAXCH];  // bit0 parallel, bit1 unrolled
+  int32_t base_ext[MAXCH], base_step[MAXCH];
+  uint8_t base_slot[MAXCH], base_flags[MAXCH];
   DXform xf[LS_MAX_XFORMS];
   // accesses of the innermost body, program order
   uint8_t acc_tensor[MAXACC], acc_store[MAXACC];
@@ -107,9 +112,12 @@ struct __align__(16) DTask {
   // tensors in first-appearance order among the accesses (CacheModel merge order)
   uint8_t t_rank[MAXT], t_nu[MAXT], t_uacc[MAXT][MAXACC], t_eb[MAXT], t_shared[MAXT];
   int32_t t_nacc[MAXT];
-  int32_t t_count0[MAXT][MAXRANK];
-  int64_t t_F0[MAXT];
   int64_t t_stride[MAXT][MAXRANK];
+  // dimension slots D = t * layout_rm + r
+  uint8_t dim_nv[MAXD], dim_base[MAXD];
+  uint8_t dim_var[MAXD][MAXDV];
+  int32_t dim_count0[MAXD];
+  uint64_t slot_dnib[NSLOT][3];  // nibble D of slot s: 1 + index of s in dim D's variable list
   int32_t n_terms;
   DTerm term[MAXTERM];
 };
@@ -117,17 +125,61 @@ struct __align__(16) DTask {
 struct ls_task {
   ls_task_desc desc;
   int device;
-  DTask host;           // host copy (u_tab points to the current device table)
-  DTask* d_task;        // current device copy
+  DTask host;     // host copy (u_tab points to the current device table)
+  DTask* d_task;  // current device copy
   std::vector<DUnroll> utab;
   std::vector<void*> retired;  // previous device copies / tables, freed on destroy
   std::vector<int> load_t, store_t;
   std::mutex mu;
   int num_sms;
+  size_t smem_score, smem_topk;
 };
 
 // ---------------------------------------------------------------------------
-// device helpers
+// per-thread candidate state, kept in shared memory ([slot][thread] layout:
+// bank-conflict free, no local-memory round trips)
+// ---------------------------------------------------------------------------
+struct Cand {
+  int32_t* ext;    // [NSLOT][TPB]
+  int32_t* step;   // [NSLOT][TPB]
+  int32_t* stage;  // [n_stage][TPB]
+  uint8_t* pos;    // [NSLOT][TPB], NOSLOT when the variable does not exist
+  uint8_t* flg;    // [NSLOT][TPB]
+  uint8_t* chain;  // [MAXCH][TPB]
+  int n;
+  uint32_t flags;
+  __device__ __forceinline__ int32_t& E(int v) { return ext[v * TPB + threadIdx.x]; }
+  __device__ __forceinline__ int32_t& St(int v) { return step[v * TPB + threadIdx.x]; }
+  __device__ __forceinline__ int32_t& G(int i) { return stage[i * TPB + threadIdx.x]; }
+  __device__ __forceinline__ uint8_t& P(int v) { return pos[v * TPB + threadIdx.x]; }
+  __device__ __forceinline__ uint8_t& Fl(int v) { return flg[v * TPB + threadIdx.x]; }
+  __device__ __forceinline__ uint8_t& C(int p) { return chain[p * TPB + threadIdx.x]; }
+};
+
+__host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+__host__ __device__ constexpr size_t cand_bytes(int n_stage) {
+  return align16(sizeof(int32_t) * NSLOT * TPB) * 2 + align16(sizeof(int32_t) * (size_t)n_stage * TPB) +
+         align16((size_t)NSLOT * TPB) * 2 + align16((size_t)MAXCH * TPB);
+}
+
+__device__ __forceinline__ Cand carve(unsigned char* p, int n_stage) {
+  Cand c;
+  c.ext = reinterpret_cast<int32_t*>(p);
+  p += align16(sizeof(int32_t) * NSLOT * TPB);
+  c.step = reinterpret_cast<int32_t*>(p);
+  p += align16(sizeof(int32_t) * NSLOT * TPB);
+  c.stage = reinterpret_cast<int32_t*>(p);
+  p += align16(sizeof(int32_t) * (size_t)n_stage * TPB);
+  c.pos = p;
+  p += align16((size_t)NSLOT * TPB);
+  c.flg = p;
+  p += align16((size_t)NSLOT * TPB);
+  c.chain = p;
+  return c;
+}
+
+// ---------------------------------------------------------------------------
+// strided-interval algebra (ls/cache.py:28-77)
 // ---------------------------------------------------------------------------
 struct SI {
   int32_t lo, hi, stride, count;
@@ -141,12 +193,9 @@ __device__ __forceinline__ uint32_t gcd_u32(uint32_t a, uint32_t b) {
   a >>= __ffs(a) - 1;
   do {
     b >>= __ffs(b) - 1;
-    if (a > b) {
-      uint32_t t = a;
-      a = b;
-      b = t;
-    }
-    b -= a;
+    uint32_t mn = min(a, b), mx = max(a, b);
+    a = mn;
+    b = mx - mn;
   } while (b);
   return a << sh;
 }
@@ -163,26 +212,21 @@ __device__ __forceinline__ SI si_sum(SI a, SI b) {
     a.hi += b.lo;
     return a;
   }
-  int32_t lo = a.lo + b.lo, hi = a.hi + b.hi;
-  if (a.exact && b.exact) {
-    SI fine = a.stride <= b.stride ? a : b;
-    SI coarse = a.stride <= b.stride ? b : a;
-    if (coarse.stride % fine.stride == 0 && (int64_t)coarse.stride <= (int64_t)fine.stride * fine.count) {
-      SI r;
-      r.lo = lo;
-      r.hi = hi;
-      r.stride = fine.stride;
-      r.count = (hi - lo) / fine.stride + 1;
-      r.exact = 1;
-      return r;
-    }
-  }
-  int32_t g = (int32_t)gcd_u32((uint32_t)a.stride, (uint32_t)b.stride);
-  int64_t est = g ? (hi - lo) / g + 1 : 1;
-  int64_t prod = (int64_t)a.count * b.count;
   SI r;
-  r.lo = lo;
-  r.hi = hi;
+  r.lo = a.lo + b.lo;
+  r.hi = a.hi + b.hi;
+  const bool af = a.stride <= b.stride;
+  const int32_t gf = af ? a.stride : b.stride, gc = af ? b.stride : a.stride;
+  const int32_t cf = af ? a.count : b.count;
+  if (a.exact && b.exact && gc % gf == 0 && (int64_t)gc <= (int64_t)gf * cf) {
+    r.stride = gf;
+    r.count = (r.hi - r.lo) / gf + 1;
+    r.exact = 1;
+    return r;
+  }
+  const int32_t g = (int32_t)gcd_u32((uint32_t)a.stride, (uint32_t)b.stride);
+  const int64_t est = g ? (r.hi - r.lo) / g + 1 : 1;
+  const int64_t prod = (int64_t)a.count * b.count;
   r.stride = g;
   r.count = (int32_t)(est < prod ? est : prod);
   r.exact = 0;
@@ -193,46 +237,31 @@ __device__ __forceinline__ SI si_sum(SI a, SI b) {
 __device__ __forceinline__ SI si_union(SI a, SI b) {
   if (a.lo == b.lo && a.hi == b.hi && a.stride == b.stride && a.count == b.count && a.exact == b.exact)
     return a;
-  int32_t lo = min(a.lo, b.lo), hi = max(a.hi, b.hi);
-  if (a.exact && b.exact && a.stride == b.stride && a.stride > 0 && (a.lo - b.lo) % a.stride == 0) {
-    if (a.lo <= b.hi + a.stride && b.lo <= a.hi + a.stride) {
-      SI r;
-      r.lo = lo;
-      r.hi = hi;
-      r.stride = a.stride;
-      r.count = (hi - lo) / a.stride + 1;
-      r.exact = 1;
-      return r;
-    }
-  }
-  uint32_t dl = (uint32_t)abs(a.lo - b.lo);
-  int32_t g = (int32_t)gcd_u32(gcd_u32((uint32_t)a.stride, (uint32_t)b.stride), dl);
-  int64_t est = g ? (hi - lo) / g + 1 : 1;
-  int64_t sum = (int64_t)a.count + b.count;
   SI r;
-  r.lo = lo;
-  r.hi = hi;
+  r.lo = min(a.lo, b.lo);
+  r.hi = max(a.hi, b.hi);
+  if (a.exact && b.exact && a.stride == b.stride && a.stride > 0 && (a.lo - b.lo) % a.stride == 0 &&
+      a.lo <= b.hi + a.stride && b.lo <= a.hi + a.stride) {
+    r.stride = a.stride;
+    r.count = (r.hi - r.lo) / a.stride + 1;
+    r.exact = 1;
+    return r;
+  }
+  const uint32_t dl = (uint32_t)abs(a.lo - b.lo);
+  const int32_t g = (int32_t)gcd_u32(gcd_u32((uint32_t)a.stride, (uint32_t)b.stride), dl);
+  const int64_t est = g ? (r.hi - r.lo) / g + 1 : 1;
+  const int64_t sum = (int64_t)a.count + b.count;
   r.stride = g;
   r.count = (int32_t)(est < sum ? est : sum);
   r.exact = 0;
   return r;
 }
 
-struct Cand {
-  int32_t ext[LS_MAX_VARS], step[LS_MAX_VARS], vw[LS_MAX_VARS];
-  int8_t pos[LS_MAX_VARS];
-  uint8_t flg[LS_MAX_VARS];
-  int8_t chain[MAXCH];
-  int n;
-  uint32_t exists;
-  uint32_t flags;
-};
-
 __device__ __forceinline__ bool present(const DTerm& t, uint32_t flags) { return (t.req & ~flags) == 0; }
 
-// expr_range (ls/cache.py:80-96): terms in name order, vars at chain
-// positions >= p expanded, others held at 0
-__device__ __forceinline__ SI expr_range(const DTask& T, const DExpr& e, const Cand& c, int p) {
+// expr_range (ls/cache.py:80-96): terms in name order; variables at chain
+// positions >= thr expanded, all others held at 0
+__device__ __forceinline__ SI expr_range(const DTask& T, const DExpr& e, Cand& c, int thr) {
   SI acc;
   acc.lo = acc.hi = e.konst;
   acc.stride = 0;
@@ -240,34 +269,21 @@ __device__ __forceinline__ SI expr_range(const DTask& T, const DExpr& e, const C
   acc.exact = 1;
   for (int k = 0; k < e.nt; ++k) {
     const DTerm& t = T.term[e.t0 + k];
-    if (!present(t, c.flags)) continue;
-    int u = t.var;
-    if (c.pos[u] < p) continue;
-    int32_t E = c.ext[u];
+    const int u = t.slot;
+    const int pu = c.P(u);
+    if (!present(t, c.flags) || pu == NOSLOT || pu < thr) continue;
+    const int32_t E = c.E(u);
     if (E == 1) continue;
-    int32_t d = t.coef * c.step[u];
+    const int32_t d = t.coef * c.St(u);
     SI s;
-    if (d > 0) {
-      s.lo = 0;
-      s.hi = d * (E - 1);
-      s.stride = d;
-    } else {
-      s.lo = d * (E - 1);
-      s.hi = 0;
-      s.stride = -d;
-    }
+    s.lo = d > 0 ? 0 : d * (E - 1);
+    s.hi = d > 0 ? d * (E - 1) : 0;
+    s.stride = abs(d);
     s.count = E;
     s.exact = 1;
     acc = si_sum(acc, s);
   }
   return acc;
-}
-
-// tensor_footprint of one dimension (ls/cache.py:117-130)
-__device__ __forceinline__ int32_t dim_count(const DTask& T, const Cand& c, int t, int d, int p) {
-  SI u = expr_range(T, T.expr[T.t_uacc[t][0]][d], c, p);
-  for (int a = 1; a < T.t_nu[t]; ++a) u = si_union(u, expr_range(T, T.expr[T.t_uacc[t][a]][d], c, p));
-  return u.count;
 }
 
 __device__ __forceinline__ int64_t unroll_lookup(const DTask& T, int64_t U, bool inner, bool* ok) {
@@ -291,86 +307,83 @@ __device__ __forceinline__ int64_t unroll_lookup(const DTask& T, int64_t U, bool
 // Apply the record's transforms to the base chain (ls/ir.py:361-474).
 __device__ int apply_transforms(const DTask& T, const ls_record& r, Cand& c) {
   c.n = T.n_base;
-  c.exists = 0;
   c.flags = r.flags;
-#pragma unroll 1
-  for (int v = 0; v < LS_MAX_VARS; ++v) c.pos[v] = -1;
-#pragma unroll 1
+#pragma unroll
+  for (int v = 0; v < NSLOT; ++v) c.P(v) = NOSLOT;
   for (int p = 0; p < T.n_base; ++p) {
-    int v = T.base_var[p];
-    c.chain[p] = (int8_t)v;
-    c.pos[v] = (int8_t)p;
-    c.ext[v] = T.base_ext[p];
-    c.step[v] = T.base_step[p];
-    c.vw[v] = T.base_vw[p];
-    c.flg[v] = T.base_flags[p];
-    c.exists |= 1u << v;
+    const int v = T.base_slot[p];
+    c.C(p) = (uint8_t)v;
+    c.P(v) = (uint8_t)p;
+    c.E(v) = T.base_ext[p];
+    c.St(v) = T.base_step[p];
+    c.Fl(v) = T.base_flags[p];
   }
-#pragma unroll 1
   for (int x = 0; x < T.n_xf; ++x) {
     const DXform& xf = T.xf[x];
     if (xf.enable_bit >= 0 && !((r.flags >> xf.enable_bit) & 1u)) continue;
-    const int v = xf.var;
+    const int v = xf.slot;
+    const bool exists = v != NOSLOT && c.P(v) != NOSLOT;
     switch (xf.kind) {
       case LS_XF_TILE:
       case LS_XF_VECTORIZE: {
-        if (v < 0 || !((c.exists >> v) & 1u)) return LS_ST_NO_LOOP;
-        int32_t F = xf.param >= 0 ? (int32_t)r.param[xf.param] : xf.value;
+        if (!exists || xf.new_slot == NOSLOT) return LS_ST_NO_LOOP;
+        const int32_t F = xf.param >= 0 ? (int32_t)r.param[xf.param] : xf.value;
+        const int32_t Ev = c.E(v);
         if (xf.kind == LS_XF_VECTORIZE) {
           if (F == 0) return LS_ST_VEC_ZERO;
-          if (c.ext[v] % F != 0) return LS_ST_VEC_DIVIDE;
+          if (Ev % F != 0) return LS_ST_VEC_DIVIDE;
         }
-        if (F < 1 || F > c.ext[v]) return LS_ST_TILE_RANGE;
+        if (F < 1 || F > Ev) return LS_ST_TILE_RANGE;
         if (c.n >= MAXCH) return LS_ST_OVERFLOW;
-        const int u = xf.new_var;
-        const int p = c.pos[v];
+        const int u = xf.new_slot;
+        const int p = c.P(v);
         for (int q = c.n; q > p + 1; --q) {
-          c.chain[q] = c.chain[q - 1];
-          c.pos[c.chain[q]] = (int8_t)q;
+          const int w = c.C(q - 1);
+          c.C(q) = (uint8_t)w;
+          c.P(w) = (uint8_t)q;
         }
-        c.chain[p + 1] = (int8_t)u;
-        c.pos[u] = (int8_t)(p + 1);
+        c.C(p + 1) = (uint8_t)u;
+        c.P(u) = (uint8_t)(p + 1);
         c.n++;
-        c.ext[u] = F;
-        c.step[u] = c.step[v];
-        c.vw[u] = xf.kind == LS_XF_VECTORIZE ? F : 0;
-        c.flg[u] = 0;
-        c.exists |= 1u << u;
-        c.ext[v] = (c.ext[v] + F - 1) / F;
-        c.step[v] *= F;
-        c.vw[v] = 0;
+        c.E(u) = F;
+        c.St(u) = c.St(v);
+        c.Fl(u) = xf.kind == LS_XF_VECTORIZE ? F_VEC : 0;
+        c.E(v) = (Ev + F - 1) / F;
+        c.St(v) *= F;
+        c.Fl(v) &= (uint8_t)~F_VEC;  // the outer loop is rebuilt without vector_width
         break;
       }
       case LS_XF_REORDER: {
         const int m = xf.n_order;
         if (m < 2) break;
-        int8_t vars[LS_MAX_ORDER];
+        uint8_t vars[LS_MAX_ORDER];
+        for (int j = 0; j < m; ++j) {
+          const int nib = (int)((r.perm >> (4 * (xf.perm_shift + j))) & 0xF);
+          const int w = nib < m ? xf.order[nib] : NOSLOT;
+          if (w == NOSLOT || c.P(w) == NOSLOT) return LS_ST_NO_LOOP;
+          vars[j] = (uint8_t)w;
+        }
         uint32_t seen = 0;
         int pmin = MAXCH, pmax = -1;
         for (int j = 0; j < m; ++j) {
-          int nib = (int)((r.perm >> (4 * (xf.perm_shift + j))) & 0xF);
-          int w = nib < m ? xf.order[nib] : -1;
-          if (w < 0 || !((c.exists >> w) & 1u)) return LS_ST_NO_LOOP;
-          vars[j] = (int8_t)w;
-        }
-        for (int j = 0; j < m; ++j) {
-          uint32_t bit = 1u << vars[j];
+          const uint32_t bit = 1u << vars[j];
           if (seen & bit) return LS_ST_REORDER_MISSING;
           seen |= bit;
-          pmin = min(pmin, (int)c.pos[vars[j]]);
-          pmax = max(pmax, (int)c.pos[vars[j]]);
+          const int pv = c.P(vars[j]);
+          pmin = min(pmin, pv);
+          pmax = max(pmax, pv);
         }
         if (pmax - pmin != m - 1) return LS_ST_REORDER_CHAIN;
         for (int j = 0; j < m; ++j) {
-          c.chain[pmin + j] = vars[j];
-          c.pos[vars[j]] = (int8_t)(pmin + j);
+          c.C(pmin + j) = vars[j];
+          c.P(vars[j]) = (uint8_t)(pmin + j);
         }
         break;
       }
       case LS_XF_UNROLL:
       case LS_XF_PARALLEL:
-        if (v < 0 || !((c.exists >> v) & 1u)) return LS_ST_NO_LOOP;
-        c.flg[v] |= xf.kind == LS_XF_UNROLL ? 2 : 1;
+        if (!exists) return LS_ST_NO_LOOP;
+        c.Fl(v) |= xf.kind == LS_XF_UNROLL ? F_UNR : F_PAR;
         break;
       default:
         return LS_ST_UNSUPPORTED;
@@ -379,167 +392,264 @@ __device__ int apply_transforms(const DTask& T, const ls_record& r, Cand& c) {
   return LS_OK;
 }
 
-// Branching (non-inlined) loops and the innermost replication factor U.
-// Returns false if an unrolled loop sits above a branching loop (its sub-chain
-// would be emitted several times: the general-tree case).
-__device__ __forceinline__ bool chain_shape(const Cand& c, int8_t* cpos, int* k_out, int64_t* U_out) {
-  int k = 0, last = -1;
-  for (int p = 0; p < c.n; ++p) {
-    int v = c.chain[p];
-    if (!c.vw[v] && !(c.flg[v] & 2)) {
-      cpos[k++] = (int8_t)p;
-      last = p;
-    }
-  }
-  int64_t U = 1;
-  for (int p = 0; p < c.n; ++p) {
-    int v = c.chain[p];
-    if (c.vw[v] || !(c.flg[v] & 2)) continue;
-    if (p < last) return false;
-    U *= c.ext[v];
-  }
-  *k_out = k;
-  *U_out = U;
-  return true;
-}
-
 __device__ __forceinline__ double rn_mul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double rn_add(double a, double b) { return __dadd_rn(a, b); }
 
 // bank_conflict_factor (ls/ptx.py:264-307) of innermost access a
-__device__ int64_t bank_factor(const DTask& T, const Cand& c, int a) {
+__device__ int64_t bank_factor(const DTask& T, Cand& c, int a) {
   const int t = T.acc_tensor[a];
   const int rank = T.t_rank[t];
-  int tid = -1;
   uint32_t used = 0;
   for (int d = 0; d < rank; ++d) {
     const DExpr& e = T.expr[a][d];
     for (int k = 0; k < e.nt; ++k)
-      if (present(T.term[e.t0 + k], c.flags)) used |= 1u << T.term[e.t0 + k].var;
+      if (present(T.term[e.t0 + k], c.flags)) used |= 1u << T.term[e.t0 + k].slot;
   }
-  if (T.tid_var >= 0 && ((used >> T.tid_var) & 1u)) {
-    tid = T.tid_var;
+  int tid = -1;
+  if (T.tid_slot >= 0 && ((used >> T.tid_slot) & 1u)) {
+    tid = T.tid_slot;
   } else {
     for (int p = 0; p < c.n; ++p) {
-      int v = c.chain[p];
-      if ((c.flg[v] & 1) && ((used >> v) & 1u)) tid = v;
+      const int v = c.C(p);
+      if ((c.Fl(v) & F_PAR) && ((used >> v) & 1u)) tid = v;
     }
   }
   if (tid < 0) return 1;  // every lane hits one word
-  int lanes = min(T.warp_size, c.ext[tid]);
+  const int lanes = min(T.warp_size, c.E(tid));
   int64_t A = 0, B = 0;
   for (int d = 0; d < rank; ++d) {
     const DExpr& e = T.expr[a][d];
     int64_t ct = 0;
     for (int k = 0; k < e.nt; ++k) {
       const DTerm& tm = T.term[e.t0 + k];
-      if (present(tm, c.flags) && tm.var == tid) ct += tm.coef;
+      if (present(tm, c.flags) && tm.slot == tid) ct += tm.coef;
     }
     A += (int64_t)e.konst * T.t_stride[t][d];
     B += ct * T.t_stride[t][d];
   }
   // words are monotone in the lane id, so equal words are adjacent
   uint8_t cnt[64];
-  for (int b = 0; b < T.banks && b < 64; ++b) cnt[b] = 0;
+  for (int b = 0; b < T.banks; ++b) cnt[b] = 0;
   int64_t prev = 0, best = 0;
   for (int l = 0; l < lanes; ++l) {
-    int64_t num = (A + B * l) * T.t_eb[t];
-    int64_t w = num >= 0 ? num / 4 : -((-num + 3) / 4);
+    const int64_t num = (A + B * l) * T.t_eb[t];
+    const int64_t w = num >= 0 ? num / 4 : -((-num + 3) / 4);
     if (l == 0 || w != prev) {
       int64_t b = w % T.banks;
       if (b < 0) b += T.banks;
-      int nc = ++cnt[b];
-      best = max(best, (int64_t)nc);
+      best = max(best, (int64_t)++cnt[b]);
     }
     prev = w;
   }
   return best;
 }
 
-// extract_features + score for one candidate.  Returns the status.
-__device__ int eval_candidate(const DTask& T, const ls_record& r, double* f, double* score) {
-  Cand c;
+// thread_cycles in line order (ls/ptx.py:225-235), for non-integral cost tables
+__device__ double ptx_work_ordered(const DTask& T, Cand& c, int k, double wi) {
+  const double* pc = T.ptx_cost;
+  double wpre[MAXCH], wpost[MAXCH];
+  int32_t rem[MAXCH];
+  {
+    double w = 1.0;
+    int j = 0;
+    for (int p = 0; p < c.n; ++p) {
+      const int v = c.C(p);
+      if (c.Fl(v) & (F_VEC | F_UNR)) continue;
+      wpre[p] = w;
+      if (!(j + 8 <= k - 1)) w *= (double)c.E(v);
+      wpost[p] = w;
+      ++j;
+    }
+  }
+  double work = 0.0;
+  int p = 0;
+  bool down = true;
+  while (true) {
+    if (down) {
+      if (p == c.n) {
+        for (int a = 0; a < T.L; ++a) work = rn_add(work, rn_mul(pc[LS_I_LOAD], wi));
+        for (int a = 0; a < T.S; ++a) {
+          work = rn_add(work, rn_mul(pc[LS_I_FMA], wi));
+          work = rn_add(work, rn_mul(pc[LS_I_STORE], wi));
+        }
+        down = false;
+        p = c.n - 1;
+        continue;
+      }
+      const int v = c.C(p);
+      const uint8_t fl = c.Fl(v);
+      if (fl & (F_VEC | F_UNR)) {
+        rem[p] = (fl & F_VEC) ? 1 : c.E(v);
+      } else {
+        work = rn_add(work, rn_mul(pc[LS_I_INIT], wpre[p]));
+      }
+      ++p;
+    } else {
+      if (p < 0) break;
+      const int v = c.C(p);
+      const uint8_t fl = c.Fl(v);
+      if (fl & (F_VEC | F_UNR)) {
+        if (--rem[p] > 0) {
+          ++p;
+          down = true;
+        } else {
+          --p;
+        }
+      } else {
+        work = rn_add(work, rn_mul(pc[LS_I_ADD], wpost[p]));
+        work = rn_add(work, rn_mul(pc[LS_I_CMP], wpost[p]));
+        work = rn_add(work, rn_mul(pc[LS_I_BRANCH], wpost[p]));
+        --p;
+      }
+    }
+  }
+  return rn_add(work, pc[LS_I_RET]);
+}
+
+// extract_features + score of one candidate (ls/cost.py:132-161).  TM x RM is
+// the compile-time tensor x dimension layout of the register-resident walk.
+template <int TM, int RM>
+__device__ int eval_candidate(const DTask& T, const ls_record& r, Cand& c, double* f, double* score) {
   int st = apply_transforms(T, r, c);
   if (st) return st;
-  int8_t cpos[MAXCH];
-  int k;
-  int64_t U;
-  if (!chain_shape(c, cpos, &k, &U)) return LS_ST_UNSUPPORTED;
-
-  // ---- movement model over the chain, innermost first (CacheModel._visit_loop)
-  int32_t cnt[MAXT][MAXRANK];
-  uint32_t dmask[MAXT][MAXRANK];
-  uint32_t tmask[MAXT];
-  int64_t Fb[MAXT], dm[MAXT];
-  uint32_t reuse = 0;
   const int nT = T.n_tensors;
+
+  // ---- movement model (CacheModel._visit_loop, ls/cache.py:167-236) ----------
+  // (a) for every tensor dimension and every variable of it, the dimension's
+  //     count once the chain walk has passed that variable (all its variables
+  //     at positions >= that variable's position expanded)
   for (int t = 0; t < nT; ++t) {
-    tmask[t] = 0;
-    for (int d = 0; d < T.t_rank[t]; ++d) {
-      uint32_t m = 0;
-      for (int a = 0; a < T.t_nu[t]; ++a) {
-        const DExpr& e = T.expr[T.t_uacc[t][a]][d];
-        for (int q = 0; q < e.nt; ++q)
-          if (present(T.term[e.t0 + q], c.flags)) m |= 1u << T.term[e.t0 + q].var;
+    for (int rr = 0; rr < T.t_rank[t]; ++rr) {
+      const int D = t * RM + rr;
+      for (int j = 0; j < T.dim_nv[D]; ++j) {
+        const int thr = c.P(T.dim_var[D][j]);
+        if (thr == NOSLOT) continue;
+        SI u = expr_range(T, T.expr[T.t_uacc[t][0]][rr], c, thr);
+        for (int a = 1; a < T.t_nu[t]; ++a) u = si_union(u, expr_range(T, T.expr[T.t_uacc[t][a]][rr], c, thr));
+        c.G(T.dim_base[D] + j) = u.count;
       }
-      dmask[t][d] = m;
-      tmask[t] |= m;
-      cnt[t][d] = T.t_count0[t][d];
     }
-    Fb[t] = T.t_F0[t];
-    dm[t] = T.t_nacc[t];
-    reuse |= 1u << t;
+  }
+  // (b) walk the chain innermost-first with counts, footprints and movement in registers
+  int32_t cur[TM * RM];
+  uint32_t tmask[TM];
+  int64_t Fb[TM], dm[TM];
+  uint32_t reuse = 0;
+#pragma unroll
+  for (int D = 0; D < TM * RM; ++D) cur[D] = T.dim_count0[D];
+#pragma unroll
+  for (int t = 0; t < TM; ++t) {
+    tmask[t] = 0;
+    dm[t] = 0;
+    Fb[t] = 0;
+    if (t < nT) {
+      int64_t F = 1;
+#pragma unroll
+      for (int rr = 0; rr < RM; ++rr) F *= cur[t * RM + rr];
+      Fb[t] = F;
+      dm[t] = T.t_nacc[t];
+      reuse |= 1u << t;
+      for (int a = 0; a < T.t_nu[t]; ++a)
+        for (int rr = 0; rr < T.t_rank[t]; ++rr) {
+          const DExpr& e = T.expr[T.t_uacc[t][a]][rr];
+          for (int q = 0; q < e.nt; ++q)
+            if (present(T.term[e.t0 + q], c.flags)) tmask[t] |= 1u << T.term[e.t0 + q].slot;
+        }
+    }
   }
   const int64_t cap = T.cap;
   for (int p = c.n - 1; p >= 0; --p) {
-    const int v = c.chain[p];
-    const int64_t E = c.ext[v];
-    int64_t single = 0;
-    for (int t = 0; t < nT; ++t) single += Fb[t];
-    for (int t = 0; t < nT; ++t) {
-      const bool uses = (tmask[t] >> v) & 1u;
-      int64_t Ff = Fb[t];
-      if (uses) {
-        Ff = 1;
-        for (int d = 0; d < T.t_rank[t]; ++d) {
-          if ((dmask[t][d] >> v) & 1u) cnt[t][d] = dim_count(T, c, t, d, p);
-          Ff *= cnt[t][d];
+    const int v = c.C(p);
+    const int64_t E = c.E(v);
+#pragma unroll
+    for (int w = 0; w < (TM * RM + 15) / 16; ++w) {
+      const uint64_t nib = T.slot_dnib[v][w];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int D = 16 * w + q;
+        if (D < TM * RM) {
+          const int x = (int)((nib >> (4 * q)) & 15u);
+          if (x) cur[D] = c.G(T.dim_base[D] + x - 1);
         }
       }
-      bool ru = (reuse >> t) & 1u;
-      if (single > cap && !uses) ru = false;
-      const int64_t per = (single <= cap || ru) ? Ff : dm[t] * E;
-      if (Ff > cap) ru = false;
-      dm[t] = per;
-      reuse = ru ? (reuse | (1u << t)) : (reuse & ~(1u << t));
-      Fb[t] = Ff;
+    }
+    int64_t single = 0;
+#pragma unroll
+    for (int t = 0; t < TM; ++t) single += Fb[t];
+#pragma unroll
+    for (int t = 0; t < TM; ++t) {
+      if (t < nT) {
+        int64_t Ff = 1;
+#pragma unroll
+        for (int rr = 0; rr < RM; ++rr) Ff *= cur[t * RM + rr];
+        const bool uses = (tmask[t] >> v) & 1u;
+        bool ru = (reuse >> t) & 1u;
+        if (single > cap && !uses) ru = false;
+        const int64_t per = (single <= cap || ru) ? Ff : dm[t] * E;
+        if (Ff > cap) ru = false;
+        dm[t] = per;
+        reuse = ru ? (reuse | (1u << t)) : (reuse & ~(1u << t));
+        Fb[t] = Ff;
+      }
     }
   }
   int64_t dmov = 0;
-  for (int t = 0; t < nT; ++t) dmov += dm[t];
+#pragma unroll
+  for (int t = 0; t < TM; ++t) dmov += dm[t];
 
+  // ---- emitted-block structure of the transformed chain -----------------------
+  // branching loops j = 0..k-1 (not unrolled/vectorized); R_j = copies of loop j
+  // emitted because unrolled loops above it inline their bodies R_j times
+  // (ls/ir.py:619-626); U = body copies in the innermost block.
+  int k = 0;
+  for (int p = 0; p < c.n; ++p) k += (c.Fl(c.C(p)) & (F_VEC | F_UNR)) ? 0 : 1;
+  int64_t W = 1, Wp = 1, R = 1, Uin = 1;
+  int64_t sumR = 0, sumW = 0, sumRl = 0, Wlast = 1, Rlast = 1;
+  int64_t ptx_loops = 0;  // sum_j R_j * (c_mov W'_{j-1} + (c_add+c_setp+c_bra) W'_j), integral costs
+  const int64_t* ic = T.ptx_icost;
+  {
+    int j = 0;
+    for (int p = 0; p < c.n; ++p) {
+      const int v = c.C(p);
+      const uint8_t fl = c.Fl(v);
+      const int64_t e = c.E(v);
+      if (fl & F_VEC) continue;
+      if (fl & F_UNR) {
+        R *= e;
+        Uin *= e;
+        continue;
+      }
+      const int64_t Wprev = Wp;
+      W *= e;
+      if (!(j + 8 <= k - 1)) Wp *= e;  // PTX counter registers repeat every 8 depths (ls/ir.py:627, ls/ptx.py:163-169)
+      sumR += R;
+      if (j < k - 1) {
+        sumW += W;
+        sumRl += R;
+      }
+      ptx_loops += R * (ic[LS_I_INIT] * Wprev + (ic[LS_I_ADD] + ic[LS_I_CMP] + ic[LS_I_BRANCH]) * Wp);
+      Wlast = W;
+      Rlast = R;
+      Uin = 1;
+      ++j;
+    }
+  }
   const int64_t L = T.L, S = T.S;
   int nf;
   if (T.family == LS_FAMILY_CPU) {
-    // counts over matched loop blocks and block cycles (ls/asm.py:250-337, ls/ilp.py:262-271)
+    // only the first emitted copy of each loop block is matched by the greedy
+    // loop_map (ls/asm.py:250-294); every block is scheduled (ls/ilp.py:262-271)
     int64_t ilp, nld = 0, nst = 0;
     bool ok;
     if (k == 0) {
-      ilp = unroll_lookup(T, U, false, &ok);
+      ilp = unroll_lookup(T, R, false, &ok);
       if (!ok) return LS_ST_UNROLL_TABLE;
     } else {
-      int64_t W = 1;
-      ilp = T.c_init + (int64_t)(k - 1) * T.c_latch + T.c_ret;
-      for (int j = 0; j + 1 < k; ++j) {
-        W *= c.ext[c.chain[cpos[j]]];
-        ilp += T.c_init * W;
-      }
-      W *= c.ext[c.chain[cpos[k - 1]]];
-      int64_t ci = unroll_lookup(T, U, true, &ok);
+      const int64_t ci = unroll_lookup(T, Uin, true, &ok);
       if (!ok) return LS_ST_UNROLL_TABLE;
-      ilp += ci * W;
-      nld = L * U * W;
-      nst = S * U * W;
+      ilp = T.c_init * (sumR - (k - 1) + sumW) + ci * (Wlast + Rlast - 1) + T.c_latch * sumRl + T.c_ret;
+      nld = L * Uin * Wlast;
+      nst = S * Uin * Wlast;
     }
     f[0] = (double)nst;  // n_fma == n_vstore: one fma per store
     f[1] = (double)nld;
@@ -548,55 +658,32 @@ __device__ int eval_candidate(const DTask& T, const ls_record& r, double* f, dou
     f[4] = (double)ilp;
     nf = LS_NFEAT_CPU;
   } else {
-    // PTX trips: a counter register repeats every 8 depths (ls/ir.py:627), so a
-    // loop with a branching loop 8 deeper in its region has no trip (ls/ptx.py:163-169)
-    int64_t Wp[MAXCH + 1];
-    Wp[0] = 1;
-    for (int j = 0; j < k; ++j) Wp[j + 1] = Wp[j] * (j + 8 <= k - 1 ? 1 : c.ext[c.chain[cpos[j]]]);
-    const int64_t Wi = Wp[k];
+    // loop_map_ptx counts every emitted copy (ls/ptx.py:90-108, 196-235)
+    const int64_t Ubody = R;  // R_{k-1} * U_inner == all unrolled extents
     double work;
     if (T.costs_integral) {
-      const int64_t* ic = T.ptx_icost;
-      int64_t w = ic[LS_I_RET];
-      for (int j = 0; j < k; ++j)
-        w += ic[LS_I_INIT] * Wp[j] + (ic[LS_I_ADD] + ic[LS_I_CMP] + ic[LS_I_BRANCH]) * Wp[j + 1];
-      w += Wi * U * (L * ic[LS_I_LOAD] + S * (ic[LS_I_FMA] + ic[LS_I_STORE]));
-      work = (double)w;
-    } else {  // line-order float accumulation, as thread_cycles does (ls/ptx.py:225-235)
-      const double* pc = T.ptx_cost;
-      work = 0.0;
-      for (int j = 0; j < k; ++j) work = rn_add(work, rn_mul(pc[LS_I_INIT], (double)Wp[j]));
-      const double wi = (double)Wi;
-      for (int64_t u = 0; u < U; ++u) {
-        for (int a = 0; a < L; ++a) work = rn_add(work, rn_mul(pc[LS_I_LOAD], wi));
-        for (int a = 0; a < S; ++a) {
-          work = rn_add(work, rn_mul(pc[LS_I_FMA], wi));
-          work = rn_add(work, rn_mul(pc[LS_I_STORE], wi));
-        }
-      }
-      for (int j = k - 1; j >= 0; --j) {
-        const double wj = (double)Wp[j + 1];
-        work = rn_add(work, rn_mul(pc[LS_I_ADD], wj));
-        work = rn_add(work, rn_mul(pc[LS_I_CMP], wj));
-        work = rn_add(work, rn_mul(pc[LS_I_BRANCH], wj));
-      }
-      work = rn_add(work, pc[LS_I_RET]);
+      work = (double)(ptx_loops + Ubody * Wp * (L * ic[LS_I_LOAD] + S * (ic[LS_I_FMA] + ic[LS_I_STORE])) +
+                      ic[LS_I_RET]);
+    } else {
+      work = ptx_work_ordered(T, c, k, (double)Wp);
     }
-    // shared-memory ops (ls/ptx.py:310-327): volume counts vector loops once
     double smem = 0.0;
-    for (int a = 0; a < T.n_acc; ++a) {
-      if (!T.t_shared[T.acc_tensor[a]]) continue;
+    if (T.has_shared) {  // shared-memory ops (ls/ptx.py:310-327): vector loops count once
       int64_t vol = 1;
-      for (int p = 0; p < c.n; ++p) vol *= c.vw[c.chain[p]] ? 1 : c.ext[c.chain[p]];
-      smem = rn_add(smem, (double)(vol * bank_factor(T, c, a)));
+      for (int p = 0; p < c.n; ++p) {
+        const int v = c.C(p);
+        vol *= (c.Fl(v) & F_VEC) ? 1 : c.E(v);
+      }
+      for (int a = 0; a < T.n_acc; ++a)
+        if (T.t_shared[T.acc_tensor[a]]) smem = rn_add(smem, (double)(vol * bank_factor(T, c, a)));
     }
     f[0] = work;
     f[1] = T.sm_underuse;
     f[2] = T.warp_slack;
     f[3] = smem;
-    f[4] = (double)(S * U * Wi);
-    f[5] = (double)(L * U * Wi);
-    f[6] = (double)(S * U * Wi);
+    f[4] = (double)(S * Ubody * Wp);
+    f[5] = (double)(L * Ubody * Wp);
+    f[6] = (double)(S * Ubody * Wp);
     nf = LS_NFEAT_GPU;
   }
   double total = 0.0;
@@ -627,25 +714,26 @@ __device__ __forceinline__ ls_record load_record(const ls_record* __restrict__ r
   return r;
 }
 
-__global__ void __launch_bounds__(256) score_kernel(const DTask* __restrict__ gtask,
+template <int TM, int RM>
+__global__ void __launch_bounds__(TPB) score_kernel(const DTask* __restrict__ gtask,
                                                     const ls_record* __restrict__ recs, int64_t n,
-                                                    double* __restrict__ scores,
-                                                    double* __restrict__ feats,
+                                                    double* __restrict__ scores, double* __restrict__ feats,
                                                     int32_t* __restrict__ status) {
-  __shared__ DTask T;
+  extern __shared__ __align__(16) unsigned char dyn[];
+  DTask& T = *reinterpret_cast<DTask*>(dyn);
   stage_task(T, gtask);
+  Cand c = carve(dyn + align16(sizeof(DTask)), T.n_stage);
   const int nf = T.family == LS_FAMILY_CPU ? LS_NFEAT_CPU : LS_NFEAT_GPU;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    ls_record r = load_record(recs, i);
+  for (int64_t i = (int64_t)blockIdx.x * TPB + threadIdx.x; i < n; i += (int64_t)gridDim.x * TPB) {
+    const ls_record r = load_record(recs, i);
     double f[LS_NFEAT_GPU];
     double s = 0.0;
-    int st = eval_candidate(T, r, f, &s);
-    if (st) s = __longlong_as_double(0x7ff8000000000000ll);
-    if (scores) scores[i] = s;
+    const int st = eval_candidate<TM, RM>(T, r, c, f, &s);
+    const double nan = __longlong_as_double(0x7ff8000000000000ll);
+    if (scores) scores[i] = st ? nan : s;
     if (status) status[i] = st;
     if (feats)
-      for (int q = 0; q < nf; ++q) feats[i * nf + q] = st ? __longlong_as_double(0x7ff8000000000000ll) : f[q];
+      for (int q = 0; q < nf; ++q) feats[i * nf + q] = st ? nan : f[q];
   }
 }
 
@@ -678,21 +766,22 @@ struct TopkState {
   int cnt;
 };
 
-// Sort buf[0..cnt) (padded to TK_BUF with +inf) and keep the k smallest.
-__device__ void topk_compact(TopkState& S, int k) {
-  const int cnt = S.cnt;
+// Sort buf[0..cnt) (padded with +inf) and keep the k smallest; returns the kept count.
+__device__ int topk_compact(TopkState& S, int k, int cnt) {
   for (int i = cnt + threadIdx.x; i < TK_BUF; i += blockDim.x) {
     S.buf[i].s = KEY_INF_S;
     S.buf[i].i = KEY_INF_I;
   }
   __syncthreads();
-  for (int size = 2; size <= TK_BUF; size <<= 1) {
+  int size0 = 2;
+  while (size0 < cnt) size0 <<= 1;  // only the occupied power-of-two prefix needs sorting
+  for (int size = 2; size <= size0; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int t = threadIdx.x; t < TK_BUF / 2; t += blockDim.x) {
-        int lo = 2 * t - (t & (stride - 1));
-        int hi = lo + stride;
-        bool up = (lo & size) == 0;
-        Key a = S.buf[lo], b = S.buf[hi];
+      for (int t = threadIdx.x; t < size0 / 2; t += blockDim.x) {
+        const int lo = 2 * t - (t & (stride - 1));
+        const int hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const Key a = S.buf[lo], b = S.buf[hi];
         if (kless(b, a) == up) {
           S.buf[lo] = b;
           S.buf[hi] = a;
@@ -701,12 +790,13 @@ __device__ void topk_compact(TopkState& S, int k) {
       __syncthreads();
     }
   }
+  const int keep = cnt < k ? cnt : k;
   if (threadIdx.x == 0) {
-    int keep = cnt < k ? cnt : k;
     S.cnt = keep;
     if (keep == k) S.thr = S.buf[k - 1];
   }
   __syncthreads();
+  return keep;
 }
 
 __device__ __forceinline__ void topk_init(TopkState& S) {
@@ -718,50 +808,56 @@ __device__ __forceinline__ void topk_init(TopkState& S) {
   __syncthreads();
 }
 
-// One round: every thread offers at most one key; compacts when the buffer
-// could overflow on the next round.
-__device__ __forceinline__ void topk_offer(TopkState& S, bool has, const Key& key, int k) {
+// Insert-if-better without a barrier; the block synchronises only when the
+// buffer could overflow within the next round (`safe` rounds are free).
+__device__ __forceinline__ void topk_offer(TopkState& S, bool has, const Key& key, int k, int& safe) {
   if (has && kless(key, S.thr)) {
-    int slot = atomicAdd(&S.cnt, 1);
+    const int slot = atomicAdd(&S.cnt, 1);
     S.buf[slot] = key;
   }
+  if (--safe > 0) return;
   __syncthreads();
-  const int c = S.cnt;
+  int c = S.cnt;
   __syncthreads();
-  if (c > TK_BUF - (int)blockDim.x) topk_compact(S, k);
+  if (c > TK_BUF - (int)blockDim.x) c = topk_compact(S, k, c);
+  safe = (TK_BUF - c) / (int)blockDim.x;
 }
 
-__global__ void __launch_bounds__(256) score_topk_kernel(const DTask* __restrict__ gtask,
-                                                         const ls_record* __restrict__ recs,
-                                                         int64_t n, int64_t base_index, int k,
-                                                         Key* __restrict__ block_out,
+template <int TM, int RM>
+__global__ void __launch_bounds__(TPB) score_topk_kernel(const DTask* __restrict__ gtask,
+                                                         const ls_record* __restrict__ recs, int64_t n,
+                                                         int64_t base_index, int k, Key* __restrict__ block_out,
                                                          unsigned long long* __restrict__ n_valid) {
-  __shared__ DTask T;
-  __shared__ TopkState S;
+  extern __shared__ __align__(16) unsigned char dyn[];
+  DTask& T = *reinterpret_cast<DTask*>(dyn);
   stage_task(T, gtask);
+  TopkState& S = *reinterpret_cast<TopkState*>(dyn + align16(sizeof(DTask)));
+  Cand c = carve(dyn + align16(sizeof(DTask)) + align16(sizeof(TopkState)), T.n_stage);
   topk_init(S);
   unsigned int valid = 0;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
+  int safe = 1;
+  for (int64_t base = (int64_t)blockIdx.x * TPB; base < n; base += (int64_t)gridDim.x * TPB) {
     const int64_t i = base + threadIdx.x;
     bool has = false;
     Key key;
     if (i < n) {
-      ls_record r = load_record(recs, i);
+      const ls_record r = load_record(recs, i);
       double f[LS_NFEAT_GPU];
       double s;
-      if (eval_candidate(T, r, f, &s) == LS_OK) {
+      if (eval_candidate<TM, RM>(T, r, c, f, &s) == LS_OK) {
         has = true;
         key.s = order_bits(s);
         key.i = base_index + i;
         ++valid;
       }
     }
-    topk_offer(S, has, key, k);
+    topk_offer(S, has, key, k, safe);
   }
-  topk_compact(S, k);
+  __syncthreads();
+  const int kept = topk_compact(S, k, S.cnt);
   for (int j = threadIdx.x; j < k; j += blockDim.x) {
     Key o;
-    if (j < S.cnt) {
+    if (j < kept) {
       o = S.buf[j];
     } else {
       o.s = KEY_INF_S;
@@ -769,7 +865,6 @@ __global__ void __launch_bounds__(256) score_topk_kernel(const DTask* __restrict
     }
     block_out[(int64_t)blockIdx.x * k + j] = o;
   }
-  // warp-reduce the valid counts, one atomic per warp
   for (int off = 16; off > 0; off >>= 1) valid += __shfl_down_sync(0xffffffffu, valid, off);
   if ((threadIdx.x & 31) == 0 && valid) atomicAdd(n_valid, (unsigned long long)valid);
 }
@@ -780,6 +875,7 @@ __global__ void __launch_bounds__(1024) merge_keys_kernel(const Key* __restrict_
                                                           int64_t* __restrict__ out_i) {
   __shared__ TopkState S;
   topk_init(S);
+  int safe = 1;
   for (int64_t base = 0; base < m; base += blockDim.x) {
     const int64_t i = base + threadIdx.x;
     bool has = false;
@@ -788,11 +884,12 @@ __global__ void __launch_bounds__(1024) merge_keys_kernel(const Key* __restrict_
       key = in[i];
       has = !(key.s == KEY_INF_S && key.i == KEY_INF_I);
     }
-    topk_offer(S, has, key, k);
+    topk_offer(S, has, key, k, safe);
   }
-  topk_compact(S, k);
+  __syncthreads();
+  const int kept = topk_compact(S, k, S.cnt);
   for (int j = threadIdx.x; j < k; j += blockDim.x) {
-    if (j < S.cnt) {
+    if (j < kept) {
       out_s[j] = from_order_bits(S.buf[j].s);
       out_i[j] = S.buf[j].i;
     } else {
@@ -817,24 +914,35 @@ __global__ void lists_to_keys_kernel(const double* __restrict__ s, const int64_t
   out[i] = k;
 }
 
-// U of every structurally supported candidate, into an open-addressing set.
-__global__ void __launch_bounds__(256) collect_unroll_kernel(const DTask* __restrict__ gtask,
+// Body-replication factor of every transformable record (U_inner, or all
+// unrolled extents when no loop branches), into an open-addressing set.
+__global__ void __launch_bounds__(TPB) collect_unroll_kernel(const DTask* __restrict__ gtask,
                                                              const ls_record* __restrict__ recs, int64_t n,
                                                              unsigned long long* __restrict__ set, int cap) {
-  __shared__ DTask T;
+  extern __shared__ __align__(16) unsigned char dyn[];
+  DTask& T = *reinterpret_cast<DTask*>(dyn);
   stage_task(T, gtask);
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    ls_record r = load_record(recs, i);
-    Cand c;
+  Cand c = carve(dyn + align16(sizeof(DTask)), T.n_stage);
+  for (int64_t i = (int64_t)blockIdx.x * TPB + threadIdx.x; i < n; i += (int64_t)gridDim.x * TPB) {
+    const ls_record r = load_record(recs, i);
     if (apply_transforms(T, r, c)) continue;
-    int8_t cpos[MAXCH];
-    int k;
-    int64_t U;
-    if (!chain_shape(c, cpos, &k, &U)) continue;
-    unsigned long long key = (unsigned long long)U;
+    int64_t R = 1, Uin = 1;
+    int k = 0;
+    for (int p = 0; p < c.n; ++p) {
+      const uint8_t fl = c.Fl(c.C(p));
+      if (fl & F_VEC) continue;
+      if (fl & F_UNR) {
+        R *= c.E(c.C(p));
+        Uin *= c.E(c.C(p));
+      } else {
+        Uin = 1;
+        ++k;
+      }
+    }
+    const unsigned long long key = (unsigned long long)(k ? Uin : R);
     unsigned int h = (unsigned int)((key * 0x9E3779B97F4A7C15ull) >> 40) % (unsigned)cap;
     for (int probe = 0; probe < cap; ++probe) {
-      unsigned long long prev = atomicCAS(&set[h], 0ull, key);
+      const unsigned long long prev = atomicCAS(&set[h], 0ull, key);
       if (prev == 0ull || prev == key) break;
       h = (h + 1) % (unsigned)cap;
     }
@@ -873,50 +981,56 @@ int build_task(const ls_task_desc& d, DTask& T, std::vector<int>& load_t, std::v
   for (int i = nl; i < d.n_nodes; ++i)
     if (d.nodes[i].kind != LS_NODE_ACCESS || d.nodes[i].parent != nl - 1)
       return fail(LS_E_UNSUPPORTED, "program is not a perfect loop chain (accesses outside the innermost loop)");
-  int ntile = 0;
+  for (int x = 0; x < d.n_xforms; ++x) {
+    const ls_xform& s = d.xforms[x];
+    if (s.var >= d.n_vars || s.new_var >= d.n_vars || s.param >= LS_MAX_PARAMS || s.enable_bit >= 32 ||
+        s.n_order < 0 || s.n_order > LS_MAX_ORDER || s.perm_shift < 0 || s.perm_shift + s.n_order > 16)
+      return fail(LS_E_ARG, "bad transform slot");
+  }
+  // ---- variable slots: only names that can exist (base loops and tile/vectorize inner loops)
+  std::vector<int> slot_of(LS_MAX_VARS, NOSLOT);
+  int ns = 0;
+  auto add_slot = [&](int v) {
+    if (v >= 0 && slot_of[v] == NOSLOT) slot_of[v] = ns++;
+  };
+  for (int p = 0; p < nl; ++p) add_slot(d.nodes[p].var);
   for (int x = 0; x < d.n_xforms; ++x)
-    if (d.xforms[x].kind == LS_XF_TILE || d.xforms[x].kind == LS_XF_VECTORIZE) ++ntile;
-  if (nl + ntile > MAXCH) return fail(LS_E_UNSUPPORTED, "transformed chain could exceed 16 loops");
+    if ((d.xforms[x].kind == LS_XF_TILE || d.xforms[x].kind == LS_XF_VECTORIZE) && d.xforms[x].var >= 0)
+      add_slot(d.xforms[x].new_var);
+  if (ns > NSLOT) return fail(LS_E_UNSUPPORTED, "transformed chain could exceed 16 loops");
+  auto S_ = [&](int v) -> uint8_t { return v < 0 ? NOSLOT : (uint8_t)slot_of[v]; };
 
   T.n_base = nl;
-  std::vector<int64_t> span(LS_MAX_VARS, 0);  // bound on step*(extent) of each var's base loop
-  std::vector<int> base_of(LS_MAX_VARS, -1);
+  std::vector<int64_t> span(LS_MAX_VARS, 0);  // step * extent of each variable's base loop
+  int ntile = 0;
   for (int p = 0; p < nl; ++p) {
     const ls_node& n = d.nodes[p];
     if (n.var < 0 || n.var >= d.n_vars || n.extent < 1 || n.step < 1 || n.extent >= (1 << 30) ||
         n.step >= (1 << 30))
       return fail(LS_E_ARG, "bad loop node");
-    T.base_var[p] = (int8_t)n.var;
+    T.base_slot[p] = S_(n.var);
     T.base_ext[p] = n.extent;
     T.base_step[p] = n.step;
-    T.base_vw[p] = n.vector_width;
-    T.base_flags[p] = (uint8_t)((n.parallel ? 1 : 0) | (n.unrolled ? 2 : 0));
+    T.base_flags[p] = (uint8_t)((n.parallel ? F_PAR : 0) | (n.unrolled ? F_UNR : 0) | (n.vector_width ? F_VEC : 0));
     span[n.var] = (int64_t)n.step * n.extent;
-    base_of[n.var] = p;
   }
-  // transforms
   T.n_xf = d.n_xforms;
   for (int x = 0; x < d.n_xforms; ++x) {
     const ls_xform& s = d.xforms[x];
     DXform& o = T.xf[x];
-    if (s.var >= d.n_vars || s.new_var >= d.n_vars || s.param >= LS_MAX_PARAMS || s.enable_bit >= 32 ||
-        s.n_order < 0 || s.n_order > LS_MAX_ORDER || s.perm_shift < 0 || s.perm_shift + s.n_order > 16)
-      return fail(LS_E_ARG, "bad transform slot");
-    if ((s.kind == LS_XF_TILE || s.kind == LS_XF_VECTORIZE) && s.new_var < 0)
-      return fail(LS_E_ARG, "tile without new_var");
     o.kind = (int8_t)s.kind;
-    o.var = (int8_t)s.var;
-    o.new_var = (int8_t)s.new_var;
+    o.slot = S_(s.var);
+    o.new_slot = (s.kind == LS_XF_TILE || s.kind == LS_XF_VECTORIZE) && s.var >= 0 ? S_(s.new_var) : NOSLOT;
     o.param = (int8_t)s.param;
     o.value = s.value;
     o.enable_bit = (int8_t)s.enable_bit;
     o.n_order = (int8_t)s.n_order;
     o.perm_shift = (int8_t)s.perm_shift;
-    for (int j = 0; j < s.n_order; ++j) o.order[j] = (int8_t)s.order[j];
+    for (int j = 0; j < s.n_order; ++j) o.order[j] = S_(s.order[j]);
+    if (s.kind == LS_XF_TILE || s.kind == LS_XF_VECTORIZE) ++ntile;
   }
   // ---- symbolic expression rewrite: final term lists with enable requirements
   // (_rewrite_exprs ls/ir.py:350-358 applied for every Tile/Vectorize of the template)
-  std::vector<uint32_t> creq(LS_MAX_VARS, 0);  // enable bits under which each var exists
   std::vector<std::vector<std::vector<HTerm>>> ex(na);
   for (int a = 0; a < na; ++a) {
     const ls_node& n = d.nodes[nl + a];
@@ -925,15 +1039,17 @@ int build_task(const ls_task_desc& d, DTask& T, std::vector<int>& load_t, std::v
     if (rank < 1 || rank > MAXRANK) return fail(LS_E_ARG, "bad rank");
     ex[a].resize(rank);
     for (int k = 0; k < rank; ++k)
-      for (int t = 0; t < n.idx[k].n_terms; ++t)
-        ex[a][k].push_back({n.idx[k].terms[t].var, n.idx[k].terms[t].coef, 0u});
+      for (int t = 0; t < n.idx[k].n_terms; ++t) {
+        const int v = n.idx[k].terms[t].var;
+        if (v < 0 || v >= d.n_vars || slot_of[v] == NOSLOT) return fail(LS_E_ARG, "index term on a non-loop var");
+        ex[a][k].push_back({v, n.idx[k].terms[t].coef, 0u});
+      }
   }
   for (int x = 0; x < d.n_xforms; ++x) {
     const ls_xform& s = d.xforms[x];
     if (s.kind != LS_XF_TILE && s.kind != LS_XF_VECTORIZE) continue;
-    if (s.var < 0) continue;
-    uint32_t bit = s.enable_bit >= 0 ? (1u << s.enable_bit) : 0u;
-    creq[s.new_var] = creq[s.var] | bit;
+    if (s.var < 0 || s.new_var < 0) continue;  // target never exists: every candidate fails there
+    const uint32_t bit = s.enable_bit >= 0 ? (1u << s.enable_bit) : 0u;
     span[s.new_var] = span[s.var];
     for (auto& acc : ex)
       for (auto& e : acc) {
@@ -943,7 +1059,6 @@ int build_task(const ls_task_desc& d, DTask& T, std::vector<int>& load_t, std::v
         for (auto& t : add) e.push_back(t);
       }
   }
-  // sort terms by name rank, check ranges, flatten
   int nt = 0;
   for (int a = 0; a < na; ++a) {
     const ls_node& n = d.nodes[nl + a];
@@ -962,7 +1077,7 @@ int build_task(const ls_task_desc& d, DTask& T, std::vector<int>& load_t, std::v
       T.expr[a][k].konst = n.idx[k].konst;
       T.expr[a][k].t0 = (int16_t)nt;
       T.expr[a][k].nt = (int16_t)e.size();
-      for (auto& t : e) T.term[nt++] = {(int32_t)t.coef, t.req, t.var};
+      for (auto& t : e) T.term[nt++] = {(int32_t)t.coef, t.req, (int32_t)slot_of[t.var]};
     }
   }
   T.n_terms = nt;
@@ -984,16 +1099,21 @@ int build_task(const ls_task_desc& d, DTask& T, std::vector<int>& load_t, std::v
   }
   T.L = L;
   T.S = S;
-  // remap acc_tensor to merge order index, keeping declaration data
-  std::vector<int> decl_of(order.size());
-  for (size_t i = 0; i < order.size(); ++i) decl_of[i] = order[i];
+  int max_rank = 0;
+  for (int t : order) max_rank = std::max(max_rank, (int)d.tensors[t].rank);
+  const int RM = (T.n_tensors <= 4 && max_rank <= 4) ? 4 : MAXRANK;
+  T.layout_rm = RM;
+  for (int D = 0; D < MAXD; ++D) T.dim_count0[D] = 1;
+  std::vector<int> decl_of(order.begin(), order.end());
   for (int a = 0; a < na; ++a)
     T.acc_tensor[a] = (uint8_t)(std::find(order.begin(), order.end(), (int)T.acc_tensor[a]) - order.begin());
+  int n_stage = 0;
   for (int t = 0; t < T.n_tensors; ++t) {
     const ls_tensor& td = d.tensors[decl_of[t]];
     T.t_rank[t] = (uint8_t)td.rank;
     T.t_eb[t] = (uint8_t)td.elem_bytes;
     T.t_shared[t] = (uint8_t)(td.shared != 0);
+    if (td.shared && d.family == LS_FAMILY_GPU) T.has_shared = 1;
     int64_t stride = 1;
     for (int k = td.rank - 1; k >= 0; --k) {
       T.t_stride[t][k] = stride;
@@ -1014,24 +1134,19 @@ int build_task(const ls_task_desc& d, DTask& T, std::vector<int>& load_t, std::v
       last = a;
     }
     T.t_nu[t] = (uint8_t)nu;
-    // nothing expanded: union of the accesses' constant points (ls/cache.py:80-96)
-    int64_t F = 1;
     for (int k = 0; k < td.rank; ++k) {
+      const int D = t * RM + k;
+      // nothing expanded: union of the accesses' constant points (ls/cache.py:80-96)
       int64_t lo = 0, hi = 0, str = 0, cnt = 1;
       bool exact = true;
       for (int q = 0; q < nu; ++q) {
-        int64_t v = T.expr[T.t_uacc[t][q]][k].konst;
+        const int64_t v = T.expr[T.t_uacc[t][q]][k].konst;
         if (q == 0) {
           lo = hi = v;
-          str = 0;
-          cnt = 1;
-          exact = true;
           continue;
         }
-        // _si_union(acc, point(v))
         if (lo == v && hi == v && str == 0 && cnt == 1 && exact) continue;
-        int64_t nlo = std::min(lo, v), nhi = std::max(hi, v);
-        int64_t g = std::abs(lo - v);
+        const int64_t nlo = std::min(lo, v), nhi = std::max(hi, v);
         auto gcd = [](int64_t a, int64_t b) {
           while (b) {
             int64_t t2 = a % b;
@@ -1040,19 +1155,37 @@ int build_task(const ls_task_desc& d, DTask& T, std::vector<int>& load_t, std::v
           }
           return a;
         };
-        g = gcd(gcd(str, 0), g);
-        int64_t est = g ? (nhi - nlo) / g + 1 : 1;
+        const int64_t g = gcd(str, std::llabs(lo - v));
+        const int64_t est = g ? (nhi - nlo) / g + 1 : 1;
         cnt = std::min(est, cnt + 1);
         lo = nlo;
         hi = nhi;
         str = g;
         exact = false;
       }
-      T.t_count0[t][k] = (int32_t)cnt;
-      F *= cnt;
+      T.dim_count0[D] = (int32_t)cnt;
+      // the dimension's loop variables (any term of any of its accesses)
+      int nv = 0;
+      for (int q = 0; q < nu; ++q) {
+        const DExpr& e = T.expr[T.t_uacc[t][q]][k];
+        for (int z = 0; z < e.nt; ++z) {
+          const int s = T.term[e.t0 + z].slot;
+          bool have = false;
+          for (int j = 0; j < nv; ++j) have |= T.dim_var[D][j] == s;
+          if (have) continue;
+          if (nv >= MAXDV) return fail(LS_E_UNSUPPORTED, "more than 8 loop variables in one tensor dimension");
+          T.dim_var[D][nv] = (uint8_t)s;
+          T.slot_dnib[s][D / 16] |= (uint64_t)(nv + 1) << (4 * (D % 16));
+          ++nv;
+        }
+      }
+      T.dim_nv[D] = (uint8_t)nv;
+      T.dim_base[D] = (uint8_t)n_stage;
+      n_stage += nv;
     }
-    T.t_F0[t] = F;
   }
+  if (n_stage > MAXSTAGE) return fail(LS_E_UNSUPPORTED, "too many (dimension, variable) pairs");
+  T.n_stage = n_stage;
   // ---- arch
   T.family = d.family;
   T.cap = d.cache_capacity;
@@ -1060,13 +1193,13 @@ int build_task(const ls_task_desc& d, DTask& T, std::vector<int>& load_t, std::v
   T.costs_integral = 1;
   for (int q = 0; q < LS_I_COUNT; ++q) {
     T.ptx_cost[q] = d.ptx_cost[q];
-    double c = d.ptx_cost[q];
+    const double c = d.ptx_cost[q];
     if (c != std::floor(c) || std::fabs(c) > 1e12) T.costs_integral = 0;
     T.ptx_icost[q] = (int64_t)c;
   }
   T.sm_underuse = d.sm_underuse;
   T.warp_slack = d.warp_slack;
-  T.tid_var = d.tid_var;
+  T.tid_slot = d.tid_var >= 0 && slot_of[d.tid_var] != NOSLOT ? slot_of[d.tid_var] : -1;
   T.banks = d.banks > 0 ? d.banks : 32;
   T.warp_size = d.warp_size > 0 ? d.warp_size : 32;
   if (T.banks > 64) return fail(LS_E_UNSUPPORTED, "more than 64 banks");
@@ -1118,10 +1251,29 @@ int add_unroll(ls_task* t, const int64_t* us, int n) {
   return upload(t);
 }
 
-int grid_for(const ls_task* t, int64_t n, int threads, int per_sm) {
-  int64_t want = (n + threads - 1) / threads;
-  int64_t cap = (int64_t)t->num_sms * per_sm;
+int grid_for(const ls_task* t, int64_t n, int per_sm) {
+  const int64_t want = (n + TPB - 1) / TPB;
+  const int64_t cap = (int64_t)t->num_sms * std::max(per_sm, 1);
   return (int)std::max<int64_t>(1, std::min(want, cap));
+}
+
+size_t smem_score(const DTask& T) { return align16(sizeof(DTask)) + cand_bytes(T.n_stage); }
+size_t smem_topk(const DTask& T) { return smem_score(T) + align16(sizeof(TopkState)); }
+
+using ScoreFn = void (*)(const DTask*, const ls_record*, int64_t, double*, double*, int32_t*);
+using TopkFn = void (*)(const DTask*, const ls_record*, int64_t, int64_t, int, Key*, unsigned long long*);
+
+ScoreFn score_fn(const DTask& T) { return T.layout_rm == 4 ? score_kernel<4, 4> : score_kernel<MAXT, MAXRANK>; }
+TopkFn topk_fn(const DTask& T) {
+  return T.layout_rm == 4 ? score_topk_kernel<4, 4> : score_topk_kernel<MAXT, MAXRANK>;
+}
+
+template <typename K>
+int blocks_per_sm(K kernel, size_t smem) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int b = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, TPB, smem);
+  return std::max(b, 1);
 }
 
 }  // namespace
@@ -1148,6 +1300,13 @@ int ls_task_create(const ls_task_desc* desc, int device, ls_task** out) {
     return rc;
   }
   cudaDeviceGetAttribute(&t->num_sms, cudaDevAttrMultiProcessorCount, device);
+  {  // keep stream-ordered workspace allocations cached across calls
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
   int64_t one = 1;
   rc = add_unroll(t, &one, 1);
   if (rc) {
@@ -1189,7 +1348,9 @@ int ls_collect_unroll(ls_task* t, const ls_record* d_records, int64_t n, int64_t
   CUDA_TRY(cudaMallocAsync(&set, sizeof(unsigned long long) * slots, s));
   CUDA_TRY(cudaMemsetAsync(set, 0, sizeof(unsigned long long) * slots, s));
   if (n > 0) {
-    collect_unroll_kernel<<<grid_for(t, n, 256, 4), 256, 0, s>>>(t->d_task, d_records, n, set, slots);
+    const size_t sm = smem_score(t->host);
+    collect_unroll_kernel<<<grid_for(t, n, blocks_per_sm(collect_unroll_kernel, sm)), TPB, sm, s>>>(
+        t->d_task, d_records, n, set, slots);
     CUDA_TRY(cudaGetLastError());
   }
   std::vector<unsigned long long> h(slots);
@@ -1210,18 +1371,23 @@ int ls_score(ls_task* t, const ls_record* d_records, int64_t n, double* d_scores
   if (n == 0) return LS_E_OK;
   CUDA_TRY(cudaSetDevice(t->device));
   cudaStream_t s = (cudaStream_t)stream;
-  score_kernel<<<grid_for(t, n, 256, 8), 256, 0, s>>>(t->d_task, d_records, n, d_scores, d_features, d_status);
+  const ScoreFn fn = score_fn(t->host);
+  const size_t sm = smem_score(t->host);
+  fn<<<grid_for(t, n, blocks_per_sm(fn, sm)), TPB, sm, s>>>(t->d_task, d_records, n, d_scores, d_features,
+                                                            d_status);
   CUDA_TRY(cudaGetLastError());
   return LS_E_OK;
 }
 
 static int topk_device(ls_task* t, const ls_record* d_records, int64_t n, int64_t base_index, int32_t k,
                        double* d_top_scores, int64_t* d_top_index, unsigned long long* d_valid, cudaStream_t s) {
-  const int grid = grid_for(t, n, 256, 2);
+  const TopkFn fn = topk_fn(t->host);
+  const size_t sm = smem_topk(t->host);
+  const int grid = grid_for(t, n, blocks_per_sm(fn, sm));
   Key* ws = nullptr;
   CUDA_TRY(cudaMallocAsync(&ws, sizeof(Key) * (size_t)grid * k, s));
   if (n > 0) {
-    score_topk_kernel<<<grid, 256, 0, s>>>(t->d_task, d_records, n, base_index, k, ws, d_valid);
+    fn<<<grid, TPB, sm, s>>>(t->d_task, d_records, n, base_index, k, ws, d_valid);
     CUDA_TRY(cudaGetLastError());
     merge_keys_kernel<<<1, 1024, 0, s>>>(ws, (int64_t)grid * k, k, d_top_scores, d_top_index);
   } else {
