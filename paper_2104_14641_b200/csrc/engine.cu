@@ -95,7 +95,9 @@ struct __align__(16) DTask {
   int32_t L, S;  // loads / stores of the innermost body
   int32_t family, costs_integral, tid_slot, n_u;
   int32_t banks, warp_size, layout_rm, n_stage;
-  int32_t has_shared, pad0;
+  int32_t has_shared, n_slots, n_chain, task_bytes;
+  int32_t has_optional, pad1;
+  uint32_t t_vmask[MAXT];  // slots used by each tensor's terms (valid when !has_optional)
   int64_t cap;
   int64_t c_init, c_latch, c_ret;
   double coef[LS_NFEAT_GPU];
@@ -157,23 +159,25 @@ struct Cand {
 };
 
 __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
-__host__ __device__ constexpr size_t cand_bytes(int n_stage) {
-  return align16(sizeof(int32_t) * NSLOT * TPB) * 2 + align16(sizeof(int32_t) * (size_t)n_stage * TPB) +
-         align16((size_t)NSLOT * TPB) * 2 + align16((size_t)MAXCH * TPB);
+__host__ __device__ constexpr size_t cand_bytes(int n_slots, int n_chain, int n_stage) {
+  return align16(sizeof(int32_t) * (size_t)n_slots * TPB) * 2 + align16(sizeof(int32_t) * (size_t)n_stage * TPB) +
+         align16((size_t)n_slots * TPB) * 2 + align16((size_t)n_chain * TPB);
 }
 
-__device__ __forceinline__ Cand carve(unsigned char* p, int n_stage) {
+// Per-thread arrays sized to the task (slots, chain length, stages) so that
+// more blocks fit per SM.
+__device__ __forceinline__ Cand carve(unsigned char* p, const DTask& T) {
   Cand c;
   c.ext = reinterpret_cast<int32_t*>(p);
-  p += align16(sizeof(int32_t) * NSLOT * TPB);
+  p += align16(sizeof(int32_t) * (size_t)T.n_slots * TPB);
   c.step = reinterpret_cast<int32_t*>(p);
-  p += align16(sizeof(int32_t) * NSLOT * TPB);
+  p += align16(sizeof(int32_t) * (size_t)T.n_slots * TPB);
   c.stage = reinterpret_cast<int32_t*>(p);
-  p += align16(sizeof(int32_t) * (size_t)n_stage * TPB);
+  p += align16(sizeof(int32_t) * (size_t)T.n_stage * TPB);
   c.pos = p;
-  p += align16((size_t)NSLOT * TPB);
+  p += align16((size_t)T.n_slots * TPB);
   c.flg = p;
-  p += align16((size_t)NSLOT * TPB);
+  p += align16((size_t)T.n_slots * TPB);
   c.chain = p;
   return c;
 }
@@ -308,8 +312,7 @@ __device__ __forceinline__ int64_t unroll_lookup(const DTask& T, int64_t U, bool
 __device__ int apply_transforms(const DTask& T, const ls_record& r, Cand& c) {
   c.n = T.n_base;
   c.flags = r.flags;
-#pragma unroll
-  for (int v = 0; v < NSLOT; ++v) c.P(v) = NOSLOT;
+  for (int v = 0; v < T.n_slots; ++v) c.P(v) = NOSLOT;
   for (int p = 0; p < T.n_base; ++p) {
     const int v = T.base_slot[p];
     c.C(p) = (uint8_t)v;
@@ -549,12 +552,16 @@ __device__ int eval_candidate(const DTask& T, const ls_record& r, Cand& c, doubl
       Fb[t] = F;
       dm[t] = T.t_nacc[t];
       reuse |= 1u << t;
-      for (int a = 0; a < T.t_nu[t]; ++a)
+      tmask[t] = T.t_vmask[t];
+      if (T.has_optional) {
+        tmask[t] = 0;
+        for (int a = 0; a < T.t_nu[t]; ++a)
         for (int rr = 0; rr < T.t_rank[t]; ++rr) {
           const DExpr& e = T.expr[T.t_uacc[t][a]][rr];
           for (int q = 0; q < e.nt; ++q)
             if (present(T.term[e.t0 + q], c.flags)) tmask[t] |= 1u << T.term[e.t0 + q].slot;
         }
+      }
     }
   }
   const int64_t cap = T.cap;
@@ -627,7 +634,8 @@ __device__ int eval_candidate(const DTask& T, const ls_record& r, Cand& c, doubl
         sumW += W;
         sumRl += R;
       }
-      ptx_loops += R * (ic[LS_I_INIT] * Wprev + (ic[LS_I_ADD] + ic[LS_I_CMP] + ic[LS_I_BRANCH]) * Wp);
+      if (T.family == LS_FAMILY_GPU)
+        ptx_loops += R * (ic[LS_I_INIT] * Wprev + (ic[LS_I_ADD] + ic[LS_I_CMP] + ic[LS_I_BRANCH]) * Wp);
       Wlast = W;
       Rlast = R;
       Uin = 1;
@@ -701,7 +709,8 @@ __device__ int eval_candidate(const DTask& T, const ls_record& r, Cand& c, doubl
 __device__ __forceinline__ void stage_task(DTask& s, const DTask* __restrict__ g) {
   const int4* src = reinterpret_cast<const int4*>(g);
   int4* dst = reinterpret_cast<int4*>(&s);
-  for (int i = threadIdx.x; i < (int)(sizeof(DTask) / 16); i += blockDim.x) dst[i] = __ldg(&src[i]);
+  const int n16 = __ldg(&g->task_bytes) / 16;  // header + used terms only
+  for (int i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = __ldg(&src[i]);
   __syncthreads();
 }
 
@@ -715,14 +724,14 @@ __device__ __forceinline__ ls_record load_record(const ls_record* __restrict__ r
 }
 
 template <int TM, int RM>
-__global__ void __launch_bounds__(TPB) score_kernel(const DTask* __restrict__ gtask,
+__global__ void __launch_bounds__(TPB, (TM * RM <= 16 ? 3 : 1)) score_kernel(const DTask* __restrict__ gtask,
                                                     const ls_record* __restrict__ recs, int64_t n,
                                                     double* __restrict__ scores, double* __restrict__ feats,
                                                     int32_t* __restrict__ status) {
   extern __shared__ __align__(16) unsigned char dyn[];
   DTask& T = *reinterpret_cast<DTask*>(dyn);
   stage_task(T, gtask);
-  Cand c = carve(dyn + align16(sizeof(DTask)), T.n_stage);
+  Cand c = carve(dyn + T.task_bytes, T);
   const int nf = T.family == LS_FAMILY_CPU ? LS_NFEAT_CPU : LS_NFEAT_GPU;
   for (int64_t i = (int64_t)blockIdx.x * TPB + threadIdx.x; i < n; i += (int64_t)gridDim.x * TPB) {
     const ls_record r = load_record(recs, i);
@@ -757,18 +766,19 @@ __device__ __forceinline__ double from_order_bits(unsigned long long o) {
   return __longlong_as_double((long long)b);
 }
 
-constexpr int TK_BUF = 2048;
 constexpr int TK_MAXK = 1024;
 
+template <int BUF>
 struct TopkState {
-  Key buf[TK_BUF];
+  Key buf[BUF];
   Key thr;
   int cnt;
 };
 
 // Sort buf[0..cnt) (padded with +inf) and keep the k smallest; returns the kept count.
-__device__ int topk_compact(TopkState& S, int k, int cnt) {
-  for (int i = cnt + threadIdx.x; i < TK_BUF; i += blockDim.x) {
+template <int BUF>
+__device__ int topk_compact(TopkState<BUF>& S, int k, int cnt) {
+  for (int i = cnt + threadIdx.x; i < BUF; i += blockDim.x) {
     S.buf[i].s = KEY_INF_S;
     S.buf[i].i = KEY_INF_I;
   }
@@ -799,7 +809,8 @@ __device__ int topk_compact(TopkState& S, int k, int cnt) {
   return keep;
 }
 
-__device__ __forceinline__ void topk_init(TopkState& S) {
+template <int BUF>
+__device__ __forceinline__ void topk_init(TopkState<BUF>& S) {
   if (threadIdx.x == 0) {
     S.cnt = 0;
     S.thr.s = KEY_INF_S;
@@ -810,7 +821,8 @@ __device__ __forceinline__ void topk_init(TopkState& S) {
 
 // Insert-if-better without a barrier; the block synchronises only when the
 // buffer could overflow within the next round (`safe` rounds are free).
-__device__ __forceinline__ void topk_offer(TopkState& S, bool has, const Key& key, int k, int& safe) {
+template <int BUF>
+__device__ __forceinline__ void topk_offer(TopkState<BUF>& S, bool has, const Key& key, int k, int& safe) {
   if (has && kless(key, S.thr)) {
     const int slot = atomicAdd(&S.cnt, 1);
     S.buf[slot] = key;
@@ -819,20 +831,20 @@ __device__ __forceinline__ void topk_offer(TopkState& S, bool has, const Key& ke
   __syncthreads();
   int c = S.cnt;
   __syncthreads();
-  if (c > TK_BUF - (int)blockDim.x) c = topk_compact(S, k, c);
-  safe = (TK_BUF - c) / (int)blockDim.x;
+  if (c > BUF - (int)blockDim.x) c = topk_compact(S, k, c);
+  safe = (BUF - c) / (int)blockDim.x;
 }
 
-template <int TM, int RM>
-__global__ void __launch_bounds__(TPB) score_topk_kernel(const DTask* __restrict__ gtask,
+template <int TM, int RM, int BUF>
+__global__ void __launch_bounds__(TPB, (TM * RM <= 16 ? 3 : 1)) score_topk_kernel(const DTask* __restrict__ gtask,
                                                          const ls_record* __restrict__ recs, int64_t n,
                                                          int64_t base_index, int k, Key* __restrict__ block_out,
                                                          unsigned long long* __restrict__ n_valid) {
   extern __shared__ __align__(16) unsigned char dyn[];
   DTask& T = *reinterpret_cast<DTask*>(dyn);
   stage_task(T, gtask);
-  TopkState& S = *reinterpret_cast<TopkState*>(dyn + align16(sizeof(DTask)));
-  Cand c = carve(dyn + align16(sizeof(DTask)) + align16(sizeof(TopkState)), T.n_stage);
+  TopkState<BUF>& S = *reinterpret_cast<TopkState<BUF>*>(dyn + T.task_bytes);
+  Cand c = carve(dyn + T.task_bytes + align16(sizeof(TopkState<BUF>)), T);
   topk_init(S);
   unsigned int valid = 0;
   int safe = 1;
@@ -873,7 +885,7 @@ __global__ void __launch_bounds__(TPB) score_topk_kernel(const DTask* __restrict
 __global__ void __launch_bounds__(1024) merge_keys_kernel(const Key* __restrict__ in, int64_t m, int k,
                                                           double* __restrict__ out_s,
                                                           int64_t* __restrict__ out_i) {
-  __shared__ TopkState S;
+  __shared__ TopkState<2048> S;
   topk_init(S);
   int safe = 1;
   for (int64_t base = 0; base < m; base += blockDim.x) {
@@ -922,7 +934,7 @@ __global__ void __launch_bounds__(TPB) collect_unroll_kernel(const DTask* __rest
   extern __shared__ __align__(16) unsigned char dyn[];
   DTask& T = *reinterpret_cast<DTask*>(dyn);
   stage_task(T, gtask);
-  Cand c = carve(dyn + align16(sizeof(DTask)), T.n_stage);
+  Cand c = carve(dyn + T.task_bytes, T);
   for (int64_t i = (int64_t)blockIdx.x * TPB + threadIdx.x; i < n; i += (int64_t)gridDim.x * TPB) {
     const ls_record r = load_record(recs, i);
     if (apply_transforms(T, r, c)) continue;
@@ -1186,6 +1198,14 @@ int build_task(const ls_task_desc& d, DTask& T, std::vector<int>& load_t, std::v
   }
   if (n_stage > MAXSTAGE) return fail(LS_E_UNSUPPORTED, "too many (dimension, variable) pairs");
   T.n_stage = n_stage;
+  T.n_slots = ns;
+  for (int q = 0; q < nt; ++q) T.has_optional |= T.term[q].req != 0;
+  for (int a = 0; a < na; ++a)
+    for (int k = 0; k < T.t_rank[T.acc_tensor[a]]; ++k)
+      for (int z = 0; z < T.expr[a][k].nt; ++z)
+        T.t_vmask[T.acc_tensor[a]] |= 1u << T.term[T.expr[a][k].t0 + z].slot;
+  T.n_chain = std::min(MAXCH, nl + ntile);
+  T.task_bytes = (int32_t)align16(offsetof(DTask, term) + sizeof(DTerm) * (size_t)nt);
   // ---- arch
   T.family = d.family;
   T.cap = d.cache_capacity;
@@ -1257,15 +1277,21 @@ int grid_for(const ls_task* t, int64_t n, int per_sm) {
   return (int)std::max<int64_t>(1, std::min(want, cap));
 }
 
-size_t smem_score(const DTask& T) { return align16(sizeof(DTask)) + cand_bytes(T.n_stage); }
-size_t smem_topk(const DTask& T) { return smem_score(T) + align16(sizeof(TopkState)); }
+size_t smem_score(const DTask& T) { return (size_t)T.task_bytes + cand_bytes(T.n_slots, T.n_chain, T.n_stage); }
+// the fused kernel's buffer must hold k plus one round of inserts
+int topk_buf(int k) { return k <= 1024 - TPB ? 1024 : 2048; }
+size_t smem_topk(const DTask& T, int k) {
+  return smem_score(T) + (topk_buf(k) == 1024 ? align16(sizeof(TopkState<1024>)) : align16(sizeof(TopkState<2048>)));
+}
 
 using ScoreFn = void (*)(const DTask*, const ls_record*, int64_t, double*, double*, int32_t*);
 using TopkFn = void (*)(const DTask*, const ls_record*, int64_t, int64_t, int, Key*, unsigned long long*);
 
 ScoreFn score_fn(const DTask& T) { return T.layout_rm == 4 ? score_kernel<4, 4> : score_kernel<MAXT, MAXRANK>; }
-TopkFn topk_fn(const DTask& T) {
-  return T.layout_rm == 4 ? score_topk_kernel<4, 4> : score_topk_kernel<MAXT, MAXRANK>;
+TopkFn topk_fn(const DTask& T, int k) {
+  if (topk_buf(k) == 1024)
+    return T.layout_rm == 4 ? score_topk_kernel<4, 4, 1024> : score_topk_kernel<MAXT, MAXRANK, 1024>;
+  return T.layout_rm == 4 ? score_topk_kernel<4, 4, 2048> : score_topk_kernel<MAXT, MAXRANK, 2048>;
 }
 
 template <typename K>
@@ -1381,8 +1407,8 @@ int ls_score(ls_task* t, const ls_record* d_records, int64_t n, double* d_scores
 
 static int topk_device(ls_task* t, const ls_record* d_records, int64_t n, int64_t base_index, int32_t k,
                        double* d_top_scores, int64_t* d_top_index, unsigned long long* d_valid, cudaStream_t s) {
-  const TopkFn fn = topk_fn(t->host);
-  const size_t sm = smem_topk(t->host);
+  const TopkFn fn = topk_fn(t->host, k);
+  const size_t sm = smem_topk(t->host, k);
   const int grid = grid_for(t, n, blocks_per_sm(fn, sm));
   Key* ws = nullptr;
   CUDA_TRY(cudaMallocAsync(&ws, sizeof(Key) * (size_t)grid * k, s));
@@ -1441,7 +1467,7 @@ int ls_score_topk_host(ls_task* t, const ls_record* h_records, int64_t n, int64_
   if (k < 1 || k > TK_MAXK) return fail(LS_E_ARG, "k must be in 1..1024");
   CUDA_TRY(cudaSetDevice(t->device));
   cudaStream_t s = (cudaStream_t)stream;
-  const int64_t CH = 1 << 20;  // records per chunk (32 MiB)
+  const int64_t CH = 1 << 18;  // records per chunk (8 MiB): copy of chunk c+1 overlaps scoring of chunk c
   const int64_t nch = std::max<int64_t>(1, (n + CH - 1) / CH);
   cudaStream_t cp;
   CUDA_TRY(cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking));
