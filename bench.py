@@ -313,13 +313,13 @@ def b200_arm(args):
                     "topk_equals_device_path": same_host and hi.tolist() == top_i.tolist() if world == 1 else None},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "score_topk_kernel + merge_keys_kernel (one ls_score_topk call)",
+                         "kernel": "score_topk_kernel (fused score + block top-k + in-kernel merge tree; one ls_score_topk call)",
                          "kernel_ms": kavg * 1e3, "algorithmic_bytes_per_launch": alg_bytes,
                          "note": "integer-ALU bound by design: ~32 B read per candidate vs thousands of "
                                  "integer ops; see profiles/ for issue-slot utilisation"},
             "cpu_baseline": cpu, "parity": parity,
             "clocks": clk.summary(),
-            "gpu_launches": args.steps * (2 + (2 if world > 1 else 0)),
+            "gpu_launches": args.steps * (1 + (2 if world > 1 else 0)),
             "n_valid_per_gpu": n_valid,
         }
         print(json.dumps(line), flush=True)

@@ -835,12 +835,59 @@ __device__ __forceinline__ void topk_offer(TopkState<BUF>& S, bool has, const Ke
   safe = (BUF - c) / (int)blockDim.x;
 }
 
+constexpr int TK_GROUP = 16;  // blocks per first-level merge group
+
+__device__ __forceinline__ Key ld_key_cg(const Key* p) {
+  Key k;
+  k.s = __ldcg(reinterpret_cast<const unsigned long long*>(p));
+  k.i = __ldcg(reinterpret_cast<const long long*>(p) + 1);
+  return k;
+}
+
+// Merge m keys from global memory into the block's buffer (streamed, k kept).
+template <int BUF>
+__device__ int merge_into(TopkState<BUF>& S, const Key* src, int64_t m, int k) {
+  topk_init(S);
+  int safe = 1;
+  for (int64_t base = 0; base < m; base += blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    bool has = false;
+    Key key;
+    if (i < m) {
+      key = ld_key_cg(src + i);
+      has = !(key.s == KEY_INF_S && key.i == KEY_INF_I);
+    }
+    topk_offer(S, has, key, k, safe);
+  }
+  __syncthreads();
+  return topk_compact(S, k, S.cnt);
+}
+
+template <int BUF>
+__device__ void write_keys(const TopkState<BUF>& S, int kept, int k, Key* out) {
+  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    Key o;
+    if (j < kept) {
+      o = S.buf[j];
+    } else {
+      o.s = KEY_INF_S;
+      o.i = KEY_INF_I;
+    }
+    out[j] = o;
+  }
+}
+
+// Fused pass: score every record, keep the block's k best, then merge the
+// block lists in a two-level tree inside the same launch: the last block of
+// each group of TK_GROUP merges its group, the last group merger writes the
+// final k (threadfence + ticket counters; no second kernel).
 template <int TM, int RM, int BUF>
-__global__ void __launch_bounds__(TPB, (TM * RM <= 16 ? 3 : 1)) score_topk_kernel(const DTask* __restrict__ gtask,
-                                                         const ls_record* __restrict__ recs, int64_t n,
-                                                         int64_t base_index, int k, Key* __restrict__ block_out,
-                                                         unsigned long long* __restrict__ n_valid) {
+__global__ void __launch_bounds__(TPB, (TM * RM <= 16 ? 3 : 1)) score_topk_kernel(
+    const DTask* __restrict__ gtask, const ls_record* __restrict__ recs, int64_t n, int64_t base_index, int k,
+    Key* __restrict__ block_out, Key* __restrict__ group_out, unsigned int* __restrict__ tickets,
+    double* __restrict__ out_s, int64_t* __restrict__ out_i, unsigned long long* __restrict__ n_valid) {
   extern __shared__ __align__(16) unsigned char dyn[];
+  __shared__ unsigned int s_ticket;
   DTask& T = *reinterpret_cast<DTask*>(dyn);
   stage_task(T, gtask);
   TopkState<BUF>& S = *reinterpret_cast<TopkState<BUF>*>(dyn + T.task_bytes);
@@ -865,20 +912,40 @@ __global__ void __launch_bounds__(TPB, (TM * RM <= 16 ? 3 : 1)) score_topk_kerne
     }
     topk_offer(S, has, key, k, safe);
   }
-  __syncthreads();
-  const int kept = topk_compact(S, k, S.cnt);
-  for (int j = threadIdx.x; j < k; j += blockDim.x) {
-    Key o;
-    if (j < kept) {
-      o = S.buf[j];
-    } else {
-      o.s = KEY_INF_S;
-      o.i = KEY_INF_I;
-    }
-    block_out[(int64_t)blockIdx.x * k + j] = o;
-  }
   for (int off = 16; off > 0; off >>= 1) valid += __shfl_down_sync(0xffffffffu, valid, off);
   if ((threadIdx.x & 31) == 0 && valid) atomicAdd(n_valid, (unsigned long long)valid);
+  __syncthreads();
+  write_keys(S, topk_compact(S, k, S.cnt), k, block_out + (int64_t)blockIdx.x * k);
+
+  // ---- level 1: last block of the group merges the group's lists
+  const int g = blockIdx.x / TK_GROUP;
+  const int ngroups = (gridDim.x + TK_GROUP - 1) / TK_GROUP;
+  const int gsize = min(TK_GROUP, (int)gridDim.x - g * TK_GROUP);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_ticket = atomicAdd(&tickets[g], 1u);
+  __syncthreads();
+  if (s_ticket != (unsigned)(gsize - 1)) return;
+  __threadfence();
+  int kept = merge_into(S, block_out + (int64_t)g * TK_GROUP * k, (int64_t)gsize * k, k);
+  write_keys(S, kept, k, group_out + (int64_t)g * k);
+  // ---- level 2: last group merger writes the final list
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_ticket = atomicAdd(&tickets[ngroups], 1u);
+  __syncthreads();
+  if (s_ticket != (unsigned)(ngroups - 1)) return;
+  __threadfence();
+  kept = merge_into(S, group_out, (int64_t)ngroups * k, k);
+  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    if (j < kept) {
+      out_s[j] = from_order_bits(S.buf[j].s);
+      out_i[j] = S.buf[j].i;
+    } else {
+      out_s[j] = __longlong_as_double(0x7ff0000000000000ll);
+      out_i[j] = -1;
+    }
+  }
 }
 
 // Merge m keys (any order, +inf padded) into the k best, written as (score, index).
@@ -1285,7 +1352,8 @@ size_t smem_topk(const DTask& T, int k) {
 }
 
 using ScoreFn = void (*)(const DTask*, const ls_record*, int64_t, double*, double*, int32_t*);
-using TopkFn = void (*)(const DTask*, const ls_record*, int64_t, int64_t, int, Key*, unsigned long long*);
+using TopkFn = void (*)(const DTask*, const ls_record*, int64_t, int64_t, int, Key*, Key*, unsigned int*, double*,
+                       int64_t*, unsigned long long*);
 
 ScoreFn score_fn(const DTask& T) { return T.layout_rm == 4 ? score_kernel<4, 4> : score_kernel<MAXT, MAXRANK>; }
 TopkFn topk_fn(const DTask& T, int k) {
@@ -1409,16 +1477,18 @@ static int topk_device(ls_task* t, const ls_record* d_records, int64_t n, int64_
                        double* d_top_scores, int64_t* d_top_index, unsigned long long* d_valid, cudaStream_t s) {
   const TopkFn fn = topk_fn(t->host, k);
   const size_t sm = smem_topk(t->host, k);
-  const int grid = grid_for(t, n, blocks_per_sm(fn, sm));
-  Key* ws = nullptr;
-  CUDA_TRY(cudaMallocAsync(&ws, sizeof(Key) * (size_t)grid * k, s));
-  if (n > 0) {
-    fn<<<grid, TPB, sm, s>>>(t->d_task, d_records, n, base_index, k, ws, d_valid);
-    CUDA_TRY(cudaGetLastError());
-    merge_keys_kernel<<<1, 1024, 0, s>>>(ws, (int64_t)grid * k, k, d_top_scores, d_top_index);
-  } else {
-    merge_keys_kernel<<<1, 1024, 0, s>>>(ws, 0, k, d_top_scores, d_top_index);
-  }
+  const int grid = n > 0 ? grid_for(t, n, blocks_per_sm(fn, sm)) : 1;
+  const int ngroups = (grid + TK_GROUP - 1) / TK_GROUP;
+  const size_t ws_keys = sizeof(Key) * ((size_t)grid + ngroups) * k;
+  const size_t ws_bytes = ws_keys + align16(sizeof(unsigned int) * (ngroups + 1));
+  unsigned char* ws = nullptr;
+  CUDA_TRY(cudaMallocAsync(&ws, ws_bytes, s));
+  Key* block_out = reinterpret_cast<Key*>(ws);
+  Key* group_out = block_out + (size_t)grid * k;
+  unsigned int* tickets = reinterpret_cast<unsigned int*>(ws + ws_keys);
+  CUDA_TRY(cudaMemsetAsync(tickets, 0, sizeof(unsigned int) * (ngroups + 1), s));
+  fn<<<grid, TPB, sm, s>>>(t->d_task, d_records, n, base_index, k, block_out, group_out, tickets, d_top_scores,
+                           d_top_index, d_valid);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaFreeAsync(ws, s));
   return LS_E_OK;
