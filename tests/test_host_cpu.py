@@ -120,3 +120,27 @@ def test_gloo_two_rank_topk_merge():
     for p in ps:
         p.join(60)
     assert res == {0: True, 1: True}
+
+
+REF = Path("/root/reference/pkg/src")
+
+
+@pytest.mark.skipif(not REF.exists(), reason="reference tree only in the build container")
+def test_reference_objects_pack_identically():
+    """The drop-in: the reference's own objects pack to the same descriptor and records."""
+    import json
+    sys.path.insert(0, str(REF))
+    import loopscout as L
+    from paper_2104_14641_b200 import arch as A, ir, workloads as W
+    from paper_2104_14641_b200.pack import pack_schedules
+    spec = W.conv2d_json(1, 8, 6, 6, 4, 3, 3)
+    sched = [{"tile": {"loop": "oc", "factor": 4}}, {"tile": {"loop": "ow", "factor": 3}},
+             {"reorder": ["n", "oc", "kw", "ic", "ow", "kh", "ow_i", "oh", "oc_i"]},
+             {"vectorize": {"loop": "ic", "width": 4}}, {"unroll": {"loop": "kw"}}]
+    for name in ("x86-avx2", "nvidia-volta"):
+        mine = pack_schedules(ir.parse_program(json.dumps(spec)), [ir.Schedule.from_json(sched)])[0]
+        theirs = pack_schedules(L.parse_program(json.dumps(spec)), [L.Schedule.from_json(sched)])[0]
+        d1 = mine.template.desc(A.load_arch(name), A.KernelLaunch.from_json(W.KERNEL_LAUNCH))
+        d2 = theirs.template.desc(L.load_arch(name), L.KernelLaunch.from_json(W.KERNEL_LAUNCH))
+        assert bytes(d1) == bytes(d2)
+        assert mine.records.tobytes() == theirs.records.tobytes()
