@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--k", type=int, default=64)
     ap.add_argument("--arch", default="x86-avx2")
     ap.add_argument("--no-baseline", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--path", type=int, default=0, help="0 auto, 1 generic kernel, 2 tabulated kernel")
     return ap.parse_args()
 
 
@@ -197,6 +198,8 @@ def b200_arm(args):
     n, k = args.n, args.k
     st, desc = workload(args.arch)
     task = Task(desc, dev)
+    if args.path:
+        task.set_path(args.path)
     recs = records_for(st, rank * n, n)
     d_rec = to_device_records(recs, dev)
     base = rank * n

@@ -47,6 +47,7 @@ extern "C" {
 #define LS_MAX_CHAIN 16    /* loops in a transformed perfect chain            */
 #define LS_NFEAT_CPU 5     /* CPU_FEATURES, ls/cost.py:24                     */
 #define LS_NFEAT_GPU 7     /* GPU_FEATURES, ls/cost.py:25-26                  */
+#define LS_MAX_AXES 16     /* axes of an attached schedule space              */
 
 /* ---- enums ---- */
 enum { LS_FAMILY_CPU = 0, LS_FAMILY_GPU = 1 };                  /* ArchSpec.family */
@@ -74,6 +75,13 @@ enum {
   LS_I_COUNT = 8
 };
 
+/* ---- scoring paths (ls_task_set_path) ---- */
+enum {
+  LS_PATH_AUTO = 0,      /* tabulated when the task is eligible, else generic            */
+  LS_PATH_GENERIC = 1,   /* per-candidate strided-interval folds (every perfect chain)   */
+  LS_PATH_TABULATED = 2  /* dimension counts looked up in a per-task table */
+};
+
 /* ---- error codes (return values) ---- */
 enum {
   LS_E_OK = 0,
@@ -95,7 +103,8 @@ enum {
   LS_ST_BAD_FEATURE = 7,     /* CostModelError non-finite/negative ls/cost.py:43-45  */
   LS_ST_UNSUPPORTED = 16,    /* transformed tree outside the device class            */
   LS_ST_UNROLL_TABLE = 17,   /* unroll product not prepared (ls_task_prepare_unroll) */
-  LS_ST_OVERFLOW = 18        /* intermediate exceeded the device integer range       */
+  LS_ST_OVERFLOW = 18,       /* intermediate exceeded the device integer range       */
+  LS_ST_POINT_RANGE = 19     /* space point outside the attached space (points API)  */
 };
 
 /* ---- task descriptor: the per-task parameter table ---- */
@@ -171,6 +180,26 @@ typedef struct {
   uint32_t tag;                  /* reserved, must be 0 */
 } ls_record;
 
+/* ---- schedule space (space_axes, ls/ir.py:517-547) for the points API ---- */
+enum {
+  LS_AX_PARAM = 0, /* tile axis: values[c] -> ls_record.param[param]                       */
+  LS_AX_PERM = 1,  /* reorder axis: values[c] OR-ed into ls_record.perm (already shifted)   */
+  LS_AX_VEC = 2,   /* vectorize axis: values[c] -> param[param]; flags bit set iff != 0     */
+  LS_AX_BIT = 3    /* unroll/parallel on-off axis: choice index c -> flags bit              */
+};
+typedef struct {
+  int32_t kind;           /* LS_AX_* */
+  int32_t param;          /* PARAM/VEC: record param slot */
+  int32_t bit;            /* VEC/BIT: enable bit */
+  int32_t n_choices;      /* >= 1 */
+  const uint64_t* values; /* host array of n_choices values (unused for BIT) */
+} ls_axis;
+
+typedef struct {
+  int32_t n_axes;
+  ls_axis axes[LS_MAX_AXES];
+} ls_space_desc;
+
 typedef struct ls_task ls_task;
 
 /* ---- entry points ---- */
@@ -184,6 +213,13 @@ int ls_abi_version(void);
 int ls_task_create(const ls_task_desc* desc, int device, ls_task** out);
 int ls_task_destroy(ls_task* task);
 int ls_task_num_features(const ls_task* task);
+/* Select the scoring path (LS_PATH_*); both give bit-identical results, the
+ * tabulated one is the fast path.  LS_E_UNSUPPORTED if the task is not
+ * eligible for LS_PATH_TABULATED.  Not thread-safe against concurrent scoring
+ * calls on the same task. */
+int ls_task_set_path(ls_task* task, int32_t path);
+/* The path scoring calls will take: LS_PATH_GENERIC or LS_PATH_TABULATED. */
+int ls_task_path(const ls_task* task);
 /* Precompute block-cycle entries for innermost-unroll products `u_values`
  * (candidates needing an unprepared product report LS_ST_UNROLL_TABLE). */
 int ls_task_prepare_unroll(ls_task* task, const int64_t* u_values, int32_t n);
@@ -223,6 +259,28 @@ int ls_topk_merge(const double* d_scores, const int64_t* d_index, int32_t n_list
 int ls_score_topk_host(ls_task* task, const ls_record* h_records, int64_t n, int64_t base_index,
                        int32_t k, double* h_top_scores, int64_t* h_top_index, int64_t* h_n_valid,
                        void* stream);
+
+/* ---- points API: candidates as space points ----
+ * A point is the mixed-radix number of a candidate's per-axis choice indices,
+ * axis 0 most significant: the flat index of the choices ThetaEncoding.decode
+ * picks (ls/es.py:57-62) over space_axes (ls/ir.py:517-547).  Points are 4- or
+ * 8-byte unsigned integers (point_bytes); a 4-byte point is an 8x smaller
+ * candidate than an ls_record.  Results are identical to scoring the records
+ * the points decode to. */
+
+/* Attach the task's schedule space (copied; replaces a previous one). */
+int ls_task_set_space(ls_task* task, const ls_space_desc* space);
+/* ls_score over points. */
+int ls_score_points(ls_task* task, const void* d_points, int32_t point_bytes, int64_t n, double* d_scores,
+                    double* d_features, int32_t* d_status, void* stream);
+/* ls_score_topk over points. */
+int ls_score_topk_points(ls_task* task, const void* d_points, int32_t point_bytes, int64_t n,
+                         int64_t base_index, int32_t k, double* d_top_scores, int64_t* d_top_index,
+                         int64_t* d_n_valid, void* stream);
+/* ls_score_topk_host over host points (H2D staged and overlapped). */
+int ls_score_topk_points_host(ls_task* task, const void* h_points, int32_t point_bytes, int64_t n,
+                              int64_t base_index, int32_t k, double* h_top_scores, int64_t* h_top_index,
+                              int64_t* h_n_valid, void* stream);
 
 #ifdef __cplusplus
 }

@@ -10,6 +10,8 @@ ABI_VERSION = 1
 MAX_TENSORS, MAX_RANK, MAX_TERMS, MAX_NODES = 8, 6, 8, 64
 MAX_VARS, MAX_XFORMS, MAX_PARAMS, MAX_ORDER, MAX_CHAIN = 32, 32, 8, 16, 16
 NFEAT_CPU, NFEAT_GPU = 5, 7
+MAX_AXES = 16
+AX_PARAM, AX_PERM, AX_VEC, AX_BIT = range(4)
 
 FAMILY = {"cpu": 0, "gpu": 1}
 TARGET = {"cpu-x86": 0, "cpu-aarch64": 1, "gpu-ptx": 2}
@@ -30,6 +32,7 @@ STATUS = {
     16: "unsupported transformed structure",
     17: "unroll product not prepared",
     18: "integer range exceeded",
+    19: "space point outside the space",
 }
 ST_OK, ST_UNSUPPORTED = 0, 16
 
@@ -76,3 +79,12 @@ class TaskDesc(C.Structure):
 RECORD_DTYPE = np.dtype([("param", "<u2", (MAX_PARAMS,)), ("perm", "<u8"), ("flags", "<u4"),
                          ("tag", "<u4")], align=True)
 assert RECORD_DTYPE.itemsize == 32
+
+
+class Axis(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("param", C.c_int32), ("bit", C.c_int32), ("n_choices", C.c_int32),
+                ("values", C.POINTER(C.c_uint64))]
+
+
+class SpaceDesc(C.Structure):
+    _fields_ = [("n_axes", C.c_int32), ("axes", Axis * MAX_AXES)]

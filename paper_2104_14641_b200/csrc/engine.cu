@@ -90,6 +90,13 @@ struct DUnroll {
 // loop flags in the per-candidate state
 constexpr uint8_t F_PAR = 1, F_UNR = 2, F_VEC = 4;
 
+// one axis of an attached schedule space (points API)
+struct DAxis {
+  int8_t kind, param, bit, pad;
+  uint32_t n, voff, pad2;
+  uint64_t magic;  // floor(2^64 / n) + 1: q = umulhi(x, magic) == x / n for x < 2^32, n >= 2
+};
+
 struct __align__(16) DTask {
   int32_t n_base, n_xf, n_acc, n_tensors;
   int32_t L, S;  // loads / stores of the innermost body
@@ -120,6 +127,25 @@ struct __align__(16) DTask {
   uint8_t dim_var[MAXD][MAXDV];
   int32_t dim_count0[MAXD];
   uint64_t slot_dnib[NSLOT][3];  // nibble D of slot s: 1 + index of s in dim D's variable list
+  // ---- tabulated path: every dimension count is a table lookup
+  int32_t fast;      // 1: the task is eligible (4x4 layout, every dimension tabulated)
+  int32_t tab_smem;  // the table is staged into shared memory
+  int32_t tab_len;   // int32 entries
+  int32_t pad3;
+  const int32_t* tab;                  // device table: [dimension][key][expanded-variable mask]
+  uint64_t chain0;                     // base chain, one slot per nibble
+  uint32_t base_exist, base_unr, base_vec, base_par;  // slot masks of the base chain
+  uint64_t vbits[NSLOT];               // bit dim_base[D] + x for every (D, x) with dim_var[D][x] == slot
+  int32_t ftab_off[16], ftab_len[16];  // per dimension slot of the 4x4 layout
+  uint32_t fsel[16];                   // (dim_base[D]) | (((1 << dim_nv[D]) - 1) << 8)
+  int8_t fk_n[16], fk_src[16][3];      // key digits: 0..7 record param, 8 + b enable bit b
+  int32_t fk_rad[16][3];
+  int32_t fk_bound[LS_MAX_PARAMS];     // largest valid value of each record param
+  int32_t tab_one, pad4;               // entry holding 1 (dimension slots the layout leaves unused)
+  // ---- attached schedule space (points API)
+  int32_t sp_n, pad5;
+  const uint64_t* sp_vals;
+  DAxis sp_ax[LS_MAX_AXES];
   int32_t n_terms;
   DTerm term[MAXTERM];
 };
@@ -134,7 +160,8 @@ struct ls_task {
   std::vector<int> load_t, store_t;
   std::mutex mu;
   int num_sms;
-  size_t smem_score, smem_topk;
+  int path;            // LS_PATH_AUTO / LS_PATH_GENERIC / LS_PATH_TABULATED
+  int32_t* d_tab;      // tabulated path's dimension-count table (owned)
 };
 
 // ---------------------------------------------------------------------------
@@ -156,6 +183,22 @@ struct Cand {
   __device__ __forceinline__ uint8_t& P(int v) { return pos[v * TPB + threadIdx.x]; }
   __device__ __forceinline__ uint8_t& Fl(int v) { return flg[v * TPB + threadIdx.x]; }
   __device__ __forceinline__ uint8_t& C(int p) { return chain[p * TPB + threadIdx.x]; }
+};
+
+// Candidate state of the tabulated path: the chain is a register (one slot
+// per nibble), loop flags are slot masks, only the extents stay in shared
+// memory (they are indexed by a data-dependent slot).
+struct FastCand {
+  int32_t* ext;  // [NSLOT][TPB]
+  uint64_t chain;
+  uint32_t unr, vec, par, exist;
+  int n;
+  uint32_t flags;
+  __device__ __forceinline__ int32_t& E(int v) { return ext[v * TPB + threadIdx.x]; }
+  __device__ __forceinline__ int C(int p) const { return (int)((chain >> (4 * p)) & 15u); }
+  __device__ __forceinline__ uint8_t Fl(int v) const {
+    return (uint8_t)((((par >> v) & 1u) ? 1 : 0) | (((unr >> v) & 1u) ? 2 : 0) | (((vec >> v) & 1u) ? 4 : 0));
+  }
 };
 
 __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -395,11 +438,115 @@ __device__ int apply_transforms(const DTask& T, const ls_record& r, Cand& c) {
   return LS_OK;
 }
 
+// record parameter p without a dynamically indexed (local-memory) array
+__device__ __forceinline__ uint32_t rparam(const ls_record& r, int p) {
+  uint64_t lo, hi;
+  memcpy(&lo, &r.param[0], 8);
+  memcpy(&hi, &r.param[4], 8);
+  return (uint32_t)(((p < 4 ? lo : hi) >> (16 * (p & 3))) & 0xFFFFu);
+}
+
+// position of slot v in a nibble-packed chain (v must be on the chain): the
+// lowest zero nibble of chain ^ v is exact (borrows only flag higher nibbles)
+__device__ __forceinline__ int chain_find(uint64_t chain, int v) {
+  const uint64_t x = chain ^ (0x1111111111111111ull * (uint64_t)v);
+  const uint64_t z = (x - 0x1111111111111111ull) & ~x & 0x8888888888888888ull;
+  return (__ffsll((long long)z) - 1) >> 2;
+}
+
+// apply_transforms on the register chain (tabulated path).  Same checks in
+// the same order as apply_transforms, hence the same status codes.
+__device__ int apply_fast(const DTask& T, const ls_record& r, FastCand& c) {
+  c.n = T.n_base;
+  c.flags = r.flags;
+  c.chain = T.chain0;
+  c.exist = T.base_exist;
+  c.unr = T.base_unr;
+  c.vec = T.base_vec;
+  c.par = T.base_par;
+  for (int p = 0; p < T.n_base; ++p) c.E(T.base_slot[p]) = T.base_ext[p];
+  for (int x = 0; x < T.n_xf; ++x) {
+    const DXform& xf = T.xf[x];
+    if (xf.enable_bit >= 0 && !((r.flags >> xf.enable_bit) & 1u)) continue;
+    const int v = xf.slot;
+    const bool exists = v != NOSLOT && ((c.exist >> v) & 1u);
+    switch (xf.kind) {
+      case LS_XF_TILE:
+      case LS_XF_VECTORIZE: {
+        if (!exists || xf.new_slot == NOSLOT) return LS_ST_NO_LOOP;
+        const int32_t F = xf.param >= 0 ? (int32_t)rparam(r, xf.param) : xf.value;
+        const int32_t Ev = c.E(v);
+        if (xf.kind == LS_XF_VECTORIZE) {
+          if (F == 0) return LS_ST_VEC_ZERO;
+          if (Ev % F != 0) return LS_ST_VEC_DIVIDE;
+        }
+        if (F < 1 || F > Ev) return LS_ST_TILE_RANGE;
+        if (c.n >= MAXCH) return LS_ST_OVERFLOW;
+        const int u = xf.new_slot;
+        const int q = chain_find(c.chain, v) + 1;  // q <= 15
+        const uint64_t low = (1ull << (4 * q)) - 1;
+        c.chain = (c.chain & low) | ((uint64_t)u << (4 * q)) | ((c.chain & ~low) << 4);
+        c.n++;
+        c.exist |= 1u << u;
+        c.E(u) = F;
+        c.E(v) = (Ev + F - 1) / F;
+        c.unr &= ~(1u << u);
+        c.par &= ~(1u << u);
+        c.vec = (c.vec & ~((1u << u) | (1u << v))) | (xf.kind == LS_XF_VECTORIZE ? (1u << u) : 0u);
+        break;
+      }
+      case LS_XF_REORDER: {
+        const int m = xf.n_order;
+        if (m < 2) break;
+        uint64_t seg = 0;
+        for (int j = 0; j < m; ++j) {
+          const int nib = (int)((r.perm >> (4 * (xf.perm_shift + j))) & 0xF);
+          const int w = nib < m ? xf.order[nib] : NOSLOT;
+          if (w == NOSLOT || !((c.exist >> w) & 1u)) return LS_ST_NO_LOOP;
+          seg |= (uint64_t)w << (4 * j);
+        }
+        uint32_t seen = 0;
+        for (int j = 0; j < m; ++j) {
+          const uint32_t bit = 1u << ((seg >> (4 * j)) & 15u);
+          if (seen & bit) return LS_ST_REORDER_MISSING;
+          seen |= bit;
+        }
+        int pmin = 0;
+        if (m != c.n) {  // m distinct loops of an n-chain: contiguous iff their positions span m - 1
+          int pmax = -1;
+          pmin = MAXCH;
+          for (int j = 0; j < m; ++j) {
+            const int pv = chain_find(c.chain, (int)((seg >> (4 * j)) & 15u));
+            pmin = min(pmin, pv);
+            pmax = max(pmax, pv);
+          }
+          if (pmax - pmin != m - 1) return LS_ST_REORDER_CHAIN;
+        }
+        const uint64_t mk = m >= 16 ? ~0ull : ((1ull << (4 * m)) - 1);
+        c.chain = (c.chain & ~(mk << (4 * pmin))) | (seg << (4 * pmin));
+        break;
+      }
+      case LS_XF_UNROLL:
+      case LS_XF_PARALLEL:
+        if (!exists) return LS_ST_NO_LOOP;
+        if (xf.kind == LS_XF_UNROLL)
+          c.unr |= 1u << v;
+        else
+          c.par |= 1u << v;
+        break;
+      default:
+        return LS_ST_UNSUPPORTED;
+    }
+  }
+  return LS_OK;
+}
+
 __device__ __forceinline__ double rn_mul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double rn_add(double a, double b) { return __dadd_rn(a, b); }
 
 // bank_conflict_factor (ls/ptx.py:264-307) of innermost access a
-__device__ int64_t bank_factor(const DTask& T, Cand& c, int a) {
+template <class CT>
+__device__ int64_t bank_factor(const DTask& T, CT& c, int a) {
   const int t = T.acc_tensor[a];
   const int rank = T.t_rank[t];
   uint32_t used = 0;
@@ -448,7 +595,8 @@ __device__ int64_t bank_factor(const DTask& T, Cand& c, int a) {
 }
 
 // thread_cycles in line order (ls/ptx.py:225-235), for non-integral cost tables
-__device__ double ptx_work_ordered(const DTask& T, Cand& c, int k, double wi) {
+template <class CT>
+__device__ double ptx_work_ordered(const DTask& T, CT& c, int k, double wi) {
   const double* pc = T.ptx_cost;
   double wpre[MAXCH], wpost[MAXCH];
   int32_t rem[MAXCH];
@@ -508,6 +656,9 @@ __device__ double ptx_work_ordered(const DTask& T, Cand& c, int k, double wi) {
   }
   return rn_add(work, pc[LS_I_RET]);
 }
+
+template <class CT>
+__device__ int features_score(const DTask& T, CT& c, int64_t dmov, double* f, double* score);
 
 // extract_features + score of one candidate (ls/cost.py:132-161).  TM x RM is
 // the compile-time tensor x dimension layout of the register-resident walk.
@@ -603,7 +754,14 @@ __device__ int eval_candidate(const DTask& T, const ls_record& r, Cand& c, doubl
   int64_t dmov = 0;
 #pragma unroll
   for (int t = 0; t < TM; ++t) dmov += dm[t];
+  return features_score(T, c, dmov, f, score);
+}
 
+// Emitted-code features + linear score of a transformed candidate (shared by
+// both paths): ls/asm.py:250-337, ls/ilp.py:262-271, ls/ptx.py:90-327,
+// ls/cost.py:132-161.
+template <class CT>
+__device__ int features_score(const DTask& T, CT& c, int64_t dmov, double* f, double* score) {
   // ---- emitted-block structure of the transformed chain -----------------------
   // branching loops j = 0..k-1 (not unrolled/vectorized); R_j = copies of loop j
   // emitted because unrolled loops above it inline their bodies R_j times
@@ -703,6 +861,241 @@ __device__ int eval_candidate(const DTask& T, const ls_record& r, Cand& c, doubl
   return LS_OK;
 }
 
+// Tabulated path: the cache model's dimension counts are
+// lookups.  For dimension D, the count after the walk has passed a set of D's
+// variables is a function of (the record fields that determine those
+// variables' extents/steps and term presence = the key, the set = a bit mask);
+// ls_task_create tabulates it once per task with the generic fold
+// (build_tab_kernel), so per candidate the walk only ORs a per-slot bit mask
+// and multiplies looked-up counts.
+// Decode a space point (mixed radix, axis 0 most significant) into the record
+// the host packer would have produced for the same choices (pack.SpaceTemplate).
+__device__ __forceinline__ int point_record(const DTask& T, uint64_t x, ls_record& r) {
+  uint64_t lo = 0, hi = 0, perm = 0;
+  uint32_t flags = 0;
+  for (int a = T.sp_n - 1; a >= 0; --a) {
+    const DAxis& ax = T.sp_ax[a];
+    uint32_t c;
+    if (a == 0) {
+      if (x >= ax.n) return LS_ST_POINT_RANGE;
+      c = (uint32_t)x;
+    } else if (ax.n == 1) {
+      c = 0;
+    } else {
+      const uint64_t q = (x >> 32) ? x / ax.n : __umul64hi(x, ax.magic);
+      c = (uint32_t)(x - q * ax.n);
+      x = q;
+    }
+    if (ax.kind == LS_AX_BIT) {
+      flags |= c << ax.bit;
+      continue;
+    }
+    const uint64_t v = __ldg(reinterpret_cast<const unsigned long long*>(T.sp_vals) + ax.voff + c);
+    if (ax.kind == LS_AX_PERM) {
+      perm |= v;
+      continue;
+    }
+    if (ax.param < 4)
+      lo |= v << (16 * ax.param);
+    else
+      hi |= v << (16 * (ax.param - 4));
+    if (ax.kind == LS_AX_VEC && v != 0) flags |= 1u << ax.bit;
+  }
+  memcpy(&r.param[0], &lo, 8);
+  memcpy(&r.param[4], &hi, 8);
+  r.perm = perm;
+  r.flags = flags;
+  r.tag = 0;
+  return LS_OK;
+}
+
+// Candidate source of the scoring kernels: SRC 0 = ls_record array, 1 = points.
+template <int SRC>
+__device__ __forceinline__ int load_cand(const DTask& T, const void* __restrict__ src, int pbytes, int64_t i,
+                                         ls_record& r);
+
+template <int TM, int RM, bool SMT>
+__device__ __forceinline__ int32_t tab_at(const int32_t* __restrict__ tab, int32_t i) {
+  if constexpr (SMT)
+    return tab[i];
+  else
+    return __ldg(&tab[i]);
+}
+
+template <int TM, int RM, bool SMT>
+__device__ int eval_fast(const DTask& T, const int32_t* __restrict__ tab, const ls_record& r, FastCand& c,
+                         double* f, double* score) {
+  const int st = apply_fast(T, r, c);
+  if (st) return st;
+  const int nT = T.n_tensors;
+  // byte offset of each dimension's row for this candidate's key
+  uint32_t kb[TM * RM];
+#pragma unroll
+  for (int D = 0; D < TM * RM; ++D) {
+    int32_t k = 0;
+    const int nd = T.fk_n[D];
+    for (int q = 0; q < nd; ++q) {
+      const int src = T.fk_src[D][q];
+      int32_t val;
+      if (src < LS_MAX_PARAMS) {
+        val = (int32_t)rparam(r, src);
+        if (val > T.fk_bound[src]) val = 0;  // only possible when no applied transform reads it
+      } else {
+        val = (int32_t)((r.flags >> (src - LS_MAX_PARAMS)) & 1u);
+      }
+      k = k * T.fk_rad[D][q] + val;
+    }
+    kb[D] = 4u * (uint32_t)(T.ftab_off[D] + (k << T.dim_nv[D]));
+  }
+  uint64_t mall = 0;
+  const char* tb = reinterpret_cast<const char*>(tab);
+  auto cnt = [&](int D) -> uint32_t {
+    const uint32_t sel = T.fsel[D];
+    const uint32_t off = kb[D] + ((uint32_t)(mall >> (sel & 0xFFu)) & (sel >> 8));
+    return (uint32_t)tab_at<TM, RM, SMT>(reinterpret_cast<const int32_t*>(tb + off), 0);
+  };
+  static_assert(RM == 4, "tabulated path uses the 4x4 layout");
+  auto prod = [&](int t) -> int64_t {
+    const uint64_t a = (uint64_t)cnt(t * 4 + 0) * cnt(t * 4 + 1);
+    const uint64_t b = (uint64_t)cnt(t * 4 + 2) * cnt(t * 4 + 3);
+    return (int64_t)(a * b);
+  };
+  uint32_t tmask[TM];
+  int64_t Fb[TM], dm[TM];
+  uint32_t reuse = 0;
+#pragma unroll
+  for (int t = 0; t < TM; ++t) {
+    tmask[t] = 0;
+    dm[t] = 0;
+    Fb[t] = 0;
+    if (t < nT) {
+      Fb[t] = prod(t);
+      dm[t] = T.t_nacc[t];
+      reuse |= 1u << t;
+      tmask[t] = T.t_vmask[t];
+      if (T.has_optional) {
+        tmask[t] = 0;
+        for (int a = 0; a < T.t_nu[t]; ++a)
+          for (int rr = 0; rr < T.t_rank[t]; ++rr) {
+            const DExpr& e = T.expr[T.t_uacc[t][a]][rr];
+            for (int q = 0; q < e.nt; ++q)
+              if (present(T.term[e.t0 + q], c.flags)) tmask[t] |= 1u << T.term[e.t0 + q].slot;
+          }
+      }
+    }
+  }
+  const int64_t cap = T.cap;
+  for (int p = c.n - 1; p >= 0; --p) {
+    const int v = c.C(p);
+    const int64_t E = c.E(v);
+    mall |= T.vbits[v];
+    int64_t single = 0;
+#pragma unroll
+    for (int t = 0; t < TM; ++t) single += Fb[t];
+#pragma unroll
+    for (int t = 0; t < TM; ++t) {
+      if (t < nT) {
+        const int64_t Ff = prod(t);
+        const bool uses = (tmask[t] >> v) & 1u;
+        bool ru = (reuse >> t) & 1u;
+        if (single > cap && !uses) ru = false;
+        const int64_t per = (single <= cap || ru) ? Ff : dm[t] * E;
+        if (Ff > cap) ru = false;
+        dm[t] = per;
+        reuse = ru ? (reuse | (1u << t)) : (reuse & ~(1u << t));
+        Fb[t] = Ff;
+      }
+    }
+  }
+  int64_t dmov = 0;
+#pragma unroll
+  for (int t = 0; t < TM; ++t) dmov += dm[t];
+  return features_score(T, c, dmov, f, score);
+}
+
+// One table entry per thread: decode (dimension, key, mask), rebuild the
+// extents/steps the key implies (apply_schedule's Tile/Vectorize arithmetic,
+// ls/ir.py:361-382, without the chain) and fold the dimension's expressions
+// exactly like the generic path (expr_range + _si_union, ls/cache.py:80-130).
+__global__ void build_tab_kernel(const DTask* __restrict__ g, int32_t* __restrict__ tab) {
+  const DTask& T = *g;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= T.tab_len) return;
+  int D = -1;
+  for (int q = 0; q < 16; ++q)
+    if (T.ftab_len[q] > 0 && e >= T.ftab_off[q] && e < T.ftab_off[q] + T.ftab_len[q]) D = q;
+  if (D < 0) {
+    if (e == T.tab_one) tab[e] = 1;
+    return;
+  }
+  const int nv = T.dim_nv[D];
+  const int loc = e - T.ftab_off[D];
+  const uint32_t mask = (uint32_t)loc & ((1u << nv) - 1u);
+  int32_t key = loc >> nv;
+  int32_t prm[LS_MAX_PARAMS];
+  for (int q = 0; q < LS_MAX_PARAMS; ++q) prm[q] = 1;
+  uint32_t flags = 0;
+  for (int q = T.fk_n[D] - 1; q >= 0; --q) {
+    const int32_t d = key % T.fk_rad[D][q];
+    key /= T.fk_rad[D][q];
+    const int src = T.fk_src[D][q];
+    if (src < LS_MAX_PARAMS)
+      prm[src] = d;
+    else
+      flags |= (uint32_t)d << (src - LS_MAX_PARAMS);
+  }
+  int32_t E[NSLOT], St[NSLOT];
+  uint32_t exist = T.base_exist;
+  for (int p = 0; p < T.n_base; ++p) {
+    E[T.base_slot[p]] = T.base_ext[p];
+    St[T.base_slot[p]] = T.base_step[p];
+  }
+  for (int x = 0; x < T.n_xf; ++x) {
+    const DXform& xf = T.xf[x];
+    if (xf.kind != LS_XF_TILE && xf.kind != LS_XF_VECTORIZE) continue;
+    if (xf.enable_bit >= 0 && !((flags >> xf.enable_bit) & 1u)) continue;
+    const int v = xf.slot, u = xf.new_slot;
+    if (v == NOSLOT || u == NOSLOT || !((exist >> v) & 1u)) continue;  // such candidates fail
+    const int32_t F = xf.param >= 0 ? prm[xf.param] : xf.value;
+    if (F < 1 || F > E[v]) continue;  // such candidates fail
+    E[u] = F;
+    St[u] = St[v];
+    E[v] = (E[v] + F - 1) / F;
+    St[v] *= F;
+    exist |= 1u << u;
+  }
+  uint32_t expanded = 0;
+  for (int x = 0; x < nv; ++x)
+    if ((mask >> x) & 1u) expanded |= 1u << T.dim_var[D][x];
+  const int t = D / 4, rr = D % 4;
+  SI u;
+  for (int a = 0; a < T.t_nu[t]; ++a) {
+    const DExpr& ex = T.expr[T.t_uacc[t][a]][rr];
+    SI acc;
+    acc.lo = acc.hi = ex.konst;
+    acc.stride = 0;
+    acc.count = 1;
+    acc.exact = 1;
+    for (int k = 0; k < ex.nt; ++k) {
+      const DTerm& tm = T.term[ex.t0 + k];
+      const int w = tm.slot;
+      if (!present(tm, flags) || !((expanded >> w) & 1u) || !((exist >> w) & 1u)) continue;
+      const int32_t Ew = E[w];
+      if (Ew == 1) continue;
+      const int32_t d = tm.coef * St[w];
+      SI s;
+      s.lo = d > 0 ? 0 : d * (Ew - 1);
+      s.hi = d > 0 ? d * (Ew - 1) : 0;
+      s.stride = abs(d);
+      s.count = Ew;
+      s.exact = 1;
+      acc = si_sum(acc, s);
+    }
+    u = a == 0 ? acc : si_union(u, acc);
+  }
+  tab[e] = u.count;
+}
+
 // ---------------------------------------------------------------------------
 // kernels
 // ---------------------------------------------------------------------------
@@ -714,6 +1107,46 @@ __device__ __forceinline__ void stage_task(DTask& s, const DTask* __restrict__ g
   __syncthreads();
 }
 
+// Path selector of the scoring kernels: 0 generic, 1 tabulated with the table
+// in global memory (L1/L2 resident), 2 tabulated with the table in shared memory.
+template <int MODE>
+__device__ __forceinline__ const int32_t* stage_tab(unsigned char* where, const DTask& T) {
+  if constexpr (MODE == 2) {
+    int32_t* dst = reinterpret_cast<int32_t*>(where);
+    for (int i = threadIdx.x; i < T.tab_len; i += blockDim.x) dst[i] = __ldg(&T.tab[i]);
+    __syncthreads();
+    return dst;
+  } else {
+    return T.tab;
+  }
+}
+
+__host__ __device__ inline size_t tab_smem_bytes(int mode, int tab_len) {
+  return mode == 2 ? align16(sizeof(int32_t) * (size_t)tab_len) : 0;
+}
+__host__ __device__ inline size_t state_bytes(int mode, int n_slots, int n_chain, int n_stage) {
+  return mode == 0 ? cand_bytes(n_slots, n_chain, n_stage) : align16(sizeof(int32_t) * (size_t)n_slots * TPB);
+}
+
+template <int TM, int RM, int MODE>
+struct Evaluator {
+  Cand c;
+  FastCand fc;
+  const int32_t* tab;
+  __device__ __forceinline__ Evaluator(const DTask& T, unsigned char* state, const int32_t* tab_) : tab(tab_) {
+    if constexpr (MODE == 0)
+      c = carve(state, T);
+    else
+      fc.ext = reinterpret_cast<int32_t*>(state);
+  }
+  __device__ __forceinline__ int operator()(const DTask& T, const ls_record& r, double* f, double* s) {
+    if constexpr (MODE == 0)
+      return eval_candidate<TM, RM>(T, r, c, f, s);
+    else
+      return eval_fast<TM, RM, MODE == 2>(T, tab, r, fc, f, s);
+  }
+};
+
 __device__ __forceinline__ ls_record load_record(const ls_record* __restrict__ recs, int64_t i) {
   const int4* p = reinterpret_cast<const int4*>(recs + i);
   int4 a = __ldg(p), b = __ldg(p + 1);
@@ -723,21 +1156,39 @@ __device__ __forceinline__ ls_record load_record(const ls_record* __restrict__ r
   return r;
 }
 
-template <int TM, int RM>
-__global__ void __launch_bounds__(TPB, (TM * RM <= 16 ? 3 : 1)) score_kernel(const DTask* __restrict__ gtask,
-                                                    const ls_record* __restrict__ recs, int64_t n,
-                                                    double* __restrict__ scores, double* __restrict__ feats,
-                                                    int32_t* __restrict__ status) {
+template <int SRC>
+__device__ __forceinline__ int load_cand(const DTask& T, const void* __restrict__ src, int pbytes, int64_t i,
+                                         ls_record& r) {
+  if constexpr (SRC == 0) {
+    r = load_record(reinterpret_cast<const ls_record*>(src), i);
+    return LS_OK;
+  } else {
+    const uint64_t x = pbytes == 4 ? (uint64_t)__ldg(reinterpret_cast<const unsigned int*>(src) + i)
+                                   : (uint64_t)__ldg(reinterpret_cast<const unsigned long long*>(src) + i);
+    return point_record(T, x, r);
+  }
+}
+
+constexpr int min_blocks(int tm, int rm, int mode) { return mode ? 3 : (tm * rm <= 16 ? 3 : 1); }
+
+template <int TM, int RM, int MODE, int SRC>
+__global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE))
+    score_kernel(const DTask* __restrict__ gtask, const void* __restrict__ src, int pbytes, int64_t n,
+                 double* __restrict__ scores, double* __restrict__ feats, int32_t* __restrict__ status) {
   extern __shared__ __align__(16) unsigned char dyn[];
   DTask& T = *reinterpret_cast<DTask*>(dyn);
   stage_task(T, gtask);
-  Cand c = carve(dyn + T.task_bytes, T);
+  unsigned char* p = dyn + T.task_bytes;
+  const int32_t* tab = stage_tab<MODE>(p, T);
+  p += tab_smem_bytes(MODE, T.tab_len);
+  Evaluator<TM, RM, MODE> ev(T, p, tab);
   const int nf = T.family == LS_FAMILY_CPU ? LS_NFEAT_CPU : LS_NFEAT_GPU;
   for (int64_t i = (int64_t)blockIdx.x * TPB + threadIdx.x; i < n; i += (int64_t)gridDim.x * TPB) {
-    const ls_record r = load_record(recs, i);
+    ls_record r;
     double f[LS_NFEAT_GPU];
     double s = 0.0;
-    const int st = eval_candidate<TM, RM>(T, r, c, f, &s);
+    int st = load_cand<SRC>(T, src, pbytes, i, r);
+    if (st == LS_OK) st = ev(T, r, f, &s);
     const double nan = __longlong_as_double(0x7ff8000000000000ll);
     if (scores) scores[i] = st ? nan : s;
     if (status) status[i] = st;
@@ -768,19 +1219,20 @@ __device__ __forceinline__ double from_order_bits(unsigned long long o) {
 
 constexpr int TK_MAXK = 1024;
 
-template <int BUF>
-struct TopkState {
-  Key buf[BUF];
+// Block top-k state in shared memory: header + `cap` keys (cap = 1024 or 2048).
+struct __align__(16) TopkState {
   Key thr;
-  int cnt;
+  int cnt, cap;
+  __device__ __forceinline__ Key* buf() { return reinterpret_cast<Key*>(this + 1); }
+  __device__ __forceinline__ const Key* buf() const { return reinterpret_cast<const Key*>(this + 1); }
 };
+__host__ __device__ constexpr size_t topk_state_bytes(int cap) { return sizeof(TopkState) + sizeof(Key) * (size_t)cap; }
 
 // Sort buf[0..cnt) (padded with +inf) and keep the k smallest; returns the kept count.
-template <int BUF>
-__device__ int topk_compact(TopkState<BUF>& S, int k, int cnt) {
-  for (int i = cnt + threadIdx.x; i < BUF; i += blockDim.x) {
-    S.buf[i].s = KEY_INF_S;
-    S.buf[i].i = KEY_INF_I;
+__device__ int topk_compact(TopkState& S, int k, int cnt) {
+  for (int i = cnt + threadIdx.x; i < S.cap; i += blockDim.x) {
+    S.buf()[i].s = KEY_INF_S;
+    S.buf()[i].i = KEY_INF_I;
   }
   __syncthreads();
   int size0 = 2;
@@ -791,10 +1243,10 @@ __device__ int topk_compact(TopkState<BUF>& S, int k, int cnt) {
         const int lo = 2 * t - (t & (stride - 1));
         const int hi = lo + stride;
         const bool up = (lo & size) == 0;
-        const Key a = S.buf[lo], b = S.buf[hi];
+        const Key a = S.buf()[lo], b = S.buf()[hi];
         if (kless(b, a) == up) {
-          S.buf[lo] = b;
-          S.buf[hi] = a;
+          S.buf()[lo] = b;
+          S.buf()[hi] = a;
         }
       }
       __syncthreads();
@@ -803,15 +1255,15 @@ __device__ int topk_compact(TopkState<BUF>& S, int k, int cnt) {
   const int keep = cnt < k ? cnt : k;
   if (threadIdx.x == 0) {
     S.cnt = keep;
-    if (keep == k) S.thr = S.buf[k - 1];
+    if (keep == k) S.thr = S.buf()[k - 1];
   }
   __syncthreads();
   return keep;
 }
 
-template <int BUF>
-__device__ __forceinline__ void topk_init(TopkState<BUF>& S) {
+__device__ __forceinline__ void topk_init(TopkState& S, int cap) {
   if (threadIdx.x == 0) {
+    S.cap = cap;
     S.cnt = 0;
     S.thr.s = KEY_INF_S;
     S.thr.i = KEY_INF_I;
@@ -821,18 +1273,20 @@ __device__ __forceinline__ void topk_init(TopkState<BUF>& S) {
 
 // Insert-if-better without a barrier; the block synchronises only when the
 // buffer could overflow within the next round (`safe` rounds are free).
-template <int BUF>
-__device__ __forceinline__ void topk_offer(TopkState<BUF>& S, bool has, const Key& key, int k, int& safe) {
+__device__ __forceinline__ void topk_offer(TopkState& S, bool has, const Key& key, int k, int& safe) {
   if (has && kless(key, S.thr)) {
     const int slot = atomicAdd(&S.cnt, 1);
-    S.buf[slot] = key;
+    S.buf()[slot] = key;
   }
   if (--safe > 0) return;
   __syncthreads();
   int c = S.cnt;
+  const bool open = S.thr.s == KEY_INF_S && S.thr.i == KEY_INF_I;
   __syncthreads();
-  if (c > BUF - (int)blockDim.x) c = topk_compact(S, k, c);
-  safe = (BUF - c) / (int)blockDim.x;
+  // compact when another round could overflow, and as soon as k keys exist
+  // without a threshold (an early threshold keeps later inserts rare)
+  if (c > S.cap - (int)blockDim.x || (open && c >= k)) c = topk_compact(S, k, c);
+  safe = (S.cap - c) / (int)blockDim.x;
 }
 
 constexpr int TK_GROUP = 16;  // blocks per first-level merge group
@@ -845,9 +1299,8 @@ __device__ __forceinline__ Key ld_key_cg(const Key* p) {
 }
 
 // Merge m keys from global memory into the block's buffer (streamed, k kept).
-template <int BUF>
-__device__ int merge_into(TopkState<BUF>& S, const Key* src, int64_t m, int k) {
-  topk_init(S);
+__device__ int merge_into(TopkState& S, const Key* src, int64_t m, int k) {
+  topk_init(S, S.cap);
   int safe = 1;
   for (int64_t base = 0; base < m; base += blockDim.x) {
     const int64_t i = base + threadIdx.x;
@@ -863,12 +1316,11 @@ __device__ int merge_into(TopkState<BUF>& S, const Key* src, int64_t m, int k) {
   return topk_compact(S, k, S.cnt);
 }
 
-template <int BUF>
-__device__ void write_keys(const TopkState<BUF>& S, int kept, int k, Key* out) {
+__device__ void write_keys(const TopkState& S, int kept, int k, Key* out) {
   for (int j = threadIdx.x; j < k; j += blockDim.x) {
     Key o;
     if (j < kept) {
-      o = S.buf[j];
+      o = S.buf()[j];
     } else {
       o.s = KEY_INF_S;
       o.i = KEY_INF_I;
@@ -881,18 +1333,21 @@ __device__ void write_keys(const TopkState<BUF>& S, int kept, int k, Key* out) {
 // block lists in a two-level tree inside the same launch: the last block of
 // each group of TK_GROUP merges its group, the last group merger writes the
 // final k (threadfence + ticket counters; no second kernel).
-template <int TM, int RM, int BUF>
-__global__ void __launch_bounds__(TPB, (TM * RM <= 16 ? 3 : 1)) score_topk_kernel(
-    const DTask* __restrict__ gtask, const ls_record* __restrict__ recs, int64_t n, int64_t base_index, int k,
+template <int TM, int RM, int MODE, int SRC>
+__global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kernel(
+    const DTask* __restrict__ gtask, const void* __restrict__ src, int pbytes, int64_t n, int64_t base_index, int k,
     Key* __restrict__ block_out, Key* __restrict__ group_out, unsigned int* __restrict__ tickets,
-    double* __restrict__ out_s, int64_t* __restrict__ out_i, unsigned long long* __restrict__ n_valid) {
+    double* __restrict__ out_s, int64_t* __restrict__ out_i, unsigned long long* __restrict__ n_valid, int cap) {
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ unsigned int s_ticket;
   DTask& T = *reinterpret_cast<DTask*>(dyn);
   stage_task(T, gtask);
-  TopkState<BUF>& S = *reinterpret_cast<TopkState<BUF>*>(dyn + T.task_bytes);
-  Cand c = carve(dyn + T.task_bytes + align16(sizeof(TopkState<BUF>)), T);
-  topk_init(S);
+  unsigned char* p = dyn + T.task_bytes;
+  const int32_t* tab = stage_tab<MODE>(p, T);
+  p += tab_smem_bytes(MODE, T.tab_len);
+  TopkState& S = *reinterpret_cast<TopkState*>(p);
+  Evaluator<TM, RM, MODE> ev(T, p + align16(topk_state_bytes(cap)), tab);
+  topk_init(S, cap);
   unsigned int valid = 0;
   int safe = 1;
   for (int64_t base = (int64_t)blockIdx.x * TPB; base < n; base += (int64_t)gridDim.x * TPB) {
@@ -900,10 +1355,10 @@ __global__ void __launch_bounds__(TPB, (TM * RM <= 16 ? 3 : 1)) score_topk_kerne
     bool has = false;
     Key key;
     if (i < n) {
-      const ls_record r = load_record(recs, i);
+      ls_record r;
       double f[LS_NFEAT_GPU];
       double s;
-      if (eval_candidate<TM, RM>(T, r, c, f, &s) == LS_OK) {
+      if (load_cand<SRC>(T, src, pbytes, i, r) == LS_OK && ev(T, r, f, &s) == LS_OK) {
         has = true;
         key.s = order_bits(s);
         key.i = base_index + i;
@@ -939,8 +1394,8 @@ __global__ void __launch_bounds__(TPB, (TM * RM <= 16 ? 3 : 1)) score_topk_kerne
   kept = merge_into(S, group_out, (int64_t)ngroups * k, k);
   for (int j = threadIdx.x; j < k; j += blockDim.x) {
     if (j < kept) {
-      out_s[j] = from_order_bits(S.buf[j].s);
-      out_i[j] = S.buf[j].i;
+      out_s[j] = from_order_bits(S.buf()[j].s);
+      out_i[j] = S.buf()[j].i;
     } else {
       out_s[j] = __longlong_as_double(0x7ff0000000000000ll);
       out_i[j] = -1;
@@ -952,8 +1407,9 @@ __global__ void __launch_bounds__(TPB, (TM * RM <= 16 ? 3 : 1)) score_topk_kerne
 __global__ void __launch_bounds__(1024) merge_keys_kernel(const Key* __restrict__ in, int64_t m, int k,
                                                           double* __restrict__ out_s,
                                                           int64_t* __restrict__ out_i) {
-  __shared__ TopkState<2048> S;
-  topk_init(S);
+  __shared__ __align__(16) unsigned char raw[topk_state_bytes(2048)];
+  TopkState& S = *reinterpret_cast<TopkState*>(raw);
+  topk_init(S, 2048);
   int safe = 1;
   for (int64_t base = 0; base < m; base += blockDim.x) {
     const int64_t i = base + threadIdx.x;
@@ -969,8 +1425,8 @@ __global__ void __launch_bounds__(1024) merge_keys_kernel(const Key* __restrict_
   const int kept = topk_compact(S, k, S.cnt);
   for (int j = threadIdx.x; j < k; j += blockDim.x) {
     if (j < kept) {
-      out_s[j] = from_order_bits(S.buf[j].s);
-      out_i[j] = S.buf[j].i;
+      out_s[j] = from_order_bits(S.buf()[j].s);
+      out_i[j] = S.buf()[j].i;
     } else {
       out_s[j] = __longlong_as_double(0x7ff0000000000000ll);
       out_i[j] = -1;
@@ -1038,6 +1494,109 @@ struct HTerm {
   int64_t coef;
   uint32_t req;
 };
+
+constexpr int64_t TAB_MAX_ENTRIES = 1 << 22;  // 16 MiB of int32 counts per task
+constexpr int64_t TAB_SMEM_MAX_BYTES = 16384;
+
+// Decide whether the task can use the tabulated path and lay out its table
+// (DESIGN.md §3.5).  A dimension's key is every record field that can change
+// the extent/step of one of its variables (Tile/Vectorize factors applied to
+// the variable or its ancestors, and their enable bits) plus the enable bits
+// of its optional terms.
+void plan_tabulated(const ls_task_desc& d, DTask& T, int RM, const std::vector<int64_t>& count_bound) {
+  T.fast = 0;
+  T.tab_len = 0;
+  if (RM != 4 || T.n_stage + 2 > 64) return;
+  for (int t = 0; t < T.n_tensors; ++t) {  // footprints are unsigned 64-bit products on this path
+    double b = 1.0;
+    for (int rr = 0; rr < T.t_rank[t]; ++rr) b *= (double)count_bound[t * RM + rr];
+    if (b >= 9.0e18) return;
+  }
+  uint32_t dep_p[NSLOT] = {0}, dep_b[NSLOT] = {0};
+  int64_t ub[NSLOT] = {0};
+  for (int p = 0; p < T.n_base; ++p) ub[T.base_slot[p]] = T.base_ext[p];
+  int64_t bound[LS_MAX_PARAMS] = {0};
+  for (int x = 0; x < T.n_xf; ++x) {
+    const DXform& xf = T.xf[x];
+    if (xf.kind != LS_XF_TILE && xf.kind != LS_XF_VECTORIZE) continue;
+    if (xf.slot == NOSLOT || xf.new_slot == NOSLOT) continue;  // always fails
+    const uint32_t pm = xf.param >= 0 ? (1u << xf.param) : 0u;
+    const uint32_t bm = xf.enable_bit >= 0 ? (1u << xf.enable_bit) : 0u;
+    dep_p[xf.slot] |= pm;
+    dep_b[xf.slot] |= bm;
+    dep_p[xf.new_slot] = dep_p[xf.slot];
+    dep_b[xf.new_slot] = dep_b[xf.slot];
+    if (xf.param >= 0) bound[xf.param] = std::max(bound[xf.param], ub[xf.slot]);
+    ub[xf.new_slot] = ub[xf.slot];
+  }
+  for (int q = 0; q < LS_MAX_PARAMS; ++q) T.fk_bound[q] = (int32_t)bound[q];
+  int64_t off = 0;
+  for (int D = 0; D < 16; ++D) {
+    T.ftab_off[D] = 0;
+    T.ftab_len[D] = 0;
+    T.fk_n[D] = 0;
+    const int t = D / 4, rr = D % 4;
+    T.fsel[D] = 0;
+    if (t >= T.n_tensors || rr >= T.t_rank[t]) continue;  // points at the constant-1 entry (below)
+    uint32_t pm = 0, bm = 0;
+    const int nv = T.dim_nv[D];
+    for (int x = 0; x < nv; ++x) {
+      pm |= dep_p[T.dim_var[D][x]];
+      bm |= dep_b[T.dim_var[D][x]];
+    }
+    for (int a = 0; a < T.t_nu[t]; ++a) {
+      const DExpr& e = T.expr[T.t_uacc[t][a]][rr];
+      for (int z = 0; z < e.nt; ++z) bm |= T.term[e.t0 + z].req;
+    }
+    int64_t len = 1;
+    int nd = 0;
+    for (int q = 0; q < LS_MAX_PARAMS; ++q) {
+      if (!((pm >> q) & 1u)) continue;
+      if (nd == 3) return;
+      T.fk_src[D][nd] = (int8_t)q;
+      T.fk_rad[D][nd] = (int32_t)(bound[q] + 1);
+      len *= bound[q] + 1;
+      ++nd;
+      if (len > TAB_MAX_ENTRIES) return;
+    }
+    for (int b = 0; b < 24; ++b) {
+      if (!((bm >> b) & 1u)) continue;
+      if (nd == 3) return;
+      T.fk_src[D][nd] = (int8_t)(LS_MAX_PARAMS + b);
+      T.fk_rad[D][nd] = 2;
+      len *= 2;
+      ++nd;
+    }
+    if (bm >> 24) return;  // enable bits >= 24 do not fit the key encoding
+    len <<= nv;
+    if (off + len > TAB_MAX_ENTRIES) return;
+    T.fk_n[D] = (int8_t)nd;
+    T.ftab_off[D] = (int32_t)off;
+    T.ftab_len[D] = (int32_t)len;
+    // stage bits sit at dim_base + 2 + x, so (mall >> dim_base) & (mask << 2) is a byte offset
+    T.fsel[D] = (uint32_t)T.dim_base[D] | ((((1u << nv) - 1u) << 2) << 8);
+    off += len;
+  }
+  T.tab_one = (int32_t)off++;  // the count of a dimension slot the layout does not use: 1
+  for (int D = 0; D < 16; ++D)
+    if (T.ftab_len[D] == 0) T.ftab_off[D] = T.tab_one;
+  for (int v = 0; v < NSLOT; ++v) T.vbits[v] = 0;
+  for (int D = 0; D < 16; ++D)
+    for (int x = 0; x < T.dim_nv[D]; ++x) T.vbits[T.dim_var[D][x]] |= 1ull << (T.dim_base[D] + 2 + x);
+  T.chain0 = ~0ull;
+  T.base_exist = T.base_unr = T.base_vec = T.base_par = 0;
+  for (int p = 0; p < T.n_base; ++p) {
+    const int v = T.base_slot[p];
+    T.chain0 = (T.chain0 & ~(15ull << (4 * p))) | ((uint64_t)v << (4 * p));
+    T.base_exist |= 1u << v;
+    if (T.base_flags[p] & F_UNR) T.base_unr |= 1u << v;
+    if (T.base_flags[p] & F_VEC) T.base_vec |= 1u << v;
+    if (T.base_flags[p] & F_PAR) T.base_par |= 1u << v;
+  }
+  T.tab_len = (int32_t)off;
+  T.tab_smem = (int64_t)sizeof(int32_t) * off <= TAB_SMEM_MAX_BYTES ? 1 : 0;
+  T.fast = 1;
+}
 
 int build_task(const ls_task_desc& d, DTask& T, std::vector<int>& load_t, std::vector<int>& store_t) {
   memset(&T, 0, sizeof(T));
@@ -1139,6 +1698,7 @@ int build_task(const ls_task_desc& d, DTask& T, std::vector<int>& load_t, std::v
       }
   }
   int nt = 0;
+  std::vector<std::vector<int64_t>> ebound(na, std::vector<int64_t>(MAXRANK, 0));
   for (int a = 0; a < na; ++a) {
     const ls_node& n = d.nodes[nl + a];
     T.acc_tensor[a] = (uint8_t)n.tensor;
@@ -1152,6 +1712,7 @@ int build_task(const ls_task_desc& d, DTask& T, std::vector<int>& load_t, std::v
       int64_t bound = std::llabs((int64_t)n.idx[k].konst);
       for (auto& t : e) bound += std::llabs(t.coef) * span[t.var] * (2ll << ntile);
       if (bound >= (1ll << 30)) return fail(LS_E_UNSUPPORTED, "index range exceeds the device int32 model");
+      ebound[a][k] = bound;
       if (nt + (int)e.size() > MAXTERM) return fail(LS_E_UNSUPPORTED, "too many index terms");
       T.expr[a][k].konst = n.idx[k].konst;
       T.expr[a][k].t0 = (int16_t)nt;
@@ -1272,6 +1833,15 @@ int build_task(const ls_task_desc& d, DTask& T, std::vector<int>& load_t, std::v
       for (int z = 0; z < T.expr[a][k].nt; ++z)
         T.t_vmask[T.acc_tensor[a]] |= 1u << T.term[T.expr[a][k].t0 + z].slot;
   T.n_chain = std::min(MAXCH, nl + ntile);
+  {  // |count| of a dimension <= hi - lo + 1 <= 2 * range bound + 1 (ls/cache.py:46-77)
+    std::vector<int64_t> cb(MAXD, 1);
+    for (int a = 0; a < na; ++a)
+      for (int k = 0; k < T.t_rank[T.acc_tensor[a]]; ++k) {
+        const int D = T.acc_tensor[a] * RM + k;
+        cb[D] = std::max(cb[D], 2 * ebound[a][k] + 1);
+      }
+    plan_tabulated(d, T, RM, cb);
+  }
   T.task_bytes = (int32_t)align16(offsetof(DTask, term) + sizeof(DTerm) * (size_t)nt);
   // ---- arch
   T.family = d.family;
@@ -1344,22 +1914,40 @@ int grid_for(const ls_task* t, int64_t n, int per_sm) {
   return (int)std::max<int64_t>(1, std::min(want, cap));
 }
 
-size_t smem_score(const DTask& T) { return (size_t)T.task_bytes + cand_bytes(T.n_slots, T.n_chain, T.n_stage); }
-// the fused kernel's buffer must hold k plus one round of inserts
-int topk_buf(int k) { return k <= 1024 - TPB ? 1024 : 2048; }
-size_t smem_topk(const DTask& T, int k) {
-  return smem_score(T) + (topk_buf(k) == 1024 ? align16(sizeof(TopkState<1024>)) : align16(sizeof(TopkState<2048>)));
+// 0 generic, 1 tabulated (table in global memory), 2 tabulated (table in shared memory)
+int mode_of(const ls_task* t) {
+  if (t->path == LS_PATH_GENERIC || !t->host.fast) return 0;
+  return t->host.tab_smem ? 2 : 1;
 }
 
-using ScoreFn = void (*)(const DTask*, const ls_record*, int64_t, double*, double*, int32_t*);
-using TopkFn = void (*)(const DTask*, const ls_record*, int64_t, int64_t, int, Key*, Key*, unsigned int*, double*,
-                       int64_t*, unsigned long long*);
+size_t smem_score(const DTask& T, int mode) {
+  return (size_t)T.task_bytes + tab_smem_bytes(mode, T.tab_len) + state_bytes(mode, T.n_slots, T.n_chain, T.n_stage);
+}
+// the fused kernel's buffer must hold k plus one round of inserts
+int topk_buf(int k) { return k <= 1024 - TPB ? 1024 : 2048; }
+size_t smem_topk(const DTask& T, int k, int mode) { return smem_score(T, mode) + align16(topk_state_bytes(topk_buf(k))); }
 
-ScoreFn score_fn(const DTask& T) { return T.layout_rm == 4 ? score_kernel<4, 4> : score_kernel<MAXT, MAXRANK>; }
-TopkFn topk_fn(const DTask& T, int k) {
-  if (topk_buf(k) == 1024)
-    return T.layout_rm == 4 ? score_topk_kernel<4, 4, 1024> : score_topk_kernel<MAXT, MAXRANK, 1024>;
-  return T.layout_rm == 4 ? score_topk_kernel<4, 4, 2048> : score_topk_kernel<MAXT, MAXRANK, 2048>;
+using ScoreFn = void (*)(const DTask*, const void*, int, int64_t, double*, double*, int32_t*);
+using TopkFn = void (*)(const DTask*, const void*, int, int64_t, int64_t, int, Key*, Key*, unsigned int*, double*,
+                       int64_t*, unsigned long long*, int);
+
+template <int SRC>
+ScoreFn score_fn_src(const DTask& T, int mode) {
+  if (mode == 1) return score_kernel<4, 4, 1, SRC>;
+  if (mode == 2) return score_kernel<4, 4, 2, SRC>;
+  return T.layout_rm == 4 ? score_kernel<4, 4, 0, SRC> : score_kernel<MAXT, MAXRANK, 0, SRC>;
+}
+template <int SRC>
+TopkFn topk_fn_src(const DTask& T, int mode) {
+  if (mode == 1) return score_topk_kernel<4, 4, 1, SRC>;
+  if (mode == 2) return score_topk_kernel<4, 4, 2, SRC>;
+  return T.layout_rm == 4 ? score_topk_kernel<4, 4, 0, SRC> : score_topk_kernel<MAXT, MAXRANK, 0, SRC>;
+}
+ScoreFn score_fn(const DTask& T, int mode, int pbytes) {
+  return pbytes ? score_fn_src<1>(T, mode) : score_fn_src<0>(T, mode);
+}
+TopkFn topk_fn(const DTask& T, int mode, int pbytes) {
+  return pbytes ? topk_fn_src<1>(T, mode) : topk_fn_src<0>(T, mode);
 }
 
 template <typename K>
@@ -1401,14 +1989,43 @@ int ls_task_create(const ls_task_desc* desc, int device, ls_task** out) {
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
   }
+  t->path = LS_PATH_AUTO;
+  t->d_tab = nullptr;
+  if (t->host.fast) {
+    if (cudaMalloc(&t->d_tab, sizeof(int32_t) * std::max(1, t->host.tab_len)) != cudaSuccess) {
+      delete t;
+      return fail(LS_E_NOMEM, "cannot allocate the dimension-count table");
+    }
+    t->host.tab = t->d_tab;
+  }
   int64_t one = 1;
   rc = add_unroll(t, &one, 1);
+  if (rc == LS_E_OK && t->host.fast && t->host.tab_len > 0) {
+    build_tab_kernel<<<(t->host.tab_len + 255) / 256, 256>>>(t->d_task, t->d_tab);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) rc = fail(LS_E_CUDA, std::string("build_tab_kernel: ") + cudaGetErrorString(e));
+  }
   if (rc) {
+    if (t->d_tab) cudaFree(t->d_tab);
     delete t;
     return rc;
   }
   *out = t;
   return LS_E_OK;
+}
+
+int ls_task_set_path(ls_task* t, int32_t path) {
+  if (!t || path < LS_PATH_AUTO || path > LS_PATH_TABULATED) return fail(LS_E_ARG, "bad argument");
+  if (path == LS_PATH_TABULATED && !t->host.fast)
+    return fail(LS_E_UNSUPPORTED, "task is not eligible for the tabulated path");
+  t->path = path;
+  return LS_E_OK;
+}
+
+int ls_task_path(const ls_task* t) {
+  if (!t) return LS_E_ARG;
+  return mode_of(t) ? LS_PATH_TABULATED : LS_PATH_GENERIC;
 }
 
 int ls_task_destroy(ls_task* t) {
@@ -1417,6 +2034,7 @@ int ls_task_destroy(ls_task* t) {
   cudaDeviceSynchronize();
   for (void* p : t->retired) cudaFree(p);
   if (t->d_task) cudaFree(t->d_task);
+  if (t->d_tab) cudaFree(t->d_tab);
   delete t;
   return LS_E_OK;
 }
@@ -1442,7 +2060,7 @@ int ls_collect_unroll(ls_task* t, const ls_record* d_records, int64_t n, int64_t
   CUDA_TRY(cudaMallocAsync(&set, sizeof(unsigned long long) * slots, s));
   CUDA_TRY(cudaMemsetAsync(set, 0, sizeof(unsigned long long) * slots, s));
   if (n > 0) {
-    const size_t sm = smem_score(t->host);
+    const size_t sm = smem_score(t->host, 0);
     collect_unroll_kernel<<<grid_for(t, n, blocks_per_sm(collect_unroll_kernel, sm)), TPB, sm, s>>>(
         t->d_task, d_records, n, set, slots);
     CUDA_TRY(cudaGetLastError());
@@ -1459,24 +2077,45 @@ int ls_collect_unroll(ls_task* t, const ls_record* d_records, int64_t n, int64_t
   return LS_E_OK;
 }
 
-int ls_score(ls_task* t, const ls_record* d_records, int64_t n, double* d_scores, double* d_features,
-             int32_t* d_status, void* stream) {
-  if (!t || n < 0 || (n && !d_records)) return fail(LS_E_ARG, "bad argument");
-  if (n == 0) return LS_E_OK;
-  CUDA_TRY(cudaSetDevice(t->device));
-  cudaStream_t s = (cudaStream_t)stream;
-  const ScoreFn fn = score_fn(t->host);
-  const size_t sm = smem_score(t->host);
-  fn<<<grid_for(t, n, blocks_per_sm(fn, sm)), TPB, sm, s>>>(t->d_task, d_records, n, d_scores, d_features,
+static int score_device(ls_task* t, const void* d_src, int pbytes, int64_t n, double* d_scores, double* d_features,
+                        int32_t* d_status, cudaStream_t s) {
+  const int mode = mode_of(t);
+  const ScoreFn fn = score_fn(t->host, mode, pbytes);
+  const size_t sm = smem_score(t->host, mode);
+  fn<<<grid_for(t, n, blocks_per_sm(fn, sm)), TPB, sm, s>>>(t->d_task, d_src, pbytes, n, d_scores, d_features,
                                                             d_status);
   CUDA_TRY(cudaGetLastError());
   return LS_E_OK;
 }
 
-static int topk_device(ls_task* t, const ls_record* d_records, int64_t n, int64_t base_index, int32_t k,
+int ls_score(ls_task* t, const ls_record* d_records, int64_t n, double* d_scores, double* d_features,
+             int32_t* d_status, void* stream) {
+  if (!t || n < 0 || (n && !d_records)) return fail(LS_E_ARG, "bad argument");
+  if (n == 0) return LS_E_OK;
+  CUDA_TRY(cudaSetDevice(t->device));
+  return score_device(t, d_records, 0, n, d_scores, d_features, d_status, (cudaStream_t)stream);
+}
+
+static int check_points(const ls_task* t, int32_t pbytes) {
+  if (pbytes != 4 && pbytes != 8) return fail(LS_E_ARG, "point_bytes must be 4 or 8");
+  if (t->host.sp_n < 1) return fail(LS_E_ARG, "no schedule space attached (ls_task_set_space)");
+  return LS_E_OK;
+}
+
+int ls_score_points(ls_task* t, const void* d_points, int32_t pbytes, int64_t n, double* d_scores,
+                    double* d_features, int32_t* d_status, void* stream) {
+  if (!t || n < 0 || (n && !d_points)) return fail(LS_E_ARG, "bad argument");
+  if (int rc = check_points(t, pbytes)) return rc;
+  if (n == 0) return LS_E_OK;
+  CUDA_TRY(cudaSetDevice(t->device));
+  return score_device(t, d_points, pbytes, n, d_scores, d_features, d_status, (cudaStream_t)stream);
+}
+
+static int topk_device(ls_task* t, const void* d_src, int pbytes, int64_t n, int64_t base_index, int32_t k,
                        double* d_top_scores, int64_t* d_top_index, unsigned long long* d_valid, cudaStream_t s) {
-  const TopkFn fn = topk_fn(t->host, k);
-  const size_t sm = smem_topk(t->host, k);
+  const int mode = mode_of(t);
+  const TopkFn fn = topk_fn(t->host, mode, pbytes);
+  const size_t sm = smem_topk(t->host, k, mode);
   const int grid = n > 0 ? grid_for(t, n, blocks_per_sm(fn, sm)) : 1;
   const int ngroups = (grid + TK_GROUP - 1) / TK_GROUP;
   const size_t ws_keys = sizeof(Key) * ((size_t)grid + ngroups) * k;
@@ -1487,19 +2126,16 @@ static int topk_device(ls_task* t, const ls_record* d_records, int64_t n, int64_
   Key* group_out = block_out + (size_t)grid * k;
   unsigned int* tickets = reinterpret_cast<unsigned int*>(ws + ws_keys);
   CUDA_TRY(cudaMemsetAsync(tickets, 0, sizeof(unsigned int) * (ngroups + 1), s));
-  fn<<<grid, TPB, sm, s>>>(t->d_task, d_records, n, base_index, k, block_out, group_out, tickets, d_top_scores,
-                           d_top_index, d_valid);
+  fn<<<grid, TPB, sm, s>>>(t->d_task, d_src, pbytes, n, base_index, k, block_out, group_out, tickets, d_top_scores,
+                           d_top_index, d_valid, topk_buf(k));
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaFreeAsync(ws, s));
   return LS_E_OK;
 }
 
-int ls_score_topk(ls_task* t, const ls_record* d_records, int64_t n, int64_t base_index, int32_t k,
-                  double* d_top_scores, int64_t* d_top_index, int64_t* d_n_valid, void* stream) {
-  if (!t || n < 0 || (n && !d_records) || !d_top_scores || !d_top_index) return fail(LS_E_ARG, "bad argument");
-  if (k < 1 || k > TK_MAXK) return fail(LS_E_ARG, "k must be in 1..1024");
+static int score_topk_any(ls_task* t, const void* d_src, int pbytes, int64_t n, int64_t base_index, int32_t k,
+                          double* d_top_scores, int64_t* d_top_index, int64_t* d_n_valid, cudaStream_t s) {
   CUDA_TRY(cudaSetDevice(t->device));
-  cudaStream_t s = (cudaStream_t)stream;
   unsigned long long* valid = reinterpret_cast<unsigned long long*>(d_n_valid);
   unsigned long long* tmp = nullptr;
   if (!valid) {
@@ -1507,9 +2143,64 @@ int ls_score_topk(ls_task* t, const ls_record* d_records, int64_t n, int64_t bas
     valid = tmp;
   }
   CUDA_TRY(cudaMemsetAsync(valid, 0, sizeof(unsigned long long), s));
-  int rc = topk_device(t, d_records, n, base_index, k, d_top_scores, d_top_index, valid, s);
+  int rc = topk_device(t, d_src, pbytes, n, base_index, k, d_top_scores, d_top_index, valid, s);
   if (tmp) cudaFreeAsync(tmp, s);
   return rc;
+}
+
+int ls_score_topk(ls_task* t, const ls_record* d_records, int64_t n, int64_t base_index, int32_t k,
+                  double* d_top_scores, int64_t* d_top_index, int64_t* d_n_valid, void* stream) {
+  if (!t || n < 0 || (n && !d_records) || !d_top_scores || !d_top_index) return fail(LS_E_ARG, "bad argument");
+  if (k < 1 || k > TK_MAXK) return fail(LS_E_ARG, "k must be in 1..1024");
+  return score_topk_any(t, d_records, 0, n, base_index, k, d_top_scores, d_top_index, d_n_valid,
+                        (cudaStream_t)stream);
+}
+
+int ls_score_topk_points(ls_task* t, const void* d_points, int32_t pbytes, int64_t n, int64_t base_index, int32_t k,
+                         double* d_top_scores, int64_t* d_top_index, int64_t* d_n_valid, void* stream) {
+  if (!t || n < 0 || (n && !d_points) || !d_top_scores || !d_top_index) return fail(LS_E_ARG, "bad argument");
+  if (k < 1 || k > TK_MAXK) return fail(LS_E_ARG, "k must be in 1..1024");
+  if (int rc = check_points(t, pbytes)) return rc;
+  return score_topk_any(t, d_points, pbytes, n, base_index, k, d_top_scores, d_top_index, d_n_valid,
+                        (cudaStream_t)stream);
+}
+
+int ls_task_set_space(ls_task* t, const ls_space_desc* sp) {
+  if (!t || !sp || sp->n_axes < 1 || sp->n_axes > LS_MAX_AXES) return fail(LS_E_ARG, "bad space");
+  std::vector<uint64_t> vals;
+  DAxis ax[LS_MAX_AXES];
+  memset(ax, 0, sizeof(ax));
+  for (int a = 0; a < sp->n_axes; ++a) {
+    const ls_axis& x = sp->axes[a];
+    if (x.kind < LS_AX_PARAM || x.kind > LS_AX_BIT || x.n_choices < 1) return fail(LS_E_ARG, "bad axis");
+    if ((x.kind == LS_AX_PARAM || x.kind == LS_AX_VEC) && (x.param < 0 || x.param >= LS_MAX_PARAMS))
+      return fail(LS_E_ARG, "bad axis param slot");
+    if ((x.kind == LS_AX_VEC || x.kind == LS_AX_BIT) && (x.bit < 0 || x.bit >= 32)) return fail(LS_E_ARG, "bad axis bit");
+    if (x.kind == LS_AX_BIT && x.n_choices > 2) return fail(LS_E_ARG, "on/off axis with more than 2 choices");
+    if (x.kind != LS_AX_BIT && !x.values) return fail(LS_E_ARG, "axis without values");
+    ax[a].kind = (int8_t)x.kind;
+    ax[a].param = (int8_t)x.param;
+    ax[a].bit = (int8_t)x.bit;
+    ax[a].n = (uint32_t)x.n_choices;
+    ax[a].voff = (uint32_t)vals.size();
+    ax[a].magic = x.n_choices >= 2 ? (~0ull / (uint64_t)x.n_choices) + 1 : 0;
+    if (x.kind != LS_AX_BIT)
+      for (int c = 0; c < x.n_choices; ++c) {
+        if ((x.kind == LS_AX_PARAM || x.kind == LS_AX_VEC) && x.values[c] > 0xFFFFu)
+          return fail(LS_E_ARG, "factor/width above 65535");
+        vals.push_back(x.values[c]);
+      }
+  }
+  std::lock_guard<std::mutex> g(t->mu);
+  CUDA_TRY(cudaSetDevice(t->device));
+  uint64_t* dv = nullptr;
+  CUDA_TRY(cudaMalloc(&dv, sizeof(uint64_t) * std::max<size_t>(1, vals.size())));
+  if (!vals.empty()) CUDA_TRY(cudaMemcpy(dv, vals.data(), sizeof(uint64_t) * vals.size(), cudaMemcpyHostToDevice));
+  t->retired.push_back(dv);
+  t->host.sp_n = sp->n_axes;
+  t->host.sp_vals = dv;
+  memcpy(t->host.sp_ax, ax, sizeof(ax));
+  return upload(t);
 }
 
 int ls_topk_merge(const double* d_scores, const int64_t* d_index, int32_t n_lists, int32_t k_in, int32_t k_out,
@@ -1531,13 +2222,11 @@ int ls_topk_merge(const double* d_scores, const int64_t* d_index, int32_t n_list
   return LS_E_OK;
 }
 
-int ls_score_topk_host(ls_task* t, const ls_record* h_records, int64_t n, int64_t base_index, int32_t k,
-                       double* h_top_scores, int64_t* h_top_index, int64_t* h_n_valid, void* stream) {
-  if (!t || n < 0 || (n && !h_records) || !h_top_scores || !h_top_index) return fail(LS_E_ARG, "bad argument");
-  if (k < 1 || k > TK_MAXK) return fail(LS_E_ARG, "k must be in 1..1024");
+static int score_topk_host_any(ls_task* t, const void* h_src, int pbytes, int64_t n, int64_t base_index, int32_t k,
+                               double* h_top_scores, int64_t* h_top_index, int64_t* h_n_valid, cudaStream_t s) {
   CUDA_TRY(cudaSetDevice(t->device));
-  cudaStream_t s = (cudaStream_t)stream;
-  const int64_t CH = 1 << 18;  // records per chunk (8 MiB): copy of chunk c+1 overlaps scoring of chunk c
+  const size_t esz = pbytes ? (size_t)pbytes : sizeof(ls_record);
+  const int64_t CH = (int64_t)((8u << 20) / esz);  // 8 MiB chunks: copy of chunk c+1 overlaps scoring of chunk c
   const int64_t nch = std::max<int64_t>(1, (n + CH - 1) / CH);
   cudaStream_t cp;
   CUDA_TRY(cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking));
@@ -1547,16 +2236,15 @@ int ls_score_topk_host(ls_task* t, const ls_record* h_records, int64_t n, int64_
     CUDA_TRY(cudaEventCreateWithFlags(&ready[b], cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&freed[b], cudaEventDisableTiming));
   }
-  ls_record* buf[2] = {nullptr, nullptr};
+  unsigned char* buf[2] = {nullptr, nullptr};
   double* ls = nullptr;
   int64_t* li = nullptr;
   unsigned long long* valid = nullptr;
   double* out_s = nullptr;
   int64_t* out_i = nullptr;
   int rc = LS_E_OK;
-  CUDA_TRY(cudaEventRecord(ev_start, s));
-  CUDA_TRY(cudaStreamWaitEvent(cp, ev_start, 0));
-  for (int b = 0; b < 2; ++b) CUDA_TRY(cudaMallocAsync(&buf[b], sizeof(ls_record) * std::min(CH, std::max<int64_t>(n, 1)), s));
+  for (int b = 0; b < 2; ++b)
+    CUDA_TRY(cudaMallocAsync(&buf[b], esz * (size_t)std::min(CH, std::max<int64_t>(n, 1)), s));
   CUDA_TRY(cudaMallocAsync(&ls, sizeof(double) * nch * k, s));
   CUDA_TRY(cudaMallocAsync(&li, sizeof(int64_t) * nch * k, s));
   CUDA_TRY(cudaMallocAsync(&valid, sizeof(unsigned long long), s));
@@ -1565,19 +2253,19 @@ int ls_score_topk_host(ls_task* t, const ls_record* h_records, int64_t n, int64_
   CUDA_TRY(cudaMemsetAsync(valid, 0, sizeof(unsigned long long), s));
   CUDA_TRY(cudaEventRecord(ev_start, s));
   CUDA_TRY(cudaStreamWaitEvent(cp, ev_start, 0));
+  const unsigned char* src = reinterpret_cast<const unsigned char*>(h_src);
   for (int64_t c = 0; c < nch && rc == LS_E_OK; ++c) {
     const int b = (int)(c & 1);
     const int64_t off = c * CH, m = std::min(CH, n - off);
     if (c >= 2) CUDA_TRY(cudaStreamWaitEvent(cp, freed[b], 0));
-    if (m > 0) CUDA_TRY(cudaMemcpyAsync(buf[b], h_records + off, sizeof(ls_record) * m, cudaMemcpyHostToDevice, cp));
+    if (m > 0) CUDA_TRY(cudaMemcpyAsync(buf[b], src + off * esz, esz * m, cudaMemcpyHostToDevice, cp));
     CUDA_TRY(cudaEventRecord(ready[b], cp));
     CUDA_TRY(cudaStreamWaitEvent(s, ready[b], 0));
-    rc = topk_device(t, buf[b], std::max<int64_t>(m, 0), base_index + off, k, ls + c * k, li + c * k, valid, s);
+    rc = topk_device(t, buf[b], pbytes, std::max<int64_t>(m, 0), base_index + off, k, ls + c * k, li + c * k, valid,
+                     s);
     CUDA_TRY(cudaEventRecord(freed[b], s));
   }
-  if (rc == LS_E_OK) {
-    rc = ls_topk_merge(ls, li, (int32_t)nch, k, k, out_s, out_i, s);
-  }
+  if (rc == LS_E_OK) rc = ls_topk_merge(ls, li, (int32_t)nch, k, k, out_s, out_i, s);
   CUDA_TRY(cudaMemcpyAsync(h_top_scores, out_s, sizeof(double) * k, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaMemcpyAsync(h_top_index, out_i, sizeof(int64_t) * k, cudaMemcpyDeviceToHost, s));
   unsigned long long hv = 0;
@@ -1598,6 +2286,24 @@ int ls_score_topk_host(ls_task* t, const ls_record* h_records, int64_t n, int64_
   }
   if (h_n_valid) *h_n_valid = (int64_t)hv;
   return rc;
+}
+
+int ls_score_topk_host(ls_task* t, const ls_record* h_records, int64_t n, int64_t base_index, int32_t k,
+                       double* h_top_scores, int64_t* h_top_index, int64_t* h_n_valid, void* stream) {
+  if (!t || n < 0 || (n && !h_records) || !h_top_scores || !h_top_index) return fail(LS_E_ARG, "bad argument");
+  if (k < 1 || k > TK_MAXK) return fail(LS_E_ARG, "k must be in 1..1024");
+  return score_topk_host_any(t, h_records, 0, n, base_index, k, h_top_scores, h_top_index, h_n_valid,
+                             (cudaStream_t)stream);
+}
+
+int ls_score_topk_points_host(ls_task* t, const void* h_points, int32_t pbytes, int64_t n, int64_t base_index,
+                              int32_t k, double* h_top_scores, int64_t* h_top_index, int64_t* h_n_valid,
+                              void* stream) {
+  if (!t || n < 0 || (n && !h_points) || !h_top_scores || !h_top_index) return fail(LS_E_ARG, "bad argument");
+  if (k < 1 || k > TK_MAXK) return fail(LS_E_ARG, "k must be in 1..1024");
+  if (int rc = check_points(t, pbytes)) return rc;
+  return score_topk_host_any(t, h_points, pbytes, n, base_index, k, h_top_scores, h_top_index, h_n_valid,
+                             (cudaStream_t)stream);
 }
 
 }  // extern "C"

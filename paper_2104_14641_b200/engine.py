@@ -44,6 +44,12 @@ def lib():
     L.ls_score_topk.argtypes = [vp, vp, i64, i64, i32, vp, vp, vp, vp]
     L.ls_topk_merge.argtypes = [vp, vp, i32, i32, i32, vp, vp, vp]
     L.ls_score_topk_host.argtypes = [vp, vp, i64, i64, i32, vp, vp, vp, vp]
+    L.ls_task_set_path.argtypes = [vp, i32]
+    L.ls_task_set_space.argtypes = [vp, vp]
+    L.ls_score_points.argtypes = [vp, vp, i32, i64, vp, vp, vp, vp]
+    L.ls_score_topk_points.argtypes = [vp, vp, i32, i64, i64, i32, vp, vp, vp, vp]
+    L.ls_score_topk_points_host.argtypes = [vp, vp, i32, i64, i64, i32, vp, vp, vp, vp]
+    L.ls_task_path.argtypes = [vp]
     if L.ls_abi_version() != abi.ABI_VERSION:
         raise EngineError("libloopscout_b200 ABI version mismatch")
     _lib = L
@@ -103,6 +109,17 @@ class Task:
         except Exception:  # noqa: BLE001
             pass
 
+    # -- scoring path -----------------------------------------------------------------
+    PATH_AUTO, PATH_GENERIC, PATH_TABULATED = 0, 1, 2
+
+    def set_path(self, path: int):
+        """Force the generic or the tabulated kernel (both bit-identical; include/loopscout_b200.h)."""
+        _check(lib().ls_task_set_path(self._h, int(path)), "ls_task_set_path")
+
+    @property
+    def path(self) -> int:
+        return lib().ls_task_path(self._h)
+
     # -- unroll table ---------------------------------------------------------------
     def prepare_unroll_for(self, d_records, stream=None):
         """Collect the innermost-unroll products these records need and precompute them."""
@@ -158,6 +175,54 @@ class Task:
             _check(lib().ls_score_topk_host(self._h, ptr, n, int(base_index), int(k), s.ctypes.data,
                                             i.ctypes.data, nv.ctypes.data, _stream(torch, stream)),
                    "ls_score_topk_host")
+        return s, i, int(nv[0])
+
+
+    # -- points API (candidates as space points) --------------------------------------
+    def set_space(self, space: "abi.SpaceDesc"):
+        """Attach a schedule space (pack.SpaceTemplate.space_desc()) for the points API."""
+        _check(lib().ls_task_set_space(self._h, C.addressof(space)), "ls_task_set_space")
+
+    def score_points(self, d_points, features: bool = True, stream=None):
+        """ls_score over a CUDA int32/int64 tensor of space points."""
+        torch = _torch()
+        n = d_points.shape[0]
+        dev = d_points.device
+        scores = torch.empty(n, dtype=torch.float64, device=dev)
+        feats = torch.empty((n, self.nfeat), dtype=torch.float64, device=dev) if features else None
+        status = torch.empty(n, dtype=torch.int32, device=dev)
+        _check(lib().ls_score_points(self._h, _dptr(d_points), d_points.element_size(), n, _dptr(scores),
+                                     _dptr(feats), _dptr(status), _stream(torch, stream)), "ls_score_points")
+        return scores, feats, status
+
+    def score_topk_points(self, d_points, k: int, base_index: int = 0, stream=None, out=None):
+        torch = _torch()
+        dev = d_points.device
+        if out is None:
+            out = (torch.empty(k, dtype=torch.float64, device=dev),
+                   torch.empty(k, dtype=torch.int64, device=dev),
+                   torch.zeros(1, dtype=torch.int64, device=dev))
+        s, i, nv = out
+        _check(lib().ls_score_topk_points(self._h, _dptr(d_points), d_points.element_size(), d_points.shape[0],
+                                          int(base_index), int(k), _dptr(s), _dptr(i), _dptr(nv),
+                                          _stream(torch, stream)), "ls_score_topk_points")
+        return s, i, nv
+
+    def score_topk_points_host(self, h_points, k: int, base_index: int = 0, stream=None):
+        """Host points (numpy uint32/uint64 or pinned torch tensor) in, host top-k out."""
+        torch = _torch()
+        if isinstance(h_points, np.ndarray):
+            h_points = np.ascontiguousarray(h_points)
+            ptr, n, eb = h_points.ctypes.data, len(h_points), h_points.itemsize
+        else:
+            ptr, n, eb = h_points.data_ptr(), h_points.shape[0], h_points.element_size()
+        s = np.empty(k, np.float64)
+        i = np.empty(k, np.int64)
+        nv = np.zeros(1, np.int64)
+        with torch.cuda.device(self.device):
+            _check(lib().ls_score_topk_points_host(self._h, ptr, eb, n, int(base_index), int(k), s.ctypes.data,
+                                                   i.ctypes.data, nv.ctypes.data, _stream(torch, stream)),
+                   "ls_score_topk_points_host")
         return s, i, int(nv[0])
 
 

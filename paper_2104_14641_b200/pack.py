@@ -418,6 +418,54 @@ class SpaceTemplate:
         recs["flags"] = flags
         return recs
 
+    # -- points API ---------------------------------------------------------------------
+    @property
+    def size(self) -> int:
+        return int(np.prod([int(n) for n in self.sizes], dtype=object))
+
+    def space_desc(self) -> abi.SpaceDesc:
+        """The space for ls_task_set_space; keeps the value arrays alive on the descriptor."""
+        if len(self.tables) > abi.MAX_AXES:
+            raise PackError(f"more than {abi.MAX_AXES} space axes")
+        d = abi.SpaceDesc()
+        d.n_axes = len(self.tables)
+        keep = []
+        for a, (kind, where, vals) in enumerate(self.tables):
+            ax = d.axes[a]
+            ax.n_choices = len(vals)
+            v = np.ascontiguousarray(np.asarray(vals).astype(np.uint64))
+            keep.append(v)
+            ax.values = v.ctypes.data_as(abi.C.POINTER(abi.C.c_uint64))
+            if kind == "param":
+                ax.kind, ax.param = abi.AX_PARAM, where
+            elif kind == "perm":
+                ax.kind = abi.AX_PERM
+            elif kind == "vec":
+                ax.kind, ax.param, ax.bit = abi.AX_VEC, where[0], where[1]
+            else:
+                ax.kind, ax.bit = abi.AX_BIT, where
+        d._keep = keep
+        return d
+
+    def points_from_indices(self, idx: np.ndarray) -> np.ndarray:
+        """Mixed-radix points (axis 0 most significant); uint32 when the space fits, else uint64."""
+        idx = np.asarray(idx, np.int64).reshape(-1, self.dim)
+        if self.size > 2 ** 64:
+            raise PackError("space larger than 2^64 points")
+        p = np.zeros(idx.shape[0], np.uint64)
+        for a, n in enumerate(self.sizes):
+            p = p * np.uint64(int(n)) + idx[:, a].astype(np.uint64)
+        return p.astype(np.uint32) if self.size <= 2 ** 32 else p
+
+    def indices_from_points(self, pts: np.ndarray) -> np.ndarray:
+        p = np.asarray(pts).astype(np.uint64)
+        out = np.zeros((len(p), self.dim), np.int64)
+        for a in range(self.dim - 1, -1, -1):
+            n = np.uint64(int(self.sizes[a]))
+            out[:, a] = (p % n).astype(np.int64)
+            p = p // n
+        return out
+
     def indices_from_theta(self, thetas: np.ndarray) -> np.ndarray:
         """ThetaEncoding.decode per row: clip(round_half_even(x), 0, n-1) (ls/es.py:57-62)."""
         t = np.asarray(thetas, np.float64).reshape(-1, self.dim)

@@ -22,13 +22,26 @@ def _engine():
     return engine
 
 
+PATHS = [1, 2]  # LS_PATH_GENERIC, LS_PATH_TABULATED (include/loopscout_b200.h)
+
+
+def _set_path(task, path):
+    """Force a scoring path; False if the task is not eligible for it."""
+    if path == 2 and task.path != 2:
+        return False
+    task.set_path(path)
+    return True
+
+
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("name", SPACE_FIXTURES)
-def test_space_fixtures_bit_exact(torch, name):
+def test_space_fixtures_bit_exact(torch, name, path):
     E = _engine()
     st, recs, z = space_case(name)
     for a in z["arches"]:
         a = str(a)
         task = E.Task(st.template.desc(arch_named(a), launch()), 0)
+        assert _set_path(task, path), "every BASELINE space is eligible for the tabulated path"
         s, f, status = task.score(E.to_device_records(recs))
         torch.cuda.synchronize()
         assert (status.cpu().numpy() == 0).all()
@@ -41,8 +54,9 @@ def _rank_params():
     return [(c["program"], a) for c in rank_cases()["cases"] for a in c["results"]]
 
 
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("program,arch", _rank_params())
-def test_rank_cases(torch, program, arch):
+def test_rank_cases(torch, program, arch, path):
     """Random valid/invalid schedules of every transform kind: scores, features and failure classes."""
     E = _engine()
     case = next(c for c in rank_cases()["cases"] if c["program"] == program)
@@ -55,6 +69,9 @@ def test_rank_cases(torch, program, arch):
             unsupported += len(g.index)
             continue
         task = E.Task(g.template.desc(ar, launch()), 0)
+        if not _set_path(task, path):
+            task.close()
+            continue
         d = E.to_device_records(g.records)
         task.prepare_unroll_for(d)
         s, f, st = task.score(d)
@@ -85,21 +102,24 @@ def test_gemm_top64_matches_reference(torch):
         task.close()
 
 
-def _conv_task(arch="x86-avx2", n=1 << 18, seed=3, reorders=512):
+def _conv_task(arch="x86-avx2", n=1 << 18, seed=3, reorders=512, path=0):
     E = _engine()
     from paper_2104_14641_b200 import workloads as W
     from paper_2104_14641_b200.pack import SpaceTemplate
     st = SpaceTemplate(W.program(W.conv2d_json()), W.conv_space(reorders, 1))
     recs = st.records_from_indices(W.distinct_indices(st.sizes, n, seed))
     task = E.Task(st.template.desc(arch_named(arch), launch()), 0)
+    if path:
+        task.set_path(path)
     return task, recs
 
 
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("arch", ["x86-avx2", "nvidia-volta"])
-def test_fused_topk_equals_full_sort_large(torch, arch):
+def test_fused_topk_equals_full_sort_large(torch, arch, path):
     """Size-independent property at 2^18: fused top-k == stable sort of the per-candidate scores."""
     E = _engine()
-    task, recs = _conv_task(arch)
+    task, recs = _conv_task(arch, path=path)
     d = E.to_device_records(recs)
     s, _, st = task.score(d, features=False)
     for k in (1, 64, 1000):
@@ -111,12 +131,13 @@ def test_fused_topk_equals_full_sort_large(torch, arch):
         assert int(nv.item()) == len(recs)
 
 
-def test_oracle_parity_sample_conv(torch):
+@pytest.mark.parametrize("path", PATHS)
+def test_oracle_parity_sample_conv(torch, path):
     """Device vs oracle on a 4096-candidate sample of the bench workload (all three arches)."""
     import pyoracle
     E = _engine()
     for a in ("x86-avx2", "aarch64-neon", "nvidia-volta"):
-        task, recs = _conv_task(a, n=4096, seed=11)
+        task, recs = _conv_task(a, n=4096, seed=11, path=path)
         s, f, st = task.score(E.to_device_records(recs))
         torch.cuda.synchronize()
         rs, rf, rst = pyoracle.evaluate(task.desc, recs, nthreads=8)
@@ -204,3 +225,63 @@ def test_score_batch_api(torch):
     want = sorted(ok, key=lambda i: (res["scores"][i], i))
     assert [r[0] for r in rows] == want
     assert sorted(i for i, _ in errors) == [i for i, e in enumerate(res["errors"]) if e is not None]
+
+
+def _es_space(name):
+    from paper_2104_14641_b200 import ir
+    from paper_2104_14641_b200.pack import SpaceTemplate
+    r = next(x for x in json.loads((GOLDEN / "es_runs.json").read_text()) if x["name"] == name)
+    return SpaceTemplate(ir.parse_program(json.dumps(r["program"])), r["space"]), r["arch"]
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("which", ["gemm1024", "conv56", "es:conv_small"])
+def test_points_equal_records(torch, which, path):
+    """Points API (space-point decode on device) == records API on the same candidates."""
+    E = _engine()
+    from paper_2104_14641_b200 import workloads as W
+    if which.startswith("es:"):
+        st, arch = _es_space(which[3:])
+        idx = W.distinct_indices(st.sizes, min(4096, st.size), 9)
+    else:
+        st, _, z = space_case(which)
+        arch = "x86-avx2"
+        idx = z["idx"]
+    for a in (arch, "nvidia-volta"):
+        task = E.Task(st.template.desc(arch_named(a), launch()), 0)
+        if not _set_path(task, path):
+            task.close()
+            continue
+        task.set_space(st.space_desc())
+        recs = st.records_from_indices(idx)
+        pts = st.points_from_indices(idx)
+        assert np.array_equal(st.indices_from_points(pts), idx)
+        d = E.to_device_records(recs)
+        task.prepare_unroll_for(d)
+        s, f, stt = task.score(d)
+        dp = torch.from_numpy(pts.view(np.int32) if pts.dtype == np.uint32 else pts.view(np.int64)).cuda()
+        ps, pf, pst = task.score_points(dp)
+        torch.cuda.synchronize()
+        assert torch.equal(stt, pst)
+        ok = stt == 0
+        assert torch.equal(s[ok], ps[ok]) and torch.equal(f[ok], pf[ok])
+        k = min(64, len(idx))
+        ts, ti, nv = task.score_topk(d, k, base_index=3)
+        qs, qi, qnv = task.score_topk_points(dp, k, base_index=3)
+        hs, hi, hnv = task.score_topk_points_host(pts, k, base_index=3)
+        torch.cuda.synchronize()
+        assert torch.equal(ti, qi) and torch.equal(ts, qs) and int(nv.item()) == int(qnv.item()) == hnv
+        assert hi.tolist() == ti.cpu().tolist() and np.array_equal(hs, ts.cpu().numpy())
+        task.close()
+
+
+def test_points_out_of_range(torch):
+    E = _engine()
+    st, _, z = space_case("gemm1024")
+    task = E.Task(st.template.desc(arch_named("x86-avx2"), launch()), 0)
+    task.set_space(st.space_desc())
+    pts = np.array([0, st.size - 1, st.size, 2 ** 32 - 1], np.uint32)
+    s, f, stt = task.score_points(torch.from_numpy(pts.view(np.int32)).cuda())
+    torch.cuda.synchronize()
+    assert stt.cpu().tolist()[2:] == [19, 19] and stt.cpu().tolist()[:2] == [0, 0]
+    task.close()

@@ -144,3 +144,23 @@ def test_reference_objects_pack_identically():
         d2 = theirs.template.desc(L.load_arch(name), L.KernelLaunch.from_json(W.KERNEL_LAUNCH))
         assert bytes(d1) == bytes(d2)
         assert mine.records.tobytes() == theirs.records.tobytes()
+
+
+def test_space_points_roundtrip():
+    """Mixed-radix space points (points API) round-trip to per-axis choice indices."""
+    import numpy as np
+    from paper_2104_14641_b200 import abi
+    from paper_2104_14641_b200 import workloads as W
+    from paper_2104_14641_b200.pack import SpaceTemplate
+    st = SpaceTemplate(W.program(W.conv2d_json()), W.conv_space(512, 1))
+    idx = W.distinct_indices(st.sizes, 5000, 4)
+    pts = st.points_from_indices(idx)
+    assert pts.dtype == np.uint32 and st.size == int(np.prod(st.sizes))
+    assert np.array_equal(st.indices_from_points(pts), idx)
+    d = st.space_desc()
+    assert d.n_axes == len(st.axes)
+    kinds = [d.axes[a].kind for a in range(d.n_axes)]
+    assert kinds.count(abi.AX_PERM) == 1 and kinds.count(abi.AX_PARAM) == 4
+    for a in range(d.n_axes):
+        vals = [d.axes[a].values[c] for c in range(d.axes[a].n_choices)]
+        assert vals == [int(v) for v in st.tables[a][2]]
