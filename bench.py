@@ -34,6 +34,8 @@ METRIC = "candidate schedules scored+ranked/sec at 1/2/4/8 B200; % HBM roofline;
 UNIT = "candidates/s"
 REORDERS = 4096  # 3136 tile points x 4096 chain orders = 12.8M distinct candidates (>= 8 x 2^20)
 RECORD_BYTES = 32
+POINT_BYTES = 4
+PROFILE_JSON = "ncu_score_topk_r01.json"
 
 
 def parse():
@@ -70,7 +72,8 @@ def config_dict(args, n):
                         f"{REORDERS} 11-loop orders = 12.8M points), {n} distinct packed candidates per GPU "
                         f"per step, score + top-{args.k} by (score, index)",
             "config": "BASELINE.json configs[1]", "arch": args.arch, "candidates_per_gpu": n, "k": args.k,
-            "record_bytes": RECORD_BYTES, "l2": "flushed between timed steps (256 MiB write)"}
+            "candidate_encoding": "space point (uint32 mixed-radix choice indices, 4 B)",
+            "l2": "flushed between timed steps (256 MiB write)"}
 
 
 # -- CPU baseline (the oracle port of the reference algorithm) ---------------------------------
@@ -174,6 +177,20 @@ class ClockSampler:
 # -- B200 arm ------------------------------------------------------------------------------------
 
 
+def _timed(step, steps, flush, stream, torch, kern=None):
+    """Device time of `steps` calls of step() (L2 flushed before each), kernel-only events around kern()."""
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for j in range(steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        ev[j][0].record(stream)
+        step(kev[j])
+        ev[j][1].record(stream)
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in ev], [a.elapsed_time(b) for a, b in kev]
+
+
 def b200_arm(args):
     import torch
     import torch.distributed as dist
@@ -181,6 +198,7 @@ def b200_arm(args):
     from paper_2104_14641_b200.build import build
     from paper_2104_14641_b200.dist import gather_topk
     from paper_2104_14641_b200.engine import Task, to_device_records
+    from paper_2104_14641_b200 import workloads as W
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -200,90 +218,109 @@ def b200_arm(args):
     task = Task(desc, dev)
     if args.path:
         task.set_path(args.path)
-    recs = records_for(st, rank * n, n)
+    task.set_space(st.space_desc())
+    idx = W.distinct_indices(st.sizes, n, 2104, start=rank * n)
+    recs = st.records_from_indices(idx)
+    pts = st.points_from_indices(idx)
+    assert pts.dtype == np.uint32
     d_rec = to_device_records(recs, dev)
+    d_pts = torch.from_numpy(pts.view(np.int32)).to(dev)
     base = rank * n
-    pinned = torch.from_numpy(recs.view(np.uint8).reshape(-1, RECORD_BYTES)).pin_memory()
+    pinned_pts = torch.from_numpy(pts.view(np.int32)).pin_memory()
+    pinned_rec = torch.from_numpy(recs.view(np.uint8).reshape(-1, RECORD_BYTES)).pin_memory()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
 
-    def step():
-        s, i, nv = task.score_topk(d_rec, k, base_index=base)
-        if world > 1:
-            s, i = gather_topk(s, i, k)
-        return s, i, nv
+    def make_step(points: bool):
+        def step(kev=None):
+            if kev:
+                kev[0].record(stream)
+            if points:
+                s, i, nv = task.score_topk_points(d_pts, k, base_index=base)
+            else:
+                s, i, nv = task.score_topk(d_rec, k, base_index=base)
+            if kev:
+                kev[1].record(stream)
+            if world > 1:
+                s, i = gather_topk(s, i, k)
+            step.out = (s, i, nv)
+        return step
 
+    step_p, step_r = make_step(True), make_step(False)
     for _ in range(max(3, args.warmup)):
-        step()
+        step_p()
+        step_r()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
 
-    # ---- device-resident throughput (value) ----
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    kern = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    def max_over_ranks(ms):
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
+
+    # ---- device-resident throughput (value: points; records as a secondary line item) ----
     with ClockSampler(dev) as clk:
         t_soak = time.perf_counter()  # keep the GPU loaded while nvidia-smi starts sampling
         while time.perf_counter() - t_soak < 1.5:
-            step()
+            step_p()
             torch.cuda.synchronize()
-        for j in range(args.steps):
-            flush.zero_()
-            torch.cuda.synchronize()
-            ev[j][0].record(stream)
-            kern[j][0].record(stream)
-            s, i, nv = task.score_topk(d_rec, k, base_index=base)
-            kern[j][1].record(stream)
-            if world > 1:
-                s, i = gather_topk(s, i, k)
-            ev[j][1].record(stream)
-        torch.cuda.synchronize()
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    kern_ms = [a.elapsed_time(b) for a, b in kern]
-    total_ms = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
+        step_ms, kern_ms = _timed(step_p, args.steps, flush, stream, torch)
+        rstep_ms, rkern_ms = _timed(step_r, args.steps, flush, stream, torch)
     if world > 1:
         dist.barrier()
-        dist.all_reduce(total_ms, op=dist.ReduceOp.MAX)
-    total_s = total_ms.item() / 1e3
+    total_s = max_over_ranks(sum(step_ms)) / 1e3
     value = world * n * args.steps / total_s
-    top_i = i.cpu().numpy()
-    n_valid = int(nv.item())
+    value_rec = world * n * args.steps / (max_over_ranks(sum(rstep_ms)) / 1e3)
+    top_i = step_p.out[1].cpu().numpy()
+    n_valid = int(step_p.out[2].item())
+    same_paths = top_i.tolist() == step_r.out[1].cpu().tolist()
 
-    # ---- end to end through the C-ABI host-buffer call (H2D + top-k D2H inside) ----
-    for _ in range(2):
-        task.score_topk_host(pinned, k, base_index=base)
-    e2e_ms = []
-    for j in range(max(3, args.steps // 2)):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        a.record(stream)
-        hs, hi, hnv = task.score_topk_host(pinned, k, base_index=base)
-        if world > 1:
-            gs, gi = gather_topk(torch.from_numpy(hs).to(dev), torch.from_numpy(hi).to(dev), k)
-            gi.cpu()
-        b.record(stream)
-        torch.cuda.synchronize()
-        e2e_ms.append(a.elapsed_time(b))
-    e2e_t = torch.tensor([sum(e2e_ms) / len(e2e_ms)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e_value = world * n / (e2e_t.item() / 1e3)
-    same_host = hi.tolist() == task.score_topk_host(pinned, k, base_index=base)[1].tolist()
+    # ---- end to end through the C-ABI host-buffer calls (H2D + top-k D2H inside the timed region) ----
+    def e2e(call, reps):
+        for _ in range(2):
+            call()
+        ms = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            a.record(stream)
+            hs, hi, hnv = call()
+            if world > 1:
+                gs, gi = gather_topk(torch.from_numpy(hs).to(dev), torch.from_numpy(hi).to(dev), k)
+                hi = gi.cpu().numpy()
+            b.record(stream)
+            torch.cuda.synchronize()
+            ms.append(a.elapsed_time(b))
+        return world * n / (max_over_ranks(sum(ms) / len(ms)) / 1e3), hi
 
-    # ---- roofline of the fused score+top-k launch pair ----
+    reps = max(3, args.steps // 2)
+    e2e_value, e2e_top = e2e(lambda: task.score_topk_points_host(pinned_pts, k, base_index=base), reps)
+    e2e_rec, e2e_rtop = e2e(lambda: task.score_topk_host(pinned_rec, k, base_index=base), reps)
+
+    # ---- roofline of the fused launch ----
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak = peaks.get("hbm_gbs", 6650.0)
     peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
     kavg = sum(kern_ms) / len(kern_ms) / 1e3
-    alg_bytes = n * RECORD_BYTES
+    alg_bytes = n * POINT_BYTES
     achieved = alg_bytes / kavg / 1e9
-    traffic = None
-    prof = ROOT / "profiles" / "ncu_score_topk_r01.json"
+    traffic, issue = None, None
+    prof = ROOT / "profiles" / PROFILE_JSON
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+            pj = json.loads(prof.read_text())
+            traffic = pj.get("dram_bytes_per_launch")
+            slots = pj.get("warp_issue_slots_per_candidate")
+            if slots:
+                clk_mhz = peaks.get("sm_max_mhz", 1965.0)
+                ceil = 4 * 148 * clk_mhz * 1e6 / slots
+                issue = {"bound": "issue", "warp_issue_slots_per_candidate": slots,
+                         "ceiling_candidates_per_s": ceil, "achieved_candidates_per_s": n / kavg,
+                         "frac": n / kavg / ceil, "source": f"profiles/{PROFILE_JSON} (ncu) + live kernel time"}
         except ValueError:
-            traffic = None
+            pass
 
     line = None
     if rank == 0:
@@ -293,14 +330,15 @@ def b200_arm(args):
         if not args.no_baseline:
             threads = cpu_cores()
             m = calibrate_sample(desc, st, threads, 10.0)
-            sample = records_for(st, 0, m)
+            sidx = W.distinct_indices(st.sizes, m, 2104)
+            sample = st.records_from_indices(sidx)
             rate, dt, cs, cst = cpu_rate(desc, sample, threads)
             cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
                    "sample": f"{m} candidates of the same workload through oracle/oracle.c (C restatement of "
                              f"the reference path) on {threads} threads, {dt:.1f} s"}
-            ds = to_device_records(sample, dev)
-            gs, _, gst = task.score(ds, features=False)
-            ts, ti, _ = task.score_topk(ds, k)
+            dsp = torch.from_numpy(st.points_from_indices(sidx).view(np.int32)).to(dev)
+            gs, _, gst = task.score_points(dsp, features=False)
+            ts, ti, _ = task.score_topk_points(dsp, k)
             torch.cuda.synchronize()
             want = sorted(range(m), key=lambda q: (cs[q], q))[:k]
             parity = {"sample": m, "scores_bit_exact": bool(np.array_equal(gs.cpu().numpy(), cs)),
@@ -311,19 +349,25 @@ def b200_arm(args):
             "warmup": args.warmup, "ms_per_step": total_s * 1e3 / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int64+f64", "data": "synthetic",
             "config": config_dict(args, n),
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n * RECORD_BYTES,
-                    "d2h_bytes_per_step": k * 16 + 8, "path": "ls_score_topk_host (C-ABI, pinned host records)",
-                    "topk_equals_device_path": same_host and hi.tolist() == top_i.tolist() if world == 1 else None},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n * POINT_BYTES,
+                    "d2h_bytes_per_step": k * 16 + 8,
+                    "path": "ls_score_topk_points_host (C-ABI, pinned host space points, 4 B each)",
+                    "topk_equals_device_path": e2e_top.tolist() == top_i.tolist() if world == 1 else None},
+            "records_path": {"value": value_rec, "e2e": e2e_rec, "record_bytes": RECORD_BYTES,
+                             "path": "ls_score_topk / ls_score_topk_host over 32-byte ls_record (rank path)",
+                             "topk_equals_points_path": same_paths and e2e_rtop.tolist() == top_i.tolist()},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "score_topk_kernel (fused score + block top-k + in-kernel merge tree; one ls_score_topk call)",
+                         "kernel": "score_topk_kernel<4,4,MODE,1> (points decode + tabulated score + block "
+                                   "top-k + in-kernel merge tree; one ls_score_topk_points call)",
                          "kernel_ms": kavg * 1e3, "algorithmic_bytes_per_launch": alg_bytes,
-                         "note": "integer-ALU bound by design: ~32 B read per candidate vs thousands of "
-                                 "integer ops; see profiles/ for issue-slot utilisation"},
+                         "note": "instruction-issue bound by design (4 B read per candidate vs thousands of "
+                                 "integer ops): see issue_roofline"},
+            "issue_roofline": issue,
             "cpu_baseline": cpu, "parity": parity,
             "clocks": clk.summary(),
             "gpu_launches": args.steps * (1 + (2 if world > 1 else 0)),
-            "n_valid_per_gpu": n_valid,
+            "n_valid_per_gpu": n_valid, "path": task.path,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -146,6 +146,12 @@ struct __align__(16) DTask {
   int32_t sp_n, pad5;
   const uint64_t* sp_vals;
   DAxis sp_ax[LS_MAX_AXES];
+  // ---- tensor tables (points path): a tensor's whole footprint per (axis choices, stage mask)
+  int32_t tt_ok, tt_len;
+  const uint64_t* tt;
+  uint32_t tt_off[4], tt_len_t[4], tt_nb[4];
+  uint32_t tt_sh[4], tt_mk[4];            // byte offset of the row entry: (mall >> tt_sh) & tt_mk
+  uint32_t tt_stride[4][LS_MAX_AXES];     // key stride of each axis (0: the axis does not affect the tensor)
   int32_t n_terms;
   DTerm term[MAXTERM];
 };
@@ -870,9 +876,14 @@ __device__ int features_score(const DTask& T, CT& c, int64_t dmov, double* f, do
 // and multiplies looked-up counts.
 // Decode a space point (mixed radix, axis 0 most significant) into the record
 // the host packer would have produced for the same choices (pack.SpaceTemplate).
-__device__ __forceinline__ int point_record(const DTask& T, uint64_t x, ls_record& r) {
+template <bool KEYS>
+__device__ __forceinline__ int point_record(const DTask& T, uint64_t x, ls_record& r, uint32_t* kt) {
   uint64_t lo = 0, hi = 0, perm = 0;
   uint32_t flags = 0;
+  if constexpr (KEYS) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) kt[t] = 0;
+  }
   for (int a = T.sp_n - 1; a >= 0; --a) {
     const DAxis& ax = T.sp_ax[a];
     uint32_t c;
@@ -885,6 +896,10 @@ __device__ __forceinline__ int point_record(const DTask& T, uint64_t x, ls_recor
       const uint64_t q = (x >> 32) ? x / ax.n : __umul64hi(x, ax.magic);
       c = (uint32_t)(x - q * ax.n);
       x = q;
+    }
+    if constexpr (KEYS) {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) kt[t] += c * T.tt_stride[t][a];
     }
     if (ax.kind == LS_AX_BIT) {
       flags |= c << ax.bit;
@@ -906,13 +921,17 @@ __device__ __forceinline__ int point_record(const DTask& T, uint64_t x, ls_recor
   r.perm = perm;
   r.flags = flags;
   r.tag = 0;
+  if constexpr (KEYS) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) kt[t] = 8u * (T.tt_off[t] + (kt[t] << T.tt_nb[t]));
+  }
   return LS_OK;
 }
 
 // Candidate source of the scoring kernels: SRC 0 = ls_record array, 1 = points.
-template <int SRC>
+template <int SRC, bool KEYS>
 __device__ __forceinline__ int load_cand(const DTask& T, const void* __restrict__ src, int pbytes, int64_t i,
-                                         ls_record& r);
+                                         ls_record& r, uint32_t* kt);
 
 template <int TM, int RM, bool SMT>
 __device__ __forceinline__ int32_t tab_at(const int32_t* __restrict__ tab, int32_t i) {
@@ -922,12 +941,71 @@ __device__ __forceinline__ int32_t tab_at(const int32_t* __restrict__ tab, int32
     return __ldg(&tab[i]);
 }
 
+// The movement walk of the tabulated paths (CacheModel._visit_loop,
+// ls/cache.py:167-236, chain form): fp(t) is tensor t's footprint for the
+// stage bits in `mall` (every variable at positions >= p expanded).
+template <int TM, class FP>
+__device__ __forceinline__ int walk_score(const DTask& T, FastCand& c, uint64_t& mall, FP fp, double* f,
+                                          double* score) {
+  const int nT = T.n_tensors;
+  uint32_t tmask[TM];
+  int64_t Fb[TM], dm[TM];
+  uint32_t reuse = 0;
+#pragma unroll
+  for (int t = 0; t < TM; ++t) {
+    tmask[t] = 0;
+    dm[t] = 0;
+    Fb[t] = 0;
+    if (t < nT) {
+      Fb[t] = fp(t);
+      dm[t] = T.t_nacc[t];
+      reuse |= 1u << t;
+      tmask[t] = T.t_vmask[t];
+      if (T.has_optional) {
+        tmask[t] = 0;
+        for (int a = 0; a < T.t_nu[t]; ++a)
+          for (int rr = 0; rr < T.t_rank[t]; ++rr) {
+            const DExpr& e = T.expr[T.t_uacc[t][a]][rr];
+            for (int q = 0; q < e.nt; ++q)
+              if (present(T.term[e.t0 + q], c.flags)) tmask[t] |= 1u << T.term[e.t0 + q].slot;
+          }
+      }
+    }
+  }
+  const int64_t cap = T.cap;
+  for (int p = c.n - 1; p >= 0; --p) {
+    const int v = c.C(p);
+    const int64_t E = c.E(v);
+    mall |= T.vbits[v];
+    int64_t single = 0;
+#pragma unroll
+    for (int t = 0; t < TM; ++t) single += Fb[t];
+#pragma unroll
+    for (int t = 0; t < TM; ++t) {
+      if (t < nT) {
+        const int64_t Ff = fp(t);
+        const bool uses = (tmask[t] >> v) & 1u;
+        bool ru = (reuse >> t) & 1u;
+        if (single > cap && !uses) ru = false;
+        const int64_t per = (single <= cap || ru) ? Ff : dm[t] * E;
+        if (Ff > cap) ru = false;
+        dm[t] = per;
+        reuse = ru ? (reuse | (1u << t)) : (reuse & ~(1u << t));
+        Fb[t] = Ff;
+      }
+    }
+  }
+  int64_t dmov = 0;
+#pragma unroll
+  for (int t = 0; t < TM; ++t) dmov += dm[t];
+  return features_score(T, c, dmov, f, score);
+}
+
 template <int TM, int RM, bool SMT>
 __device__ int eval_fast(const DTask& T, const int32_t* __restrict__ tab, const ls_record& r, FastCand& c,
                          double* f, double* score) {
   const int st = apply_fast(T, r, c);
   if (st) return st;
-  const int nT = T.n_tensors;
   // byte offset of each dimension's row for this candidate's key
   uint32_t kb[TM * RM];
 #pragma unroll
@@ -960,63 +1038,89 @@ __device__ int eval_fast(const DTask& T, const int32_t* __restrict__ tab, const 
     const uint64_t b = (uint64_t)cnt(t * 4 + 2) * cnt(t * 4 + 3);
     return (int64_t)(a * b);
   };
-  uint32_t tmask[TM];
-  int64_t Fb[TM], dm[TM];
-  uint32_t reuse = 0;
-#pragma unroll
-  for (int t = 0; t < TM; ++t) {
-    tmask[t] = 0;
-    dm[t] = 0;
-    Fb[t] = 0;
-    if (t < nT) {
-      Fb[t] = prod(t);
-      dm[t] = T.t_nacc[t];
-      reuse |= 1u << t;
-      tmask[t] = T.t_vmask[t];
-      if (T.has_optional) {
-        tmask[t] = 0;
-        for (int a = 0; a < T.t_nu[t]; ++a)
-          for (int rr = 0; rr < T.t_rank[t]; ++rr) {
-            const DExpr& e = T.expr[T.t_uacc[t][a]][rr];
-            for (int q = 0; q < e.nt; ++q)
-              if (present(T.term[e.t0 + q], c.flags)) tmask[t] |= 1u << T.term[e.t0 + q].slot;
-          }
-      }
-    }
-  }
-  const int64_t cap = T.cap;
-  for (int p = c.n - 1; p >= 0; --p) {
-    const int v = c.C(p);
-    const int64_t E = c.E(v);
-    mall |= T.vbits[v];
-    int64_t single = 0;
-#pragma unroll
-    for (int t = 0; t < TM; ++t) single += Fb[t];
-#pragma unroll
-    for (int t = 0; t < TM; ++t) {
-      if (t < nT) {
-        const int64_t Ff = prod(t);
-        const bool uses = (tmask[t] >> v) & 1u;
-        bool ru = (reuse >> t) & 1u;
-        if (single > cap && !uses) ru = false;
-        const int64_t per = (single <= cap || ru) ? Ff : dm[t] * E;
-        if (Ff > cap) ru = false;
-        dm[t] = per;
-        reuse = ru ? (reuse | (1u << t)) : (reuse & ~(1u << t));
-        Fb[t] = Ff;
-      }
-    }
-  }
-  int64_t dmov = 0;
-#pragma unroll
-  for (int t = 0; t < TM; ++t) dmov += dm[t];
-  return features_score(T, c, dmov, f, score);
+  return walk_score<TM>(T, c, mall, prod, f, score);
 }
 
-// One table entry per thread: decode (dimension, key, mask), rebuild the
-// extents/steps the key implies (apply_schedule's Tile/Vectorize arithmetic,
-// ls/ir.py:361-382, without the chain) and fold the dimension's expressions
-// exactly like the generic path (expr_range + _si_union, ls/cache.py:80-130).
+// Extents/steps of every slot for given record params/flags: apply_schedule's
+// Tile/Vectorize arithmetic (ls/ir.py:361-382) without the chain.  Transforms
+// that would make a candidate fail are skipped (such candidates never look
+// their counts up).
+__device__ void sim_slots(const DTask& T, const int32_t* prm, uint32_t flags, int32_t* E, int32_t* St,
+                          uint32_t& exist) {
+  exist = T.base_exist;
+  for (int p = 0; p < T.n_base; ++p) {
+    E[T.base_slot[p]] = T.base_ext[p];
+    St[T.base_slot[p]] = T.base_step[p];
+  }
+  for (int x = 0; x < T.n_xf; ++x) {
+    const DXform& xf = T.xf[x];
+    if (xf.kind != LS_XF_TILE && xf.kind != LS_XF_VECTORIZE) continue;
+    if (xf.enable_bit >= 0 && !((flags >> xf.enable_bit) & 1u)) continue;
+    const int v = xf.slot, u = xf.new_slot;
+    if (v == NOSLOT || u == NOSLOT || !((exist >> v) & 1u)) continue;
+    const int32_t F = xf.param >= 0 ? prm[xf.param] : xf.value;
+    if (F < 1 || F > E[v]) continue;
+    E[u] = F;
+    St[u] = St[v];
+    E[v] = (E[v] + F - 1) / F;
+    St[v] *= F;
+    exist |= 1u << u;
+  }
+}
+
+// Count of dimension D (4x4 layout) with the variables of `mask` (bit x =
+// dim_var[D][x]) expanded: the generic fold, expr_range + _si_union
+// (ls/cache.py:80-130) in the same order.
+__device__ int32_t dim_count(const DTask& T, int D, uint32_t mask, uint32_t flags, const int32_t* E, const int32_t* St,
+                             uint32_t exist) {
+  uint32_t expanded = 0;
+  for (int x = 0; x < T.dim_nv[D]; ++x)
+    if ((mask >> x) & 1u) expanded |= 1u << T.dim_var[D][x];
+  const int t = D / 4, rr = D % 4;
+  SI u;
+  for (int a = 0; a < T.t_nu[t]; ++a) {
+    const DExpr& ex = T.expr[T.t_uacc[t][a]][rr];
+    SI acc;
+    acc.lo = acc.hi = ex.konst;
+    acc.stride = 0;
+    acc.count = 1;
+    acc.exact = 1;
+    for (int k = 0; k < ex.nt; ++k) {
+      const DTerm& tm = T.term[ex.t0 + k];
+      const int w = tm.slot;
+      if (!present(tm, flags) || !((expanded >> w) & 1u) || !((exist >> w) & 1u)) continue;
+      const int32_t Ew = E[w];
+      if (Ew == 1) continue;
+      const int32_t d = tm.coef * St[w];
+      SI s;
+      s.lo = d > 0 ? 0 : d * (Ew - 1);
+      s.hi = d > 0 ? d * (Ew - 1) : 0;
+      s.stride = abs(d);
+      s.count = Ew;
+      s.exact = 1;
+      acc = si_sum(acc, s);
+    }
+    u = a == 0 ? acc : si_union(u, acc);
+  }
+  return u.count;
+}
+
+// Tensor-table path (points only): one 8-byte lookup gives a tensor footprint.
+template <int TM>
+__device__ int eval_tensor(const DTask& T, const ls_record& r, const uint32_t* kt, FastCand& c, double* f,
+                           double* score) {
+  const int st = apply_fast(T, r, c);
+  if (st) return st;
+  uint64_t mall = 0;
+  const char* tb = reinterpret_cast<const char*>(T.tt);
+  auto fp = [&](int t) -> int64_t {
+    const uint32_t off = kt[t] + ((uint32_t)(mall >> T.tt_sh[t]) & T.tt_mk[t]);
+    return (int64_t)__ldg(reinterpret_cast<const unsigned long long*>(tb + off));
+  };
+  return walk_score<TM>(T, c, mall, fp, f, score);
+}
+
+// One dimension-table entry per thread: decode (dimension, key, mask).
 __global__ void build_tab_kernel(const DTask* __restrict__ g, int32_t* __restrict__ tab) {
   const DTask& T = *g;
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1045,55 +1149,53 @@ __global__ void build_tab_kernel(const DTask* __restrict__ g, int32_t* __restric
       flags |= (uint32_t)d << (src - LS_MAX_PARAMS);
   }
   int32_t E[NSLOT], St[NSLOT];
-  uint32_t exist = T.base_exist;
-  for (int p = 0; p < T.n_base; ++p) {
-    E[T.base_slot[p]] = T.base_ext[p];
-    St[T.base_slot[p]] = T.base_step[p];
-  }
-  for (int x = 0; x < T.n_xf; ++x) {
-    const DXform& xf = T.xf[x];
-    if (xf.kind != LS_XF_TILE && xf.kind != LS_XF_VECTORIZE) continue;
-    if (xf.enable_bit >= 0 && !((flags >> xf.enable_bit) & 1u)) continue;
-    const int v = xf.slot, u = xf.new_slot;
-    if (v == NOSLOT || u == NOSLOT || !((exist >> v) & 1u)) continue;  // such candidates fail
-    const int32_t F = xf.param >= 0 ? prm[xf.param] : xf.value;
-    if (F < 1 || F > E[v]) continue;  // such candidates fail
-    E[u] = F;
-    St[u] = St[v];
-    E[v] = (E[v] + F - 1) / F;
-    St[v] *= F;
-    exist |= 1u << u;
-  }
-  uint32_t expanded = 0;
-  for (int x = 0; x < nv; ++x)
-    if ((mask >> x) & 1u) expanded |= 1u << T.dim_var[D][x];
-  const int t = D / 4, rr = D % 4;
-  SI u;
-  for (int a = 0; a < T.t_nu[t]; ++a) {
-    const DExpr& ex = T.expr[T.t_uacc[t][a]][rr];
-    SI acc;
-    acc.lo = acc.hi = ex.konst;
-    acc.stride = 0;
-    acc.count = 1;
-    acc.exact = 1;
-    for (int k = 0; k < ex.nt; ++k) {
-      const DTerm& tm = T.term[ex.t0 + k];
-      const int w = tm.slot;
-      if (!present(tm, flags) || !((expanded >> w) & 1u) || !((exist >> w) & 1u)) continue;
-      const int32_t Ew = E[w];
-      if (Ew == 1) continue;
-      const int32_t d = tm.coef * St[w];
-      SI s;
-      s.lo = d > 0 ? 0 : d * (Ew - 1);
-      s.hi = d > 0 ? d * (Ew - 1) : 0;
-      s.stride = abs(d);
-      s.count = Ew;
-      s.exact = 1;
-      acc = si_sum(acc, s);
+  uint32_t exist;
+  sim_slots(T, prm, flags, E, St, exist);
+  tab[e] = dim_count(T, D, mask, flags, E, St, exist);
+}
+
+// One tensor-table entry per thread: decode (tensor, axis choices, mask of all
+// the tensor's stage bits); the entry is the tensor footprint, the product of
+// its dimension counts (ls/cache.py:117-130).
+__global__ void build_ttab_kernel(const DTask* __restrict__ g, uint64_t* __restrict__ tt) {
+  const DTask& T = *g;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= T.tt_len) return;
+  int t = -1;
+  for (int q = 0; q < T.n_tensors && q < 4; ++q)
+    if (e >= T.tt_off[q] && e < (int64_t)T.tt_off[q] + T.tt_len_t[q]) t = q;
+  if (t < 0) return;
+  const int nb = T.tt_nb[t];
+  const uint32_t loc = (uint32_t)(e - T.tt_off[t]);
+  const uint32_t mask = loc & ((1u << nb) - 1u);
+  const uint32_t key = loc >> nb;
+  int32_t prm[LS_MAX_PARAMS];
+  for (int q = 0; q < LS_MAX_PARAMS; ++q) prm[q] = 1;
+  uint32_t flags = 0;
+  for (int a = 0; a < T.sp_n; ++a) {
+    const uint32_t stride = T.tt_stride[t][a];
+    if (!stride) continue;
+    const DAxis& ax = T.sp_ax[a];
+    const uint32_t c = (key / stride) % ax.n;
+    if (ax.kind == LS_AX_BIT) {
+      flags |= c << ax.bit;
+      continue;
     }
-    u = a == 0 ? acc : si_union(u, acc);
+    const uint64_t v = T.sp_vals[ax.voff + c];
+    prm[ax.param] = (int32_t)v;
+    if (ax.kind == LS_AX_VEC && v != 0) flags |= 1u << ax.bit;
   }
-  tab[e] = u.count;
+  int32_t E[NSLOT], St[NSLOT];
+  uint32_t exist;
+  sim_slots(T, prm, flags, E, St, exist);
+  uint64_t F = 1;
+  const int tb = T.dim_base[t * 4];
+  for (int rr = 0; rr < T.t_rank[t]; ++rr) {
+    const int D = t * 4 + rr;
+    const uint32_t m = (mask >> (T.dim_base[D] - tb)) & ((1u << T.dim_nv[D]) - 1u);
+    F *= (uint64_t)(uint32_t)dim_count(T, D, m, flags, E, St, exist);
+  }
+  tt[e] = F;
 }
 
 // ---------------------------------------------------------------------------
@@ -1139,9 +1241,12 @@ struct Evaluator {
     else
       fc.ext = reinterpret_cast<int32_t*>(state);
   }
-  __device__ __forceinline__ int operator()(const DTask& T, const ls_record& r, double* f, double* s) {
+  __device__ __forceinline__ int operator()(const DTask& T, const ls_record& r, const uint32_t* kt, double* f,
+                                            double* s) {
     if constexpr (MODE == 0)
       return eval_candidate<TM, RM>(T, r, c, f, s);
+    else if constexpr (MODE == 3)
+      return eval_tensor<TM>(T, r, kt, fc, f, s);
     else
       return eval_fast<TM, RM, MODE == 2>(T, tab, r, fc, f, s);
   }
@@ -1156,16 +1261,16 @@ __device__ __forceinline__ ls_record load_record(const ls_record* __restrict__ r
   return r;
 }
 
-template <int SRC>
+template <int SRC, bool KEYS>
 __device__ __forceinline__ int load_cand(const DTask& T, const void* __restrict__ src, int pbytes, int64_t i,
-                                         ls_record& r) {
+                                         ls_record& r, uint32_t* kt) {
   if constexpr (SRC == 0) {
     r = load_record(reinterpret_cast<const ls_record*>(src), i);
     return LS_OK;
   } else {
     const uint64_t x = pbytes == 4 ? (uint64_t)__ldg(reinterpret_cast<const unsigned int*>(src) + i)
                                    : (uint64_t)__ldg(reinterpret_cast<const unsigned long long*>(src) + i);
-    return point_record(T, x, r);
+    return point_record<KEYS>(T, x, r, kt);
   }
 }
 
@@ -1185,10 +1290,11 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE))
   const int nf = T.family == LS_FAMILY_CPU ? LS_NFEAT_CPU : LS_NFEAT_GPU;
   for (int64_t i = (int64_t)blockIdx.x * TPB + threadIdx.x; i < n; i += (int64_t)gridDim.x * TPB) {
     ls_record r;
+    uint32_t kt[4];
     double f[LS_NFEAT_GPU];
     double s = 0.0;
-    int st = load_cand<SRC>(T, src, pbytes, i, r);
-    if (st == LS_OK) st = ev(T, r, f, &s);
+    int st = load_cand<SRC, MODE == 3>(T, src, pbytes, i, r, kt);
+    if (st == LS_OK) st = ev(T, r, kt, f, &s);
     const double nan = __longlong_as_double(0x7ff8000000000000ll);
     if (scores) scores[i] = st ? nan : s;
     if (status) status[i] = st;
@@ -1356,9 +1462,10 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kern
     Key key;
     if (i < n) {
       ls_record r;
+      uint32_t kt[4];
       double f[LS_NFEAT_GPU];
       double s;
-      if (load_cand<SRC>(T, src, pbytes, i, r) == LS_OK && ev(T, r, f, &s) == LS_OK) {
+      if (load_cand<SRC, MODE == 3>(T, src, pbytes, i, r, kt) == LS_OK && ev(T, r, kt, f, &s) == LS_OK) {
         has = true;
         key.s = order_bits(s);
         key.i = base_index + i;
@@ -1496,26 +1603,14 @@ struct HTerm {
 };
 
 constexpr int64_t TAB_MAX_ENTRIES = 1 << 22;  // 16 MiB of int32 counts per task
-constexpr int64_t TAB_SMEM_MAX_BYTES = 16384;
+constexpr int64_t TT_MAX_ENTRIES = 1 << 21;   // 16 MiB of uint64 footprints per task
 
-// Decide whether the task can use the tabulated path and lay out its table
-// (DESIGN.md §3.5).  A dimension's key is every record field that can change
-// the extent/step of one of its variables (Tile/Vectorize factors applied to
-// the variable or its ancestors, and their enable bits) plus the enable bits
-// of its optional terms.
-void plan_tabulated(const ls_task_desc& d, DTask& T, int RM, const std::vector<int64_t>& count_bound) {
-  T.fast = 0;
-  T.tab_len = 0;
-  if (RM != 4 || T.n_stage + 2 > 64) return;
-  for (int t = 0; t < T.n_tensors; ++t) {  // footprints are unsigned 64-bit products on this path
-    double b = 1.0;
-    for (int rr = 0; rr < T.t_rank[t]; ++rr) b *= (double)count_bound[t * RM + rr];
-    if (b >= 9.0e18) return;
-  }
-  uint32_t dep_p[NSLOT] = {0}, dep_b[NSLOT] = {0};
-  int64_t ub[NSLOT] = {0};
+// Record params / enable bits that can change each slot's extent/step
+// (Tile/Vectorize on the slot or on the loop it was split from).
+void slot_deps(const DTask& T, uint32_t* dep_p, uint32_t* dep_b, int64_t* ub, int64_t* pbound) {
+  for (int v = 0; v < NSLOT; ++v) dep_p[v] = dep_b[v] = 0, ub[v] = 0;
+  for (int q = 0; q < LS_MAX_PARAMS; ++q) pbound[q] = 0;
   for (int p = 0; p < T.n_base; ++p) ub[T.base_slot[p]] = T.base_ext[p];
-  int64_t bound[LS_MAX_PARAMS] = {0};
   for (int x = 0; x < T.n_xf; ++x) {
     const DXform& xf = T.xf[x];
     if (xf.kind != LS_XF_TILE && xf.kind != LS_XF_VECTORIZE) continue;
@@ -1526,9 +1621,90 @@ void plan_tabulated(const ls_task_desc& d, DTask& T, int RM, const std::vector<i
     dep_b[xf.slot] |= bm;
     dep_p[xf.new_slot] = dep_p[xf.slot];
     dep_b[xf.new_slot] = dep_b[xf.slot];
-    if (xf.param >= 0) bound[xf.param] = std::max(bound[xf.param], ub[xf.slot]);
+    if (xf.param >= 0) pbound[xf.param] = std::max(pbound[xf.param], ub[xf.slot]);
     ub[xf.new_slot] = ub[xf.slot];
   }
+}
+
+// dependencies of dimension D (4x4 layout): its variables' slots + its optional terms
+void dim_deps(const DTask& T, int D, const uint32_t* dep_p, const uint32_t* dep_b, uint32_t& pm, uint32_t& bm) {
+  const int t = D / 4, rr = D % 4;
+  pm = bm = 0;
+  for (int x = 0; x < T.dim_nv[D]; ++x) {
+    pm |= dep_p[T.dim_var[D][x]];
+    bm |= dep_b[T.dim_var[D][x]];
+  }
+  for (int a = 0; a < T.t_nu[t]; ++a) {
+    const DExpr& e = T.expr[T.t_uacc[t][a]][rr];
+    for (int z = 0; z < e.nt; ++z) bm |= T.term[e.t0 + z].req;
+  }
+}
+
+// Tensor tables for the points path: key = the choices of the space axes that
+// can change one of the tensor's dimension counts (mixed radix), row = all of
+// the tensor's stage bits.  Needs the dimension-table plan (T.fast).
+bool plan_tensor_tables(DTask& T) {
+  T.tt_len = 0;
+  if (!T.fast || T.sp_n < 1 || T.n_tensors > 4) return false;
+  uint32_t dep_p[NSLOT], dep_b[NSLOT];
+  int64_t ub[NSLOT], pbound[LS_MAX_PARAMS];
+  slot_deps(T, dep_p, dep_b, ub, pbound);
+  int64_t off = 0;
+  for (int t = 0; t < 4; ++t) {
+    T.tt_off[t] = T.tt_len_t[t] = T.tt_nb[t] = T.tt_sh[t] = T.tt_mk[t] = 0;
+    for (int a = 0; a < LS_MAX_AXES; ++a) T.tt_stride[t][a] = 0;
+    if (t >= T.n_tensors) continue;
+    uint32_t pm = 0, bm = 0;
+    int nb = 0;
+    for (int rr = 0; rr < T.t_rank[t]; ++rr) {
+      uint32_t p, b;
+      dim_deps(T, t * 4 + rr, dep_p, dep_b, p, b);
+      pm |= p;
+      bm |= b;
+      nb += T.dim_nv[t * 4 + rr];
+    }
+    if (nb > 20) return false;
+    int64_t keys = 1;
+    for (int a = T.sp_n - 1; a >= 0; --a) {
+      const DAxis& ax = T.sp_ax[a];
+      const bool hit = ((ax.kind == LS_AX_PARAM || ax.kind == LS_AX_VEC) && ((pm >> ax.param) & 1u)) ||
+                       ((ax.kind == LS_AX_VEC || ax.kind == LS_AX_BIT) && ((bm >> ax.bit) & 1u));
+      if (!hit) continue;
+      T.tt_stride[t][a] = (uint32_t)keys;
+      keys *= ax.n;
+      if (keys > TT_MAX_ENTRIES) return false;
+    }
+    const int64_t len = keys << nb;
+    if (off + len > TT_MAX_ENTRIES) return false;
+    T.tt_off[t] = (uint32_t)off;
+    T.tt_len_t[t] = (uint32_t)len;
+    T.tt_nb[t] = (uint32_t)nb;
+    T.tt_sh[t] = (uint32_t)T.dim_base[t * 4];
+    T.tt_mk[t] = ((1u << nb) - 1u) << 3;
+    off += len;
+  }
+  T.tt_len = (int32_t)off;
+  return off > 0;
+}
+constexpr int64_t TAB_SMEM_MAX_BYTES = 16384;
+
+// Decide whether the task can use the tabulated path and lay out its table
+// (DESIGN.md §3.5).  A dimension's key is every record field that can change
+// the extent/step of one of its variables (Tile/Vectorize factors applied to
+// the variable or its ancestors, and their enable bits) plus the enable bits
+// of its optional terms.
+void plan_tabulated(const ls_task_desc& d, DTask& T, int RM, const std::vector<int64_t>& count_bound) {
+  T.fast = 0;
+  T.tab_len = 0;
+  if (RM != 4 || T.n_stage + 3 > 64) return;
+  for (int t = 0; t < T.n_tensors; ++t) {  // footprints are unsigned 64-bit products on this path
+    double b = 1.0;
+    for (int rr = 0; rr < T.t_rank[t]; ++rr) b *= (double)count_bound[t * RM + rr];
+    if (b >= 9.0e18) return;
+  }
+  uint32_t dep_p[NSLOT], dep_b[NSLOT];
+  int64_t ub[NSLOT], bound[LS_MAX_PARAMS];
+  slot_deps(T, dep_p, dep_b, ub, bound);
   for (int q = 0; q < LS_MAX_PARAMS; ++q) T.fk_bound[q] = (int32_t)bound[q];
   int64_t off = 0;
   for (int D = 0; D < 16; ++D) {
@@ -1538,16 +1714,9 @@ void plan_tabulated(const ls_task_desc& d, DTask& T, int RM, const std::vector<i
     const int t = D / 4, rr = D % 4;
     T.fsel[D] = 0;
     if (t >= T.n_tensors || rr >= T.t_rank[t]) continue;  // points at the constant-1 entry (below)
-    uint32_t pm = 0, bm = 0;
+    uint32_t pm, bm;
     const int nv = T.dim_nv[D];
-    for (int x = 0; x < nv; ++x) {
-      pm |= dep_p[T.dim_var[D][x]];
-      bm |= dep_b[T.dim_var[D][x]];
-    }
-    for (int a = 0; a < T.t_nu[t]; ++a) {
-      const DExpr& e = T.expr[T.t_uacc[t][a]][rr];
-      for (int z = 0; z < e.nt; ++z) bm |= T.term[e.t0 + z].req;
-    }
+    dim_deps(T, D, dep_p, dep_b, pm, bm);
     int64_t len = 1;
     int nd = 0;
     for (int q = 0; q < LS_MAX_PARAMS; ++q) {
@@ -1573,8 +1742,8 @@ void plan_tabulated(const ls_task_desc& d, DTask& T, int RM, const std::vector<i
     T.fk_n[D] = (int8_t)nd;
     T.ftab_off[D] = (int32_t)off;
     T.ftab_len[D] = (int32_t)len;
-    // stage bits sit at dim_base + 2 + x, so (mall >> dim_base) & (mask << 2) is a byte offset
-    T.fsel[D] = (uint32_t)T.dim_base[D] | ((((1u << nv) - 1u) << 2) << 8);
+    // stage bits sit at dim_base + 3 + x, so (mall >> (dim_base + 1)) & (mask << 2) is a byte offset
+    T.fsel[D] = (uint32_t)(T.dim_base[D] + 1) | ((((1u << nv) - 1u) << 2) << 8);
     off += len;
   }
   T.tab_one = (int32_t)off++;  // the count of a dimension slot the layout does not use: 1
@@ -1582,7 +1751,7 @@ void plan_tabulated(const ls_task_desc& d, DTask& T, int RM, const std::vector<i
     if (T.ftab_len[D] == 0) T.ftab_off[D] = T.tab_one;
   for (int v = 0; v < NSLOT; ++v) T.vbits[v] = 0;
   for (int D = 0; D < 16; ++D)
-    for (int x = 0; x < T.dim_nv[D]; ++x) T.vbits[T.dim_var[D][x]] |= 1ull << (T.dim_base[D] + 2 + x);
+    for (int x = 0; x < T.dim_nv[D]; ++x) T.vbits[T.dim_var[D][x]] |= 1ull << (T.dim_base[D] + 3 + x);
   T.chain0 = ~0ull;
   T.base_exist = T.base_unr = T.base_vec = T.base_par = 0;
   for (int p = 0; p < T.n_base; ++p) {
@@ -1915,8 +2084,9 @@ int grid_for(const ls_task* t, int64_t n, int per_sm) {
 }
 
 // 0 generic, 1 tabulated (table in global memory), 2 tabulated (table in shared memory)
-int mode_of(const ls_task* t) {
+int mode_of(const ls_task* t, bool points = false) {
   if (t->path == LS_PATH_GENERIC || !t->host.fast) return 0;
+  if (points && t->host.tt_ok) return 3;
   return t->host.tab_smem ? 2 : 1;
 }
 
@@ -1933,12 +2103,16 @@ using TopkFn = void (*)(const DTask*, const void*, int, int64_t, int64_t, int, K
 
 template <int SRC>
 ScoreFn score_fn_src(const DTask& T, int mode) {
+  if constexpr (SRC == 1)
+    if (mode == 3) return score_kernel<4, 4, 3, 1>;
   if (mode == 1) return score_kernel<4, 4, 1, SRC>;
   if (mode == 2) return score_kernel<4, 4, 2, SRC>;
   return T.layout_rm == 4 ? score_kernel<4, 4, 0, SRC> : score_kernel<MAXT, MAXRANK, 0, SRC>;
 }
 template <int SRC>
 TopkFn topk_fn_src(const DTask& T, int mode) {
+  if constexpr (SRC == 1)
+    if (mode == 3) return score_topk_kernel<4, 4, 3, 1>;
   if (mode == 1) return score_topk_kernel<4, 4, 1, SRC>;
   if (mode == 2) return score_topk_kernel<4, 4, 2, SRC>;
   return T.layout_rm == 4 ? score_topk_kernel<4, 4, 0, SRC> : score_topk_kernel<MAXT, MAXRANK, 0, SRC>;
@@ -2079,7 +2253,7 @@ int ls_collect_unroll(ls_task* t, const ls_record* d_records, int64_t n, int64_t
 
 static int score_device(ls_task* t, const void* d_src, int pbytes, int64_t n, double* d_scores, double* d_features,
                         int32_t* d_status, cudaStream_t s) {
-  const int mode = mode_of(t);
+  const int mode = mode_of(t, pbytes != 0);
   const ScoreFn fn = score_fn(t->host, mode, pbytes);
   const size_t sm = smem_score(t->host, mode);
   fn<<<grid_for(t, n, blocks_per_sm(fn, sm)), TPB, sm, s>>>(t->d_task, d_src, pbytes, n, d_scores, d_features,
@@ -2113,7 +2287,7 @@ int ls_score_points(ls_task* t, const void* d_points, int32_t pbytes, int64_t n,
 
 static int topk_device(ls_task* t, const void* d_src, int pbytes, int64_t n, int64_t base_index, int32_t k,
                        double* d_top_scores, int64_t* d_top_index, unsigned long long* d_valid, cudaStream_t s) {
-  const int mode = mode_of(t);
+  const int mode = mode_of(t, pbytes != 0);
   const TopkFn fn = topk_fn(t->host, mode, pbytes);
   const size_t sm = smem_topk(t->host, k, mode);
   const int grid = n > 0 ? grid_for(t, n, blocks_per_sm(fn, sm)) : 1;
@@ -2200,7 +2374,24 @@ int ls_task_set_space(ls_task* t, const ls_space_desc* sp) {
   t->host.sp_n = sp->n_axes;
   t->host.sp_vals = dv;
   memcpy(t->host.sp_ax, ax, sizeof(ax));
-  return upload(t);
+  t->host.tt_ok = 0;
+  t->host.tt = nullptr;
+  const bool tables = plan_tensor_tables(t->host);
+  uint64_t* dtt = nullptr;
+  if (tables) {
+    CUDA_TRY(cudaMalloc(&dtt, sizeof(uint64_t) * (size_t)t->host.tt_len));
+    t->retired.push_back(dtt);
+    t->host.tt = dtt;
+  }
+  if (int rc = upload(t)) return rc;
+  if (tables) {
+    build_ttab_kernel<<<(unsigned)((t->host.tt_len + 255) / 256), 256>>>(t->d_task, dtt);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaDeviceSynchronize());
+    t->host.tt_ok = 1;
+    return upload(t);
+  }
+  return LS_E_OK;
 }
 
 int ls_topk_merge(const double* d_scores, const int64_t* d_index, int32_t n_lists, int32_t k_in, int32_t k_out,
