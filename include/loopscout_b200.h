@@ -79,7 +79,9 @@ enum {
 enum {
   LS_PATH_AUTO = 0,      /* tabulated when the task is eligible, else generic            */
   LS_PATH_GENERIC = 1,   /* per-candidate strided-interval folds (every perfect chain)   */
-  LS_PATH_TABULATED = 2  /* dimension counts looked up in a per-task table */
+  LS_PATH_TABULATED = 2, /* dimension counts looked up in a per-task table */
+  LS_PATH_SPACE = 3      /* points calls on tile+reorder spaces: chain order per reorder choice,
+                            fused walk + closed-form terms; else as TABULATED      */
 };
 
 /* ---- error codes (return values) ---- */
@@ -213,13 +215,16 @@ int ls_abi_version(void);
 int ls_task_create(const ls_task_desc* desc, int device, ls_task** out);
 int ls_task_destroy(ls_task* task);
 int ls_task_num_features(const ls_task* task);
-/* Select the scoring path (LS_PATH_*); both give bit-identical results, the
- * tabulated one is the fast path.  LS_E_UNSUPPORTED if the task is not
- * eligible for LS_PATH_TABULATED.  Not thread-safe against concurrent scoring
- * calls on the same task. */
+/* Select the scoring path (LS_PATH_*); all give bit-identical results.
+ * LS_PATH_AUTO takes the fastest eligible one.  LS_E_UNSUPPORTED if the task
+ * is not eligible for LS_PATH_TABULATED / LS_PATH_SPACE.  Not thread-safe
+ * against concurrent scoring calls on the same task. */
 int ls_task_set_path(ls_task* task, int32_t path);
-/* The path scoring calls will take: LS_PATH_GENERIC or LS_PATH_TABULATED. */
+/* The path record calls (ls_score*) take: LS_PATH_GENERIC or LS_PATH_TABULATED. */
 int ls_task_path(const ls_task* task);
+/* The path points calls (ls_score*_points*) take: LS_PATH_GENERIC,
+ * LS_PATH_TABULATED or LS_PATH_SPACE (needs ls_task_set_space first). */
+int ls_task_points_path(const ls_task* task);
 /* Precompute block-cycle entries for innermost-unroll products `u_values`
  * (candidates needing an unprepared product report LS_ST_UNROLL_TABLE). */
 int ls_task_prepare_unroll(ls_task* task, const int64_t* u_values, int32_t n);

@@ -152,6 +152,24 @@ struct __align__(16) DTask {
   uint32_t tt_off[4], tt_len_t[4], tt_nb[4];
   uint32_t tt_sh[4], tt_mk[4];            // byte offset of the row entry: (mall >> tt_sh) & tt_mk
   uint32_t tt_stride[4][LS_MAX_AXES];     // key stride of each axis (0: the axis does not affect the tensor)
+  // ---- space-specialised points path: tile + reorder spaces whose transformed
+  //      chain order is a function of the reorder choice alone
+  int32_t sp_ok, sp_nchain;     // eligible + tables built; chain length after the tiles
+  const uint64_t* sp_chain;     // per reorder choice: final chain, one slot per nibble
+  const int32_t* sp_pstat;      // per reorder choice: status of apply_schedule with valid tiles
+  int64_t c_inner1;             // innermost-block cycles with no unrolling (CPU family)
+  // group tables of the space path: a tensor's dimensions are split into <= 2
+  // groups; a group's table holds the product of its dimension counts, rows of 2^nb entries (stage
+  // mask of nb <= 6 variables) keyed by the tile-axis choices, staged into shared memory.  Group slot
+  // g = 2t + j owns bits 8g..8g+7 of the stage word, holding 4 * its stage mask (a byte offset).
+  int32_t sd_len, sd_pad;             // uint32 entries (entries 0..3: the ones row)
+  const int32_t* sd_tab;
+  uint32_t sd_off[8];                 // byte offset of each group slot's table
+  uint32_t sd_S[LS_MAX_AXES][8];      // byte stride of one choice of each axis in each group table
+  uint64_t vb8[NSLOT];                // per loop slot: its stage bits in every group slot
+  int8_t sd_gd[8][4];                 // dimension slots of each group (-1: none)
+  int8_t sd_gx[8][4];                 // bit offset of each of them within the group's stage mask
+  int8_t sd_nb[8];                    // stage bits of each group (rows of 2^nb entries)
   int32_t n_terms;
   DTerm term[MAXTERM];
 };
@@ -877,7 +895,7 @@ __device__ int features_score(const DTask& T, CT& c, int64_t dmov, double* f, do
 // Decode a space point (mixed radix, axis 0 most significant) into the record
 // the host packer would have produced for the same choices (pack.SpaceTemplate).
 template <bool KEYS>
-__device__ __forceinline__ int point_record(const DTask& T, uint64_t x, ls_record& r, uint32_t* kt) {
+__device__ __forceinline__ int point_record(const DTask& T, uint64_t x, ls_record& r, uint32_t* kt, uint32_t& pch) {
   uint64_t lo = 0, hi = 0, perm = 0;
   uint32_t flags = 0;
   if constexpr (KEYS) {
@@ -908,6 +926,7 @@ __device__ __forceinline__ int point_record(const DTask& T, uint64_t x, ls_recor
     const uint64_t v = __ldg(reinterpret_cast<const unsigned long long*>(T.sp_vals) + ax.voff + c);
     if (ax.kind == LS_AX_PERM) {
       perm |= v;
+      pch = c;
       continue;
     }
     if (ax.param < 4)
@@ -931,7 +950,7 @@ __device__ __forceinline__ int point_record(const DTask& T, uint64_t x, ls_recor
 // Candidate source of the scoring kernels: SRC 0 = ls_record array, 1 = points.
 template <int SRC, bool KEYS>
 __device__ __forceinline__ int load_cand(const DTask& T, const void* __restrict__ src, int pbytes, int64_t i,
-                                         ls_record& r, uint32_t* kt);
+                                         ls_record& r, uint32_t* kt, uint32_t& pch);
 
 template <int TM, int RM, bool SMT>
 __device__ __forceinline__ int32_t tab_at(const int32_t* __restrict__ tab, int32_t i) {
@@ -1120,6 +1139,220 @@ __device__ int eval_tensor(const DTask& T, const ls_record& r, const uint32_t* k
   return walk_score<TM>(T, c, mall, fp, f, score);
 }
 
+// Space-specialised points path.  Eligible spaces only hold
+// tile-factor and reorder axes over unconditional Tile transforms followed by
+// one Reorder, with no unroll/vector/parallel marks: every loop of the
+// transformed chain branches, its order is a function of the reorder choice
+// alone (tabulated per choice by ls_task_set_space) and only the extents
+// depend on the tile choices.  The movement walk, the emitted-block terms and
+// the score then fuse into one innermost-first pass over the chain:
+//   CPU  sum_{j<n-1} W_j      = E_0(1 + E_1(1 + ... E_{n-2}))       (Horner, exact integers)
+//        ilp = c_init (1 + sum W) + c_inner(1) W_{n-1} + c_latch (n-1) + c_ret
+//   PTX  W'_j uses extent 1 for loops 8+ above the innermost (counter-register wrap),
+//        sum_j W'_{j-1} = 1 + A, sum_j W'_j = A + W'_{n-1}, A = sum_{j<n-1} W'_j
+// which are the general closed forms of features_score with every R_j = 1.
+template <int TM>
+__device__ int eval_space(const DTask& T, const int32_t* __restrict__ sdt, const void* __restrict__ src, int pbytes,
+                          int64_t i, FastCand& c, double* f, double* score) {
+  // ---- decode the space point (mixed radix, axis 0 most significant): tile factors into the
+  //      record's parameter slots, the reorder choice, the dimension-table row offsets
+  uint64_t x = pbytes == 4 ? (uint64_t)__ldg(reinterpret_cast<const unsigned int*>(src) + i)
+                           : (uint64_t)__ldg(reinterpret_cast<const unsigned long long*>(src) + i);
+  uint32_t kd[TM * 2];
+#pragma unroll
+  for (int g = 0; g < TM * 2; ++g) kd[g] = T.sd_off[g];
+  uint64_t lo = 0, hi = 0;
+  uint32_t pch = 0;
+  for (int a = T.sp_n - 1; a >= 0; --a) {
+    const DAxis& ax = T.sp_ax[a];
+    uint32_t ch;
+    if (a == 0) {
+      if (x >= ax.n) return LS_ST_POINT_RANGE;
+      ch = (uint32_t)x;
+    } else if (ax.n == 1) {
+      ch = 0;
+    } else {
+      const uint64_t q = (x >> 32) ? x / ax.n : __umul64hi(x, ax.magic);
+      ch = (uint32_t)(x - q * ax.n);
+      x = q;
+    }
+    if (ax.kind == LS_AX_PERM) {
+      pch = ch;
+      continue;
+    }
+    const uint64_t v = __ldg(reinterpret_cast<const unsigned long long*>(T.sp_vals) + ax.voff + ch);
+    if (ax.param < 4)
+      lo |= v << (16 * ax.param);
+    else
+      hi |= v << (16 * (ax.param - 4));
+#pragma unroll
+    for (int g = 0; g < TM * 2; ++g) kd[g] += ch * T.sd_S[a][g];
+  }
+  ls_record r;
+  memcpy(&r.param[0], &lo, 8);
+  memcpy(&r.param[4], &hi, 8);
+  // ---- extents: Tile arithmetic in template order (ls/ir.py:361-382), with the
+  //      checks of apply_fast that a tile factor can fail
+  for (int p = 0; p < T.n_base; ++p) c.E(T.base_slot[p]) = T.base_ext[p];
+  for (int q = 0; q < T.n_xf; ++q) {
+    const DXform& xf = T.xf[q];
+    if (xf.kind != LS_XF_TILE) continue;
+    const int32_t F = xf.param >= 0 ? (int32_t)rparam(r, xf.param) : xf.value;
+    const int32_t Ev = c.E(xf.slot);
+    if (F < 1 || F > Ev) return LS_ST_TILE_RANGE;
+    c.E(xf.new_slot) = F;
+    c.E(xf.slot) = (Ev + F - 1) / F;
+  }
+  const int pst = __ldg(T.sp_pstat + pch);
+  if (pst) return pst;
+  const uint64_t chain = __ldg(reinterpret_cast<const unsigned long long*>(T.sp_chain) + pch);
+  const int n = T.sp_nchain;
+  // ---- movement walk (ls/cache.py:167-236, chain form): a tensor footprint is
+  //      the product of its dimension counts (ls/cache.py:117-130) = the product
+  //      of its two group entries, shared-memory lookups at (row of this
+  //      candidate, stage mask so far)
+  const char* tb = reinterpret_cast<const char*>(sdt);
+  uint64_t mall = 0;
+  auto grp = [&](int g) -> uint32_t {
+    return *reinterpret_cast<const uint32_t*>(tb + kd[g] + ((uint32_t)(mall >> (8 * g)) & 0xFFu));
+  };
+  auto fp = [&](int t) -> int64_t { return (int64_t)((uint64_t)grp(2 * t) * grp(2 * t + 1)); };
+  uint32_t vm[TM];
+  int64_t Fb[TM], dm[TM];
+  bool ru[TM];
+#pragma unroll
+  for (int t = 0; t < TM; ++t) {
+    vm[t] = T.t_vmask[t];
+    Fb[t] = fp(t);
+    dm[t] = T.t_nacc[t];
+    ru[t] = true;
+  }
+  const int64_t cap = T.cap;
+  const bool cpu = T.family == LS_FAMILY_CPU;
+  int64_t P = 1, H = 0;  // product of all extents; Horner sum of the outer prefix products
+  for (int p = n - 1; p >= 0; --p) {
+    const int v = (int)((chain >> (4 * p)) & 15u);
+    const int64_t E = c.E(v);
+    mall |= T.vb8[v];
+    int64_t single = 0;
+#pragma unroll
+    for (int t = 0; t < TM; ++t) single += Fb[t];
+    const bool over = single > cap;
+#pragma unroll
+    for (int t = 0; t < TM; ++t) {
+      const bool uses = (vm[t] >> v) & 1u;
+      const int64_t Ff = fp(t);
+      const bool r0 = ru[t] && !(over && !uses);
+      dm[t] = (!over || r0) ? Ff : (int64_t)((uint64_t)dm[t] * (uint32_t)E);
+      ru[t] = r0 && !(Ff > cap);
+      Fb[t] = Ff;
+    }
+    const int64_t Ee = (cpu || p + 8 > n - 1) ? E : 1;  // PTX: no trip 8+ levels above the innermost
+    if (p < n - 1) H = Ee * (1 + H);
+    P *= Ee;
+  }
+  int64_t dmov = 0;
+#pragma unroll
+  for (int t = 0; t < TM; ++t) dmov += dm[t];
+  const int64_t L = T.L, S = T.S;
+  double total = 0.0;
+  if (cpu) {
+    const int64_t ilp = T.c_init * (1 + H) + T.c_inner1 * P + T.c_latch * (n - 1) + T.c_ret;
+    f[0] = (double)(S * P);
+    f[1] = (double)(L * P);
+    f[2] = (double)(S * P);
+    f[3] = (double)dmov;
+    f[4] = (double)ilp;
+#pragma unroll
+    for (int q = 0; q < LS_NFEAT_CPU; ++q) {
+      if (!(f[q] >= 0.0) || isinf(f[q])) return LS_ST_BAD_FEATURE;
+      total = rn_add(total, rn_mul(T.coef[q], f[q]));
+    }
+  } else {
+    const int64_t* ic = T.ptx_icost;
+    const int64_t loops = ic[LS_I_INIT] * (1 + H) + (ic[LS_I_ADD] + ic[LS_I_CMP] + ic[LS_I_BRANCH]) * (H + P);
+    f[0] = (double)(loops + P * (L * ic[LS_I_LOAD] + S * (ic[LS_I_FMA] + ic[LS_I_STORE])) + ic[LS_I_RET]);
+    f[1] = T.sm_underuse;
+    f[2] = T.warp_slack;
+    f[3] = 0.0;
+    f[4] = (double)(S * P);
+    f[5] = (double)(L * P);
+    f[6] = (double)(S * P);
+#pragma unroll
+    for (int q = 0; q < LS_NFEAT_GPU; ++q) {
+      if (!(f[q] >= 0.0) || isinf(f[q])) return LS_ST_BAD_FEATURE;
+      total = rn_add(total, rn_mul(T.coef[q], f[q]));
+    }
+  }
+  *score = total;
+  return LS_OK;
+}
+
+// One group-table entry per thread: decode (group slot, tile-axis choices, stage
+// mask); the entry is the product of the group's dimension counts (same fold as
+// build_tab_kernel).  Products that do not fit 32 bits raise *overflow.
+__global__ void build_sdt_kernel(const DTask* __restrict__ g, const int32_t* __restrict__ rows,
+                                 uint32_t* __restrict__ tab, int32_t* __restrict__ overflow) {
+  const DTask& T = *g;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= T.sd_len) return;
+  if (e < 4) {  // the ones row (group slots without dimensions)
+    tab[e] = 1;
+    return;
+  }
+  int G = -1;
+  for (int q = 0; q < 8; ++q)
+    if (rows[q] && e >= (int)T.sd_off[q] / 4 && e < (int)T.sd_off[q] / 4 + (rows[q] << T.sd_nb[q])) G = q;
+  if (G < 0) return;
+  const int loc = e - (int)T.sd_off[G] / 4;
+  const uint32_t mask = (uint32_t)loc & ((1u << T.sd_nb[G]) - 1u);
+  const uint32_t key = (uint32_t)loc >> T.sd_nb[G];
+  int32_t prm[LS_MAX_PARAMS];
+  for (int q = 0; q < LS_MAX_PARAMS; ++q) prm[q] = 1;
+  for (int a = 0; a < T.sp_n; ++a) {
+    const uint32_t stride = T.sd_S[a][G] >> (2 + T.sd_nb[G]);
+    if (!stride) continue;
+    const DAxis& ax = T.sp_ax[a];
+    const uint32_t ch = (key / stride) % ax.n;
+    prm[ax.param] = (int32_t)T.sp_vals[ax.voff + ch];
+  }
+  int32_t E[NSLOT], St[NSLOT];
+  uint32_t exist;
+  sim_slots(T, prm, 0u, E, St, exist);
+  uint64_t F = 1;
+  for (int j = 0; j < 4; ++j) {
+    const int D = T.sd_gd[G][j];
+    if (D < 0) continue;
+    const uint32_t m = (mask >> T.sd_gx[G][j]) & ((1u << T.dim_nv[D]) - 1u);
+    F *= (uint64_t)(uint32_t)dim_count(T, D, m, 0u, E, St, exist);
+  }
+  if (F > 0xFFFFFFFFull) {
+    atomicExch(overflow, 1);
+    F = 0;
+  }
+  tab[e] = (uint32_t)F;
+}
+
+// Per reorder choice: the transformed chain and the status of apply_fast with
+// every tile factor 1 (always in range), i.e. what the reorder alone decides.
+__global__ void build_pchain_kernel(const DTask* __restrict__ g, int32_t pax, uint64_t* __restrict__ chain,
+                                    int32_t* __restrict__ pst) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  const DTask& T = *g;
+  const int pc = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n = pax >= 0 ? (int)T.sp_ax[pax].n : 1;
+  FastCand c;
+  c.ext = reinterpret_cast<int32_t*>(dyn);
+  if (pc >= n) return;
+  ls_record r;
+  memset(&r, 0, sizeof(r));
+  for (int q = 0; q < LS_MAX_PARAMS; ++q) r.param[q] = 1;
+  r.perm = pax >= 0 ? T.sp_vals[T.sp_ax[pax].voff + pc] : 0;
+  const int st = apply_fast(T, r, c);
+  pst[pc] = st;
+  chain[pc] = st ? 0 : c.chain;
+}
+
 // One dimension-table entry per thread: decode (dimension, key, mask).
 __global__ void build_tab_kernel(const DTask* __restrict__ g, int32_t* __restrict__ tab) {
   const DTask& T = *g;
@@ -1213,9 +1446,11 @@ __device__ __forceinline__ void stage_task(DTask& s, const DTask* __restrict__ g
 // in global memory (L1/L2 resident), 2 tabulated with the table in shared memory.
 template <int MODE>
 __device__ __forceinline__ const int32_t* stage_tab(unsigned char* where, const DTask& T) {
-  if constexpr (MODE == 2) {
+  if constexpr (MODE == 2 || MODE == 4) {
     int32_t* dst = reinterpret_cast<int32_t*>(where);
-    for (int i = threadIdx.x; i < T.tab_len; i += blockDim.x) dst[i] = __ldg(&T.tab[i]);
+    const int32_t* src = MODE == 2 ? T.tab : T.sd_tab;
+    const int len = MODE == 2 ? T.tab_len : T.sd_len;
+    for (int i = threadIdx.x; i < len; i += blockDim.x) dst[i] = __ldg(&src[i]);
     __syncthreads();
     return dst;
   } else {
@@ -1223,8 +1458,9 @@ __device__ __forceinline__ const int32_t* stage_tab(unsigned char* where, const 
   }
 }
 
-__host__ __device__ inline size_t tab_smem_bytes(int mode, int tab_len) {
-  return mode == 2 ? align16(sizeof(int32_t) * (size_t)tab_len) : 0;
+__host__ __device__ inline size_t tab_smem_bytes(int mode, const DTask& T) {
+  return mode == 2 ? align16(sizeof(int32_t) * (size_t)T.tab_len)
+                   : mode == 4 ? align16(sizeof(int32_t) * (size_t)T.sd_len) : 0;
 }
 __host__ __device__ inline size_t state_bytes(int mode, int n_slots, int n_chain, int n_stage) {
   return mode == 0 ? cand_bytes(n_slots, n_chain, n_stage) : align16(sizeof(int32_t) * (size_t)n_slots * TPB);
@@ -1241,8 +1477,8 @@ struct Evaluator {
     else
       fc.ext = reinterpret_cast<int32_t*>(state);
   }
-  __device__ __forceinline__ int operator()(const DTask& T, const ls_record& r, const uint32_t* kt, double* f,
-                                            double* s) {
+  __device__ __forceinline__ int operator()(const DTask& T, const ls_record& r, const uint32_t* kt, uint32_t pch,
+                                            double* f, double* s) {
     if constexpr (MODE == 0)
       return eval_candidate<TM, RM>(T, r, c, f, s);
     else if constexpr (MODE == 3)
@@ -1263,18 +1499,18 @@ __device__ __forceinline__ ls_record load_record(const ls_record* __restrict__ r
 
 template <int SRC, bool KEYS>
 __device__ __forceinline__ int load_cand(const DTask& T, const void* __restrict__ src, int pbytes, int64_t i,
-                                         ls_record& r, uint32_t* kt) {
+                                         ls_record& r, uint32_t* kt, uint32_t& pch) {
   if constexpr (SRC == 0) {
     r = load_record(reinterpret_cast<const ls_record*>(src), i);
     return LS_OK;
   } else {
     const uint64_t x = pbytes == 4 ? (uint64_t)__ldg(reinterpret_cast<const unsigned int*>(src) + i)
                                    : (uint64_t)__ldg(reinterpret_cast<const unsigned long long*>(src) + i);
-    return point_record<KEYS>(T, x, r, kt);
+    return point_record<KEYS>(T, x, r, kt, pch);
   }
 }
 
-constexpr int min_blocks(int tm, int rm, int mode) { return mode ? 3 : (tm * rm <= 16 ? 3 : 1); }
+constexpr int min_blocks(int tm, int rm, int mode) { return mode == 4 ? 3 : mode ? 3 : (tm * rm <= 16 ? 3 : 1); }
 
 template <int TM, int RM, int MODE, int SRC>
 __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE))
@@ -1285,7 +1521,7 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE))
   stage_task(T, gtask);
   unsigned char* p = dyn + T.task_bytes;
   const int32_t* tab = stage_tab<MODE>(p, T);
-  p += tab_smem_bytes(MODE, T.tab_len);
+  p += tab_smem_bytes(MODE, T);
   Evaluator<TM, RM, MODE> ev(T, p, tab);
   const int nf = T.family == LS_FAMILY_CPU ? LS_NFEAT_CPU : LS_NFEAT_GPU;
   for (int64_t i = (int64_t)blockIdx.x * TPB + threadIdx.x; i < n; i += (int64_t)gridDim.x * TPB) {
@@ -1293,8 +1529,14 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE))
     uint32_t kt[4];
     double f[LS_NFEAT_GPU];
     double s = 0.0;
-    int st = load_cand<SRC, MODE == 3>(T, src, pbytes, i, r, kt);
-    if (st == LS_OK) st = ev(T, r, kt, f, &s);
+    int st;
+    if constexpr (MODE == 4) {
+      st = eval_space<TM>(T, tab, src, pbytes, i, ev.fc, f, &s);
+    } else {
+      uint32_t pch = 0;
+      st = load_cand<SRC, MODE == 3>(T, src, pbytes, i, r, kt, pch);
+      if (st == LS_OK) st = ev(T, r, kt, pch, f, &s);
+    }
     const double nan = __longlong_as_double(0x7ff8000000000000ll);
     if (scores) scores[i] = st ? nan : s;
     if (status) status[i] = st;
@@ -1325,16 +1567,27 @@ __device__ __forceinline__ double from_order_bits(unsigned long long o) {
 
 constexpr int TK_MAXK = 1024;
 
-// Block top-k state in shared memory: header + `cap` keys (cap = 1024 or 2048).
+// Block top-k state in shared memory: header + two key buffers of `cap` keys
+// (cap = 1024 or 2048).  The current buffer is an unsorted multiset of keys
+// below `thr`; compaction keeps exactly the k smallest by radix selection of
+// the k-th key (no sort), and only the final list of a launch is sorted.
 struct __align__(16) TopkState {
   Key thr;
-  int cnt, cap;
-  __device__ __forceinline__ Key* buf() { return reinterpret_cast<Key*>(this + 1); }
-  __device__ __forceinline__ const Key* buf() const { return reinterpret_cast<const Key*>(this + 1); }
+  int cnt, cap, cur, cnt2;
+  unsigned int hist[256];
+  int sel_bucket, sel_rank, sel_count, pad;
+  __device__ __forceinline__ Key* buf() { return reinterpret_cast<Key*>(this + 1) + (cur ? cap : 0); }
+  __device__ __forceinline__ const Key* buf() const {
+    return reinterpret_cast<const Key*>(this + 1) + (cur ? cap : 0);
+  }
+  __device__ __forceinline__ Key* other() { return reinterpret_cast<Key*>(this + 1) + (cur ? 0 : cap); }
 };
-__host__ __device__ constexpr size_t topk_state_bytes(int cap) { return sizeof(TopkState) + sizeof(Key) * (size_t)cap; }
+__host__ __device__ constexpr size_t topk_state_bytes(int cap) {
+  return sizeof(TopkState) + 2 * sizeof(Key) * (size_t)cap;
+}
 
-// Sort buf[0..cnt) (padded with +inf) and keep the k smallest; returns the kept count.
+// Sort buf[0..cnt) (padded with +inf) and keep the k smallest; returns the kept
+// count.  Used once per launch, on the final <= k keys.
 __device__ int topk_compact(TopkState& S, int k, int cnt) {
   for (int i = cnt + threadIdx.x; i < S.cap; i += blockDim.x) {
     S.buf()[i].s = KEY_INF_S;
@@ -1367,10 +1620,98 @@ __device__ int topk_compact(TopkState& S, int k, int cnt) {
   return keep;
 }
 
+// 8-bit digit d (0 = most significant) of the 128-bit key (s, i).
+__device__ __forceinline__ unsigned key_digit(const Key& x, int d) {
+  const unsigned long long w = d < 8 ? x.s : (unsigned long long)x.i;
+  return (unsigned)(w >> (56 - 8 * (d & 7))) & 0xFFu;
+}
+
+// Keep exactly the k smallest keys of the buffer (all of them when cnt <= k)
+// and set thr to the k-th: MSD radix selection of the k-th key over 8-bit
+// digits of (score bits, index) until its bucket holds one key, then one
+// filtering pass into the other buffer.  Keys are distinct (unique indices),
+// so the k-th key and the kept set are unique.  Returns the kept count.
+__device__ int topk_select(TopkState& S, int k) {
+  const int c = S.cnt;
+  if (c <= k) return c;
+  unsigned long long ps = 0, pi = 0, ms = 0, mi = 0;  // known digits of the k-th key (block-uniform)
+  int rank = k;                                       // its rank among keys matching the known digits
+  for (int d = 0; d < 16; ++d) {
+    for (int b = threadIdx.x; b < 256; b += blockDim.x) S.hist[b] = 0;
+    __syncthreads();
+    for (int j = threadIdx.x; j < c; j += blockDim.x) {
+      const Key x = S.buf()[j];
+      if ((x.s & ms) == ps && ((unsigned long long)x.i & mi) == pi) atomicAdd(&S.hist[key_digit(x, d)], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const int l = threadIdx.x;
+      unsigned h[8], sum = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) sum += (h[q] = S.hist[8 * l + q]);
+      unsigned incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (l >= o) incl += y;
+      }
+      const unsigned excl = incl - sum;
+      if (excl < (unsigned)rank && (unsigned)rank <= incl) {
+        unsigned cum = excl;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (cum + h[q] >= (unsigned)rank) {
+            S.sel_bucket = 8 * l + q;
+            S.sel_rank = rank - (int)cum;
+            S.sel_count = (int)h[q];
+            break;
+          }
+          cum += h[q];
+        }
+      }
+    }
+    __syncthreads();
+    const unsigned long long b = (unsigned long long)S.sel_bucket;
+    const int sh = 56 - 8 * (d & 7);
+    if (d < 8) {
+      ps |= b << sh;
+      ms |= 0xFFull << sh;
+    } else {
+      pi |= b << sh;
+      mi |= 0xFFull << sh;
+    }
+    rank = S.sel_rank;
+    const bool done = S.sel_count == 1;
+    __syncthreads();
+    if (done) break;
+  }
+  // the k-th key is the only one matching the selected digits
+  for (int j = threadIdx.x; j < c; j += blockDim.x) {
+    const Key x = S.buf()[j];
+    if ((x.s & ms) == ps && ((unsigned long long)x.i & mi) == pi) S.thr = x;
+  }
+  if (threadIdx.x == 0) S.cnt2 = 0;
+  __syncthreads();
+  const Key thr = S.thr;
+  Key* dst = S.other();
+  for (int j = threadIdx.x; j < c; j += blockDim.x) {
+    const Key x = S.buf()[j];
+    if (!kless(thr, x)) dst[atomicAdd(&S.cnt2, 1)] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    S.cur ^= 1;
+    S.cnt = S.cnt2;
+  }
+  __syncthreads();
+  return k;
+}
+
 __device__ __forceinline__ void topk_init(TopkState& S, int cap) {
   if (threadIdx.x == 0) {
     S.cap = cap;
     S.cnt = 0;
+    S.cur = 0;
     S.thr.s = KEY_INF_S;
     S.thr.i = KEY_INF_I;
   }
@@ -1389,9 +1730,9 @@ __device__ __forceinline__ void topk_offer(TopkState& S, bool has, const Key& ke
   int c = S.cnt;
   const bool open = S.thr.s == KEY_INF_S && S.thr.i == KEY_INF_I;
   __syncthreads();
-  // compact when another round could overflow, and as soon as k keys exist
+  // select when another round could overflow, and as soon as k keys exist
   // without a threshold (an early threshold keeps later inserts rare)
-  if (c > S.cap - (int)blockDim.x || (open && c >= k)) c = topk_compact(S, k, c);
+  if (c > S.cap - (int)blockDim.x || (open && c > k)) c = topk_select(S, k);
   safe = (S.cap - c) / (int)blockDim.x;
 }
 
@@ -1405,7 +1746,8 @@ __device__ __forceinline__ Key ld_key_cg(const Key* p) {
 }
 
 // Merge m keys from global memory into the block's buffer (streamed, k kept).
-__device__ int merge_into(TopkState& S, const Key* src, int64_t m, int k) {
+// (sorted: the kept keys end ascending; otherwise they stay an unsorted set)
+__device__ int merge_into(TopkState& S, const Key* src, int64_t m, int k, bool sorted) {
   topk_init(S, S.cap);
   int safe = 1;
   for (int64_t base = 0; base < m; base += blockDim.x) {
@@ -1419,7 +1761,8 @@ __device__ int merge_into(TopkState& S, const Key* src, int64_t m, int k) {
     topk_offer(S, has, key, k, safe);
   }
   __syncthreads();
-  return topk_compact(S, k, S.cnt);
+  const int kept = topk_select(S, k);
+  return sorted ? topk_compact(S, k, kept) : kept;
 }
 
 __device__ void write_keys(const TopkState& S, int kept, int k, Key* out) {
@@ -1450,7 +1793,7 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kern
   stage_task(T, gtask);
   unsigned char* p = dyn + T.task_bytes;
   const int32_t* tab = stage_tab<MODE>(p, T);
-  p += tab_smem_bytes(MODE, T.tab_len);
+  p += tab_smem_bytes(MODE, T);
   TopkState& S = *reinterpret_cast<TopkState*>(p);
   Evaluator<TM, RM, MODE> ev(T, p + align16(topk_state_bytes(cap)), tab);
   topk_init(S, cap);
@@ -1465,7 +1808,15 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kern
       uint32_t kt[4];
       double f[LS_NFEAT_GPU];
       double s;
-      if (load_cand<SRC, MODE == 3>(T, src, pbytes, i, r, kt) == LS_OK && ev(T, r, kt, f, &s) == LS_OK) {
+      int st;
+      if constexpr (MODE == 4) {
+        st = eval_space<TM>(T, tab, src, pbytes, i, ev.fc, f, &s);
+      } else {
+        uint32_t pch = 0;
+        st = load_cand<SRC, MODE == 3>(T, src, pbytes, i, r, kt, pch);
+        if (st == LS_OK) st = ev(T, r, kt, pch, f, &s);
+      }
+      if (st == LS_OK) {
         has = true;
         key.s = order_bits(s);
         key.i = base_index + i;
@@ -1477,7 +1828,7 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kern
   for (int off = 16; off > 0; off >>= 1) valid += __shfl_down_sync(0xffffffffu, valid, off);
   if ((threadIdx.x & 31) == 0 && valid) atomicAdd(n_valid, (unsigned long long)valid);
   __syncthreads();
-  write_keys(S, topk_compact(S, k, S.cnt), k, block_out + (int64_t)blockIdx.x * k);
+  write_keys(S, topk_select(S, k), k, block_out + (int64_t)blockIdx.x * k);
 
   // ---- level 1: last block of the group merges the group's lists
   const int g = blockIdx.x / TK_GROUP;
@@ -1489,7 +1840,7 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kern
   __syncthreads();
   if (s_ticket != (unsigned)(gsize - 1)) return;
   __threadfence();
-  int kept = merge_into(S, block_out + (int64_t)g * TK_GROUP * k, (int64_t)gsize * k, k);
+  int kept = merge_into(S, block_out + (int64_t)g * TK_GROUP * k, (int64_t)gsize * k, k, false);
   write_keys(S, kept, k, group_out + (int64_t)g * k);
   // ---- level 2: last group merger writes the final list
   __threadfence();
@@ -1498,7 +1849,7 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kern
   __syncthreads();
   if (s_ticket != (unsigned)(ngroups - 1)) return;
   __threadfence();
-  kept = merge_into(S, group_out, (int64_t)ngroups * k, k);
+  kept = merge_into(S, group_out, (int64_t)ngroups * k, k, true);
   for (int j = threadIdx.x; j < k; j += blockDim.x) {
     if (j < kept) {
       out_s[j] = from_order_bits(S.buf()[j].s);
@@ -1511,12 +1862,12 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kern
 }
 
 // Merge m keys (any order, +inf padded) into the k best, written as (score, index).
-__global__ void __launch_bounds__(1024) merge_keys_kernel(const Key* __restrict__ in, int64_t m, int k,
-                                                          double* __restrict__ out_s,
-                                                          int64_t* __restrict__ out_i) {
-  __shared__ __align__(16) unsigned char raw[topk_state_bytes(2048)];
+__global__ void __launch_bounds__(TPB) merge_keys_kernel(const Key* __restrict__ in, int64_t m, int k,
+                                                         double* __restrict__ out_s, int64_t* __restrict__ out_i,
+                                                         int cap) {
+  extern __shared__ __align__(16) unsigned char raw[];
   TopkState& S = *reinterpret_cast<TopkState*>(raw);
-  topk_init(S, 2048);
+  topk_init(S, cap);
   int safe = 1;
   for (int64_t base = 0; base < m; base += blockDim.x) {
     const int64_t i = base + threadIdx.x;
@@ -1529,7 +1880,7 @@ __global__ void __launch_bounds__(1024) merge_keys_kernel(const Key* __restrict_
     topk_offer(S, has, key, k, safe);
   }
   __syncthreads();
-  const int kept = topk_compact(S, k, S.cnt);
+  const int kept = topk_compact(S, k, topk_select(S, k));
   for (int j = threadIdx.x; j < k; j += blockDim.x) {
     if (j < kept) {
       out_s[j] = from_order_bits(S.buf()[j].s);
@@ -1681,12 +2032,141 @@ bool plan_tensor_tables(DTask& T) {
     T.tt_nb[t] = (uint32_t)nb;
     T.tt_sh[t] = (uint32_t)T.dim_base[t * 4];
     T.tt_mk[t] = ((1u << nb) - 1u) << 3;
+
     off += len;
   }
   T.tt_len = (int32_t)off;
   return off > 0;
 }
 constexpr int64_t TAB_SMEM_MAX_BYTES = 16384;
+
+// Eligibility of the space-specialised points path: unconditional
+// tiles on existing loops, then at most one reorder; tile-factor and reorder axes
+// only; no unroll/vector marks, shared tensors or optional terms.  pax: the
+// reorder axis (-1: none).
+bool plan_space(DTask& T, int& pax) {
+  pax = -1;
+  if (!T.fast || T.tt_len <= 0 || T.has_shared || T.has_optional || T.base_unr || T.base_vec) return false;
+  if (T.family == LS_FAMILY_GPU && !T.costs_integral) return false;
+  uint32_t exist = T.base_exist;
+  int ntile = 0, last_tile = -1, reorder = -1;
+  for (int x = 0; x < T.n_xf; ++x) {
+    const DXform& xf = T.xf[x];
+    if (xf.enable_bit >= 0) return false;
+    if (xf.kind == LS_XF_TILE) {
+      if (xf.slot == NOSLOT || xf.new_slot == NOSLOT || !((exist >> xf.slot) & 1u) || ((exist >> xf.new_slot) & 1u))
+        return false;
+      exist |= 1u << xf.new_slot;
+      ++ntile;
+      last_tile = x;
+    } else if (xf.kind == LS_XF_REORDER) {
+      if (reorder >= 0) return false;
+      reorder = x;
+    } else {
+      return false;
+    }
+  }
+  if (reorder >= 0 && reorder < last_tile) return false;
+  if (T.n_base + ntile > MAXCH) return false;
+  for (int a = 0; a < T.sp_n; ++a) {
+    if (T.sp_ax[a].kind == LS_AX_PERM) {
+      if (pax >= 0) return false;
+      pax = a;
+    } else if (T.sp_ax[a].kind != LS_AX_PARAM) {
+      return false;
+    }
+  }
+  T.sp_nchain = T.n_base + ntile;
+  return true;
+}
+
+constexpr int64_t SD_MAX_ENTRIES = 8192;  // 32 KiB of shared memory
+
+// Group tables of the space path.  Every tensor's dimensions
+// whose count can vary are split into at most two groups (one when the whole
+// tensor fits), each with a table of 64-entry rows (stage mask <= 6 bits) keyed
+// by the choices of the tile axes that can change one of its dimensions; the
+// split minimising the entries is taken.  rows[g] = row count of group slot g.
+bool plan_space_groups(DTask& T, int32_t* rows) {
+  uint32_t dep_p[NSLOT], dep_b[NSLOT];
+  int64_t ub[NSLOT], pb[LS_MAX_PARAMS];
+  slot_deps(T, dep_p, dep_b, ub, pb);
+  memset(T.sd_S, 0, sizeof(T.sd_S));
+  memset(T.vb8, 0, sizeof(T.vb8));
+  memset(T.sd_gd, -1, sizeof(T.sd_gd));
+  memset(T.sd_gx, 0, sizeof(T.sd_gx));
+  memset(T.sd_nb, 0, sizeof(T.sd_nb));
+  for (int g = 0; g < 8; ++g) T.sd_off[g] = 0, rows[g] = 0;
+  if (T.n_tensors > 4) return false;
+  int64_t off = 4;  // entries 0..3: the ones row
+  for (int t = 0; t < T.n_tensors; ++t) {
+    int dims[4], nd = 0;
+    uint32_t pmask[4];
+    for (int rr = 0; rr < T.t_rank[t]; ++rr) {
+      const int D = t * 4 + rr;
+      bool varies = false;
+      for (int x = 0; x < T.dim_nv[D]; ++x) varies |= ub[T.dim_var[D][x]] > 1;
+      if (!varies && T.dim_count0[D] == 1) continue;  // the count stays 1
+      uint32_t pm, bm;
+      dim_deps(T, D, dep_p, dep_b, pm, bm);
+      pmask[nd] = pm;
+      dims[nd++] = D;
+    }
+    // choose the split (bit j of `sel`: dimension j goes to group 1) with the fewest entries
+    int64_t best = -1;
+    int best_sel = 0;
+    for (int sel = 0; sel < (1 << nd); ++sel) {
+      if (nd && (sel >> (nd - 1)) & 1) continue;  // symmetric splits: the last dimension stays in group 0
+      int64_t total = 0;
+      bool ok = true;
+      for (int j = 0; j < 2 && ok; ++j) {
+        uint32_t pm = 0;
+        int nb = 0, members = 0;
+        for (int q = 0; q < nd; ++q)
+          if (((sel >> q) & 1) == j) pm |= pmask[q], nb += T.dim_nv[dims[q]], ++members;
+        if (!members) continue;
+        if (nb > 6) ok = false;
+        int64_t keys = 1;
+        for (int a = 0; a < T.sp_n && ok; ++a)
+          if (T.sp_ax[a].kind == LS_AX_PARAM && ((pm >> T.sp_ax[a].param) & 1u)) keys *= T.sp_ax[a].n;
+        total += keys << nb;
+        if (total > SD_MAX_ENTRIES) ok = false;
+      }
+      if (ok && (best < 0 || total < best)) best = total, best_sel = sel;
+    }
+    if (best < 0) return false;
+    for (int j = 0; j < 2; ++j) {
+      const int G = 2 * t + j;
+      uint32_t pm = 0;
+      int nb = 0, m = 0;
+      for (int q = 0; q < nd; ++q) {
+        if (((best_sel >> q) & 1) != j) continue;
+        const int D = dims[q];
+        T.sd_gd[G][m] = (int8_t)D;
+        T.sd_gx[G][m] = (int8_t)nb;
+        for (int x = 0; x < T.dim_nv[D]; ++x) T.vb8[T.dim_var[D][x]] |= 1ull << (8 * G + 2 + nb + x);
+        nb += T.dim_nv[D];
+        pm |= pmask[q];
+        ++m;
+      }
+      if (!m) continue;
+      T.sd_nb[G] = (int8_t)nb;
+      int64_t keys = 1;
+      for (int a = T.sp_n - 1; a >= 0; --a) {
+        const DAxis& ax = T.sp_ax[a];
+        if (ax.kind != LS_AX_PARAM || !((pm >> ax.param) & 1u)) continue;
+        T.sd_S[a][G] = (uint32_t)((keys << nb) * 4);
+        keys *= ax.n;
+      }
+      if (off + (keys << nb) > SD_MAX_ENTRIES) return false;
+      T.sd_off[G] = (uint32_t)(off * 4);
+      rows[G] = (int32_t)keys;
+      off += keys << nb;
+    }
+  }
+  T.sd_len = (int32_t)off;
+  return true;
+}
 
 // Decide whether the task can use the tabulated path and lay out its table
 // (DESIGN.md §3.5).  A dimension's key is every record field that can change
@@ -2045,6 +2525,8 @@ int upload(ls_task* t) {
   CUDA_TRY(cudaMemcpy(dtab, t->utab.data(), sizeof(DUnroll) * t->utab.size(), cudaMemcpyHostToDevice));
   t->host.u_tab = dtab;
   t->host.n_u = (int32_t)t->utab.size();
+  for (const DUnroll& e : t->utab)
+    if (e.u == 1) t->host.c_inner1 = e.c_inner;
   CUDA_TRY(cudaMalloc(&dnew, sizeof(DTask)));
   CUDA_TRY(cudaMemcpy(dnew, &t->host, sizeof(DTask), cudaMemcpyHostToDevice));
   if (t->d_task) t->retired.push_back(t->d_task);
@@ -2083,18 +2565,20 @@ int grid_for(const ls_task* t, int64_t n, int per_sm) {
   return (int)std::max<int64_t>(1, std::min(want, cap));
 }
 
-// 0 generic, 1 tabulated (table in global memory), 2 tabulated (table in shared memory)
+// 0 generic, 1 tabulated (table in global memory), 2 tabulated (table in shared memory),
+// 3 tensor tables (points), 4 space-specialised (points)
 int mode_of(const ls_task* t, bool points = false) {
   if (t->path == LS_PATH_GENERIC || !t->host.fast) return 0;
+  if (points && t->host.sp_ok && t->path != LS_PATH_TABULATED) return 4;
   if (points && t->host.tt_ok) return 3;
   return t->host.tab_smem ? 2 : 1;
 }
 
 size_t smem_score(const DTask& T, int mode) {
-  return (size_t)T.task_bytes + tab_smem_bytes(mode, T.tab_len) + state_bytes(mode, T.n_slots, T.n_chain, T.n_stage);
+  return (size_t)T.task_bytes + tab_smem_bytes(mode, T) + state_bytes(mode, T.n_slots, T.n_chain, T.n_stage);
 }
 // the fused kernel's buffer must hold k plus one round of inserts
-int topk_buf(int k) { return k <= 1024 - TPB ? 1024 : 2048; }
+int topk_buf(int k) { return k <= 512 - TPB ? 512 : k <= 1024 - TPB ? 1024 : 2048; }
 size_t smem_topk(const DTask& T, int k, int mode) { return smem_score(T, mode) + align16(topk_state_bytes(topk_buf(k))); }
 
 using ScoreFn = void (*)(const DTask*, const void*, int, int64_t, double*, double*, int32_t*);
@@ -2103,16 +2587,34 @@ using TopkFn = void (*)(const DTask*, const void*, int, int64_t, int64_t, int, K
 
 template <int SRC>
 ScoreFn score_fn_src(const DTask& T, int mode) {
-  if constexpr (SRC == 1)
+  if constexpr (SRC == 1) {
+    if (mode == 4) {
+      switch (T.n_tensors) {
+        case 1: return score_kernel<1, 4, 4, 1>;
+        case 2: return score_kernel<2, 4, 4, 1>;
+        case 3: return score_kernel<3, 4, 4, 1>;
+        default: return score_kernel<4, 4, 4, 1>;
+      }
+    }
     if (mode == 3) return score_kernel<4, 4, 3, 1>;
+  }
   if (mode == 1) return score_kernel<4, 4, 1, SRC>;
   if (mode == 2) return score_kernel<4, 4, 2, SRC>;
   return T.layout_rm == 4 ? score_kernel<4, 4, 0, SRC> : score_kernel<MAXT, MAXRANK, 0, SRC>;
 }
 template <int SRC>
 TopkFn topk_fn_src(const DTask& T, int mode) {
-  if constexpr (SRC == 1)
+  if constexpr (SRC == 1) {
+    if (mode == 4) {
+      switch (T.n_tensors) {
+        case 1: return score_topk_kernel<1, 4, 4, 1>;
+        case 2: return score_topk_kernel<2, 4, 4, 1>;
+        case 3: return score_topk_kernel<3, 4, 4, 1>;
+        default: return score_topk_kernel<4, 4, 4, 1>;
+      }
+    }
     if (mode == 3) return score_topk_kernel<4, 4, 3, 1>;
+  }
   if (mode == 1) return score_topk_kernel<4, 4, 1, SRC>;
   if (mode == 2) return score_topk_kernel<4, 4, 2, SRC>;
   return T.layout_rm == 4 ? score_topk_kernel<4, 4, 0, SRC> : score_topk_kernel<MAXT, MAXRANK, 0, SRC>;
@@ -2190,8 +2692,8 @@ int ls_task_create(const ls_task_desc* desc, int device, ls_task** out) {
 }
 
 int ls_task_set_path(ls_task* t, int32_t path) {
-  if (!t || path < LS_PATH_AUTO || path > LS_PATH_TABULATED) return fail(LS_E_ARG, "bad argument");
-  if (path == LS_PATH_TABULATED && !t->host.fast)
+  if (!t || path < LS_PATH_AUTO || path > LS_PATH_SPACE) return fail(LS_E_ARG, "bad argument");
+  if ((path == LS_PATH_TABULATED || path == LS_PATH_SPACE) && !t->host.fast)
     return fail(LS_E_UNSUPPORTED, "task is not eligible for the tabulated path");
   t->path = path;
   return LS_E_OK;
@@ -2200,6 +2702,12 @@ int ls_task_set_path(ls_task* t, int32_t path) {
 int ls_task_path(const ls_task* t) {
   if (!t) return LS_E_ARG;
   return mode_of(t) ? LS_PATH_TABULATED : LS_PATH_GENERIC;
+}
+
+int ls_task_points_path(const ls_task* t) {
+  if (!t) return LS_E_ARG;
+  const int m = mode_of(t, true);
+  return m == 4 ? LS_PATH_SPACE : m ? LS_PATH_TABULATED : LS_PATH_GENERIC;
 }
 
 int ls_task_destroy(ls_task* t) {
@@ -2384,11 +2892,43 @@ int ls_task_set_space(ls_task* t, const ls_space_desc* sp) {
     t->host.tt = dtt;
   }
   if (int rc = upload(t)) return rc;
+  t->host.sp_ok = 0;
   if (tables) {
     build_ttab_kernel<<<(unsigned)((t->host.tt_len + 255) / 256), 256>>>(t->d_task, dtt);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaDeviceSynchronize());
     t->host.tt_ok = 1;
+    int pax = -1;
+    int32_t rows[16] = {0};
+    if (plan_space(t->host, pax) && plan_space_groups(t->host, rows)) {
+      const int np = pax >= 0 ? (int)t->host.sp_ax[pax].n : 1;
+      uint64_t* dch = nullptr;
+      int32_t *dst = nullptr, *drows = nullptr, *dovf = nullptr;
+      uint32_t* dsd = nullptr;
+      CUDA_TRY(cudaMalloc(&dch, sizeof(uint64_t) * np));
+      t->retired.push_back(dch);
+      CUDA_TRY(cudaMalloc(&dst, sizeof(int32_t) * np));
+      t->retired.push_back(dst);
+      CUDA_TRY(cudaMalloc(&dsd, sizeof(int32_t) * t->host.sd_len));
+      t->retired.push_back(dsd);
+      CUDA_TRY(cudaMalloc(&drows, sizeof(rows) + sizeof(int32_t)));
+      t->retired.push_back(drows);
+      CUDA_TRY(cudaMemcpy(drows, rows, sizeof(rows), cudaMemcpyHostToDevice));
+      dovf = drows + 16;
+      CUDA_TRY(cudaMemset(dovf, 0, sizeof(int32_t)));
+      if (int rc = upload(t)) return rc;
+      const size_t sm = sizeof(int32_t) * NSLOT * TPB;
+      build_pchain_kernel<<<(np + TPB - 1) / TPB, TPB, sm>>>(t->d_task, pax, dch, dst);
+      CUDA_TRY(cudaGetLastError());
+      build_sdt_kernel<<<(t->host.sd_len + 255) / 256, 256>>>(t->d_task, drows, dsd, dovf);
+      CUDA_TRY(cudaGetLastError());
+      int32_t ovf = 0;
+      CUDA_TRY(cudaMemcpy(&ovf, dovf, sizeof(int32_t), cudaMemcpyDeviceToHost));
+      t->host.sp_chain = dch;
+      t->host.sp_pstat = dst;
+      t->host.sd_tab = reinterpret_cast<const int32_t*>(dsd);
+      t->host.sp_ok = ovf ? 0 : 1;  // a group product beyond 32 bits: keep the tensor-table path
+    }
     return upload(t);
   }
   return LS_E_OK;
@@ -2407,7 +2947,9 @@ int ls_topk_merge(const double* d_scores, const int64_t* d_index, int32_t n_list
     lists_to_keys_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(d_scores, d_index, m, keys);
     CUDA_TRY(cudaGetLastError());
   }
-  merge_keys_kernel<<<1, 1024, 0, s>>>(keys, m, k_out, d_out_scores, d_out_index);
+  const size_t msm = topk_state_bytes(topk_buf(k_out));
+  cudaFuncSetAttribute(merge_keys_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm);
+  merge_keys_kernel<<<1, TPB, msm, s>>>(keys, m, k_out, d_out_scores, d_out_index, topk_buf(k_out));
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaFreeAsync(keys, s));
   return LS_E_OK;

@@ -50,6 +50,7 @@ def lib():
     L.ls_score_topk_points.argtypes = [vp, vp, i32, i64, i64, i32, vp, vp, vp, vp]
     L.ls_score_topk_points_host.argtypes = [vp, vp, i32, i64, i64, i32, vp, vp, vp, vp]
     L.ls_task_path.argtypes = [vp]
+    L.ls_task_points_path.argtypes = [vp]
     if L.ls_abi_version() != abi.ABI_VERSION:
         raise EngineError("libloopscout_b200 ABI version mismatch")
     _lib = L
@@ -110,15 +111,21 @@ class Task:
             pass
 
     # -- scoring path -----------------------------------------------------------------
-    PATH_AUTO, PATH_GENERIC, PATH_TABULATED = 0, 1, 2
+    PATH_AUTO, PATH_GENERIC, PATH_TABULATED, PATH_SPACE = 0, 1, 2, 3
 
     def set_path(self, path: int):
-        """Force the generic or the tabulated kernel (both bit-identical; include/loopscout_b200.h)."""
+        """Force a scoring kernel (all bit-identical; LS_PATH_* in include/loopscout_b200.h)."""
         _check(lib().ls_task_set_path(self._h, int(path)), "ls_task_set_path")
 
     @property
     def path(self) -> int:
+        """Path of the record calls (LS_PATH_GENERIC / LS_PATH_TABULATED)."""
         return lib().ls_task_path(self._h)
+
+    @property
+    def points_path(self) -> int:
+        """Path of the points calls (LS_PATH_GENERIC / LS_PATH_TABULATED / LS_PATH_SPACE)."""
+        return lib().ls_task_points_path(self._h)
 
     # -- unroll table ---------------------------------------------------------------
     def prepare_unroll_for(self, d_records, stream=None):

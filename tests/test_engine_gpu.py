@@ -27,10 +27,13 @@ PATHS = [1, 2]  # LS_PATH_GENERIC, LS_PATH_TABULATED (include/loopscout_b200.h)
 
 def _set_path(task, path):
     """Force a scoring path; False if the task is not eligible for it."""
-    if path == 2 and task.path != 2:
+    if path in (2, 3) and task.path != 2:
         return False
     task.set_path(path)
     return True
+
+
+POINT_PATHS = [1, 2, 3]  # + LS_PATH_SPACE (points calls only)
 
 
 @pytest.mark.parametrize("path", PATHS)
@@ -234,7 +237,7 @@ def _es_space(name):
     return SpaceTemplate(ir.parse_program(json.dumps(r["program"])), r["space"]), r["arch"]
 
 
-@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("path", POINT_PATHS)
 @pytest.mark.parametrize("which", ["gemm1024", "conv56", "es:conv_small"])
 def test_points_equal_records(torch, which, path):
     """Points API (space-point decode on device) == records API on the same candidates."""
@@ -253,6 +256,8 @@ def test_points_equal_records(torch, which, path):
             task.close()
             continue
         task.set_space(st.space_desc())
+        if path == 3 and not which.startswith("es:"):
+            assert task.points_path == 3, "tile+reorder BASELINE spaces take the space-specialised path"
         recs = st.records_from_indices(idx)
         pts = st.points_from_indices(idx)
         assert np.array_equal(st.indices_from_points(pts), idx)
@@ -284,4 +289,79 @@ def test_points_out_of_range(torch):
     s, f, stt = task.score_points(torch.from_numpy(pts.view(np.int32)).cuda())
     torch.cuda.synchronize()
     assert stt.cpu().tolist()[2:] == [19, 19] and stt.cpu().tolist()[:2] == [0, 0]
+    task.close()
+
+
+@pytest.mark.parametrize("path", POINT_PATHS)
+@pytest.mark.parametrize("name", SPACE_FIXTURES)
+def test_space_fixtures_points_bit_exact(torch, name, path):
+    """Every BASELINE space through the points API on every points path == the reference's outputs."""
+    E = _engine()
+    st, _, z = space_case(name)
+    pts = st.points_from_indices(z["idx"])
+    dp = torch.from_numpy(pts.view(np.int32) if pts.dtype == np.uint32 else pts.view(np.int64)).cuda()
+    for a in z["arches"]:
+        a = str(a)
+        task = E.Task(st.template.desc(arch_named(a), launch()), 0)
+        assert _set_path(task, path)
+        task.set_space(st.space_desc())
+        assert task.points_path == path
+        s, f, status = task.score_points(dp)
+        torch.cuda.synchronize()
+        assert (status.cpu().numpy() == 0).all()
+        np.testing.assert_array_equal(f.cpu().numpy(), z[f"feats_{a}"])
+        np.testing.assert_array_equal(s.cpu().numpy(), z[f"scores_{a}"])
+        ts, ti, nv = task.score_topk_points(dp, 64)
+        want = sorted(range(len(pts)), key=lambda q: (z[f"scores_{a}"][q], q))[:64]
+        assert ti.cpu().tolist() == want and int(nv.item()) == len(pts)
+        task.close()
+
+
+@pytest.mark.parametrize("reorder", [["i", "i_i", "j"], ["j", "i_i"], ["k", "i"], ["i", "q"]])
+def test_space_path_failing_reorders(torch, reorder):
+    """Reorder sets that are valid, non-contiguous (REORDER_CHAIN) or name a missing loop (NO_LOOP):
+    the space-specialised path reports the same status and scores as the generic record path."""
+    import itertools
+    E = _engine()
+    from paper_2104_14641_b200 import workloads as W
+    from paper_2104_14641_b200.pack import SpaceTemplate
+    prog = W.program(W.matmul_json(64))
+    space = {"tile": {"i": W.divisors(64), "j": [1, 2, 8]},
+             "reorder": [list(p) for p in itertools.permutations(reorder)]}
+    st = SpaceTemplate(prog, space)
+    idx = W.distinct_indices(st.sizes, int(st.size), 3)
+    for a in ("x86-avx2", "aarch64-neon", "nvidia-volta"):
+        task = E.Task(st.template.desc(arch_named(a), launch()), 0)
+        task.set_space(st.space_desc())
+        assert task.points_path == 3
+        pts = st.points_from_indices(idx)
+        dp = torch.from_numpy(pts.view(np.int32)).cuda()
+        ps, pf, pst = task.score_points(dp)
+        task.set_path(1)
+        s, f, stt = task.score(E.to_device_records(st.records_from_indices(idx)))
+        torch.cuda.synchronize()
+        assert torch.equal(stt, pst)
+        ok = stt == 0
+        assert torch.equal(s[ok], ps[ok]) and torch.equal(f[ok], pf[ok])
+        task.close()
+
+
+@pytest.mark.parametrize("k", [1, 7, 64, 300, 1024])
+def test_topk_selection_ties(torch, k):
+    """Radix-selected block lists and merge tree under heavy score ties: equal to a stable sort."""
+    E = _engine()
+    st, _, z = space_case("gemm1024")
+    task = E.Task(st.template.desc(arch_named("x86-avx2"), launch()), 0)
+    task.set_space(st.space_desc())
+    from paper_2104_14641_b200 import workloads as W
+    idx = np.concatenate([W.distinct_indices(st.sizes, 200000, 5)] * 3)  # every score 3x (and more ties)
+    pts = st.points_from_indices(idx)
+    dp = torch.from_numpy(pts.view(np.int32)).cuda()
+    s, _, _ = task.score_points(dp, features=False)
+    ts, ti, nv = task.score_topk_points(dp, k, base_index=11)
+    torch.cuda.synchronize()
+    sc = s.cpu().numpy()
+    want = np.lexsort((np.arange(len(sc)), sc))[:k]
+    assert (ti.cpu().numpy() - 11).tolist() == want.tolist()
+    assert np.array_equal(ts.cpu().numpy(), sc[want])
     task.close()

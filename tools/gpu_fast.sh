@@ -1,15 +1,13 @@
-# round-1 tabulated path: parity + A/B bench + launch list + one full ncu capture
+# build, GPU parity, A/B bench of the points paths (auto = space-specialised), launch list
 set -x
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?
 timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
 tail -30 gpurun_out/pytest_gpu.log
-timeout 300 python bench.py --path 1 --no-baseline > gpurun_out/bench_p1.log 2>&1; echo b1=$?
+timeout 300 python bench.py --no-baseline > gpurun_out/bench_auto.log 2>&1; echo b0=$?
 timeout 300 python bench.py --path 2 --no-baseline > gpurun_out/bench_p2.log 2>&1; echo b2=$?
-timeout 300 python bench.py --path 2 --no-baseline --arch nvidia-volta > gpurun_out/bench_p2v.log 2>&1; echo b2v=$?
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-baseline > gpurun_out/ncu_launch_bench.log 2>&1; echo ncu1=$?
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:score_topk_kernel -s 3 -c 1 -o gpurun_out/topk_full python bench.py --steps 2 --warmup 1 --no-baseline > gpurun_out/ncu_full.log 2>&1; echo ncu2=$?
-grep -h '"value"' gpurun_out/bench_p*.log | python -c "
+timeout 300 python bench.py --no-baseline --arch nvidia-volta > gpurun_out/bench_v.log 2>&1; echo bv=$?
+grep -h '"value"' gpurun_out/bench_auto.log gpurun_out/bench_p2.log gpurun_out/bench_v.log | python -c "
 import sys, json
 for l in sys.stdin:
-    d = json.loads(l); print(d['config']['arch'], d['value']/1e9, d['e2e']['value']/1e9, d['roofline']['kernel_ms'])"
+    d = json.loads(l); print(d['config']['arch'], d['path'], 'value', d['value']/1e9, 'e2e', d['e2e']['value']/1e9, 'kms', d['roofline']['kernel_ms'], 'rec', d['records_path']['value']/1e9)"
