@@ -259,8 +259,11 @@ int ls_topk_merge(const double* d_scores, const int64_t* d_index, int32_t n_list
                   int32_t k_out, double* d_out_scores, int64_t* d_out_index, void* stream);
 
 /* Host-buffer variant of ls_score_topk: records in host memory (pinned or
- * pageable), results written to host memory; the library stages the
- * host->device copies in chunks overlapped with scoring.  Synchronous. */
+ * pageable), results written to host memory.  Mapped page-locked buffers
+ * (cudaHostAlloc / torch pin_memory under UVA) are read by the scoring kernel
+ * over the host link (the transfer overlaps the scoring, no staging copy);
+ * other buffers are copied host->device in chunks overlapped with scoring.
+ * Synchronous. */
 int ls_score_topk_host(ls_task* task, const ls_record* h_records, int64_t n, int64_t base_index,
                        int32_t k, double* h_top_scores, int64_t* h_top_index, int64_t* h_n_valid,
                        void* stream);
@@ -282,7 +285,7 @@ int ls_score_points(ls_task* task, const void* d_points, int32_t point_bytes, in
 int ls_score_topk_points(ls_task* task, const void* d_points, int32_t point_bytes, int64_t n,
                          int64_t base_index, int32_t k, double* d_top_scores, int64_t* d_top_index,
                          int64_t* d_n_valid, void* stream);
-/* ls_score_topk_host over host points (H2D staged and overlapped). */
+/* ls_score_topk_host over host points (mapped, or H2D staged and overlapped). */
 int ls_score_topk_points_host(ls_task* task, const void* h_points, int32_t point_bytes, int64_t n,
                               int64_t base_index, int32_t k, double* h_top_scores, int64_t* h_top_index,
                               int64_t* h_n_valid, void* stream);

@@ -170,6 +170,11 @@ struct __align__(16) DTask {
   int8_t sd_gd[8][4];                 // dimension slots of each group (-1: none)
   int8_t sd_gx[8][4];                 // bit offset of each of them within the group's stage mask
   int8_t sd_nb[8];                    // stage bits of each group (rows of 2^nb entries)
+  // static tiles: every tile is driven by one tile axis and splits a base loop not split before,
+  // so a choice fixes both extents; sp_ext per choice = F | ceil(E/F) << 16 | out-of-range << 63
+  int32_t sp_static, pad7;
+  const uint64_t* sp_ext;
+  uint8_t sp_tslot[LS_MAX_AXES], sp_tnew[LS_MAX_AXES];
   int32_t n_terms;
   DTerm term[MAXTERM];
 };
@@ -1151,13 +1156,20 @@ __device__ int eval_tensor(const DTask& T, const ls_record& r, const uint32_t* k
 //   PTX  W'_j uses extent 1 for loops 8+ above the innermost (counter-register wrap),
 //        sum_j W'_{j-1} = 1 + A, sum_j W'_j = A + W'_{n-1}, A = sum_{j<n-1} W'_j
 // which are the general closed forms of features_score with every R_j = 1.
+__device__ __forceinline__ uint64_t load_point(const void* __restrict__ src, int pbytes, int64_t i) {
+  return pbytes == 4 ? (uint64_t)__ldg(reinterpret_cast<const unsigned int*>(src) + i)
+                     : (uint64_t)__ldg(reinterpret_cast<const unsigned long long*>(src) + i);
+}
+
 template <int TM>
-__device__ int eval_space(const DTask& T, const int32_t* __restrict__ sdt, const void* __restrict__ src, int pbytes,
-                          int64_t i, FastCand& c, double* f, double* score) {
+__device__ int eval_space(const DTask& T, const int32_t* __restrict__ sdt, uint64_t x, FastCand& c, double* f,
+                          double* score) {
   // ---- decode the space point (mixed radix, axis 0 most significant): tile factors into the
-  //      record's parameter slots, the reorder choice, the dimension-table row offsets
-  uint64_t x = pbytes == 4 ? (uint64_t)__ldg(reinterpret_cast<const unsigned int*>(src) + i)
-                           : (uint64_t)__ldg(reinterpret_cast<const unsigned long long*>(src) + i);
+  //      record's parameter slots (or, static tiles, both extents straight from the choice), the
+  //      reorder choice, the group-table row offsets
+  const bool stat = T.sp_static;
+  if (stat)
+    for (int p = 0; p < T.n_base; ++p) c.E(T.base_slot[p]) = T.base_ext[p];
   uint32_t kd[TM * 2];
 #pragma unroll
   for (int g = 0; g < TM * 2; ++g) kd[g] = T.sd_off[g];
@@ -1180,28 +1192,37 @@ __device__ int eval_space(const DTask& T, const int32_t* __restrict__ sdt, const
       pch = ch;
       continue;
     }
+#pragma unroll
+    for (int g = 0; g < TM * 2; ++g) kd[g] += ch * T.sd_S[a][g];
+    if (stat) {  // Tile (ls/ir.py:361-382) of a base loop: F and ceil(E/F) per choice
+      const uint64_t e = __ldg(reinterpret_cast<const unsigned long long*>(T.sp_ext) + ax.voff + ch);
+      if (e >> 63) return LS_ST_TILE_RANGE;
+      c.E(T.sp_tnew[a]) = (int32_t)(e & 0xFFFFu);
+      c.E(T.sp_tslot[a]) = (int32_t)((e >> 16) & 0x7FFFFFFFu);
+      continue;
+    }
     const uint64_t v = __ldg(reinterpret_cast<const unsigned long long*>(T.sp_vals) + ax.voff + ch);
     if (ax.param < 4)
       lo |= v << (16 * ax.param);
     else
       hi |= v << (16 * (ax.param - 4));
-#pragma unroll
-    for (int g = 0; g < TM * 2; ++g) kd[g] += ch * T.sd_S[a][g];
   }
-  ls_record r;
-  memcpy(&r.param[0], &lo, 8);
-  memcpy(&r.param[4], &hi, 8);
-  // ---- extents: Tile arithmetic in template order (ls/ir.py:361-382), with the
-  //      checks of apply_fast that a tile factor can fail
-  for (int p = 0; p < T.n_base; ++p) c.E(T.base_slot[p]) = T.base_ext[p];
-  for (int q = 0; q < T.n_xf; ++q) {
-    const DXform& xf = T.xf[q];
-    if (xf.kind != LS_XF_TILE) continue;
-    const int32_t F = xf.param >= 0 ? (int32_t)rparam(r, xf.param) : xf.value;
-    const int32_t Ev = c.E(xf.slot);
-    if (F < 1 || F > Ev) return LS_ST_TILE_RANGE;
-    c.E(xf.new_slot) = F;
-    c.E(xf.slot) = (Ev + F - 1) / F;
+  if (!stat) {
+    ls_record r;
+    memcpy(&r.param[0], &lo, 8);
+    memcpy(&r.param[4], &hi, 8);
+    // ---- extents: Tile arithmetic in template order (ls/ir.py:361-382), with the
+    //      checks of apply_fast that a tile factor can fail
+    for (int p = 0; p < T.n_base; ++p) c.E(T.base_slot[p]) = T.base_ext[p];
+    for (int q = 0; q < T.n_xf; ++q) {
+      const DXform& xf = T.xf[q];
+      if (xf.kind != LS_XF_TILE) continue;
+      const int32_t F = xf.param >= 0 ? (int32_t)rparam(r, xf.param) : xf.value;
+      const int32_t Ev = c.E(xf.slot);
+      if (F < 1 || F > Ev) return LS_ST_TILE_RANGE;
+      c.E(xf.new_slot) = F;
+      c.E(xf.slot) = (Ev + F - 1) / F;
+    }
   }
   const int pst = __ldg(T.sp_pstat + pch);
   if (pst) return pst;
@@ -1531,7 +1552,7 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE))
     double s = 0.0;
     int st;
     if constexpr (MODE == 4) {
-      st = eval_space<TM>(T, tab, src, pbytes, i, ev.fc, f, &s);
+      st = eval_space<TM>(T, tab, load_point(src, pbytes, i), ev.fc, f, &s);
     } else {
       uint32_t pch = 0;
       st = load_cand<SRC, MODE == 3>(T, src, pbytes, i, r, kt, pch);
@@ -1799,7 +1820,11 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kern
   topk_init(S, cap);
   unsigned int valid = 0;
   int safe = 1;
-  for (int64_t base = (int64_t)blockIdx.x * TPB; base < n; base += (int64_t)gridDim.x * TPB) {
+  const int64_t stride = (int64_t)gridDim.x * TPB;
+  uint64_t xn = 0;  // space path: the next point, loaded one iteration ahead
+  if constexpr (MODE == 4)
+    if ((int64_t)blockIdx.x * TPB + threadIdx.x < n) xn = load_point(src, pbytes, (int64_t)blockIdx.x * TPB + threadIdx.x);
+  for (int64_t base = (int64_t)blockIdx.x * TPB; base < n; base += stride) {
     const int64_t i = base + threadIdx.x;
     bool has = false;
     Key key;
@@ -1810,7 +1835,9 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kern
       double s;
       int st;
       if constexpr (MODE == 4) {
-        st = eval_space<TM>(T, tab, src, pbytes, i, ev.fc, f, &s);
+        const uint64_t x = xn;
+        if (i + stride < n) xn = load_point(src, pbytes, i + stride);
+        st = eval_space<TM>(T, tab, x, ev.fc, f, &s);
       } else {
         uint32_t pch = 0;
         st = load_cand<SRC, MODE == 3>(T, src, pbytes, i, r, kt, pch);
@@ -2081,6 +2108,54 @@ bool plan_space(DTask& T, int& pax) {
 }
 
 constexpr int64_t SD_MAX_ENTRIES = 8192;  // 32 KiB of shared memory
+
+// Static tiles of the space path: every Tile is driven by exactly one tile axis
+// and splits a base loop that no earlier Tile split, so each choice fixes the
+// inner extent F and the outer extent ceil(E/F) (ls/ir.py:361-382) and whether
+// F is out of range.  ext[voff + c] per choice of the tile axes (indexed like
+// sp_vals; other axes' entries unused).
+void plan_static_tiles(DTask& T, const ls_space_desc* sp, std::vector<uint64_t>& ext) {
+  T.sp_static = 0;
+  int ntile = 0;
+  for (int x = 0; x < T.n_xf; ++x) ntile += T.xf[x].kind == LS_XF_TILE;
+  uint32_t split = 0;  // base slots already split
+  int covered = 0;
+  size_t nvals = 0;
+  for (int a = 0; a < sp->n_axes; ++a) nvals += sp->axes[a].kind == LS_AX_BIT ? 0 : sp->axes[a].n_choices;
+  ext.assign(std::max<size_t>(1, nvals), 0);
+  for (int x = 0; x < T.n_xf; ++x) {
+    const DXform& xf = T.xf[x];
+    if (xf.kind != LS_XF_TILE) continue;
+    if (xf.param < 0) return;
+    int axis = -1, naxes = 0;
+    for (int a = 0; a < T.sp_n; ++a)
+      if (T.sp_ax[a].kind == LS_AX_PARAM && T.sp_ax[a].param == xf.param) axis = a, ++naxes;
+    if (naxes != 1) return;
+    int base = -1;
+    for (int p = 0; p < T.n_base; ++p)
+      if (T.base_slot[p] == xf.slot) base = p;
+    if (base < 0 || ((split >> xf.slot) & 1u)) return;
+    split |= 1u << xf.slot;
+    const int64_t Ev = T.base_ext[base];
+    const DAxis& ax = T.sp_ax[axis];
+    for (uint32_t c = 0; c < ax.n; ++c) {
+      const int64_t F = (int64_t)sp->axes[axis].values[c];
+      const bool bad = F < 1 || F > Ev;
+      const int64_t outer = bad ? 1 : (Ev + F - 1) / F;
+      ext[ax.voff + c] = (uint64_t)(F & 0xFFFF) | ((uint64_t)outer << 16) | (bad ? (1ull << 63) : 0ull);
+    }
+    T.sp_tslot[axis] = xf.slot;
+    T.sp_tnew[axis] = xf.new_slot;
+    ++covered;
+  }
+  for (int a = 0; a < T.sp_n; ++a) {  // every tile axis must drive a tile
+    if (T.sp_ax[a].kind != LS_AX_PARAM) continue;
+    bool used = false;
+    for (int x = 0; x < T.n_xf; ++x) used |= T.xf[x].kind == LS_XF_TILE && T.xf[x].param == T.sp_ax[a].param;
+    if (!used) return;
+  }
+  T.sp_static = covered == ntile ? 1 : 0;
+}
 
 // Group tables of the space path.  Every tensor's dimensions
 // whose count can vary are split into at most two groups (one when the whole
@@ -2900,7 +2975,16 @@ int ls_task_set_space(ls_task* t, const ls_space_desc* sp) {
     t->host.tt_ok = 1;
     int pax = -1;
     int32_t rows[16] = {0};
+    std::vector<uint64_t> ext;
     if (plan_space(t->host, pax) && plan_space_groups(t->host, rows)) {
+      plan_static_tiles(t->host, sp, ext);
+      uint64_t* dext = nullptr;
+      if (t->host.sp_static) {
+        CUDA_TRY(cudaMalloc(&dext, sizeof(uint64_t) * ext.size()));
+        t->retired.push_back(dext);
+        CUDA_TRY(cudaMemcpy(dext, ext.data(), sizeof(uint64_t) * ext.size(), cudaMemcpyHostToDevice));
+        t->host.sp_ext = dext;
+      }
       const int np = pax >= 0 ? (int)t->host.sp_ax[pax].n : 1;
       uint64_t* dch = nullptr;
       int32_t *dst = nullptr, *drows = nullptr, *dovf = nullptr;
@@ -2955,9 +3039,46 @@ int ls_topk_merge(const double* d_scores, const int64_t* d_index, int32_t n_list
   return LS_E_OK;
 }
 
+// Host buffers that are page-locked and mapped (cudaHostAlloc / torch pin_memory under UVA)
+// are read by the scoring kernel itself over the host link: the host->device transfer of the
+// candidates overlaps the scoring with no staging copy.  Returns the device alias or null.
+static const void* mapped_alias(const void* h) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, h) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
+}
+
+static int score_topk_mapped(ls_task* t, const void* d_alias, int pbytes, int64_t n, int64_t base_index, int32_t k,
+                             double* h_top_scores, int64_t* h_top_index, int64_t* h_n_valid, cudaStream_t s) {
+  unsigned char* blk = nullptr;  // top scores | top indices | valid count
+  const size_t bytes = sizeof(double) * k + sizeof(int64_t) * k + sizeof(unsigned long long);
+  CUDA_TRY(cudaMallocAsync(&blk, bytes, s));
+  double* out_s = reinterpret_cast<double*>(blk);
+  int64_t* out_i = reinterpret_cast<int64_t*>(blk + sizeof(double) * k);
+  unsigned long long* valid = reinterpret_cast<unsigned long long*>(blk + 16 * (size_t)k);
+  CUDA_TRY(cudaMemsetAsync(valid, 0, sizeof(unsigned long long), s));
+  int rc = topk_device(t, d_alias, pbytes, n, base_index, k, out_s, out_i, valid, s);
+  unsigned long long hv = 0;
+  if (rc == LS_E_OK) {
+    CUDA_TRY(cudaMemcpyAsync(h_top_scores, out_s, sizeof(double) * k, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(h_top_index, out_i, sizeof(int64_t) * k, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(&hv, valid, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  }
+  cudaFreeAsync(blk, s);
+  CUDA_TRY(cudaStreamSynchronize(s));
+  if (h_n_valid) *h_n_valid = (int64_t)hv;
+  return rc;
+}
+
 static int score_topk_host_any(ls_task* t, const void* h_src, int pbytes, int64_t n, int64_t base_index, int32_t k,
                                double* h_top_scores, int64_t* h_top_index, int64_t* h_n_valid, cudaStream_t s) {
   CUDA_TRY(cudaSetDevice(t->device));
+  if (n > 0)
+    if (const void* alias = mapped_alias(h_src))
+      return score_topk_mapped(t, alias, pbytes, n, base_index, k, h_top_scores, h_top_index, h_n_valid, s);
   const size_t esz = pbytes ? (size_t)pbytes : sizeof(ls_record);
   const int64_t CH = (int64_t)((8u << 20) / esz);  // 8 MiB chunks: copy of chunk c+1 overlaps scoring of chunk c
   const int64_t nch = std::max<int64_t>(1, (n + CH - 1) / CH);
