@@ -290,6 +290,40 @@ int ls_score_topk_points_host(ls_task* task, const void* h_points, int32_t point
                               int64_t base_index, int32_t k, double* h_top_scores, int64_t* h_top_index,
                               int64_t* h_n_valid, void* stream);
 
+/* ---- ES search on device (throughput mode of optimize, ls/es.py:130-204) ----
+ * Every generation runs on the device with no host round trip: Gaussian noise
+ * from Philox4x32-10 keyed by (seed, generation) with counter (member, pair)
+ * and Box-Muller (not numpy's PCG64 stream: trajectories differ from the
+ * reference's optimize; es.optimize is the exact-trajectory parity mode),
+ * ThetaEncoding.decode, the memo of distinct schedules keyed by space point,
+ * scoring of new points, the rank-shaped update and the incumbent trace.  The
+ * task needs an attached space (ls_task_set_space); axes follow space_axes. */
+typedef struct {
+  double alpha, sigma;          /* EsParams (ls/es.py:26-41) */
+  int32_t population, iterations;
+  uint64_t seed;
+  int32_t rank_normalize, pad;
+} ls_es_params;
+
+typedef struct ls_es ls_es;
+
+/* Allocate a run (memo table sized for min(space, population*iterations+1)
+ * distinct schedules).  h_theta0: start vector (NULL: ThetaEncoding.initial). */
+int ls_es_create(ls_task* task, const ls_es_params* params, const double* h_theta0, ls_es** out);
+/* Enqueue the start point and every generation (one CUDA graph per generation) on `stream`. */
+int ls_es_run(ls_es* es, void* stream);
+/* After ls_es_run: theta history [iterations+1][dim], trace [iterations] (best score after
+ * each generation), distinct evaluations, first failure (0 none; else generation+1 (0: the
+ * start point) << 40 | member << 8 | LS_ST_*) and best score.  Any pointer may be NULL.  Synchronous. */
+int ls_es_result(ls_es* es, double* h_theta_hist, double* h_trace, int64_t* h_evaluations, int64_t* h_error,
+                 double* h_best_score, void* stream);
+/* Distinct evaluated schedules (space points, scores) in discovery order, at most `cap`;
+ * *h_count = total.  Synchronous. */
+int ls_es_evaluated(ls_es* es, uint64_t* h_points, double* h_scores, int64_t cap, int64_t* h_count, void* stream);
+/* The Gaussian noise of a generation, [population][dim] float64 on the device (diagnostic). */
+int ls_es_noise(ls_es* es, int32_t generation, double* d_out, void* stream);
+int ls_es_destroy(ls_es* es);
+
 #ifdef __cplusplus
 }
 #endif

@@ -88,3 +88,10 @@ class Axis(C.Structure):
 
 class SpaceDesc(C.Structure):
     _fields_ = [("n_axes", C.c_int32), ("axes", Axis * MAX_AXES)]
+
+
+class EsParams(C.Structure):
+    """ls_es_params (include/loopscout_b200.h): EsParams of ls/es.py:26-41."""
+    _fields_ = [("alpha", C.c_double), ("sigma", C.c_double), ("population", C.c_int32),
+                ("iterations", C.c_int32), ("seed", C.c_uint64), ("rank_normalize", C.c_int32),
+                ("pad", C.c_int32)]

@@ -3161,3 +3161,6 @@ int ls_score_topk_points_host(ls_task* t, const void* h_points, int32_t pbytes, 
 }
 
 }  // extern "C"
+
+// ES generation loop on device
+#include "es.cuh"

@@ -51,6 +51,12 @@ def lib():
     L.ls_score_topk_points_host.argtypes = [vp, vp, i32, i64, i64, i32, vp, vp, vp, vp]
     L.ls_task_path.argtypes = [vp]
     L.ls_task_points_path.argtypes = [vp]
+    L.ls_es_create.argtypes = [vp, vp, vp, C.POINTER(vp)]
+    L.ls_es_run.argtypes = [vp, vp]
+    L.ls_es_result.argtypes = [vp, vp, vp, vp, vp, vp, vp]
+    L.ls_es_evaluated.argtypes = [vp, vp, vp, i64, vp, vp]
+    L.ls_es_noise.argtypes = [vp, i32, vp, vp]
+    L.ls_es_destroy.argtypes = [vp]
     if L.ls_abi_version() != abi.ABI_VERSION:
         raise EngineError("libloopscout_b200 ABI version mismatch")
     _lib = L
@@ -241,3 +247,73 @@ def topk_merge(scores, index, n_lists: int, k_in: int, k_out: int, stream=None):
     _check(lib().ls_topk_merge(_dptr(scores), _dptr(index), int(n_lists), int(k_in), int(k_out),
                                _dptr(out_s), _dptr(out_i), _stream(torch, stream)), "ls_topk_merge")
     return out_s, out_i
+
+
+class EsRun:
+    """A device ES run over a task's attached space (ls_es_* in include/loopscout_b200.h)."""
+
+    def __init__(self, task: Task, alpha: float, sigma: float, population: int, iterations: int, seed: int,
+                 rank_normalize: bool = True, theta0=None):
+        self.task = task
+        self.dim = None
+        p = abi.EsParams(alpha=float(alpha), sigma=float(sigma), population=int(population),
+                         iterations=int(iterations), seed=int(seed) & (2 ** 64 - 1),
+                         rank_normalize=1 if rank_normalize else 0)
+        self.params = p
+        th = None if theta0 is None else np.ascontiguousarray(theta0, np.float64)
+        h = C.c_void_p()
+        with _torch().cuda.device(task.device):
+            _check(lib().ls_es_create(task._h, C.addressof(p), None if th is None else th.ctypes.data,
+                                      C.byref(h)), "ls_es_create")
+        self._h = h
+
+    def run(self, stream=None):
+        torch = _torch()
+        with torch.cuda.device(self.task.device):
+            _check(lib().ls_es_run(self._h, _stream(torch, stream)), "ls_es_run")
+
+    def result(self, dim: int, stream=None):
+        """(theta history [iters+1, dim], trace [iters], evaluations, error code, best score)."""
+        torch = _torch()
+        it = self.params.iterations
+        hist = np.zeros((it + 1, dim), np.float64)
+        trace = np.zeros(it, np.float64)
+        ev = np.zeros(1, np.int64)
+        err = np.zeros(1, np.int64)
+        best = np.zeros(1, np.float64)
+        with torch.cuda.device(self.task.device):
+            _check(lib().ls_es_result(self._h, hist.ctypes.data, trace.ctypes.data, ev.ctypes.data,
+                                      err.ctypes.data, best.ctypes.data, _stream(torch, stream)), "ls_es_result")
+        return hist, trace, int(ev[0]), int(err[0]), float(best[0])
+
+    def evaluated(self, stream=None):
+        """Distinct evaluated (points uint64, scores float64) in discovery order."""
+        torch = _torch()
+        cnt = np.zeros(1, np.int64)
+        with torch.cuda.device(self.task.device):
+            _check(lib().ls_es_evaluated(self._h, None, None, 0, cnt.ctypes.data, _stream(torch, stream)),
+                   "ls_es_evaluated")
+            m = int(cnt[0])
+            pts = np.zeros(m, np.uint64)
+            sc = np.zeros(m, np.float64)
+            _check(lib().ls_es_evaluated(self._h, pts.ctypes.data, sc.ctypes.data, m, cnt.ctypes.data,
+                                         _stream(torch, stream)), "ls_es_evaluated")
+        return pts, sc
+
+    def noise(self, generation: int, dim: int, stream=None):
+        torch = _torch()
+        out = torch.empty((self.params.population, dim), dtype=torch.float64, device=f"cuda:{self.task.device}")
+        with torch.cuda.device(self.task.device):
+            _check(lib().ls_es_noise(self._h, int(generation), _dptr(out), _stream(torch, stream)), "ls_es_noise")
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().ls_es_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass

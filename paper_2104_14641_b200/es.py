@@ -18,7 +18,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .engine import Task, to_device_records
+from .engine import EsRun, Task, to_device_records
 from .ir import Schedule, space_axes
 from .pack import SpaceTemplate
 from .arch import CPU_FEATURES, GPU_FEATURES, FeatureVector
@@ -216,3 +216,68 @@ def optimize(program, space: dict, arch, params: EsParams, jobs=None, launch=Non
         evaluations=len(obj.by_key),
         diagnostics=diagnostics,
     )
+
+
+def _error_text(err: int) -> str:
+    from . import abi
+    gen, member, st = err >> 40, (err >> 8) & ((1 << 32) - 1), err & 0xFF
+    where = "start point" if gen == 0 else f"population candidate {member} failed at iteration {gen - 1}"
+    return f"{where}: {abi.STATUS.get(st, st)}"
+
+
+def optimize_device(program, space: dict, arch, params: EsParams, jobs=None, launch=None, device: int = 0,
+                    materialize: bool = True) -> OptimizeResult:
+    """ES search with every generation on the device (throughput mode, include/loopscout_b200.h ls_es_*).
+
+    Same API, EsParams, centroid start, decode, memo of distinct schedules,
+    rank-shaped update and incumbent rule as optimize (ls/es.py:130-204); the
+    Gaussian noise is Philox4x32-10 + Box-Muller on the device instead of
+    numpy's PCG64, so the trajectory is not the reference's (optimize above is
+    the exact-trajectory mode).  `jobs` is accepted for API parity and unused.
+    materialize=False skips building the evaluated dict (JSON keys) for large runs.
+    """
+    axes = tuple(space_axes(program, space))
+    if not axes:
+        raise SearchError("empty schedule space")
+    st = SpaceTemplate(program, space)
+    task = Task(st.template.desc(arch, launch), device)
+    try:
+        task.set_space(st.space_desc())
+        if task.has_unroll:  # block cycles for every body-replication product the space can produce
+            if st.size > 1 << 22:
+                raise SearchError("device ES: unroll axes over a space above 2^22 points are not supported")
+            idx = st.indices_from_points(np.arange(st.size, dtype=np.uint64))
+            task.prepare_unroll_for(to_device_records(st.records_from_indices(idx), device))
+        run = EsRun(task, params.alpha, params.sigma, params.population, params.iterations, params.seed,
+                    params.rank_normalize)
+        try:
+            run.run()
+            hist, trace, evaluations, err, best = run.result(st.dim)
+            if err:
+                raise SearchError(_error_text(err))
+            pts, scores = run.evaluated()
+        finally:
+            run.close()
+        single = all(len(ax.choices) == 1 for ax in axes)
+        key_of = lambda p: json.dumps(st.schedule_of(st.indices_from_points(np.array([p]))[0]).to_json())  # noqa: E731
+        # incumbent: min over distinct schedules by (score, JSON key) (ls/es.py:189, 197)
+        ties = [int(p) for p, s in zip(pts, scores) if s == best]
+        bk = min((key_of(p) for p in ties))
+        best_pt = next(p for p in ties if key_of(p) == bk)
+        import torch
+        dp = torch.tensor([int(best_pt)], dtype=torch.int64, device=f"cuda:{device}")
+        _, bf, _ = task.score_points(dp, features=True)
+        bf = bf.cpu().numpy()[0]
+        names = CPU_FEATURES if arch.family == "cpu" else GPU_FEATURES
+        evaluated = {key_of(p): float(s) for p, s in zip(pts, scores)} if materialize else {}
+        return OptimizeResult(
+            best_schedule=Schedule.from_json(json.loads(bk)),
+            best_score=float(best),
+            best_features=FeatureVector(tuple(zip(names, map(float, bf)))),
+            trace=[float(x) for x in trace] if not single else [float(best)],
+            evaluated=evaluated,
+            evaluations=evaluations,
+            diagnostics=[],
+        )
+    finally:
+        task.close()

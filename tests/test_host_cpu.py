@@ -164,3 +164,31 @@ def test_space_points_roundtrip():
     for a in range(d.n_axes):
         vals = [d.axes[a].values[c] for c in range(d.axes[a].n_choices)]
         assert vals == [int(v) for v in st.tables[a][2]]
+
+
+def test_philox_known_answers_and_normals():
+    """The device ES noise generator (es.cuh) restated in numpy, pinned by Random123's KAT vectors."""
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1] / "oracle"))
+    import es_oracle as E
+    for c, k, out in E.PHILOX_KAT:
+        assert [int(x) for x in E.philox4x32_10(*c, *k)] == list(out)
+    z = E.normals(7, 3, 200000, 5)
+    assert abs(z.mean()) < 0.01 and abs(z.std() - 1) < 0.01
+    assert np.array_equal(E.normals(7, 3, 10, 5), E.normals(7, 3, 200000, 5)[:10])
+
+
+def test_es_oracle_update_matches_host_es():
+    """es_oracle's update == the package's host ES formula (ls/es.py:74-93) on random data."""
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1] / "oracle"))
+    import es_oracle as E
+    from paper_2104_14641_b200.es import EsParams, es_update
+    rng = np.random.default_rng(1)
+    for rank in (True, False):
+        th, vals, eps = rng.normal(size=4), rng.normal(size=32), rng.normal(size=(32, 4))
+        vals[3] = vals[5]
+        p = EsParams(alpha=0.1, sigma=0.7, population=32, rank_normalize=rank)
+        assert np.array_equal(E.es_update(th, 0.1, 0.7, 32, vals, eps, rank), es_update(th, p, vals, eps))
