@@ -48,7 +48,13 @@ def parse():
     ap.add_argument("--k", type=int, default=64)
     ap.add_argument("--arch", default="x86-avx2")
     ap.add_argument("--no-baseline", action="store_true", help="skip the CPU baseline leg")
-    ap.add_argument("--path", type=int, default=0, help="0 auto, 1 generic kernel, 2 tabulated kernel")
+    ap.add_argument("--path", type=int, default=0, help="0 auto, 1 generic, 2 tabulated, 3 space-specialised")
+    ap.add_argument("--workload", default="conv", choices=["conv", "bert", "resnet50-es", "sweep"],
+                    help="conv: BASELINE configs[1] (the headline); bert: configs[3]; resnet50-es: configs[2]; "
+                         "sweep: configs[4]")
+    ap.add_argument("--population", type=int, default=1 << 20, help="resnet50-es: ES population per generation")
+    ap.add_argument("--generations", type=int, default=20, help="resnet50-es: generations per task")
+    ap.add_argument("--sigma", type=float, default=2.0, help="resnet50-es: ES sigma")
     return ap.parse_args()
 
 
@@ -188,7 +194,11 @@ def _timed(step, steps, flush, stream, torch, kern=None):
         step(kev[j])
         ev[j][1].record(stream)
     torch.cuda.synchronize()
-    return [a.elapsed_time(b) for a, b in ev], [a.elapsed_time(b) for a, b in kev]
+    try:
+        kms = [a.elapsed_time(b) for a, b in kev]
+    except ValueError:  # the step does not bracket a single kernel
+        kms = None
+    return [a.elapsed_time(b) for a, b in ev], kms
 
 
 def b200_arm(args):
@@ -376,10 +386,214 @@ def b200_arm(args):
     task.close()
 
 
+# -- extra workloads (BASELINE configs 3-5; the headline is `conv`) ----------------------------------
+
+
+def _dist_setup(torch, dist):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    else:
+        torch.cuda.set_device(0)
+    if rank == 0:
+        from paper_2104_14641_b200.build import build
+        build()
+    if world > 1:
+        dist.barrier()
+    return world, rank, torch.cuda.current_device()
+
+
+def _max_ms(torch, dist, world, dev, ms):
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.item()
+
+
+def _emit(line, world, dist):
+    if int(os.environ.get("RANK", "0")) == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def bert_arm(args):
+    """configs[3]: BERT-base dense + batch_matmul tasks, 2^22 distinct candidates per generation
+    (spread over the 5 tasks, each sharded across ranks), fused score + top-k per task."""
+    import torch
+    import torch.distributed as dist
+    from paper_2104_14641_b200 import workloads as W
+    from paper_2104_14641_b200.arch import KernelLaunch, load_arch
+    from paper_2104_14641_b200.dist import gather_topk
+    from paper_2104_14641_b200.engine import Task
+    from paper_2104_14641_b200.pack import SpaceTemplate
+    world, rank, dev = _dist_setup(torch, dist)
+    tasks = W.bert_tasks()
+    total = 1 << 22
+    jobs = []
+    for j, (name, spec, space) in enumerate(tasks):
+        st = SpaceTemplate(W.program(spec), space)
+        n_task = min(total // len(tasks), int(st.size)) // world
+        task = Task(st.template.desc(load_arch(args.arch), KernelLaunch.from_json(W.KERNEL_LAUNCH)), dev)
+        task.set_space(st.space_desc())
+        pts = st.points_from_indices(W.distinct_indices(st.sizes, n_task, 40 + j, start=rank * n_task))
+        jobs.append((name, task, torch.from_numpy(pts.view(np.int32)).to(dev), n_task, task.points_path))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        for name, task, d, n_task, _ in jobs:
+            s, i, nv = task.score_topk_points(d, args.k, base_index=rank * n_task)
+            if world > 1:
+                gather_topk(s, i, args.k)
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    with ClockSampler(dev) as clk:
+        ms, _ = _timed(lambda kev=None: step(), args.steps, flush, stream, torch)
+    per_step = sum(n for _, _, _, n, _ in jobs) * world
+    tot = _max_ms(torch, dist, world, dev, sum(ms)) / 1e3
+    line = {"metric": METRIC, "value": per_step * args.steps / tot, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot * 1e3 / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64+f64",
+            "data": "synthetic",
+            "config": {"workload": "BERT-base (seq 128, batch 8) dense 1024x768x768 / 1024x3072x768 / "
+                                   "1024x768x3072 + batch_matmul 96x128x128x64 / 96x128x64x128 schedule spaces "
+                                   "(divisor tiles x chain orders), 2^22 distinct candidates per generation, "
+                                   f"score + top-{args.k} per task", "config": "BASELINE.json configs[3]",
+                       "arch": args.arch, "candidates_per_step": per_step, "k": args.k,
+                       "tasks": {name: {"candidates_per_gpu": n, "points_path": pp} for name, _, _, n, pp in jobs},
+                       "l2": "flushed between timed steps (256 MiB write)"},
+            "clocks": clk.summary(), "gpu_launches": args.steps * len(jobs) * (1 + (2 if world > 1 else 0))}
+    for _, task, _, _, _ in jobs:
+        task.close()
+    _emit(line, world, dist)
+
+
+def resnet_es_arm(args):
+    """configs[2]: the ResNet-50 task set, a `generations`-generation ES per task with every
+    generation on the device (Philox noise, decode, memo, scoring, rank sort, update); tasks
+    round-robin over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_2104_14641_b200 import workloads as W
+    from paper_2104_14641_b200.arch import KernelLaunch, load_arch
+    from paper_2104_14641_b200.engine import EsRun, Task
+    from paper_2104_14641_b200.pack import SpaceTemplate
+    world, rank, dev = _dist_setup(torch, dist)
+    tasks = W.resnet50_tasks()
+    mine = [t for j, t in enumerate(tasks) if j % world == rank]
+    runs = []
+    for name, spec, space in mine:
+        st = SpaceTemplate(W.program(spec), space)
+        task = Task(st.template.desc(load_arch(args.arch), KernelLaunch.from_json(W.KERNEL_LAUNCH)), dev)
+        task.set_space(st.space_desc())
+        run = EsRun(task, 0.05, args.sigma, args.population, args.generations, 2104)
+        runs.append((name, st, task, run))
+    stream = torch.cuda.current_stream()
+
+    def step():
+        for _, _, _, run in runs:
+            run.run()
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    with ClockSampler(dev) as clk:
+        ms, _ = _timed(lambda kev=None: step(), args.steps, flush, stream, torch)
+    distinct = 0
+    paths = {}
+    for name, st, task, run in runs:
+        _, trace, ev, err, best = run.result(st.dim)
+        assert err == 0, (name, err)
+        distinct += ev
+        paths[name] = task.points_path
+    dt = torch.tensor([distinct], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(dt)
+    tot = _max_ms(torch, dist, world, dev, sum(ms)) / 1e3
+    members = len(tasks) * args.generations * args.population
+    line = {"metric": "ES population members scored+ranked/sec (configs[2]: ResNet-50 task set, on-device ES)",
+            "value": members * args.steps / tot, "unit": "members/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": tot * 1e3 / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int64+f64", "data": "synthetic",
+            "distinct_schedules_per_s": float(dt.item()) * args.steps / tot,
+            "config": {"workload": f"ResNet-50 v1.5 conv/dense task set ({len(tasks)} tasks), "
+                                   f"{args.generations}-generation ES per task, population {args.population}, "
+                                   f"sigma {args.sigma}, every generation on device (Philox noise, decode, memo, "
+                                   "score, CUB rank sort, update; one CUDA graph per generation)",
+                       "config": "BASELINE.json configs[2]", "arch": args.arch,
+                       "distinct_schedules_per_step": float(dt.item()), "points_paths": paths,
+                       "l2": "flushed between timed steps (256 MiB write)"},
+            "clocks": clk.summary(), "gpu_launches": args.steps * len(mine) * (1 + 4 * args.generations)}
+    for _, _, task, run in runs:
+        run.close()
+        task.close()
+    _emit(line, world, dist)
+
+
+def sweep_arm(args):
+    """configs[4]: n = 2^20 .. 2^26 distinct conv candidates per step, sharded over the ranks
+    (strong scaling per n), fused score + top-k + all-gather merge; one line with every n."""
+    import torch
+    import torch.distributed as dist
+    from paper_2104_14641_b200 import workloads as W
+    from paper_2104_14641_b200.arch import KernelLaunch, load_arch
+    from paper_2104_14641_b200.dist import gather_topk
+    from paper_2104_14641_b200.engine import Task
+    from paper_2104_14641_b200.pack import SpaceTemplate
+    world, rank, dev = _dist_setup(torch, dist)
+    st = SpaceTemplate(W.program(W.conv2d_json()), W.conv_space(21504, 1))  # 3136 x 21504 > 2^26 points
+    task = Task(st.template.desc(load_arch(args.arch), KernelLaunch.from_json(W.KERNEL_LAUNCH)), dev)
+    task.set_space(st.space_desc())
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    rows = []
+    for e in range(20, 27):
+        n = (1 << e) // world
+        pts = st.points_from_indices(W.distinct_indices(st.sizes, n, 2104, start=rank * n))
+        d = torch.from_numpy(pts.view(np.int32)).to(dev)
+        del pts
+
+        def step(kev=None):
+            s, i, nv = task.score_topk_points(d, args.k, base_index=rank * n)
+            if world > 1:
+                gather_topk(s, i, args.k)
+        for _ in range(3):
+            step()
+        torch.cuda.synchronize()
+        steps = max(3, args.steps // 4)
+        ms, _ = _timed(step, steps, flush, stream, torch)
+        tot = _max_ms(torch, dist, world, dev, sum(ms)) / 1e3
+        rows.append({"n": 1 << e, "value": (1 << e) * steps / tot, "ms_per_step": tot * 1e3 / steps})
+        del d
+    peak = max(r["value"] for r in rows)
+    line = {"metric": METRIC, "value": rows[-1]["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": rows[-1]["ms_per_step"], "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int64+f64", "data": "synthetic",
+            "config": {"workload": "resnet50 conv2d 56x56x64->64 3x3 space with 21504 chain orders (67.4M points); "
+                                   "n = 2^20..2^26 distinct candidates per step sharded over the GPUs, "
+                                   f"score + top-{args.k}", "config": "BASELINE.json configs[4]", "arch": args.arch,
+                       "l2": "flushed between timed steps (256 MiB write)"},
+            "sweep": rows, "peak_value": peak, "gpu_launches": None}
+    task.close()
+    _emit(line, world, dist)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         reference_arm(args)
+    elif args.workload == "bert":
+        bert_arm(args)
+    elif args.workload == "resnet50-es":
+        resnet_es_arm(args)
+    elif args.workload == "sweep":
+        sweep_arm(args)
     else:
         b200_arm(args)
 

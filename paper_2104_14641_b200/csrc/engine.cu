@@ -1597,6 +1597,7 @@ struct __align__(16) TopkState {
   int cnt, cap, cur, cnt2;
   unsigned int hist[256];
   int sel_bucket, sel_rank, sel_count, pad;
+  unsigned long long and_s, or_s, and_i, or_i;  // common-prefix reduction of the buffered keys
   __device__ __forceinline__ Key* buf() { return reinterpret_cast<Key*>(this + 1) + (cur ? cap : 0); }
   __device__ __forceinline__ const Key* buf() const {
     return reinterpret_cast<const Key*>(this + 1) + (cur ? cap : 0);
@@ -1610,23 +1611,24 @@ __host__ __device__ constexpr size_t topk_state_bytes(int cap) {
 // Sort buf[0..cnt) (padded with +inf) and keep the k smallest; returns the kept
 // count.  Used once per launch, on the final <= k keys.
 __device__ int topk_compact(TopkState& S, int k, int cnt) {
-  for (int i = cnt + threadIdx.x; i < S.cap; i += blockDim.x) {
-    S.buf()[i].s = KEY_INF_S;
-    S.buf()[i].i = KEY_INF_I;
-  }
-  __syncthreads();
+  Key* const B = S.buf();
   int size0 = 2;
   while (size0 < cnt) size0 <<= 1;  // only the occupied power-of-two prefix needs sorting
+  for (int i = cnt + threadIdx.x; i < size0; i += blockDim.x) {
+    B[i].s = KEY_INF_S;
+    B[i].i = KEY_INF_I;
+  }
+  __syncthreads();
   for (int size = 2; size <= size0; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
       for (int t = threadIdx.x; t < size0 / 2; t += blockDim.x) {
         const int lo = 2 * t - (t & (stride - 1));
         const int hi = lo + stride;
         const bool up = (lo & size) == 0;
-        const Key a = S.buf()[lo], b = S.buf()[hi];
+        const Key a = B[lo], b = B[hi];
         if (kless(b, a) == up) {
-          S.buf()[lo] = b;
-          S.buf()[hi] = a;
+          B[lo] = b;
+          B[hi] = a;
         }
       }
       __syncthreads();
@@ -1635,7 +1637,7 @@ __device__ int topk_compact(TopkState& S, int k, int cnt) {
   const int keep = cnt < k ? cnt : k;
   if (threadIdx.x == 0) {
     S.cnt = keep;
-    if (keep == k) S.thr = S.buf()[k - 1];
+    if (keep == k) S.thr = B[k - 1];
   }
   __syncthreads();
   return keep;
@@ -1652,17 +1654,76 @@ __device__ __forceinline__ unsigned key_digit(const Key& x, int d) {
 // digits of (score bits, index) until its bucket holds one key, then one
 // filtering pass into the other buffer.  Keys are distinct (unique indices),
 // so the k-th key and the kept set are unique.  Returns the kept count.
+__device__ __forceinline__ unsigned long long warp_and64(unsigned long long x) {
+  return ((unsigned long long)__reduce_and_sync(0xffffffffu, (unsigned)(x >> 32)) << 32) |
+         __reduce_and_sync(0xffffffffu, (unsigned)x);
+}
+__device__ __forceinline__ unsigned long long warp_or64(unsigned long long x) {
+  return ((unsigned long long)__reduce_or_sync(0xffffffffu, (unsigned)(x >> 32)) << 32) |
+         __reduce_or_sync(0xffffffffu, (unsigned)x);
+}
+
 __device__ int topk_select(TopkState& S, int k) {
   const int c = S.cnt;
   if (c <= k) return c;
+  const Key* const B = S.buf();
+  const int lane = threadIdx.x & 31;
+  const int c_up = (c + blockDim.x - 1) / blockDim.x * blockDim.x;  // warp-uniform trip count
+  // digits every buffered key shares are skipped: AND / OR of the keys
+  if (threadIdx.x == 0) {
+    S.and_s = S.and_i = ~0ull;
+    S.or_s = S.or_i = 0ull;
+  }
+  __syncthreads();
+  {
+    unsigned long long as = ~0ull, os = 0, ai = ~0ull, oi = 0;
+    for (int j = threadIdx.x; j < c; j += blockDim.x) {
+      const Key x = B[j];
+      as &= x.s;
+      os |= x.s;
+      ai &= (unsigned long long)x.i;
+      oi |= (unsigned long long)x.i;
+    }
+    as = warp_and64(as);
+    os = warp_or64(os);
+    ai = warp_and64(ai);
+    oi = warp_or64(oi);
+    if (lane == 0) {
+      atomicAnd(&S.and_s, as);
+      atomicOr(&S.or_s, os);
+      atomicAnd(&S.and_i, ai);
+      atomicOr(&S.or_i, oi);
+    }
+  }
+  __syncthreads();
   unsigned long long ps = 0, pi = 0, ms = 0, mi = 0;  // known digits of the k-th key (block-uniform)
-  int rank = k;                                       // its rank among keys matching the known digits
-  for (int d = 0; d < 16; ++d) {
+  int d0;
+  {
+    const unsigned long long xs = S.and_s ^ S.or_s, xi = S.and_i ^ S.or_i;
+    if (xs) {
+      d0 = __clzll((long long)xs) / 8;
+      ms = d0 ? ~0ull << (64 - 8 * d0) : 0ull;
+      ps = S.and_s & ms;
+    } else {
+      ms = ~0ull;
+      ps = S.and_s;
+      d0 = xi ? 8 + __clzll((long long)xi) / 8 : 16;
+      mi = d0 > 8 && d0 < 16 ? ~0ull << (64 - 8 * (d0 - 8)) : (d0 == 16 ? ~0ull : 0ull);
+      pi = S.and_i & mi;
+    }
+  }
+  int rank = k;  // rank of the k-th key among keys matching the known digits
+  for (int d = d0; d < 16; ++d) {
     for (int b = threadIdx.x; b < 256; b += blockDim.x) S.hist[b] = 0;
     __syncthreads();
-    for (int j = threadIdx.x; j < c; j += blockDim.x) {
-      const Key x = S.buf()[j];
-      if ((x.s & ms) == ps && ((unsigned long long)x.i & mi) == pi) atomicAdd(&S.hist[key_digit(x, d)], 1u);
+    for (int j = threadIdx.x; j < c_up; j += blockDim.x) {  // warp-aggregated histogram
+      unsigned dig = 0x100u;
+      if (j < c) {
+        const Key x = B[j];
+        if ((x.s & ms) == ps && ((unsigned long long)x.i & mi) == pi) dig = key_digit(x, d);
+      }
+      const unsigned peers = __match_any_sync(0xffffffffu, dig);
+      if (dig < 0x100u && (__ffs(peers) - 1) == lane) atomicAdd(&S.hist[dig], (unsigned)__popc(peers));
     }
     __syncthreads();
     if (threadIdx.x < 32) {
@@ -1708,7 +1769,7 @@ __device__ int topk_select(TopkState& S, int k) {
   }
   // the k-th key is the only one matching the selected digits
   for (int j = threadIdx.x; j < c; j += blockDim.x) {
-    const Key x = S.buf()[j];
+    const Key x = B[j];
     if ((x.s & ms) == ps && ((unsigned long long)x.i & mi) == pi) S.thr = x;
   }
   if (threadIdx.x == 0) S.cnt2 = 0;
@@ -1716,7 +1777,7 @@ __device__ int topk_select(TopkState& S, int k) {
   const Key thr = S.thr;
   Key* dst = S.other();
   for (int j = threadIdx.x; j < c; j += blockDim.x) {
-    const Key x = S.buf()[j];
+    const Key x = B[j];
     if (!kless(thr, x)) dst[atomicAdd(&S.cnt2, 1)] = x;
   }
   __syncthreads();
@@ -1759,6 +1820,17 @@ __device__ __forceinline__ void topk_offer(TopkState& S, bool has, const Key& ke
 
 constexpr int TK_GROUP = 16;  // blocks per first-level merge group
 
+// Phase timestamps of the fused kernel (LS_TRACE=1, tools/ only): per block
+// [start, staged, main loop done, block list written, group merged, final written].
+__device__ unsigned long long* g_trace = nullptr;
+__device__ __forceinline__ void trace_mark(int slot) {
+  if (g_trace && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_trace[blockIdx.x * 8 + slot] = t;
+  }
+}
+
 __device__ __forceinline__ Key ld_key_cg(const Key* p) {
   Key k;
   k.s = __ldcg(reinterpret_cast<const unsigned long long*>(p));
@@ -1768,21 +1840,33 @@ __device__ __forceinline__ Key ld_key_cg(const Key* p) {
 
 // Merge m keys from global memory into the block's buffer (streamed, k kept).
 // (sorted: the kept keys end ascending; otherwise they stay an unsorted set)
+// Keys are loaded in chunks of cap - k (four per thread in flight), appended
+// below the running threshold, and a selection follows each chunk.
 __device__ int merge_into(TopkState& S, const Key* src, int64_t m, int k, bool sorted) {
   topk_init(S, S.cap);
-  int safe = 1;
-  for (int64_t base = 0; base < m; base += blockDim.x) {
-    const int64_t i = base + threadIdx.x;
-    bool has = false;
-    Key key;
-    if (i < m) {
-      key = ld_key_cg(src + i);
-      has = !(key.s == KEY_INF_S && key.i == KEY_INF_I);
+  const int chunk = S.cap - k;
+  for (int64_t base = 0; base < m; base += chunk) {
+    const int64_t lim = min(m, base + chunk);
+    for (int64_t j0 = base; j0 < lim; j0 += 4 * (int64_t)blockDim.x) {
+      Key key[4];
+      bool has[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t i = j0 + q * (int64_t)blockDim.x + threadIdx.x;
+        has[q] = i < lim;
+        if (has[q]) key[q] = ld_key_cg(src + i);
+      }
+      const Key thr = S.thr;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (has[q] && !(key[q].s == KEY_INF_S && key[q].i == KEY_INF_I) && kless(key[q], thr))
+          S.buf()[atomicAdd(&S.cnt, 1)] = key[q];
     }
-    topk_offer(S, has, key, k, safe);
+    __syncthreads();
+    topk_select(S, k);
   }
   __syncthreads();
-  const int kept = topk_select(S, k);
+  const int kept = min(S.cnt, k);
   return sorted ? topk_compact(S, k, kept) : kept;
 }
 
@@ -1799,6 +1883,159 @@ __device__ void write_keys(const TopkState& S, int kept, int k, Key* out) {
   }
 }
 
+// Write the kept keys ascending as (score, index), +inf / -1 padded to k.
+// kept <= blockDim: every thread ranks one key by counting the smaller ones
+// (keys are distinct); otherwise a bitonic sort.
+__device__ void write_sorted(TopkState& S, int kept, int k, double* __restrict__ out_s, int64_t* __restrict__ out_i) {
+  if (kept <= (int)blockDim.x) {
+    __syncthreads();
+    if ((int)threadIdx.x < kept) {
+      const Key x = S.buf()[threadIdx.x];
+      int r = 0;
+      for (int j = 0; j < kept; ++j) r += kless(S.buf()[j], x) ? 1 : 0;
+      out_s[r] = from_order_bits(x.s);
+      out_i[r] = x.i;
+    }
+  } else {
+    kept = topk_compact(S, k, kept);
+    for (int j = threadIdx.x; j < kept; j += blockDim.x) {
+      out_s[j] = from_order_bits(S.buf()[j].s);
+      out_i[j] = S.buf()[j].i;
+    }
+  }
+  for (int j = kept + threadIdx.x; j < k; j += blockDim.x) {
+    out_s[j] = __longlong_as_double(0x7ff0000000000000ll);
+    out_i[j] = -1;
+  }
+}
+
+// Smallest of the block's kept keys (+inf when none) to *out.
+__device__ void write_block_min(const TopkState& S, int kept, Key* out) {
+  __shared__ Key wmin[TPB / 32];
+  Key m;
+  m.s = KEY_INF_S;
+  m.i = KEY_INF_I;
+  for (int j = threadIdx.x; j < kept; j += blockDim.x) {
+    const Key x = S.buf()[j];
+    if (kless(x, m)) m = x;
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    Key o;
+    o.s = __shfl_down_sync(0xffffffffu, m.s, off);
+    o.i = __shfl_down_sync(0xffffffffu, m.i, off);
+    if (kless(o, m)) m = o;
+  }
+  if ((threadIdx.x & 31) == 0) wmin[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+      if (kless(wmin[w], m)) m = wmin[w];
+    *out = m;
+  }
+}
+
+// Sort B[0..cnt) ascending in shared memory (bitonic over the next power of two,
+// +inf padded; B must hold it).
+__device__ void bitonic_sort(Key* B, int cnt) {
+  int size0 = 2;
+  while (size0 < cnt) size0 <<= 1;
+  for (int i = cnt + threadIdx.x; i < size0; i += blockDim.x) {
+    B[i].s = KEY_INF_S;
+    B[i].i = KEY_INF_I;
+  }
+  __syncthreads();
+  for (int size = 2; size <= size0; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = threadIdx.x; t < size0 / 2; t += blockDim.x) {
+        const int lo = 2 * t - (t & (stride - 1));
+        const int hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const Key a = B[lo], b = B[hi];
+        if (kless(b, a) == up) {
+          B[lo] = b;
+          B[hi] = a;
+        }
+      }
+      __syncthreads();
+    }
+}
+
+// Second stage of the fused top-k when k is small next to the grid (the
+// fused kernel wrote every block's k best and its minimum).  T = the k-th
+// smallest block minimum bounds the global k-th key from above (the k minima
+// are k real keys <= T), so only list keys <= T can be in the answer: every
+// block finds T, filters its share of the lists into `surv`, and the last
+// block ranks the survivors (~k of them) into the sorted output.
+__global__ void __launch_bounds__(TPB) merge_filter_kernel(const Key* __restrict__ block_out,
+                                                           const Key* __restrict__ mins, int nblk, int k,
+                                                           Key* __restrict__ surv, unsigned int* __restrict__ ctr,
+                                                           double* __restrict__ out_s, int64_t* __restrict__ out_i,
+                                                           int cap) {
+  extern __shared__ __align__(16) unsigned char raw[];
+  __shared__ unsigned int s_ticket;
+  __shared__ Key s_T;
+  TopkState& S = *reinterpret_cast<TopkState*>(raw);
+  trace_mark(4);
+  // T: the k-th smallest block minimum (bitonic sort of the minima in shared memory)
+  Key* B = S.buf();
+  __shared__ int s_n;
+  if (threadIdx.x == 0) {
+    s_n = 0;
+    s_T.s = KEY_INF_S;
+    s_T.i = KEY_INF_I;
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < nblk; j += blockDim.x) {
+    const Key x = ld_key_cg(mins + j);
+    if (!(x.s == KEY_INF_S && x.i == KEY_INF_I)) B[atomicAdd(&s_n, 1)] = x;
+  }
+  __syncthreads();
+  const int nm = s_n;
+  if (nm >= k) {
+    bitonic_sort(B, nm);
+    if (threadIdx.x == 0) s_T = B[k - 1];
+  }
+  __syncthreads();
+  const Key T = s_T;  // +inf (no filtering) when there are fewer than k minima
+  trace_mark(5);
+  const int64_t m = (int64_t)nblk * k;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    const Key x = ld_key_cg(block_out + i);
+    if (!(x.s == KEY_INF_S && x.i == KEY_INF_I) && !kless(T, x)) surv[atomicAdd(&ctr[0], 1u)] = x;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_ticket = atomicAdd(&ctr[1], 1u);
+  __syncthreads();
+  trace_mark(6);
+  if (s_ticket != gridDim.x - 1) return;
+  __threadfence();
+  const int c = (int)__ldcg(&ctr[0]);
+  if (g_trace && threadIdx.x == 0) g_trace[blockIdx.x * 8 + 3] = 1000000000000ull + (unsigned long long)c;
+  Key* buf = S.buf();
+  if (c <= (int)blockDim.x) {  // rank the survivors directly; the k smallest land at their rank
+    __syncthreads();
+    if ((int)threadIdx.x < c) buf[threadIdx.x] = ld_key_cg(surv + threadIdx.x);
+    __syncthreads();
+    if ((int)threadIdx.x < c) {
+      const Key x = buf[threadIdx.x];
+      int r = 0;
+      for (int q = 0; q < c; ++q) r += kless(buf[q], x) ? 1 : 0;
+      if (r < k) {
+        out_s[r] = from_order_bits(x.s);
+        out_i[r] = x.i;
+      }
+    }
+    for (int j = c + threadIdx.x; j < k; j += blockDim.x) {
+      out_s[j] = __longlong_as_double(0x7ff0000000000000ll);
+      out_i[j] = -1;
+    }
+  } else {
+    write_sorted(S, merge_into(S, surv, c, k, false), k, out_s, out_i);
+  }
+  trace_mark(7);
+}
+
 // Fused pass: score every record, keep the block's k best, then merge the
 // block lists in a two-level tree inside the same launch: the last block of
 // each group of TK_GROUP merges its group, the last group merger writes the
@@ -1807,10 +2044,12 @@ template <int TM, int RM, int MODE, int SRC>
 __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kernel(
     const DTask* __restrict__ gtask, const void* __restrict__ src, int pbytes, int64_t n, int64_t base_index, int k,
     Key* __restrict__ block_out, Key* __restrict__ group_out, unsigned int* __restrict__ tickets,
-    double* __restrict__ out_s, int64_t* __restrict__ out_i, unsigned long long* __restrict__ n_valid, int cap) {
+    double* __restrict__ out_s, int64_t* __restrict__ out_i, unsigned long long* __restrict__ n_valid, int cap,
+    Key* __restrict__ mins) {
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ unsigned int s_ticket;
   DTask& T = *reinterpret_cast<DTask*>(dyn);
+  trace_mark(0);
   stage_task(T, gtask);
   unsigned char* p = dyn + T.task_bytes;
   const int32_t* tab = stage_tab<MODE>(p, T);
@@ -1818,17 +2057,22 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kern
   TopkState& S = *reinterpret_cast<TopkState*>(p);
   Evaluator<TM, RM, MODE> ev(T, p + align16(topk_state_bytes(cap)), tab);
   topk_init(S, cap);
+  trace_mark(1);
   unsigned int valid = 0;
   int safe = 1;
-  const int64_t stride = (int64_t)gridDim.x * TPB;
+  // every block takes a contiguous range of ceil(n / grid) candidates, so all
+  // blocks run the same number of rounds and the work per SM is balanced
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t b0 = min(n, (int64_t)blockIdx.x * per), b1 = min(n, b0 + per);
+  const int64_t stride = TPB;
   uint64_t xn = 0;  // space path: the next point, loaded one iteration ahead
   if constexpr (MODE == 4)
-    if ((int64_t)blockIdx.x * TPB + threadIdx.x < n) xn = load_point(src, pbytes, (int64_t)blockIdx.x * TPB + threadIdx.x);
-  for (int64_t base = (int64_t)blockIdx.x * TPB; base < n; base += stride) {
+    if (b0 + threadIdx.x < b1) xn = load_point(src, pbytes, b0 + threadIdx.x);
+  for (int64_t base = b0; base < b0 + per; base += stride) {
     const int64_t i = base + threadIdx.x;
     bool has = false;
     Key key;
-    if (i < n) {
+    if (i < b1) {
       ls_record r;
       uint32_t kt[4];
       double f[LS_NFEAT_GPU];
@@ -1836,7 +2080,7 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kern
       int st;
       if constexpr (MODE == 4) {
         const uint64_t x = xn;
-        if (i + stride < n) xn = load_point(src, pbytes, i + stride);
+        if (i + stride < b1) xn = load_point(src, pbytes, i + stride);
         st = eval_space<TM>(T, tab, x, ev.fc, f, &s);
       } else {
         uint32_t pch = 0;
@@ -1844,9 +2088,9 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kern
         if (st == LS_OK) st = ev(T, r, kt, pch, f, &s);
       }
       if (st == LS_OK) {
-        has = true;
         key.s = order_bits(s);
         key.i = base_index + i;
+        has = true;
         ++valid;
       }
     }
@@ -1855,7 +2099,15 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kern
   for (int off = 16; off > 0; off >>= 1) valid += __shfl_down_sync(0xffffffffu, valid, off);
   if ((threadIdx.x & 31) == 0 && valid) atomicAdd(n_valid, (unsigned long long)valid);
   __syncthreads();
-  write_keys(S, topk_select(S, k), k, block_out + (int64_t)blockIdx.x * k);
+  trace_mark(2);
+  const int kept0 = topk_select(S, k);
+  write_keys(S, kept0, k, block_out + (int64_t)blockIdx.x * k);
+  if (mins) {  // second stage: merge_filter_kernel
+    write_block_min(S, kept0, mins + blockIdx.x);
+    trace_mark(3);
+    return;
+  }
+  trace_mark(3);
 
   // ---- level 1: last block of the group merges the group's lists
   const int g = blockIdx.x / TK_GROUP;
@@ -1869,6 +2121,7 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kern
   __threadfence();
   int kept = merge_into(S, block_out + (int64_t)g * TK_GROUP * k, (int64_t)gsize * k, k, false);
   write_keys(S, kept, k, group_out + (int64_t)g * k);
+  trace_mark(4);
   // ---- level 2: last group merger writes the final list
   __threadfence();
   __syncthreads();
@@ -1876,16 +2129,9 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kern
   __syncthreads();
   if (s_ticket != (unsigned)(ngroups - 1)) return;
   __threadfence();
-  kept = merge_into(S, group_out, (int64_t)ngroups * k, k, true);
-  for (int j = threadIdx.x; j < k; j += blockDim.x) {
-    if (j < kept) {
-      out_s[j] = from_order_bits(S.buf()[j].s);
-      out_i[j] = S.buf()[j].i;
-    } else {
-      out_s[j] = __longlong_as_double(0x7ff0000000000000ll);
-      out_i[j] = -1;
-    }
-  }
+  kept = merge_into(S, group_out, (int64_t)ngroups * k, k, false);
+  write_sorted(S, kept, k, out_s, out_i);
+  trace_mark(5);
 }
 
 // Merge m keys (any order, +inf padded) into the k best, written as (score, index).
@@ -1907,16 +2153,7 @@ __global__ void __launch_bounds__(TPB) merge_keys_kernel(const Key* __restrict__
     topk_offer(S, has, key, k, safe);
   }
   __syncthreads();
-  const int kept = topk_compact(S, k, topk_select(S, k));
-  for (int j = threadIdx.x; j < k; j += blockDim.x) {
-    if (j < kept) {
-      out_s[j] = from_order_bits(S.buf()[j].s);
-      out_i[j] = S.buf()[j].i;
-    } else {
-      out_s[j] = __longlong_as_double(0x7ff0000000000000ll);
-      out_i[j] = -1;
-    }
-  }
+  write_sorted(S, topk_select(S, k), k, out_s, out_i);
 }
 
 __global__ void lists_to_keys_kernel(const double* __restrict__ s, const int64_t* __restrict__ idx, int64_t m,
@@ -2653,12 +2890,12 @@ size_t smem_score(const DTask& T, int mode) {
   return (size_t)T.task_bytes + tab_smem_bytes(mode, T) + state_bytes(mode, T.n_slots, T.n_chain, T.n_stage);
 }
 // the fused kernel's buffer must hold k plus one round of inserts
-int topk_buf(int k) { return k <= 512 - TPB ? 512 : k <= 1024 - TPB ? 1024 : 2048; }
+int topk_buf(int k) { return k <= 1024 - TPB ? 1024 : 2048; }
 size_t smem_topk(const DTask& T, int k, int mode) { return smem_score(T, mode) + align16(topk_state_bytes(topk_buf(k))); }
 
 using ScoreFn = void (*)(const DTask*, const void*, int, int64_t, double*, double*, int32_t*);
 using TopkFn = void (*)(const DTask*, const void*, int, int64_t, int64_t, int, Key*, Key*, unsigned int*, double*,
-                       int64_t*, unsigned long long*, int);
+                       int64_t*, unsigned long long*, int, Key*);
 
 template <int SRC>
 ScoreFn score_fn_src(const DTask& T, int mode) {
@@ -2875,18 +3112,68 @@ static int topk_device(ls_task* t, const void* d_src, int pbytes, int64_t n, int
   const size_t sm = smem_topk(t->host, k, mode);
   const int grid = n > 0 ? grid_for(t, n, blocks_per_sm(fn, sm)) : 1;
   const int ngroups = (grid + TK_GROUP - 1) / TK_GROUP;
-  const size_t ws_keys = sizeof(Key) * ((size_t)grid + ngroups) * k;
-  const size_t ws_bytes = ws_keys + align16(sizeof(unsigned int) * (ngroups + 1));
+  // two-stage merge (block-minima bound, merge_filter_kernel) when the grid has plenty of
+  // blocks per answer key; else the in-kernel merge tree
+  const bool two = 4 * k <= grid && grid <= topk_buf(k);
+  const size_t ws_keys = sizeof(Key) * (two ? (size_t)grid * (2 * k + 1) : ((size_t)grid + ngroups) * k);
+  const int nctr = two ? 2 : ngroups + 1;
+  const size_t ws_bytes = ws_keys + align16(sizeof(unsigned int) * nctr);
   unsigned char* ws = nullptr;
   CUDA_TRY(cudaMallocAsync(&ws, ws_bytes, s));
   Key* block_out = reinterpret_cast<Key*>(ws);
-  Key* group_out = block_out + (size_t)grid * k;
+  Key* group_out = block_out + (size_t)grid * k;   // tree: group lists; two-stage: survivors
+  Key* mins = two ? group_out + (size_t)grid * k : nullptr;
   unsigned int* tickets = reinterpret_cast<unsigned int*>(ws + ws_keys);
-  CUDA_TRY(cudaMemsetAsync(tickets, 0, sizeof(unsigned int) * (ngroups + 1), s));
+  CUDA_TRY(cudaMemsetAsync(tickets, 0, sizeof(unsigned int) * nctr, s));
+  unsigned long long* tr = nullptr;
+  const char* tr_env = getenv("LS_TRACE");
+  if (tr_env && tr_env[0] == '1') {  // phase timestamps to stderr (profiling aid)
+    CUDA_TRY(cudaMalloc(&tr, sizeof(unsigned long long) * 8 * grid));
+    CUDA_TRY(cudaMemset(tr, 0, sizeof(unsigned long long) * 8 * grid));
+    CUDA_TRY(cudaMemcpyToSymbol(g_trace, &tr, sizeof(tr)));
+  }
   fn<<<grid, TPB, sm, s>>>(t->d_task, d_src, pbytes, n, base_index, k, block_out, group_out, tickets, d_top_scores,
-                           d_top_index, d_valid, topk_buf(k));
+                           d_top_index, d_valid, topk_buf(k), mins);
   CUDA_TRY(cudaGetLastError());
+  if (two) {
+    const size_t msm = topk_state_bytes(topk_buf(k));
+    static thread_local bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(merge_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm);
+      attr = true;
+    }
+    const int g2 = (int)std::max<int64_t>(1, std::min<int64_t>(4 * t->num_sms, ((int64_t)grid * k + TPB - 1) / TPB));
+    merge_filter_kernel<<<g2, TPB, msm, s>>>(block_out, mins, grid, k, group_out, tickets, d_top_scores, d_top_index,
+                                             topk_buf(k));
+    CUDA_TRY(cudaGetLastError());
+  }
   CUDA_TRY(cudaFreeAsync(ws, s));
+  if (tr) {
+    std::vector<unsigned long long> h((size_t)8 * grid);
+    CUDA_TRY(cudaStreamSynchronize(s));
+    CUDA_TRY(cudaMemcpy(h.data(), tr, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost));
+    unsigned long long* nul = nullptr;
+    CUDA_TRY(cudaMemcpyToSymbol(g_trace, &nul, sizeof(nul)));
+    cudaFree(tr);
+    unsigned long long t0 = ~0ull, surv = 0;
+    for (int b = 0; b < grid; ++b) t0 = std::min(t0, h[b * 8]);
+    for (int b = 0; b < grid; ++b)
+      if (h[b * 8 + 3] >= 1000000000000ull) surv = h[b * 8 + 3] - 1000000000000ull, h[b * 8 + 3] = 0;
+    double avg[8] = {0}, mx[8] = {0};
+    for (int q = 0; q < 8; ++q) {
+      int cnt = 0;
+      for (int b = 0; b < grid; ++b)
+        if (h[b * 8 + q] > t0) {
+          const double v = (double)(h[b * 8 + q] - t0) / 1e3;
+          avg[q] += v, mx[q] = std::max(mx[q], v), ++cnt;
+        }
+      if (cnt) avg[q] /= cnt;
+    }
+    fprintf(stderr, "LS_TRACE n=%lld grid=%d us(avg/max): staged %.1f/%.1f main %.1f/%.1f listed %.1f/%.1f | "
+            "tree group %.1f final %.1f | two-stage start %.1f T %.1f filtered %.1f final %.1f survivors %llu\n",
+            (long long)n, grid, avg[1], mx[1], avg[2], mx[2], avg[3], mx[3], mx[4], mx[5], mx[4], mx[5], mx[6],
+            mx[7], surv);
+  }
   return LS_E_OK;
 }
 

@@ -146,3 +146,54 @@ def _feistel(total: int, x: np.ndarray, seed: int) -> np.ndarray:
 
 KERNEL_LAUNCH = {"grid_blocks": 160, "threads_per_block": 256, "registers_per_thread": 32,
                  "shared_mem_per_block": 4096}
+
+
+def bert_tasks(reorders: int = 720) -> list:
+    """Config 4: BERT-base (seq 128, batch 8 -> M = 1024 tokens) dense + batch_matmul tasks
+    (SURVEY.md §8d1 (4)): (name, program spec, space) with divisor tiles and chain orders."""
+    out = []
+    for (m, n, k) in ((1024, 768, 768), (1024, 3072, 768), (1024, 768, 3072)):
+        chain = tiled_chain(["i", "j", "k"], ["i", "j", "k"])
+        perms = [list(p) for p in itertools.permutations(chain)][:reorders]
+        out.append((f"dense_{m}_{n}_{k}", matmul_json(m, n, k),
+                    {"tile": {"i": divisors(m), "j": divisors(n), "k": divisors(k)}, "reorder": perms}))
+    for (b, m, n, k) in ((96, 128, 128, 64), (96, 128, 64, 128)):
+        chain = tiled_chain(["b", "i", "j", "k"], ["i", "j", "k"])
+        out.append((f"bmm_{b}_{m}_{n}_{k}", batch_matmul_json(b, m, n, k),
+                    {"tile": {"i": divisors(m), "j": divisors(n), "k": divisors(k)},
+                     "reorder": random_perms(chain, reorders, 10)}))
+    return out
+
+
+def resnet50_tasks(reorders: int = 512) -> list:
+    """Config 3: the distinct conv2d / dense layers of ResNet-50 v1.5 at batch 1 (torchvision
+    layout: stride on the 3x3 of each bottleneck, 1x1/2 downsamples), SURVEY.md §8d1 (3).
+    (name, program spec, space): tile oc/oh/ow/ic by divisors + `reorders` 11-loop orders;
+    the dense layer tiles j/k by divisors + every 6-loop order."""
+    layers = [("conv1", dict(oc=64, oh=112, ow=112, ic=3, kh=7, kw=7, stride=2))]
+    ch_in, hw = 64, 56
+    for stage, (width, blocks) in enumerate(((64, 3), (128, 4), (256, 6), (512, 3))):
+        out_ch = width * 4
+        down = 1 if stage == 0 else 2
+        in_hw = hw if stage == 0 else hw * 2
+        layers += [(f"s{stage}_reduce_a", dict(oc=width, oh=in_hw, ow=in_hw, ic=ch_in, kh=1, kw=1)),
+                   (f"s{stage}_conv3_a", dict(oc=width, oh=hw, ow=hw, ic=width, kh=3, kw=3, stride=down)),
+                   (f"s{stage}_expand", dict(oc=out_ch, oh=hw, ow=hw, ic=width, kh=1, kw=1)),
+                   (f"s{stage}_downsample", dict(oc=out_ch, oh=hw, ow=hw, ic=ch_in, kh=1, kw=1, stride=down))]
+        if blocks > 1:
+            layers += [(f"s{stage}_reduce_b", dict(oc=width, oh=hw, ow=hw, ic=out_ch, kh=1, kw=1))]
+            if stage > 0:
+                layers += [(f"s{stage}_conv3_b", dict(oc=width, oh=hw, ow=hw, ic=width, kh=3, kw=3))]
+        ch_in, hw = out_ch, max(7, hw // 2)
+    out = []
+    chain = tiled_chain(["n", "oc", "oh", "ow", "ic", "kh", "kw"], ["ic", "oc", "oh", "ow"])
+    for i, (name, sh) in enumerate(layers):
+        spec = conv2d_json(n=1, **sh)
+        space = {"tile": {v: divisors(sh[v]) for v in ("ic", "oc", "oh", "ow")},
+                 "reorder": random_perms(chain, reorders, 100 + i)}
+        out.append((name, spec, space))
+    dchain = tiled_chain(["i", "j", "k"], ["j", "k"])
+    out.append(("fc1000", matmul_json(1, 1000, 2048),
+                {"tile": {"j": divisors(1000), "k": divisors(2048)},
+                 "reorder": [list(p) for p in itertools.permutations(dchain)]}))
+    return out

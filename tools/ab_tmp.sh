@@ -1,3 +1,8 @@
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
-timeout 600 python -m pytest tests/test_es_device.py -x -q > gpurun_out/pytest_es.log 2>&1; echo pytest_es=$?
-tail -40 gpurun_out/pytest_es.log
+timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
+tail -3 gpurun_out/pytest_gpu.log
+python tools/trace_topk.py 2>&1 | grep LS_TRACE | tail -3
+timeout 300 python bench.py --no-baseline > gpurun_out/bench_auto.log 2>&1
+tail -1 gpurun_out/bench_auto.log | python -c "import sys,json; d=json.loads(sys.stdin.read()); print('auto', d['value']/1e9, d['e2e']['value']/1e9, d['roofline']['kernel_ms'])"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 12 python tools/trace_topk.py > gpurun_out/ncu_k2.log 2>&1
+grep -E "gpu__time" gpurun_out/ncu_k2.log | tail -6
