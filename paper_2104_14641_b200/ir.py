@@ -330,3 +330,71 @@ def space_axes(p, space: dict) -> list:
         p.find_loop(loop)
         axes.append(SpaceAxis(f"parallel:{loop}", ((), (Parallel(loop),))))
     return axes
+
+
+# -- failure messages ---------------------------------------------------------------
+
+
+def failure_message(program, schedule) -> "tuple[str, str] | None":
+    """(exception type, message) apply_schedule raises for `schedule`, or None.
+
+    The device reports a failed candidate as a status code; the text the
+    reference's exception carries (ls/ir.py:151, 361-470) is rebuilt here for
+    the diagnostics of a failed candidate only, by replaying the transforms
+    over the loop names and extents of a perfect chain (the device class).
+    Scores and features always come from the device.
+    """
+    chain = []  # [name, extent] outermost first
+    node = program.body
+    while len(node) == 1 and type(node[0]).__name__ == "LoopNode":
+        chain.append([node[0].var, node[0].extent])
+        node = node[0].children
+    names = {v for v, _ in chain}
+
+    def find(v):
+        for j, (name, _) in enumerate(chain):
+            if name == v:
+                return j
+        raise ProgramError(f"no loop named {v!r}")
+
+    def tile(v, factor):
+        j = find(v)
+        ext = chain[j][1]
+        if factor < 1 or factor > ext:
+            raise ProgramError(f"tile factor {factor} out of range for loop {v!r} (extent {ext})")
+        inner = v + "_i"
+        while inner in names:
+            inner += "_"
+        names.add(inner)
+        chain[j][1] = -(-ext // factor)
+        chain.insert(j + 1, [inner, factor])
+
+    try:
+        for t in schedule.transforms:
+            kind = type(t).__name__
+            if kind == "Tile":
+                tile(t.loop, t.factor)
+            elif kind == "Vectorize":
+                ext = chain[find(t.loop)][1]
+                if ext % t.width != 0:
+                    raise ProgramError(f"vectorize width {t.width} does not divide extent {ext} of {t.loop!r}")
+                tile(t.loop, t.width)
+            elif kind == "Reorder":
+                order = tuple(t.order)
+                if len(order) < 2:
+                    continue
+                pos = [find(v) for v in order]
+                if len(set(order)) != len(order):
+                    raise ProgramError(f"reorder {order!r}: missing loops")
+                if max(pos) - min(pos) != len(order) - 1:
+                    raise ProgramError(f"reorder {order!r}: loops do not form a perfect nest chain")
+                lo = min(pos)
+                seg = {v: e for v, e in chain[lo:lo + len(order)]}
+                chain[lo:lo + len(order)] = [[v, seg[v]] for v in order]
+            else:  # Unroll / Parallel: existence only
+                find(t.loop)
+    except ProgramError as e:
+        return "ProgramError", str(e)
+    except ZeroDivisionError as e:
+        return "ZeroDivisionError", str(e)
+    return None
