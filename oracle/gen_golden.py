@@ -442,11 +442,62 @@ def es_fixture():
     print(f"es: {len(runs)} optimize runs")
 
 
+def cli_fixture():
+    """Reference CLI outputs (rank --json with failures, search --json --trace) on files under golden/cli."""
+    import contextlib
+    import io
+    from loopscout import cli as ref_cli
+    d = OUT / "cli"
+    d.mkdir(exist_ok=True)
+    rc = json.loads((OUT / "rank_cases.json").read_text())
+    runs = []
+    for pname in ("matmul48", "conv_small", "neg_stride", "deep9"):
+        case = next(c for c in rc["cases"] if c["program"] == pname)
+        (d / f"{pname}.json").write_text(json.dumps(rc["programs"][pname]))
+        (d / f"{pname}_scheds.json").write_text(json.dumps(case["schedules"]))
+        for arch in ("x86-avx2", "nvidia-volta"):
+            argv = ["rank", str(d / f"{pname}.json"), str(d / f"{pname}_scheds.json"), "--arch", arch, "--json",
+                    "--jobs", "1"] + (["--launch", str(d / "launch.json")] if arch == "nvidia-volta" else [])
+            runs.append((f"rank_{pname}_{arch}", argv, None))
+    (d / "launch.json").write_text(json.dumps(LAUNCH))
+    es_runs = json.loads((OUT / "es_runs.json").read_text())
+    for r in es_runs:
+        (d / f"es_{r['name']}.json").write_text(json.dumps(r["program"]))
+        (d / f"es_{r['name']}_space.json").write_text(json.dumps(r["space"]))
+        arch = r["arch"]
+        arch_arg = str(d / f"{arch}.toml") if arch in CUSTOM_ARCHS else arch
+        if arch in CUSTOM_ARCHS:
+            (d / f"{arch}.toml").write_text(CUSTOM_ARCHS[arch])
+        p = r["params"]
+        argv = ["search", str(d / f"es_{r['name']}.json"), str(d / f"es_{r['name']}_space.json"), "--arch", arch_arg,
+                "--json", "--jobs", "1", "--top-k", "5", "--seed", str(p.get("seed", 0)),
+                "--population", str(p.get("population", 32)), "--iterations", str(p.get("iterations", 100)),
+                "--sigma", str(p.get("sigma", 0.3))]
+        if p.get("rank_normalize") is False:
+            argv.append("--no-rank-normalize")
+        if "nvidia" in arch or "gpu" in arch:
+            argv += ["--launch", str(d / "launch.json")]
+        runs.append((f"search_{r['name']}", argv, f"search_{r['name']}_trace.csv"))
+    manifest = []
+    for name, argv, trace in runs:
+        if trace:
+            argv = argv + ["--trace", str(d / trace)]
+        buf = io.StringIO()
+        with contextlib.redirect_stdout(buf):
+            code = ref_cli.main(argv)
+        assert code == 0, (name, code)
+        (d / f"{name}.out").write_text(buf.getvalue())
+        rel = [a.replace(str(d) + "/", "{dir}/") for a in argv]
+        manifest.append({"name": name, "argv": rel, "trace": trace})
+    (d / "manifest.json").write_text(json.dumps(manifest, indent=1))
+    print(f"cli: {len(manifest)} reference CLI runs")
+
+
 def main():
     OUT.mkdir(parents=True, exist_ok=True)
     for name in CUSTOM_ARCHS:  # write the TOMLs before the pool forks (no write races)
         ref_arch(name)
-    which = set(sys.argv[1:]) or {"gemm", "conv", "bert", "rank", "trees", "emit", "es"}
+    which = set(sys.argv[1:]) or {"gemm", "conv", "bert", "rank", "trees", "emit", "es", "cli"}
     if "gemm" in which:
         space_fixture("gemm1024", W.matmul_json(1024), W.gemm_space(1024), 4096, 0,
                       ["x86-avx2", "aarch64-neon", "nvidia-volta"])
@@ -472,6 +523,8 @@ def main():
         emit_fixture()
     if "es" in which:
         es_fixture()
+    if "cli" in which:
+        cli_fixture()
 
 
 if __name__ == "__main__":

@@ -192,3 +192,20 @@ def test_es_oracle_update_matches_host_es():
         vals[3] = vals[5]
         p = EsParams(alpha=0.1, sigma=0.7, population=32, rank_normalize=rank)
         assert np.array_equal(E.es_update(th, 0.1, 0.7, 32, vals, eps, rank), es_update(th, p, vals, eps))
+
+
+def test_failure_messages_match_reference_errors():
+    """ir.failure_message rebuilds the exception text of every failing golden rank case (2350)."""
+    import json
+    from golden_util import rank_cases
+    from paper_2104_14641_b200 import ir
+    r = rank_cases()
+    n = 0
+    for c in r["cases"]:
+        prog = ir.parse_program(json.dumps(r["programs"][c["program"]]))
+        msgs = [ir.failure_message(prog, ir.Schedule.from_json(s)) for s in c["schedules"]]
+        for res in c["results"].values():
+            for m, e in zip(msgs, res["errors"]):
+                assert (None if m is None else f"{m[0]}: {m[1]}") == e
+                n += e is not None
+    assert n == 2350
