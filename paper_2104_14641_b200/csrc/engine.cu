@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <climits>
 #include <cmath>
 #include <cstdint>
@@ -172,9 +173,11 @@ struct __align__(16) DTask {
   int8_t sd_nb[8];                    // stage bits of each group (rows of 2^nb entries)
   // static tiles: every tile is driven by one tile axis and splits a base loop not split before,
   // so a choice fixes both extents; sp_ext per choice = F | ceil(E/F) << 16 | out-of-range << 63
-  int32_t sp_static, pad7;
+  int32_t sp_static, sp_narrow;         // static tiles; walk values proven to fit 32 bits (MODE 5)
   const uint64_t* sp_ext;
   uint8_t sp_tslot[LS_MAX_AXES], sp_tnew[LS_MAX_AXES];
+  int32_t sp_n_untiled, pad8;            // static tiles: base loops no tile splits
+  uint8_t sp_untiled[MAXCH], sp_untiled_pos[MAXCH];
   int32_t n_terms;
   DTerm term[MAXTERM];
 };
@@ -1161,15 +1164,15 @@ __device__ __forceinline__ uint64_t load_point(const void* __restrict__ src, int
                      : (uint64_t)__ldg(reinterpret_cast<const unsigned long long*>(src) + i);
 }
 
-template <int TM>
+template <int TM, bool NARROW>
 __device__ int eval_space(const DTask& T, const int32_t* __restrict__ sdt, uint64_t x, FastCand& c, double* f,
                           double* score) {
   // ---- decode the space point (mixed radix, axis 0 most significant): tile factors into the
   //      record's parameter slots (or, static tiles, both extents straight from the choice), the
   //      reorder choice, the group-table row offsets
   const bool stat = T.sp_static;
-  if (stat)
-    for (int p = 0; p < T.n_base; ++p) c.E(T.base_slot[p]) = T.base_ext[p];
+  if (stat)  // base loops no tile splits (the tiles write both extents of theirs)
+    for (int q = 0; q < T.sp_n_untiled; ++q) c.E(T.sp_untiled[q]) = T.base_ext[T.sp_untiled_pos[q]];
   uint32_t kd[TM * 2];
 #pragma unroll
   for (int g = 0; g < TM * 2; ++g) kd[g] = T.sd_off[g];
@@ -1237,34 +1240,44 @@ __device__ int eval_space(const DTask& T, const int32_t* __restrict__ sdt, uint6
   auto grp = [&](int g) -> uint32_t {
     return *reinterpret_cast<const uint32_t*>(tb + kd[g] + ((uint32_t)(mall >> (8 * g)) & 0xFFu));
   };
-  auto fp = [&](int t) -> int64_t { return (int64_t)((uint64_t)grp(2 * t) * grp(2 * t + 1)); };
+  // NARROW: the host proved every footprint, their sum and every movement fit 32 bits
+  using W = typename std::conditional<NARROW, uint32_t, int64_t>::type;
+  auto fp = [&](int t) -> W {
+    if constexpr (NARROW)
+      return grp(2 * t) * grp(2 * t + 1);
+    else
+      return (int64_t)((uint64_t)grp(2 * t) * grp(2 * t + 1));
+  };
   uint32_t vm[TM];
-  int64_t Fb[TM], dm[TM];
+  W Fb[TM], dm[TM];
   bool ru[TM];
 #pragma unroll
   for (int t = 0; t < TM; ++t) {
     vm[t] = T.t_vmask[t];
     Fb[t] = fp(t);
-    dm[t] = T.t_nacc[t];
+    dm[t] = (W)T.t_nacc[t];
     ru[t] = true;
   }
-  const int64_t cap = T.cap;
+  const W cap = (W)T.cap;
   const bool cpu = T.family == LS_FAMILY_CPU;
   int64_t P = 1, H = 0;  // product of all extents; Horner sum of the outer prefix products
   for (int p = n - 1; p >= 0; --p) {
     const int v = (int)((chain >> (4 * p)) & 15u);
     const int64_t E = c.E(v);
     mall |= T.vb8[v];
-    int64_t single = 0;
+    W single = 0;
 #pragma unroll
     for (int t = 0; t < TM; ++t) single += Fb[t];
     const bool over = single > cap;
 #pragma unroll
     for (int t = 0; t < TM; ++t) {
       const bool uses = (vm[t] >> v) & 1u;
-      const int64_t Ff = fp(t);
+      const W Ff = fp(t);
       const bool r0 = ru[t] && !(over && !uses);
-      dm[t] = (!over || r0) ? Ff : (int64_t)((uint64_t)dm[t] * (uint32_t)E);
+      if constexpr (NARROW)
+        dm[t] = (!over || r0) ? Ff : dm[t] * (uint32_t)E;
+      else
+        dm[t] = (!over || r0) ? Ff : (int64_t)((uint64_t)dm[t] * (uint32_t)E);
       ru[t] = r0 && !(Ff > cap);
       Fb[t] = Ff;
     }
@@ -1274,7 +1287,7 @@ __device__ int eval_space(const DTask& T, const int32_t* __restrict__ sdt, uint6
   }
   int64_t dmov = 0;
 #pragma unroll
-  for (int t = 0; t < TM; ++t) dmov += dm[t];
+  for (int t = 0; t < TM; ++t) dmov += (int64_t)dm[t];
   const int64_t L = T.L, S = T.S;
   double total = 0.0;
   if (cpu) {
@@ -1313,7 +1326,8 @@ __device__ int eval_space(const DTask& T, const int32_t* __restrict__ sdt, uint6
 // mask); the entry is the product of the group's dimension counts (same fold as
 // build_tab_kernel).  Products that do not fit 32 bits raise *overflow.
 __global__ void build_sdt_kernel(const DTask* __restrict__ g, const int32_t* __restrict__ rows,
-                                 uint32_t* __restrict__ tab, int32_t* __restrict__ overflow) {
+                                 uint32_t* __restrict__ tab, int32_t* __restrict__ overflow,
+                                 unsigned int* __restrict__ gmax) {
   const DTask& T = *g;
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= T.sd_len) return;
@@ -1351,6 +1365,7 @@ __global__ void build_sdt_kernel(const DTask* __restrict__ g, const int32_t* __r
     atomicExch(overflow, 1);
     F = 0;
   }
+  atomicMax(&gmax[G], (unsigned int)F);
   tab[e] = (uint32_t)F;
 }
 
@@ -1467,7 +1482,7 @@ __device__ __forceinline__ void stage_task(DTask& s, const DTask* __restrict__ g
 // in global memory (L1/L2 resident), 2 tabulated with the table in shared memory.
 template <int MODE>
 __device__ __forceinline__ const int32_t* stage_tab(unsigned char* where, const DTask& T) {
-  if constexpr (MODE == 2 || MODE == 4) {
+  if constexpr (MODE == 2 || MODE >= 4) {
     int32_t* dst = reinterpret_cast<int32_t*>(where);
     const int32_t* src = MODE == 2 ? T.tab : T.sd_tab;
     const int len = MODE == 2 ? T.tab_len : T.sd_len;
@@ -1481,7 +1496,7 @@ __device__ __forceinline__ const int32_t* stage_tab(unsigned char* where, const 
 
 __host__ __device__ inline size_t tab_smem_bytes(int mode, const DTask& T) {
   return mode == 2 ? align16(sizeof(int32_t) * (size_t)T.tab_len)
-                   : mode == 4 ? align16(sizeof(int32_t) * (size_t)T.sd_len) : 0;
+                   : mode >= 4 ? align16(sizeof(int32_t) * (size_t)T.sd_len) : 0;
 }
 __host__ __device__ inline size_t state_bytes(int mode, int n_slots, int n_chain, int n_stage) {
   return mode == 0 ? cand_bytes(n_slots, n_chain, n_stage) : align16(sizeof(int32_t) * (size_t)n_slots * TPB);
@@ -1531,7 +1546,7 @@ __device__ __forceinline__ int load_cand(const DTask& T, const void* __restrict_
   }
 }
 
-constexpr int min_blocks(int tm, int rm, int mode) { return mode == 4 ? 3 : mode ? 3 : (tm * rm <= 16 ? 3 : 1); }
+constexpr int min_blocks(int tm, int rm, int mode) { return mode ? 3 : (tm * rm <= 16 ? 3 : 1); }
 
 template <int TM, int RM, int MODE, int SRC>
 __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE))
@@ -1551,8 +1566,8 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE))
     double f[LS_NFEAT_GPU];
     double s = 0.0;
     int st;
-    if constexpr (MODE == 4) {
-      st = eval_space<TM>(T, tab, load_point(src, pbytes, i), ev.fc, f, &s);
+    if constexpr (MODE >= 4) {
+      st = eval_space<TM, MODE == 5>(T, tab, load_point(src, pbytes, i), ev.fc, f, &s);
     } else {
       uint32_t pch = 0;
       st = load_cand<SRC, MODE == 3>(T, src, pbytes, i, r, kt, pch);
@@ -2066,7 +2081,7 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kern
   const int64_t b0 = min(n, (int64_t)blockIdx.x * per), b1 = min(n, b0 + per);
   const int64_t stride = TPB;
   uint64_t xn = 0;  // space path: the next point, loaded one iteration ahead
-  if constexpr (MODE == 4)
+  if constexpr (MODE >= 4)
     if (b0 + threadIdx.x < b1) xn = load_point(src, pbytes, b0 + threadIdx.x);
   for (int64_t base = b0; base < b0 + per; base += stride) {
     const int64_t i = base + threadIdx.x;
@@ -2078,10 +2093,10 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kern
       double f[LS_NFEAT_GPU];
       double s;
       int st;
-      if constexpr (MODE == 4) {
+      if constexpr (MODE >= 4) {
         const uint64_t x = xn;
         if (i + stride < b1) xn = load_point(src, pbytes, i + stride);
-        st = eval_space<TM>(T, tab, x, ev.fc, f, &s);
+        st = eval_space<TM, MODE == 5>(T, tab, x, ev.fc, f, &s);
       } else {
         uint32_t pch = 0;
         st = load_cand<SRC, MODE == 3>(T, src, pbytes, i, r, kt, pch);
@@ -2385,6 +2400,12 @@ void plan_static_tiles(DTask& T, const ls_space_desc* sp, std::vector<uint64_t>&
     T.sp_tnew[axis] = xf.new_slot;
     ++covered;
   }
+  T.sp_n_untiled = 0;
+  for (int p = 0; p < T.n_base; ++p)
+    if (!((split >> T.base_slot[p]) & 1u)) {
+      T.sp_untiled[T.sp_n_untiled] = T.base_slot[p];
+      T.sp_untiled_pos[T.sp_n_untiled++] = (uint8_t)p;
+    }
   for (int a = 0; a < T.sp_n; ++a) {  // every tile axis must drive a tile
     if (T.sp_ax[a].kind != LS_AX_PARAM) continue;
     bool used = false;
@@ -2881,7 +2902,7 @@ int grid_for(const ls_task* t, int64_t n, int per_sm) {
 // 3 tensor tables (points), 4 space-specialised (points)
 int mode_of(const ls_task* t, bool points = false) {
   if (t->path == LS_PATH_GENERIC || !t->host.fast) return 0;
-  if (points && t->host.sp_ok && t->path != LS_PATH_TABULATED) return 4;
+  if (points && t->host.sp_ok && t->path != LS_PATH_TABULATED) return t->host.sp_narrow ? 5 : 4;
   if (points && t->host.tt_ok) return 3;
   return t->host.tab_smem ? 2 : 1;
 }
@@ -2908,6 +2929,14 @@ ScoreFn score_fn_src(const DTask& T, int mode) {
         default: return score_kernel<4, 4, 4, 1>;
       }
     }
+    if (mode == 5) {
+      switch (T.n_tensors) {
+        case 1: return score_kernel<1, 4, 5, 1>;
+        case 2: return score_kernel<2, 4, 5, 1>;
+        case 3: return score_kernel<3, 4, 5, 1>;
+        default: return score_kernel<4, 4, 5, 1>;
+      }
+    }
     if (mode == 3) return score_kernel<4, 4, 3, 1>;
   }
   if (mode == 1) return score_kernel<4, 4, 1, SRC>;
@@ -2923,6 +2952,14 @@ TopkFn topk_fn_src(const DTask& T, int mode) {
         case 2: return score_topk_kernel<2, 4, 4, 1>;
         case 3: return score_topk_kernel<3, 4, 4, 1>;
         default: return score_topk_kernel<4, 4, 4, 1>;
+      }
+    }
+    if (mode == 5) {
+      switch (T.n_tensors) {
+        case 1: return score_topk_kernel<1, 4, 5, 1>;
+        case 2: return score_topk_kernel<2, 4, 5, 1>;
+        case 3: return score_topk_kernel<3, 4, 5, 1>;
+        default: return score_topk_kernel<4, 4, 5, 1>;
       }
     }
     if (mode == 3) return score_topk_kernel<4, 4, 3, 1>;
@@ -3019,7 +3056,7 @@ int ls_task_path(const ls_task* t) {
 int ls_task_points_path(const ls_task* t) {
   if (!t) return LS_E_ARG;
   const int m = mode_of(t, true);
-  return m == 4 ? LS_PATH_SPACE : m ? LS_PATH_TABULATED : LS_PATH_GENERIC;
+  return m >= 4 ? LS_PATH_SPACE : m ? LS_PATH_TABULATED : LS_PATH_GENERIC;
 }
 
 int ls_task_destroy(ls_task* t) {
@@ -3282,19 +3319,58 @@ int ls_task_set_space(ls_task* t, const ls_space_desc* sp) {
       t->retired.push_back(dst);
       CUDA_TRY(cudaMalloc(&dsd, sizeof(int32_t) * t->host.sd_len));
       t->retired.push_back(dsd);
-      CUDA_TRY(cudaMalloc(&drows, sizeof(rows) + sizeof(int32_t)));
+      CUDA_TRY(cudaMalloc(&drows, sizeof(rows) + sizeof(int32_t) * 9));
       t->retired.push_back(drows);
       CUDA_TRY(cudaMemcpy(drows, rows, sizeof(rows), cudaMemcpyHostToDevice));
       dovf = drows + 16;
-      CUDA_TRY(cudaMemset(dovf, 0, sizeof(int32_t)));
+      CUDA_TRY(cudaMemset(dovf, 0, sizeof(int32_t) * 9));  // overflow flag + per-group maxima
       if (int rc = upload(t)) return rc;
       const size_t sm = sizeof(int32_t) * NSLOT * TPB;
       build_pchain_kernel<<<(np + TPB - 1) / TPB, TPB, sm>>>(t->d_task, pax, dch, dst);
       CUDA_TRY(cudaGetLastError());
-      build_sdt_kernel<<<(t->host.sd_len + 255) / 256, 256>>>(t->d_task, drows, dsd, dovf);
+      build_sdt_kernel<<<(t->host.sd_len + 255) / 256, 256>>>(t->d_task, drows, dsd, dovf,
+                                                              reinterpret_cast<unsigned int*>(dovf + 1));
       CUDA_TRY(cudaGetLastError());
-      int32_t ovf = 0;
-      CUDA_TRY(cudaMemcpy(&ovf, dovf, sizeof(int32_t), cudaMemcpyDeviceToHost));
+      int32_t ovf_g[9] = {0};
+      CUDA_TRY(cudaMemcpy(ovf_g, dovf, sizeof(ovf_g), cudaMemcpyDeviceToHost));
+      const int32_t ovf = ovf_g[0];
+      {  // MODE 5 (32-bit walk): every footprint, their sum and every movement below 2^32.
+        // A dimension count with variables S expanded is at most (unique accesses) x the product of
+        // their extents (_si_sum counts <= the product, _si_union <= the sum), so a footprint is
+        // <= K_t * P^m_t and a movement <= max(accesses, K_t) * P^m_t, with P the product of all
+        // transformed extents, K_t = unique accesses ^ rank, m_t = most dimensions sharing a variable.
+        const unsigned int* gm = reinterpret_cast<const unsigned int*>(ovf_g + 1);
+        double fsum = 0, prod = 1;
+        bool divides = true;
+        for (int q = 0; q < t->host.n_base; ++q) prod *= t->host.base_ext[q];
+        for (int a = 0; a < t->host.sp_n; ++a)
+          if (t->host.sp_ax[a].kind == LS_AX_PARAM)
+            for (uint32_t c = 0; c < t->host.sp_ax[a].n; ++c) {
+              const uint64_t F = sp->axes[a].values[c];
+              int base = -1;
+              for (int q = 0; q < t->host.n_base; ++q)
+                for (int x = 0; x < t->host.n_xf; ++x)
+                  if (t->host.xf[x].kind == LS_XF_TILE && t->host.xf[x].param == t->host.sp_ax[a].param &&
+                      t->host.base_slot[q] == t->host.xf[x].slot)
+                    base = q;
+              if (base < 0 || F == 0 || t->host.base_ext[base] % (int64_t)F != 0) divides = false;
+            }
+        if (!divides) prod *= std::pow(2.0, (double)t->host.sp_n);  // ceil(E/F) * F < 2E per tile
+        bool fits = t->host.sp_static && t->host.cap < 4294967295ll;
+        for (int q = 0; q < t->host.n_tensors; ++q) {
+          fsum += (double)std::max(1u, gm[2 * q]) * (double)std::max(1u, gm[2 * q + 1]);
+          int m = 1;
+          for (int v = 0; v < NSLOT; ++v) {
+            int dims = 0;
+            for (int r = 0; r < t->host.t_rank[q]; ++r)
+              for (int x = 0; x < t->host.dim_nv[q * 4 + r]; ++x) dims += t->host.dim_var[q * 4 + r][x] == v;
+            m = std::max(m, dims);
+          }
+          const double K = std::pow((double)t->host.t_nu[q], (double)t->host.t_rank[q]);
+          if (std::max((double)t->host.t_nacc[q], K) * std::pow(prod, (double)m) >= 4294967295.0) fits = false;
+        }
+        t->host.sp_narrow = fits && fsum < 4294967295.0;
+      }
       t->host.sp_chain = dch;
       t->host.sp_pstat = dst;
       t->host.sd_tab = reinterpret_cast<const int32_t*>(dsd);

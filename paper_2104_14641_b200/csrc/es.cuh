@@ -97,8 +97,8 @@ template <int TM, int RM, int MODE>
 __device__ __forceinline__ int score_point(const DTask& T, const int32_t* tab, Evaluator<TM, RM, MODE>& ev,
                                            uint64_t x, double* s) {
   double f[LS_NFEAT_GPU];
-  if constexpr (MODE == 4) {
-    return eval_space<TM>(T, tab, x, ev.fc, f, s);
+  if constexpr (MODE >= 4) {
+    return eval_space<TM, MODE == 5>(T, tab, x, ev.fc, f, s);
   } else {
     ls_record r;
     uint32_t kt[4];
@@ -268,6 +268,14 @@ EsGenFn es_gen_fn(const DTask& T, int mode) {
       case 2: return es_gen_kernel<2, 4, 4>;
       case 3: return es_gen_kernel<3, 4, 4>;
       default: return es_gen_kernel<4, 4, 4>;
+    }
+  }
+  if (mode == 5) {
+    switch (T.n_tensors) {
+      case 1: return es_gen_kernel<1, 4, 5>;
+      case 2: return es_gen_kernel<2, 4, 5>;
+      case 3: return es_gen_kernel<3, 4, 5>;
+      default: return es_gen_kernel<4, 4, 5>;
     }
   }
   if (mode == 3) return es_gen_kernel<4, 4, 3>;
