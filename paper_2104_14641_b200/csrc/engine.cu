@@ -1546,7 +1546,7 @@ __device__ __forceinline__ int load_cand(const DTask& T, const void* __restrict_
   }
 }
 
-constexpr int min_blocks(int tm, int rm, int mode) { return mode ? 3 : (tm * rm <= 16 ? 3 : 1); }
+constexpr int min_blocks(int tm, int rm, int mode) { return mode == 5 ? 3 : mode ? 3 : (tm * rm <= 16 ? 3 : 1); }
 
 template <int TM, int RM, int MODE, int SRC>
 __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE))
@@ -1603,24 +1603,22 @@ __device__ __forceinline__ double from_order_bits(unsigned long long o) {
 
 constexpr int TK_MAXK = 1024;
 
-// Block top-k state in shared memory: header + two key buffers of `cap` keys
-// (cap = 1024 or 2048).  The current buffer is an unsorted multiset of keys
-// below `thr`; compaction keeps exactly the k smallest by radix selection of
-// the k-th key (no sort), and only the final list of a launch is sorted.
+// Block top-k state in shared memory: header + a key buffer of `cap` keys
+// (cap = 1024 or 2048, <= 8 per thread).  The buffer is an unsorted multiset of
+// keys below `thr`; compaction keeps exactly the k smallest by radix selection
+// of the k-th key (no sort), filtering in place through registers; only the
+// final list of a launch is sorted.
 struct __align__(16) TopkState {
   Key thr;
-  int cnt, cap, cur, cnt2;
+  int cnt, cap, cnt2, pad0;
   unsigned int hist[256];
   int sel_bucket, sel_rank, sel_count, pad;
   unsigned long long and_s, or_s, and_i, or_i;  // common-prefix reduction of the buffered keys
-  __device__ __forceinline__ Key* buf() { return reinterpret_cast<Key*>(this + 1) + (cur ? cap : 0); }
-  __device__ __forceinline__ const Key* buf() const {
-    return reinterpret_cast<const Key*>(this + 1) + (cur ? cap : 0);
-  }
-  __device__ __forceinline__ Key* other() { return reinterpret_cast<Key*>(this + 1) + (cur ? 0 : cap); }
+  __device__ __forceinline__ Key* buf() { return reinterpret_cast<Key*>(this + 1); }
+  __device__ __forceinline__ const Key* buf() const { return reinterpret_cast<const Key*>(this + 1); }
 };
 __host__ __device__ constexpr size_t topk_state_bytes(int cap) {
-  return sizeof(TopkState) + 2 * sizeof(Key) * (size_t)cap;
+  return sizeof(TopkState) + sizeof(Key) * (size_t)cap;
 }
 
 // Sort buf[0..cnt) (padded with +inf) and keep the k smallest; returns the kept
@@ -1790,16 +1788,29 @@ __device__ int topk_select(TopkState& S, int k) {
   if (threadIdx.x == 0) S.cnt2 = 0;
   __syncthreads();
   const Key thr = S.thr;
-  Key* dst = S.other();
-  for (int j = threadIdx.x; j < c; j += blockDim.x) {
-    const Key x = B[j];
-    if (!kless(thr, x)) dst[atomicAdd(&S.cnt2, 1)] = x;
+  // in place, 4 keys per thread per chunk: a chunk's reads end (barrier) before
+  // its writes, and writes land below the keys read so far, so they never reach
+  // a later chunk's unread keys
+  Key* const W = S.buf();
+  for (int base = 0; base < c; base += 4 * blockDim.x) {
+    Key keep[4];
+    bool kp[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = base + threadIdx.x + q * blockDim.x;
+      kp[q] = false;
+      if (j < c) {
+        keep[q] = B[j];
+        kp[q] = !kless(thr, keep[q]);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (kp[q]) W[atomicAdd(&S.cnt2, 1)] = keep[q];
+    __syncthreads();
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    S.cur ^= 1;
-    S.cnt = S.cnt2;
-  }
+  if (threadIdx.x == 0) S.cnt = S.cnt2;
   __syncthreads();
   return k;
 }
@@ -1808,7 +1819,6 @@ __device__ __forceinline__ void topk_init(TopkState& S, int cap) {
   if (threadIdx.x == 0) {
     S.cap = cap;
     S.cnt = 0;
-    S.cur = 0;
     S.thr.s = KEY_INF_S;
     S.thr.i = KEY_INF_I;
   }
