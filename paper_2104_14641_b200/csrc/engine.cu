@@ -194,6 +194,9 @@ struct ls_task {
   int num_sms;
   int path;            // LS_PATH_AUTO / LS_PATH_GENERIC / LS_PATH_TABULATED
   int32_t* d_tab;      // tabulated path's dimension-count table (owned)
+  unsigned char* stage = nullptr;  // pinned staging of the host-buffer calls' results
+  size_t stage_bytes = 0;
+  bool stage_busy = false;
 };
 
 // ---------------------------------------------------------------------------
@@ -2985,12 +2988,36 @@ TopkFn topk_fn(const DTask& T, int mode, int pbytes) {
   return pbytes ? topk_fn_src<1>(T, mode) : topk_fn_src<0>(T, mode);
 }
 
+// Resident blocks per SM of a kernel at a dynamic shared-memory size (cached:
+// the attribute and occupancy queries cost host time on every scoring call).
+// The kernel's dynamic shared-memory limit only ever grows, so a cached launch
+// at a smaller size stays valid after a larger one.
 template <typename K>
 int blocks_per_sm(K kernel, size_t smem) {
-  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<const void*, size_t>, int>> cache;
+  static std::vector<std::pair<const void*, size_t>> limit;
+  const void* f = reinterpret_cast<const void*>(kernel);
+  std::lock_guard<std::mutex> g(mu);
+  bool raise = true;
+  for (auto& e : limit)
+    if (e.first == f) {
+      raise = smem > e.second;
+      if (raise) e.second = smem;
+    }
+  if (raise) {
+    bool known = false;
+    for (auto& e : limit) known |= e.first == f;
+    if (!known) limit.push_back({f, smem});
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  }
+  for (auto& e : cache)
+    if (e.first.first == f && e.first.second == smem) return e.second;
   int b = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, TPB, smem);
-  return std::max(b, 1);
+  b = std::max(b, 1);
+  cache.push_back({{f, smem}, b});
+  return b;
 }
 
 }  // namespace
@@ -3076,6 +3103,7 @@ int ls_task_destroy(ls_task* t) {
   for (void* p : t->retired) cudaFree(p);
   if (t->d_task) cudaFree(t->d_task);
   if (t->d_tab) cudaFree(t->d_tab);
+  if (t->stage) cudaFreeHost(t->stage);
   delete t;
   return LS_E_OK;
 }
@@ -3152,8 +3180,11 @@ int ls_score_points(ls_task* t, const void* d_points, int32_t pbytes, int64_t n,
   return score_device(t, d_points, pbytes, n, d_scores, d_features, d_status, (cudaStream_t)stream);
 }
 
+// h_out != null: the top-k scores, indices and the valid count live in the
+// workspace and come back in one copy to h_out ([k] f64, [k] i64, u64).
 static int topk_device(ls_task* t, const void* d_src, int pbytes, int64_t n, int64_t base_index, int32_t k,
-                       double* d_top_scores, int64_t* d_top_index, unsigned long long* d_valid, cudaStream_t s) {
+                       double* d_top_scores, int64_t* d_top_index, unsigned long long* d_valid, cudaStream_t s,
+                       void* h_out = nullptr) {
   const int mode = mode_of(t, pbytes != 0);
   const TopkFn fn = topk_fn(t->host, mode, pbytes);
   const size_t sm = smem_topk(t->host, k, mode);
@@ -3164,14 +3195,21 @@ static int topk_device(ls_task* t, const void* d_src, int pbytes, int64_t n, int
   const bool two = 4 * k <= grid && grid <= topk_buf(k);
   const size_t ws_keys = sizeof(Key) * (two ? (size_t)grid * (2 * k + 1) : ((size_t)grid + ngroups) * k);
   const int nctr = two ? 2 : ngroups + 1;
-  const size_t ws_bytes = ws_keys + align16(sizeof(unsigned int) * nctr);
+  const size_t ctr_bytes = align16(sizeof(unsigned int) * nctr) + (h_out ? 16 : 0);  // + the valid count
+  const size_t out_bytes = h_out ? 16 * (size_t)k : 0;
+  const size_t ws_bytes = ws_keys + ctr_bytes + out_bytes;
   unsigned char* ws = nullptr;
   CUDA_TRY(cudaMallocAsync(&ws, ws_bytes, s));
   Key* block_out = reinterpret_cast<Key*>(ws);
   Key* group_out = block_out + (size_t)grid * k;   // tree: group lists; two-stage: survivors
   Key* mins = two ? group_out + (size_t)grid * k : nullptr;
   unsigned int* tickets = reinterpret_cast<unsigned int*>(ws + ws_keys);
-  CUDA_TRY(cudaMemsetAsync(tickets, 0, sizeof(unsigned int) * nctr, s));
+  if (h_out) {  // outputs in the workspace: [k] scores, [k] indices, then the count (zeroed with the tickets)
+    d_valid = reinterpret_cast<unsigned long long*>(ws + ws_keys + ctr_bytes - 16);
+    d_top_scores = reinterpret_cast<double*>(ws + ws_keys + ctr_bytes);
+    d_top_index = reinterpret_cast<int64_t*>(d_top_scores + k);
+  }
+  CUDA_TRY(cudaMemsetAsync(tickets, 0, ctr_bytes, s));
   unsigned long long* tr = nullptr;
   const char* tr_env = getenv("LS_TRACE");
   if (tr_env && tr_env[0] == '1') {  // phase timestamps to stderr (profiling aid)
@@ -3185,14 +3223,18 @@ static int topk_device(ls_task* t, const void* d_src, int pbytes, int64_t n, int
   if (two) {
     const size_t msm = topk_state_bytes(topk_buf(k));
     static thread_local bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(merge_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm);
+    if (!attr) {  // the largest state this kernel is launched with
+      cudaFuncSetAttribute(merge_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)topk_state_bytes(2048));
       attr = true;
     }
     const int g2 = (int)std::max<int64_t>(1, std::min<int64_t>(4 * t->num_sms, ((int64_t)grid * k + TPB - 1) / TPB));
     merge_filter_kernel<<<g2, TPB, msm, s>>>(block_out, mins, grid, k, group_out, tickets, d_top_scores, d_top_index,
                                              topk_buf(k));
     CUDA_TRY(cudaGetLastError());
+  }
+  if (h_out) {  // scores | indices | count, contiguous from d_valid's 16-byte slot onwards
+    CUDA_TRY(cudaMemcpyAsync(h_out, ws + ws_keys + ctr_bytes - 16, 16 + out_bytes, cudaMemcpyDeviceToHost, s));
   }
   CUDA_TRY(cudaFreeAsync(ws, s));
   if (tr) {
@@ -3426,23 +3468,43 @@ static const void* mapped_alias(const void* h) {
 
 static int score_topk_mapped(ls_task* t, const void* d_alias, int pbytes, int64_t n, int64_t base_index, int32_t k,
                              double* h_top_scores, int64_t* h_top_index, int64_t* h_n_valid, cudaStream_t s) {
-  unsigned char* blk = nullptr;  // top scores | top indices | valid count
-  const size_t bytes = sizeof(double) * k + sizeof(int64_t) * k + sizeof(unsigned long long);
-  CUDA_TRY(cudaMallocAsync(&blk, bytes, s));
-  double* out_s = reinterpret_cast<double*>(blk);
-  int64_t* out_i = reinterpret_cast<int64_t*>(blk + sizeof(double) * k);
-  unsigned long long* valid = reinterpret_cast<unsigned long long*>(blk + 16 * (size_t)k);
-  CUDA_TRY(cudaMemsetAsync(valid, 0, sizeof(unsigned long long), s));
-  int rc = topk_device(t, d_alias, pbytes, n, base_index, k, out_s, out_i, valid, s);
-  unsigned long long hv = 0;
-  if (rc == LS_E_OK) {
-    CUDA_TRY(cudaMemcpyAsync(h_top_scores, out_s, sizeof(double) * k, cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaMemcpyAsync(h_top_index, out_i, sizeof(int64_t) * k, cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaMemcpyAsync(&hv, valid, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  // pinned staging block: count (16 B slot) | scores | indices, filled by one D2H copy
+  unsigned char* stage = nullptr;
+  const size_t need = 16 + 16 * (size_t)k;
+  {
+    std::lock_guard<std::mutex> g(t->mu);
+    if (!t->stage_busy) {
+      if (t->stage_bytes < need) {
+        if (t->stage) cudaFreeHost(t->stage);
+        t->stage = nullptr;
+        t->stage_bytes = 0;
+        CUDA_TRY(cudaMallocHost(&t->stage, need));
+        t->stage_bytes = need;
+      }
+      t->stage_busy = true;
+      stage = t->stage;
+    }
   }
-  cudaFreeAsync(blk, s);
-  CUDA_TRY(cudaStreamSynchronize(s));
-  if (h_n_valid) *h_n_valid = (int64_t)hv;
+  bool own = false;
+  if (!stage) {  // concurrent host call on this task: a private staging block
+    CUDA_TRY(cudaMallocHost(&stage, need));
+    own = true;
+  }
+  int rc = topk_device(t, d_alias, pbytes, n, base_index, k, nullptr, nullptr, nullptr, s, stage);
+  if (rc == LS_E_OK) {
+    CUDA_TRY(cudaStreamSynchronize(s));
+    unsigned long long hv = 0;
+    memcpy(&hv, stage, 8);
+    memcpy(h_top_scores, stage + 16, sizeof(double) * k);
+    memcpy(h_top_index, stage + 16 + 8 * (size_t)k, sizeof(int64_t) * k);
+    if (h_n_valid) *h_n_valid = (int64_t)hv;
+  }
+  if (own) {
+    cudaFreeHost(stage);
+  } else {
+    std::lock_guard<std::mutex> g(t->mu);
+    t->stage_busy = false;
+  }
   return rc;
 }
 
