@@ -379,8 +379,10 @@ def b200_arm(args):
             "issue_roofline": issue,
             "cpu_baseline": cpu, "parity": parity,
             "clocks": clk.summary(),
-            "gpu_launches": args.steps * (1 + (2 if world > 1 else 0)),
-            "n_valid_per_gpu": n_valid, "path": task.path,
+            # per step: the fused kernel + the minima-bound merge (k <= grid / 4), and for N > 1 the
+            # all-gathered lists' lists_to_keys + merge_keys kernels (the memsets are not ours)
+            "gpu_launches": args.steps * (1 + (1 if 4 * args.k <= 3 * 148 else 0) + (2 if world > 1 else 0)),
+            "n_valid_per_gpu": n_valid, "path": task.path, "points_path": task.points_path,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -475,7 +477,7 @@ def bert_arm(args):
                        "arch": args.arch, "candidates_per_step": per_step, "k": args.k,
                        "tasks": {name: {"candidates_per_gpu": n, "points_path": pp} for name, _, _, n, pp in jobs},
                        "l2": "flushed between timed steps (256 MiB write)"},
-            "clocks": clk.summary(), "gpu_launches": args.steps * len(jobs) * (1 + (2 if world > 1 else 0))}
+            "clocks": clk.summary(), "gpu_launches": args.steps * len(jobs) * (2 + (2 if world > 1 else 0))}
     for _, task, _, _, _ in jobs:
         task.close()
     _emit(line, world, dist)

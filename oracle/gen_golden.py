@@ -442,6 +442,88 @@ def es_fixture():
     print(f"es: {len(runs)} optimize runs")
 
 
+def random_tree_schedule(rng: random.Random, prog):
+    """A random Tile / Reorder / Parallel list on a tree program, valid or not."""
+    loops = {lp.var: lp for lp in prog.loops()}
+    ext = {v: lp.extent for v, lp in loops.items()}
+    kids = {v: [c.var if hasattr(c, "var") else None for c in lp.children] for v, lp in loops.items()}
+    sched = []
+    names = list(loops)
+    for v in rng.sample(names, rng.randint(0, min(len(names), 3))):
+        e = ext[v]
+        r = rng.random()
+        f = rng.choice([d for d in range(1, e + 1) if e % d == 0]) if r < 0.7 else (
+            rng.randint(1, e) if r < 0.95 else rng.choice([0, e + 1]))
+        sched.append({"tile": {"loop": v, "factor": f}})
+        inner = v + "_i"
+        while inner in kids:
+            inner += "_"
+        kids[inner] = kids[v]
+        kids[v] = [inner]
+        ext[inner] = max(f, 1)
+        ext[v] = math.ceil(e / max(f, 1))
+    if rng.random() < 0.8:
+        if rng.random() < 0.8:  # a single-child chain from a random loop
+            v = rng.choice(list(kids))
+            seg = [v]
+            while len(kids[seg[-1]]) == 1 and kids[seg[-1]][0] is not None and rng.random() < 0.85:
+                seg.append(kids[seg[-1]][0])
+            if len(seg) >= 2:
+                sched.append({"reorder": rng.sample(seg, len(seg))})
+        else:  # any set of names (mostly invalid)
+            seg = rng.sample(list(kids), min(len(kids), rng.randint(2, 4)))
+            if rng.random() < 0.1:
+                seg.append("nope")
+            sched.append({"reorder": seg})
+    for v in rng.sample(list(kids), rng.randint(0, min(2, len(kids)))):
+        sched.append({"parallel": {"loop": v}})
+    return sched
+
+
+def tree_rank_fixture(n_per=60, seed=77):
+    """Scheduled tree programs (imperfect nests, siblings, top-level accesses, deep nests) through
+    the reference: scores / features / errors per arch."""
+    sys.path.insert(0, "/root/reference/pkg/tests")
+    import helpers as H
+    from loopscout.ir import serialize_program
+    trees = json.loads((OUT / "trees.json").read_text())
+    progs = {k: v["program"] for k, v in trees.items() if k in ("two_mm_64_8", "two_mm_16_4", "interposed",
+                                                               "trace_layout") or k.startswith("random_nest_")}
+    mixed = H.build([H.tensor("A", [16, 16]), H.tensor("B", [16]), H.tensor("C", [16, 16])],
+                    [H.acc("B", "load", ["0"]),
+                     H.loop("i", 16, [H.acc("B", "load", ["i"]),
+                                      H.loop("j", 16, [H.acc("A", "load", ["i", "j"]),
+                                                       H.acc("C", "store", ["j", "i"])]),
+                                      H.acc("B", "store", ["i"]),
+                                      H.loop("k", 8, [H.acc("C", "load", ["i", "2*k"])])]),
+                     H.loop("m", 4, [H.acc("A", "load", ["m", "m"])])])
+    progs["mixed_levels"] = json.loads(serialize_program(mixed))
+    deep = H.loop("d9", 2, [H.acc("A", "load", ["d0 + d9"]), H.acc("A", "store", ["d1"])])
+    for k in range(8, -1, -1):
+        deep = H.loop(f"d{k}", 2, [deep] + ([H.loop(f"s{k}", 3, [H.acc("A", "load", [f"s{k}"])])] if k == 3 else []))
+    progs["deep_branch"] = json.loads(serialize_program(H.build([H.tensor("A", [32])], [deep])))
+    rng = random.Random(seed)
+    arches = ["x86-avx2", "aarch64-neon", "nvidia-volta", "odd-x86", "odd-gpu"]
+    cases, jobs = [], []
+    for pname, spec in progs.items():
+        prog = L.parse_program(json.dumps(spec))
+        scheds = [[]] + [random_tree_schedule(rng, prog) for _ in range(n_per)]
+        cases.append({"program": pname, "schedules": scheds, "results": {a: {} for a in arches}})
+        for a in arches:
+            jobs.extend((json.dumps(spec), sch, a) for sch in scheds)
+    res = run_pool(jobs)
+    k = 0
+    for c in cases:
+        for a, r in c["results"].items():
+            outs = res[k:k + len(c["schedules"])]
+            k += len(c["schedules"])
+            r["scores"] = [o[0] for o in outs]
+            r["features"] = [o[1] for o in outs]
+            r["errors"] = [o[2] for o in outs]
+    (OUT / "tree_rank.json").write_text(json.dumps({"programs": progs, "cases": cases}, separators=(",", ":")))
+    print(f"tree_rank: {len(jobs)} evaluations")
+
+
 def cli_fixture():
     """Reference CLI outputs (rank --json with failures, search --json --trace) on files under golden/cli."""
     import contextlib
@@ -497,7 +579,7 @@ def main():
     OUT.mkdir(parents=True, exist_ok=True)
     for name in CUSTOM_ARCHS:  # write the TOMLs before the pool forks (no write races)
         ref_arch(name)
-    which = set(sys.argv[1:]) or {"gemm", "conv", "bert", "rank", "trees", "emit", "es", "cli"}
+    which = set(sys.argv[1:]) or {"gemm", "conv", "bert", "rank", "trees", "emit", "es", "cli", "tree_rank"}
     if "gemm" in which:
         space_fixture("gemm1024", W.matmul_json(1024), W.gemm_space(1024), 4096, 0,
                       ["x86-avx2", "aarch64-neon", "nvidia-volta"])
@@ -525,6 +607,8 @@ def main():
         es_fixture()
     if "cli" in which:
         cli_fixture()
+    if "tree_rank" in which:
+        tree_rank_fixture()
 
 
 if __name__ == "__main__":

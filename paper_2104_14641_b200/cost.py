@@ -17,7 +17,7 @@ import numpy as np
 
 from . import abi
 from .arch import CPU_FEATURES, GPU_FEATURES, FeatureVector
-from .engine import Task, to_device_records
+from .engine import EngineError, Task, to_device_records
 from .pack import PackError, pack_schedules
 
 
@@ -68,7 +68,13 @@ def score_batch(program, schedules, arch, launch=None, device: int = 0, features
         if g.template is None:
             status[g.index] = abi.ST_UNSUPPORTED
             continue
-        task = Task(g.template.desc(arch, launch), device)
+        try:
+            task = Task(g.template.desc(arch, launch), device)
+        except EngineError as e:
+            if "(-3)" not in str(e):  # LS_E_UNSUPPORTED: outside the device class, per candidate
+                raise
+            status[g.index] = abi.ST_UNSUPPORTED
+            continue
         d_rec = to_device_records(g.records, device)
         task.prepare_unroll_for(d_rec)
         s, f, st = task.score(d_rec, features=features)

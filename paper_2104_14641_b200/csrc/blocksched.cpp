@@ -305,4 +305,19 @@ int64_t body_block_cycles(const ls_task_desc& d, const std::vector<int>& load_t,
   return schedule_block(e.out, d);
 }
 
+// A tree loop's header block: its direct accesses (loads, then fma + store per
+// store) followed by the first child loop's counter init, or by its own latch
+// when it has no child loop (ls/ir.py:628-654 with the block splits of
+// ls/asm.py:155-167).  The counter register does not interact with the body.
+int64_t group_block_cycles(const ls_task_desc& d, const std::vector<int>& load_t, const std::vector<int>& store_t,
+                           bool with_latch) {
+  Emitter e{d.target};
+  e.body(load_t, store_t);
+  if (with_latch)
+    e.latch(1, 7, 1);
+  else
+    e.init(2);
+  return schedule_block(e.out, d);
+}
+
 }  // namespace lsb

@@ -30,6 +30,8 @@
 
 namespace lsb {
 void fixed_block_cycles(const ls_task_desc& d, int64_t* c_init, int64_t* c_latch, int64_t* c_ret);
+int64_t group_block_cycles(const ls_task_desc& d, const std::vector<int>& load_t, const std::vector<int>& store_t,
+                           bool with_latch);
 int64_t body_block_cycles(const ls_task_desc& d, const std::vector<int>& load_t,
                           const std::vector<int>& store_t, int64_t U, bool with_latch);
 }  // namespace lsb
@@ -178,6 +180,12 @@ struct __align__(16) DTask {
   uint8_t sp_tslot[LS_MAX_AXES], sp_tnew[LS_MAX_AXES];
   int32_t sp_n_untiled, pad8;            // static tiles: base loops no tile splits
   uint8_t sp_untiled[MAXCH], sp_untiled_pos[MAXCH];
+  // ---- general trees: unified node ids, accesses 0..tr_na-1 (preorder), loops
+  //      tr_na + j for base loop j (preorder; header j = base_slot/ext/step/flags[j]), tile loops after
+  int32_t tree, tr_nl, tr_na, tr_root_first;
+  int8_t tr_parent[32], tr_first[32], tr_next[32];
+  uint8_t tr_nld[MAXCH], tr_nst[MAXCH];  // per base loop: its direct loads / stores (one access group)
+  int64_t tr_c_hi[MAXCH], tr_c_hl[MAXCH];  // cycles of [group body + counter init] / [group body + latch]
   int32_t n_terms;
   DTerm term[MAXTERM];
 };
@@ -1372,6 +1380,428 @@ __global__ void build_sdt_kernel(const DTask* __restrict__ g, const int32_t* __r
   tab[e] = (uint32_t)F;
 }
 
+// ---------------------------------------------------------------------------
+// General trees: imperfect nests, sibling loops, accesses at
+// any level; Tile / Reorder / Parallel transforms (Unroll / Vectorize and
+// unrolled or vector base loops stay outside the device class).  One thread
+// per candidate; the transformed tree lives in the thread's local memory.
+// ---------------------------------------------------------------------------
+constexpr int TR_N = 32;  // unified node ids: accesses, then loops (<= 16 each)
+
+struct TreeCand {
+  int8_t par[TR_N], first[TR_N], nxt[TR_N];
+  int8_t ord[TR_N];                 // preorder of all nodes
+  uint8_t pre[TR_N], pend[TR_N];    // preorder position, end of the subtree
+  uint8_t dep[TR_N];
+  uint8_t hs[NSLOT], hf[NSLOT];     // per loop j (node tr_na + j): var slot, flags
+  int32_t he[NSLOT], hst[NSLOT];    //   extent, step
+  int8_t grp[NSLOT];                //   access group (base loop id) hanging under it, -1 none
+  int8_t nos[NSLOT];                // loop j of each var slot, -1 none
+  int nl, nn, root;
+};
+
+// apply_schedule on the tree (ls/ir.py:361-474), same checks in the same order
+__device__ int tree_apply(const DTask& T, const ls_record& r, TreeCand& c) {
+  const int na = T.tr_na;
+  c.nl = T.tr_nl;
+  c.root = T.tr_root_first;
+  for (int i = 0; i < na + c.nl; ++i) {
+    c.par[i] = T.tr_parent[i];
+    c.first[i] = T.tr_first[i];
+    c.nxt[i] = T.tr_next[i];
+  }
+  for (int v = 0; v < NSLOT; ++v) c.nos[v] = -1;
+  for (int j = 0; j < c.nl; ++j) {
+    c.hs[j] = T.base_slot[j];
+    c.he[j] = T.base_ext[j];
+    c.hst[j] = T.base_step[j];
+    c.hf[j] = T.base_flags[j];
+    c.grp[j] = (int8_t)j;
+    c.nos[T.base_slot[j]] = (int8_t)j;
+  }
+  for (int x = 0; x < T.n_xf; ++x) {
+    const DXform& xf = T.xf[x];
+    if (xf.enable_bit >= 0 && !((r.flags >> xf.enable_bit) & 1u)) continue;
+    const int j = xf.slot != NOSLOT ? c.nos[xf.slot] : -1;
+    if (xf.kind == LS_XF_TILE) {
+      if (j < 0 || xf.new_slot == NOSLOT) return LS_ST_NO_LOOP;
+      const int32_t F = xf.param >= 0 ? (int32_t)rparam(r, xf.param) : xf.value;
+      const int32_t E = c.he[j];
+      if (F < 1 || F > E) return LS_ST_TILE_RANGE;
+      if (c.nl >= NSLOT) return LS_ST_OVERFLOW;
+      const int u = c.nl++;
+      const int nj = na + j, nu = na + u;
+      c.hs[u] = xf.new_slot;
+      c.he[u] = F;
+      c.hst[u] = c.hst[j];
+      c.hf[u] = 0;
+      c.grp[u] = c.grp[j];
+      c.grp[j] = -1;
+      c.nos[xf.new_slot] = (int8_t)u;
+      c.he[j] = (E + F - 1) / F;
+      c.hst[j] *= F;
+      c.first[nu] = c.first[nj];  // the inner loop takes the children (ls/ir.py:369-381)
+      for (int ch = c.first[nu]; ch >= 0; ch = c.nxt[ch]) c.par[ch] = (int8_t)nu;
+      c.first[nj] = (int8_t)nu;
+      c.nxt[nu] = -1;
+      c.par[nu] = (int8_t)nj;
+    } else if (xf.kind == LS_XF_REORDER) {
+      const int m = xf.n_order;
+      if (m < 2) continue;
+      int8_t ids[LS_MAX_ORDER];
+      for (int q = 0; q < m; ++q) {  // find_loop of every name first (ls/ir.py:388)
+        const int nib = (int)((r.perm >> (4 * (xf.perm_shift + q))) & 0xF);
+        const int w = nib < m ? xf.order[nib] : NOSLOT;
+        if (w == NOSLOT || c.nos[w] < 0) return LS_ST_NO_LOOP;
+        ids[q] = c.nos[w];
+      }
+      uint32_t seen = 0;
+      for (int q = 0; q < m; ++q) {
+        if ((seen >> ids[q]) & 1u) return LS_ST_REORDER_MISSING;
+        seen |= 1u << ids[q];
+      }
+      // the shallowest named loop, then down through only children (chain_ok, ls/ir.py:392-402)
+      int top = -1, topd = 1 << 20;
+      for (int q = 0; q < m; ++q) {
+        int d = 0;
+        for (int a = c.par[na + ids[q]]; a >= 0; a = c.par[a]) ++d;
+        if (d < topd) topd = d, top = ids[q];
+      }
+      int8_t seq[LS_MAX_ORDER];
+      seq[0] = (int8_t)top;
+      for (int q = 1; q < m; ++q) {
+        const int cur = na + seq[q - 1];
+        const int ch = c.first[cur];
+        if (ch < 0 || c.nxt[ch] >= 0 || ch < na || !((seen >> (ch - na)) & 1u)) return LS_ST_REORDER_CHAIN;
+        seq[q] = (int8_t)(ch - na);
+      }
+      uint8_t hs[LS_MAX_ORDER], hf[LS_MAX_ORDER];
+      int32_t he[LS_MAX_ORDER], hst[LS_MAX_ORDER];
+      for (int q = 0; q < m; ++q) hs[q] = c.hs[ids[q]], hf[q] = c.hf[ids[q]], he[q] = c.he[ids[q]], hst[q] = c.hst[ids[q]];
+      for (int q = 0; q < m; ++q) {  // position q of the chain takes the header of order[q] (ls/ir.py:406-412)
+        const int j2 = seq[q];
+        c.hs[j2] = hs[q], c.hf[j2] = hf[q], c.he[j2] = he[q], c.hst[j2] = hst[q];
+        c.nos[hs[q]] = (int8_t)j2;
+      }
+    } else if (xf.kind == LS_XF_PARALLEL) {
+      if (j < 0) return LS_ST_NO_LOOP;
+      c.hf[j] |= F_PAR;
+    } else {
+      return LS_ST_UNSUPPORTED;
+    }
+  }
+  // preorder numbering, depths, subtree ends
+  c.nn = na + c.nl;
+  int idx = 0, n = c.root, d = 0;
+  while (n >= 0) {
+    c.pre[n] = (uint8_t)idx;
+    c.ord[idx++] = (int8_t)n;
+    c.dep[n] = (uint8_t)d;
+    if (n >= na && c.first[n] >= 0) {
+      n = c.first[n];
+      ++d;
+      continue;
+    }
+    while (n >= 0) {
+      c.pend[n] = (uint8_t)idx;
+      if (c.nxt[n] >= 0) {
+        n = c.nxt[n];
+        break;
+      }
+      n = c.par[n];
+      --d;
+    }
+  }
+  return LS_OK;
+}
+
+// expr_range (ls/cache.py:80-96) with the loops of `L`'s subtree expanded (and L itself when full)
+__device__ __forceinline__ SI tree_expr_range(const DTask& T, const DExpr& e, const TreeCand& c, uint32_t flags,
+                                              int L, bool full) {
+  SI acc;
+  acc.lo = acc.hi = e.konst;
+  acc.stride = 0;
+  acc.count = 1;
+  acc.exact = 1;
+  const int na = T.tr_na;
+  for (int k = 0; k < e.nt; ++k) {
+    const DTerm& tm = T.term[e.t0 + k];
+    if (!present(tm, flags)) continue;
+    const int j = c.nos[tm.slot];
+    if (j < 0) continue;
+    const int nd = na + j;
+    const bool in = (c.pre[nd] > c.pre[L] && c.pre[nd] < c.pend[L]) || (full && nd == L);
+    if (!in) continue;
+    const int32_t E = c.he[j];
+    if (E == 1) continue;
+    const int32_t dd = tm.coef * c.hst[j];
+    SI s;
+    s.lo = dd > 0 ? 0 : dd * (E - 1);
+    s.hi = dd > 0 ? dd * (E - 1) : 0;
+    s.stride = abs(dd);
+    s.count = E;
+    s.exact = 1;
+    acc = si_sum(acc, s);
+  }
+  return acc;
+}
+
+// tensor_footprint (ls/cache.py:117-130): the union of the accesses of tensor t
+// under loop node L in DFS order, product over dimensions
+__device__ int64_t tree_footprint(const DTask& T, const TreeCand& c, uint32_t flags, int L, int t, bool full) {
+  int64_t card = 1;
+  for (int rr = 0; rr < T.t_rank[t]; ++rr) {
+    SI u;
+    bool any = false;
+    for (int q = c.pre[L] + 1; q < c.pend[L]; ++q) {
+      const int a = c.ord[q];
+      if (a >= T.tr_na || T.acc_tensor[a] != t) continue;
+      const SI x = tree_expr_range(T, T.expr[a][rr], c, flags, L, full);
+      u = any ? si_union(u, x) : x;
+      any = true;
+    }
+    card *= u.count;
+  }
+  return card;
+}
+
+__device__ int eval_tree(const DTask& T, const ls_record& r, double* f, double* score) {
+  TreeCand c;
+  const int st = tree_apply(T, r, c);
+  if (st) return st;
+  const int na = T.tr_na, nT = T.n_tensors;
+  const uint32_t flags = r.flags;
+  const int64_t cap = T.cap;
+  // ---- movement model (ls/cache.py:133-236), loops in reverse preorder (children first)
+  int64_t dm[NSLOT][MAXT];
+  uint8_t rb[NSLOT], pres[NSLOT];
+  for (int q = c.nn - 1; q >= 0; --q) {
+    const int L = c.ord[q];
+    if (L < na) continue;
+    const int j = L - na;
+    int64_t m_dm[MAXT];
+    uint32_t m_pres = 0, m_reuse = 0xFFu;
+    for (int t = 0; t < nT; ++t) m_dm[t] = 0;
+    for (int ch = c.first[L]; ch >= 0; ch = c.nxt[ch]) {
+      if (ch < na) {
+        const int t = T.acc_tensor[ch];
+        m_pres |= 1u << t;
+        m_dm[t] += 1;
+      } else {
+        const int k = ch - na;
+        for (int t = 0; t < nT; ++t)
+          if ((pres[k] >> t) & 1u) {
+            m_pres |= 1u << t;
+            m_dm[t] += dm[k][t];
+            if (!((rb[k] >> t) & 1u)) m_reuse &= ~(1u << t);
+          }
+      }
+    }
+    int64_t single = 0, ffull[MAXT];
+    uint32_t uses = 0;
+    for (int t = 0; t < nT; ++t) {
+      if (!((m_pres >> t) & 1u)) continue;
+      single += tree_footprint(T, c, flags, L, t, false);
+      ffull[t] = tree_footprint(T, c, flags, L, t, true);
+      for (int q2 = c.pre[L] + 1; q2 < c.pend[L]; ++q2) {  // any access of t indexed by this loop's variable
+        const int a = c.ord[q2];
+        if (a >= na || T.acc_tensor[a] != t) continue;
+        for (int rr = 0; rr < T.t_rank[t]; ++rr) {
+          const DExpr& e = T.expr[a][rr];
+          for (int k = 0; k < e.nt; ++k)
+            if (present(T.term[e.t0 + k], flags) && T.term[e.t0 + k].slot == c.hs[j]) uses |= 1u << t;
+        }
+      }
+    }
+    if (single > cap) m_reuse &= uses | ~m_pres;
+    for (int t = 0; t < nT; ++t) {
+      if (!((m_pres >> t) & 1u)) continue;
+      const int64_t per = (single <= cap || ((m_reuse >> t) & 1u)) ? ffull[t] : m_dm[t] * c.he[j];
+      if (ffull[t] > cap) m_reuse &= ~(1u << t);
+      dm[j][t] = per;
+    }
+    rb[j] = (uint8_t)m_reuse;
+    pres[j] = (uint8_t)m_pres;
+  }
+  int64_t dmov = 0;
+  for (int n = c.root; n >= 0; n = c.nxt[n]) {
+    if (n < na) {
+      dmov += 1;
+    } else {
+      for (int t = 0; t < nT; ++t)
+        if ((pres[n - na] >> t) & 1u) dmov += dm[n - na][t];
+    }
+  }
+  // ---- emitted code (ls/ir.py:557-659): every loop branches; W = trips of the enclosing loops
+  int64_t W[NSLOT], Wp[NSLOT];
+  uint8_t height[NSLOT];
+  for (int q = c.nn - 1; q >= 0; --q) {  // subtree heights: PTX counter registers repeat every 8 depths
+    const int L = c.ord[q];
+    if (L < na) continue;
+    int h = 0;
+    for (int ch = c.first[L]; ch >= 0; ch = c.nxt[ch])
+      if (ch >= na) h = max(h, height[ch - na] + 1);
+    height[L - na] = (uint8_t)h;
+  }
+  int64_t nld = 0, nst = 0, ilp = 0, ptx_loops = 0, wld = 0, wst = 0;
+  const int64_t* ic = T.ptx_icost;
+  int ntop = 0;
+  for (int q = 0; q < c.nn; ++q) {
+    const int L = c.ord[q];
+    if (L < na) continue;
+    const int j = L - na, p = c.par[L];
+    const int64_t Wpar = p >= 0 ? W[p - na] : 1, Wppar = p >= 0 ? Wp[p - na] : 1;
+    W[j] = Wpar * c.he[j];
+    Wp[j] = Wppar * (height[j] >= 8 ? 1 : c.he[j]);  // no trip when a loop sits 8 deeper (ls/ptx.py:163-169)
+    if (p < 0) ++ntop;
+    const int g = c.grp[j];
+    const int64_t gl = g >= 0 ? T.tr_nld[g] : 0, gs = g >= 0 ? T.tr_nst[g] : 0;
+    nld += gl * W[j];
+    nst += gs * W[j];
+    wld += gl * Wp[j];
+    wst += gs * Wp[j];
+    int nch = 0;
+    for (int ch = c.first[L]; ch >= 0; ch = c.nxt[ch]) nch += ch >= na;
+    if (T.family == LS_FAMILY_CPU) {
+      // header block [group body + first child's init | own latch] x W, then between
+      // consecutive child loops one init block and after the last one the latch block
+      const int64_t hdr = nch ? (g >= 0 ? T.tr_c_hi[g] : T.c_init) : (g >= 0 ? T.tr_c_hl[g] : T.c_latch);
+      ilp += hdr * W[j];
+      if (nch) ilp += T.c_init * (nch - 1) + T.c_latch;
+    } else {
+      ptx_loops += ic[LS_I_INIT] * Wppar + (ic[LS_I_ADD] + ic[LS_I_CMP] + ic[LS_I_BRANCH]) * Wp[j];
+    }
+  }
+  int nf;
+  if (T.family == LS_FAMILY_CPU) {
+    ilp += T.c_init * ntop + T.c_ret;  // the top-level init blocks and `ret`
+    f[0] = (double)nst;
+    f[1] = (double)nld;
+    f[2] = (double)nst;
+    f[3] = (double)dmov;
+    f[4] = (double)ilp;
+    nf = LS_NFEAT_CPU;
+  } else {
+    double work;
+    if (T.costs_integral) {
+      work = (double)(ptx_loops + wld * ic[LS_I_LOAD] + wst * (ic[LS_I_FMA] + ic[LS_I_STORE]) + ic[LS_I_RET]);
+    } else {  // thread_cycles in line order (ls/ptx.py:225-235): enter / exit events of a DFS
+      const double* pc = T.ptx_cost;
+      work = 0.0;
+      int n = c.root;
+      while (n >= 0) {
+        if (n >= na) {
+          const int j = n - na, p = c.par[n];
+          work = rn_add(work, rn_mul(pc[LS_I_INIT], (double)(p >= 0 ? Wp[p - na] : 1)));
+          const int g = c.grp[j];
+          const double w = (double)Wp[j];
+          if (g >= 0) {
+            for (int a = 0; a < T.tr_nld[g]; ++a) work = rn_add(work, rn_mul(pc[LS_I_LOAD], w));
+            for (int a = 0; a < T.tr_nst[g]; ++a) {
+              work = rn_add(work, rn_mul(pc[LS_I_FMA], w));
+              work = rn_add(work, rn_mul(pc[LS_I_STORE], w));
+            }
+          }
+          int ch = c.first[n];
+          while (ch >= 0 && ch < na) ch = c.nxt[ch];  // first child loop
+          if (ch >= 0) {
+            n = ch;
+            continue;
+          }
+        }
+        // leave n (its latch) and climb until a next sibling loop exists
+        while (n >= 0) {
+          if (n >= na) {
+            const double w = (double)Wp[n - na];
+            work = rn_add(work, rn_mul(pc[LS_I_ADD], w));
+            work = rn_add(work, rn_mul(pc[LS_I_CMP], w));
+            work = rn_add(work, rn_mul(pc[LS_I_BRANCH], w));
+          }
+          int s2 = c.nxt[n];
+          while (s2 >= 0 && s2 < na) s2 = c.nxt[s2];
+          if (s2 >= 0) {
+            n = s2;
+            break;
+          }
+          n = c.par[n];
+        }
+      }
+      work = rn_add(work, pc[LS_I_RET]);
+    }
+    double smem = 0.0;
+    if (T.has_shared) {  // smem_ops_feature (ls/ptx.py:310-327): vol = product of the enclosing extents
+      for (int q = 0; q < c.nn; ++q) {
+        const int a = c.ord[q];
+        if (a >= na || !T.t_shared[T.acc_tensor[a]]) continue;
+        const int p = c.par[a];
+        const int64_t vol = p >= 0 ? W[p - na] : 1;
+        // tid: `tid`, else the last preorder parallel loop indexing the access (ls/ptx.py:298-307)
+        uint32_t used = 0;
+        const int t = T.acc_tensor[a];
+        for (int rr = 0; rr < T.t_rank[t]; ++rr) {
+          const DExpr& e = T.expr[a][rr];
+          for (int k = 0; k < e.nt; ++k)
+            if (present(T.term[e.t0 + k], flags)) used |= 1u << T.term[e.t0 + k].slot;
+        }
+        int tid = -1;
+        if (T.tid_slot >= 0 && ((used >> T.tid_slot) & 1u)) {
+          tid = T.tid_slot;
+        } else {
+          for (int q2 = 0; q2 < c.nn; ++q2) {
+            const int L = c.ord[q2];
+            if (L >= na && (c.hf[L - na] & F_PAR) && ((used >> c.hs[L - na]) & 1u)) tid = c.hs[L - na];
+          }
+        }
+        int64_t best = 1;
+        if (tid >= 0 && c.nos[tid] >= 0) {
+          const int lanes = min(T.warp_size, c.he[c.nos[tid]]);
+          int64_t A = 0, B = 0;
+          for (int rr = 0; rr < T.t_rank[t]; ++rr) {
+            const DExpr& e = T.expr[a][rr];
+            int64_t ct = 0;
+            for (int k = 0; k < e.nt; ++k) {
+              const DTerm& tm = T.term[e.t0 + k];
+              if (present(tm, flags) && tm.slot == tid) ct += tm.coef;
+            }
+            A += (int64_t)e.konst * T.t_stride[t][rr];
+            B += ct * T.t_stride[t][rr];
+          }
+          uint8_t cnt[64];
+          for (int b = 0; b < T.banks; ++b) cnt[b] = 0;
+          int64_t prev = 0;
+          best = 0;
+          for (int l = 0; l < lanes; ++l) {
+            const int64_t num = (A + B * l) * T.t_eb[t];
+            const int64_t w = num >= 0 ? num / 4 : -((-num + 3) / 4);
+            if (l == 0 || w != prev) {
+              int64_t b = w % T.banks;
+              if (b < 0) b += T.banks;
+              best = max(best, (int64_t)++cnt[b]);
+            }
+            prev = w;
+          }
+        }
+        smem = rn_add(smem, (double)(vol * best));
+      }
+    }
+    f[0] = work;
+    f[1] = T.sm_underuse;
+    f[2] = T.warp_slack;
+    f[3] = smem;
+    f[4] = (double)wst;
+    f[5] = (double)wld;
+    f[6] = (double)wst;
+    nf = LS_NFEAT_GPU;
+  }
+  double total = 0.0;
+  for (int q = 0; q < nf; ++q) {
+    if (!(f[q] >= 0.0) || isinf(f[q])) return LS_ST_BAD_FEATURE;
+    total = rn_add(total, rn_mul(T.coef[q], f[q]));
+  }
+  *score = total;
+  return LS_OK;
+}
+
 // Per reorder choice: the transformed chain and the status of apply_fast with
 // every tile factor 1 (always in range), i.e. what the reorder alone decides.
 __global__ void build_pchain_kernel(const DTask* __restrict__ g, int32_t pax, uint64_t* __restrict__ chain,
@@ -1485,7 +1915,7 @@ __device__ __forceinline__ void stage_task(DTask& s, const DTask* __restrict__ g
 // in global memory (L1/L2 resident), 2 tabulated with the table in shared memory.
 template <int MODE>
 __device__ __forceinline__ const int32_t* stage_tab(unsigned char* where, const DTask& T) {
-  if constexpr (MODE == 2 || MODE >= 4) {
+  if constexpr (MODE == 2 || MODE == 4 || MODE == 5) {
     int32_t* dst = reinterpret_cast<int32_t*>(where);
     const int32_t* src = MODE == 2 ? T.tab : T.sd_tab;
     const int len = MODE == 2 ? T.tab_len : T.sd_len;
@@ -1499,10 +1929,12 @@ __device__ __forceinline__ const int32_t* stage_tab(unsigned char* where, const 
 
 __host__ __device__ inline size_t tab_smem_bytes(int mode, const DTask& T) {
   return mode == 2 ? align16(sizeof(int32_t) * (size_t)T.tab_len)
-                   : mode >= 4 ? align16(sizeof(int32_t) * (size_t)T.sd_len) : 0;
+                   : (mode == 4 || mode == 5) ? align16(sizeof(int32_t) * (size_t)T.sd_len) : 0;
 }
 __host__ __device__ inline size_t state_bytes(int mode, int n_slots, int n_chain, int n_stage) {
-  return mode == 0 ? cand_bytes(n_slots, n_chain, n_stage) : align16(sizeof(int32_t) * (size_t)n_slots * TPB);
+  return mode == 0   ? cand_bytes(n_slots, n_chain, n_stage)
+         : mode == 6 ? 0  // the tree path keeps its state in local memory
+                     : align16(sizeof(int32_t) * (size_t)n_slots * TPB);
 }
 
 template <int TM, int RM, int MODE>
@@ -1520,6 +1952,8 @@ struct Evaluator {
                                             double* f, double* s) {
     if constexpr (MODE == 0)
       return eval_candidate<TM, RM>(T, r, c, f, s);
+    else if constexpr (MODE == 6)
+      return eval_tree(T, r, f, s);
     else if constexpr (MODE == 3)
       return eval_tensor<TM>(T, r, kt, fc, f, s);
     else
@@ -1549,7 +1983,7 @@ __device__ __forceinline__ int load_cand(const DTask& T, const void* __restrict_
   }
 }
 
-constexpr int min_blocks(int tm, int rm, int mode) { return mode == 5 ? 3 : mode ? 3 : (tm * rm <= 16 ? 3 : 1); }
+constexpr int min_blocks(int tm, int rm, int mode) { return mode == 6 ? 1 : mode ? 3 : (tm * rm <= 16 ? 3 : 1); }
 
 template <int TM, int RM, int MODE, int SRC>
 __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE))
@@ -1569,7 +2003,7 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE))
     double f[LS_NFEAT_GPU];
     double s = 0.0;
     int st;
-    if constexpr (MODE >= 4) {
+    if constexpr (MODE == 4 || MODE == 5) {
       st = eval_space<TM, MODE == 5>(T, tab, load_point(src, pbytes, i), ev.fc, f, &s);
     } else {
       uint32_t pch = 0;
@@ -2094,7 +2528,7 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kern
   const int64_t b0 = min(n, (int64_t)blockIdx.x * per), b1 = min(n, b0 + per);
   const int64_t stride = TPB;
   uint64_t xn = 0;  // space path: the next point, loaded one iteration ahead
-  if constexpr (MODE >= 4)
+  if constexpr (MODE == 4 || MODE == 5)
     if (b0 + threadIdx.x < b1) xn = load_point(src, pbytes, b0 + threadIdx.x);
   for (int64_t base = b0; base < b0 + per; base += stride) {
     const int64_t i = base + threadIdx.x;
@@ -2106,7 +2540,7 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kern
       double f[LS_NFEAT_GPU];
       double s;
       int st;
-      if constexpr (MODE >= 4) {
+      if constexpr (MODE == 4 || MODE == 5) {
         const uint64_t x = xn;
         if (i + stride < b1) xn = load_point(src, pbytes, i + stride);
         st = eval_space<TM, MODE == 5>(T, tab, x, ev.fc, f, &s);
@@ -2602,18 +3036,31 @@ int build_task(const ls_task_desc& d, DTask& T, std::vector<int>& load_t, std::v
   if (!((d.family == LS_FAMILY_CPU && (d.target == LS_TARGET_X86 || d.target == LS_TARGET_AARCH64)) ||
         (d.family == LS_FAMILY_GPU && d.target == LS_TARGET_PTX)))
     return fail(LS_E_UNSUPPORTED, "family/target combination not supported");
-  // ---- perfect chain: loops 0..L-1 each the only child of the previous, accesses under the last
-  int nl = 0;
-  while (nl < d.n_nodes && d.nodes[nl].kind == LS_NODE_LOOP) {
-    if (d.nodes[nl].parent != nl - 1) return fail(LS_E_UNSUPPORTED, "program is not a perfect loop chain");
-    ++nl;
+  // ---- loops and accesses in preorder; a perfect chain (loops 0..L-1 each the only child
+  //      of the previous, every access under the last) takes the chain kernels, any other
+  //      tree the tree kernel
+  std::vector<int> loop_nodes, acc_nodes;
+  for (int i = 0; i < d.n_nodes; ++i) {
+    if (d.nodes[i].parent < -1 || d.nodes[i].parent >= i) return fail(LS_E_ARG, "nodes must be in preorder");
+    if (d.nodes[i].parent >= 0 && d.nodes[d.nodes[i].parent].kind != LS_NODE_LOOP)
+      return fail(LS_E_ARG, "parent of a node must be a loop");
+    (d.nodes[i].kind == LS_NODE_LOOP ? loop_nodes : acc_nodes).push_back(i);
   }
-  if (nl == 0 || nl > MAXCH) return fail(LS_E_UNSUPPORTED, "program is not a perfect loop chain of <= 16 loops");
-  const int na = d.n_nodes - nl;
-  if (na < 1 || na > MAXACC) return fail(LS_E_UNSUPPORTED, "innermost body must hold 1..16 accesses");
-  for (int i = nl; i < d.n_nodes; ++i)
-    if (d.nodes[i].kind != LS_NODE_ACCESS || d.nodes[i].parent != nl - 1)
-      return fail(LS_E_UNSUPPORTED, "program is not a perfect loop chain (accesses outside the innermost loop)");
+  const int nl = (int)loop_nodes.size(), na = (int)acc_nodes.size();
+  bool chain = nl >= 1;
+  for (int p = 0; p < nl && chain; ++p) chain = loop_nodes[p] == p && d.nodes[p].parent == p - 1;
+  for (int a = 0; a < na && chain; ++a) chain = d.nodes[acc_nodes[a]].parent == nl - 1;
+  T.tree = chain ? 0 : 1;
+  if (nl == 0 || nl > MAXCH) return fail(LS_E_UNSUPPORTED, "program must have 1..16 loops");
+  if (na < 1 || na > MAXACC) return fail(LS_E_UNSUPPORTED, "program must hold 1..16 accesses");
+  if (T.tree) {
+    for (int p = 0; p < nl; ++p)
+      if (d.nodes[loop_nodes[p]].unrolled || d.nodes[loop_nodes[p]].vector_width)
+        return fail(LS_E_UNSUPPORTED, "tree programs with unrolled or vector loops are outside the device class");
+    for (int x = 0; x < d.n_xforms; ++x)
+      if (d.xforms[x].kind == LS_XF_UNROLL || d.xforms[x].kind == LS_XF_VECTORIZE)
+        return fail(LS_E_UNSUPPORTED, "Unroll / Vectorize on a tree program are outside the device class");
+  }
   for (int x = 0; x < d.n_xforms; ++x) {
     const ls_xform& s = d.xforms[x];
     if (s.var >= d.n_vars || s.new_var >= d.n_vars || s.param >= LS_MAX_PARAMS || s.enable_bit >= 32 ||
@@ -2626,7 +3073,7 @@ int build_task(const ls_task_desc& d, DTask& T, std::vector<int>& load_t, std::v
   auto add_slot = [&](int v) {
     if (v >= 0 && slot_of[v] == NOSLOT) slot_of[v] = ns++;
   };
-  for (int p = 0; p < nl; ++p) add_slot(d.nodes[p].var);
+  for (int p = 0; p < nl; ++p) add_slot(d.nodes[loop_nodes[p]].var);
   for (int x = 0; x < d.n_xforms; ++x)
     if ((d.xforms[x].kind == LS_XF_TILE || d.xforms[x].kind == LS_XF_VECTORIZE) && d.xforms[x].var >= 0)
       add_slot(d.xforms[x].new_var);
@@ -2637,7 +3084,7 @@ int build_task(const ls_task_desc& d, DTask& T, std::vector<int>& load_t, std::v
   std::vector<int64_t> span(LS_MAX_VARS, 0);  // step * extent of each variable's base loop
   int ntile = 0;
   for (int p = 0; p < nl; ++p) {
-    const ls_node& n = d.nodes[p];
+    const ls_node& n = d.nodes[loop_nodes[p]];
     if (n.var < 0 || n.var >= d.n_vars || n.extent < 1 || n.step < 1 || n.extent >= (1 << 30) ||
         n.step >= (1 << 30))
       return fail(LS_E_ARG, "bad loop node");
@@ -2666,7 +3113,7 @@ int build_task(const ls_task_desc& d, DTask& T, std::vector<int>& load_t, std::v
   // (_rewrite_exprs ls/ir.py:350-358 applied for every Tile/Vectorize of the template)
   std::vector<std::vector<std::vector<HTerm>>> ex(na);
   for (int a = 0; a < na; ++a) {
-    const ls_node& n = d.nodes[nl + a];
+    const ls_node& n = d.nodes[acc_nodes[a]];
     if (n.tensor < 0 || n.tensor >= d.n_tensors) return fail(LS_E_ARG, "bad tensor index");
     const int rank = d.tensors[n.tensor].rank;
     if (rank < 1 || rank > MAXRANK) return fail(LS_E_ARG, "bad rank");
@@ -2695,7 +3142,7 @@ int build_task(const ls_task_desc& d, DTask& T, std::vector<int>& load_t, std::v
   int nt = 0;
   std::vector<std::vector<int64_t>> ebound(na, std::vector<int64_t>(MAXRANK, 0));
   for (int a = 0; a < na; ++a) {
-    const ls_node& n = d.nodes[nl + a];
+    const ls_node& n = d.nodes[acc_nodes[a]];
     T.acc_tensor[a] = (uint8_t)n.tensor;
     T.acc_store[a] = (uint8_t)n.is_store;
     for (size_t k = 0; k < ex[a].size(); ++k) {
@@ -2760,8 +3207,8 @@ int build_task(const ls_task_desc& d, DTask& T, std::vector<int>& load_t, std::v
       T.t_nacc[t]++;
       bool same = last >= 0;
       for (int k = 0; same && k < td.rank; ++k) {
-        const ls_expr& x = d.nodes[nl + a].idx[k];
-        const ls_expr& y = d.nodes[nl + last].idx[k];
+        const ls_expr& x = d.nodes[acc_nodes[a]].idx[k];
+        const ls_expr& y = d.nodes[acc_nodes[last]].idx[k];
         same = x.konst == y.konst && x.n_terms == y.n_terms &&
                memcmp(x.terms, y.terms, sizeof(ls_term) * x.n_terms) == 0;
       }
@@ -2808,7 +3255,10 @@ int build_task(const ls_task_desc& d, DTask& T, std::vector<int>& load_t, std::v
           bool have = false;
           for (int j = 0; j < nv; ++j) have |= T.dim_var[D][j] == s;
           if (have) continue;
-          if (nv >= MAXDV) return fail(LS_E_UNSUPPORTED, "more than 8 loop variables in one tensor dimension");
+          if (nv >= MAXDV) {
+            if (T.tree) break;  // the chain kernels' per-dimension stages; unused on trees
+            return fail(LS_E_UNSUPPORTED, "more than 8 loop variables in one tensor dimension");
+          }
           T.dim_var[D][nv] = (uint8_t)s;
           T.slot_dnib[s][D / 16] |= (uint64_t)(nv + 1) << (4 * (D % 16));
           ++nv;
@@ -2819,7 +3269,7 @@ int build_task(const ls_task_desc& d, DTask& T, std::vector<int>& load_t, std::v
       n_stage += nv;
     }
   }
-  if (n_stage > MAXSTAGE) return fail(LS_E_UNSUPPORTED, "too many (dimension, variable) pairs");
+  if (n_stage > MAXSTAGE && !T.tree) return fail(LS_E_UNSUPPORTED, "too many (dimension, variable) pairs");
   T.n_stage = n_stage;
   T.n_slots = ns;
   for (int q = 0; q < nt; ++q) T.has_optional |= T.term[q].req != 0;
@@ -2835,7 +3285,7 @@ int build_task(const ls_task_desc& d, DTask& T, std::vector<int>& load_t, std::v
         const int D = T.acc_tensor[a] * RM + k;
         cb[D] = std::max(cb[D], 2 * ebound[a][k] + 1);
       }
-    plan_tabulated(d, T, RM, cb);
+    if (!T.tree) plan_tabulated(d, T, RM, cb);
   }
   T.task_bytes = (int32_t)align16(offsetof(DTask, term) + sizeof(DTerm) * (size_t)nt);
   // ---- arch
@@ -2860,6 +3310,44 @@ int build_task(const ls_task_desc& d, DTask& T, std::vector<int>& load_t, std::v
     for (int q = 0; q < LS_I_COUNT; ++q)
       if (d.klass[q] < 0 || d.klass[q] >= LS_I_COUNT) return fail(LS_E_ARG, "bad class id");
     lsb::fixed_block_cycles(d, &T.c_init, &T.c_latch, &T.c_ret);
+  }
+  if (T.tree) {  // ---- the base tree over unified ids and the per-loop access groups
+    std::vector<int> id_of(d.n_nodes);
+    for (int a = 0; a < na; ++a) id_of[acc_nodes[a]] = a;
+    for (int p = 0; p < nl; ++p) id_of[loop_nodes[p]] = na + p;
+    for (int i = 0; i < 32; ++i) T.tr_parent[i] = T.tr_first[i] = T.tr_next[i] = -1;
+    T.tr_root_first = -1;
+    std::vector<int> last_child(32, -1);
+    int last_top = -1;
+    for (int i = 0; i < d.n_nodes; ++i) {  // preorder: children appear in order
+      const int id = id_of[i], par = d.nodes[i].parent;
+      const int pid = par >= 0 ? id_of[par] : -1;
+      T.tr_parent[id] = (int8_t)pid;
+      int& prev = pid >= 0 ? last_child[pid] : last_top;
+      if (prev < 0) {
+        if (pid >= 0)
+          T.tr_first[pid] = (int8_t)id;
+        else
+          T.tr_root_first = id;
+      } else {
+        T.tr_next[prev] = (int8_t)id;
+      }
+      prev = id;
+    }
+    T.tr_nl = nl;
+    T.tr_na = na;
+    for (int p = 0; p < nl; ++p) {  // the group of base loop p: its direct accesses, loads then stores
+      std::vector<int> lt, st;
+      for (int a = 0; a < na; ++a)
+        if (d.nodes[acc_nodes[a]].parent == loop_nodes[p])
+          (d.nodes[acc_nodes[a]].is_store ? st : lt).push_back(d.nodes[acc_nodes[a]].tensor);
+      T.tr_nld[p] = (uint8_t)lt.size();
+      T.tr_nst[p] = (uint8_t)st.size();
+      if (d.family == LS_FAMILY_CPU) {
+        T.tr_c_hi[p] = lsb::group_block_cycles(d, lt, st, false);
+        T.tr_c_hl[p] = lsb::group_block_cycles(d, lt, st, true);
+      }
+    }
   }
   return LS_E_OK;
 }
@@ -2914,6 +3402,7 @@ int grid_for(const ls_task* t, int64_t n, int per_sm) {
 // 0 generic, 1 tabulated (table in global memory), 2 tabulated (table in shared memory),
 // 3 tensor tables (points), 4 space-specialised (points)
 int mode_of(const ls_task* t, bool points = false) {
+  if (t->host.tree) return 6;
   if (t->path == LS_PATH_GENERIC || !t->host.fast) return 0;
   if (points && t->host.sp_ok && t->path != LS_PATH_TABULATED) return t->host.sp_narrow ? 5 : 4;
   if (points && t->host.tt_ok) return 3;
@@ -2952,6 +3441,7 @@ ScoreFn score_fn_src(const DTask& T, int mode) {
     }
     if (mode == 3) return score_kernel<4, 4, 3, 1>;
   }
+  if (mode == 6) return score_kernel<4, 4, 6, SRC>;
   if (mode == 1) return score_kernel<4, 4, 1, SRC>;
   if (mode == 2) return score_kernel<4, 4, 2, SRC>;
   return T.layout_rm == 4 ? score_kernel<4, 4, 0, SRC> : score_kernel<MAXT, MAXRANK, 0, SRC>;
@@ -2977,6 +3467,7 @@ TopkFn topk_fn_src(const DTask& T, int mode) {
     }
     if (mode == 3) return score_topk_kernel<4, 4, 3, 1>;
   }
+  if (mode == 6) return score_topk_kernel<4, 4, 6, SRC>;
   if (mode == 1) return score_topk_kernel<4, 4, 1, SRC>;
   if (mode == 2) return score_topk_kernel<4, 4, 2, SRC>;
   return T.layout_rm == 4 ? score_topk_kernel<4, 4, 0, SRC> : score_topk_kernel<MAXT, MAXRANK, 0, SRC>;
@@ -3087,13 +3578,14 @@ int ls_task_set_path(ls_task* t, int32_t path) {
 
 int ls_task_path(const ls_task* t) {
   if (!t) return LS_E_ARG;
-  return mode_of(t) ? LS_PATH_TABULATED : LS_PATH_GENERIC;
+  const int m = mode_of(t);
+  return (m >= 1 && m <= 3) ? LS_PATH_TABULATED : LS_PATH_GENERIC;
 }
 
 int ls_task_points_path(const ls_task* t) {
   if (!t) return LS_E_ARG;
   const int m = mode_of(t, true);
-  return m >= 4 ? LS_PATH_SPACE : m ? LS_PATH_TABULATED : LS_PATH_GENERIC;
+  return (m == 4 || m == 5) ? LS_PATH_SPACE : (m >= 1 && m <= 3) ? LS_PATH_TABULATED : LS_PATH_GENERIC;
 }
 
 int ls_task_destroy(ls_task* t) {
@@ -3122,6 +3614,10 @@ int ls_task_prepare_unroll(ls_task* t, const int64_t* u, int32_t n) {
 int ls_collect_unroll(ls_task* t, const ls_record* d_records, int64_t n, int64_t* h_values, int32_t cap,
                       int32_t* h_count, void* stream) {
   if (!t || !h_values || !h_count || cap < 1) return fail(LS_E_ARG, "bad argument");
+  if (t->host.tree) {  // no Unroll on the tree path: nothing to prepare
+    *h_count = 0;
+    return LS_E_OK;
+  }
   CUDA_TRY(cudaSetDevice(t->device));
   cudaStream_t s = (cudaStream_t)stream;
   const int slots = 4096;

@@ -97,7 +97,7 @@ template <int TM, int RM, int MODE>
 __device__ __forceinline__ int score_point(const DTask& T, const int32_t* tab, Evaluator<TM, RM, MODE>& ev,
                                            uint64_t x, double* s) {
   double f[LS_NFEAT_GPU];
-  if constexpr (MODE >= 4) {
+  if constexpr (MODE == 4 || MODE == 5) {
     return eval_space<TM, MODE == 5>(T, tab, x, ev.fc, f, s);
   } else {
     ls_record r;
@@ -278,6 +278,7 @@ EsGenFn es_gen_fn(const DTask& T, int mode) {
       default: return es_gen_kernel<4, 4, 5>;
     }
   }
+  if (mode == 6) return es_gen_kernel<4, 4, 6>;
   if (mode == 3) return es_gen_kernel<4, 4, 3>;
   if (mode == 2) return es_gen_kernel<4, 4, 2>;
   if (mode == 1) return es_gen_kernel<4, 4, 1>;

@@ -341,33 +341,53 @@ def failure_message(program, schedule) -> "tuple[str, str] | None":
     The device reports a failed candidate as a status code; the text the
     reference's exception carries (ls/ir.py:151, 361-470) is rebuilt here for
     the diagnostics of a failed candidate only, by replaying the transforms
-    over the loop names and extents of a perfect chain (the device class).
-    Scores and features always come from the device.
+    over the loop names, extents and nesting of the program tree.  Scores and
+    features always come from the device.
     """
-    chain = []  # [name, extent] outermost first
-    node = program.body
-    while len(node) == 1 and type(node[0]).__name__ == "LoopNode":
-        chain.append([node[0].var, node[0].extent])
-        node = node[0].children
-    names = {v for v, _ in chain}
+    # loop tree: name -> [extent, parent name | None, [child names and access markers]]
+    loops = {}
+    top = []
+
+    def add(n, parent):
+        if type(n).__name__ != "LoopNode":
+            return None
+        loops[n.var] = [n.extent, parent, []]
+        for ch in n.children:
+            nm = add(ch, n.var)
+            loops[n.var][2].append(nm if nm is not None else "<access>")
+        return n.var
+
+    for n in program.body:
+        nm = add(n, None)
+        top.append(nm if nm is not None else "<access>")
+    names = set(loops)
 
     def find(v):
-        for j, (name, _) in enumerate(chain):
-            if name == v:
-                return j
-        raise ProgramError(f"no loop named {v!r}")
+        if v not in loops:
+            raise ProgramError(f"no loop named {v!r}")
+        return loops[v]
 
     def tile(v, factor):
-        j = find(v)
-        ext = chain[j][1]
+        node = find(v)
+        ext = node[0]
         if factor < 1 or factor > ext:
             raise ProgramError(f"tile factor {factor} out of range for loop {v!r} (extent {ext})")
         inner = v + "_i"
         while inner in names:
             inner += "_"
         names.add(inner)
-        chain[j][1] = -(-ext // factor)
-        chain.insert(j + 1, [inner, factor])
+        loops[inner] = [factor, v, node[2]]
+        for ch in node[2]:
+            if ch in loops:
+                loops[ch][1] = inner
+        node[0] = -(-ext // factor)
+        node[2] = [inner]
+
+    def depth(v):
+        d, p = 0, loops[v][1]
+        while p is not None:
+            d, p = d + 1, loops[p][1]
+        return d
 
     try:
         for t in schedule.transforms:
@@ -375,7 +395,7 @@ def failure_message(program, schedule) -> "tuple[str, str] | None":
             if kind == "Tile":
                 tile(t.loop, t.factor)
             elif kind == "Vectorize":
-                ext = chain[find(t.loop)][1]
+                ext = find(t.loop)[0]
                 if ext % t.width != 0:
                     raise ProgramError(f"vectorize width {t.width} does not divide extent {ext} of {t.loop!r}")
                 tile(t.loop, t.width)
@@ -383,14 +403,35 @@ def failure_message(program, schedule) -> "tuple[str, str] | None":
                 order = tuple(t.order)
                 if len(order) < 2:
                     continue
-                pos = [find(v) for v in order]
+                for v in order:
+                    find(v)
                 if len(set(order)) != len(order):
                     raise ProgramError(f"reorder {order!r}: missing loops")
-                if max(pos) - min(pos) != len(order) - 1:
-                    raise ProgramError(f"reorder {order!r}: loops do not form a perfect nest chain")
-                lo = min(pos)
-                seg = {v: e for v, e in chain[lo:lo + len(order)]}
-                chain[lo:lo + len(order)] = [[v, seg[v]] for v in order]
+                cur = min(order, key=depth)  # stable: the first shallowest name
+                for _ in range(len(order) - 1):
+                    kids = loops[cur][2]
+                    if len(kids) != 1 or kids[0] not in order:
+                        raise ProgramError(f"reorder {order!r}: loops do not form a perfect nest chain")
+                    cur = kids[0]
+                # headers move, the structure stays: extents follow the names
+                seq = [min(order, key=depth)]
+                for _ in range(len(order) - 1):
+                    seq.append(loops[seq[-1]][2][0])
+                ext = {v: loops[v][0] for v in order}
+                kids_of_last = loops[seq[-1]][2]
+                parent_of_first = loops[seq[0]][1]
+                for i, v in enumerate(order):
+                    loops[v][0] = ext[v]
+                    loops[v][1] = parent_of_first if i == 0 else order[i - 1]
+                    loops[v][2] = [order[i + 1]] if i + 1 < len(order) else kids_of_last
+                for ch in kids_of_last:
+                    if ch in loops:
+                        loops[ch][1] = order[-1]
+                if parent_of_first is not None:
+                    pk = loops[parent_of_first][2]
+                    pk[pk.index(seq[0])] = order[0]
+                else:
+                    top[top.index(seq[0])] = order[0]
             else:  # Unroll / Parallel: existence only
                 find(t.loop)
     except ProgramError as e:

@@ -119,3 +119,27 @@ def test_emit_text_byte_identical():
         d = g.template.desc(arch_named("nvidia-volta"), launch())
         tgt = abi.TARGET[c["target"]]
         assert pyoracle.emit_text(d, g.records[0], tgt) == c["text"], (c["program"], c["schedule"])
+
+
+def test_oracle_scheduled_trees():
+    """The C oracle on scheduled tree programs == the reference (tests/golden/tree_rank.json)."""
+    import json
+    from golden_util import GOLDEN, arch_named, launch, status_of_error
+    from paper_2104_14641_b200 import ir
+    from paper_2104_14641_b200.pack import pack_schedules
+    tr = json.loads((GOLDEN / "tree_rank.json").read_text())
+    for case in tr["cases"]:
+        prog = ir.parse_program(json.dumps(tr["programs"][case["program"]]))
+        scheds = [ir.Schedule.from_json(s) for s in case["schedules"]]
+        groups = pack_schedules(prog, scheds)
+        for a, res in case["results"].items():
+            arch = arch_named(a)
+            for g in groups:
+                assert g.template is not None
+                s, f, st = pyoracle.evaluate(g.template.desc(arch, launch()), g.records)
+                for j, i in enumerate(g.index):
+                    want = status_of_error(res["errors"][i])
+                    assert st[j] == want, (case["program"], a, i)
+                    if want == 0:
+                        assert s[j] == res["scores"][i]
+                        assert f[j].tolist() == res["features"][i]
