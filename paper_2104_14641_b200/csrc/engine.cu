@@ -2039,6 +2039,9 @@ __device__ __forceinline__ double from_order_bits(unsigned long long o) {
 }
 
 constexpr int TK_MAXK = 1024;
+#ifndef TOPK_CAP_SMALL
+#define TOPK_CAP_SMALL 1
+#endif
 
 // Block top-k state in shared memory: header + a key buffer of `cap` keys
 // (cap = 1024 or 2048, <= 8 per thread).  The buffer is an unsorted multiset of
@@ -3413,7 +3416,7 @@ size_t smem_score(const DTask& T, int mode) {
   return (size_t)T.task_bytes + tab_smem_bytes(mode, T) + state_bytes(mode, T.n_slots, T.n_chain, T.n_stage);
 }
 // the fused kernel's buffer must hold k plus one round of inserts
-int topk_buf(int k) { return k <= 1024 - TPB ? 1024 : 2048; }
+int topk_buf(int k) { return TOPK_CAP_SMALL && k <= 1024 - TPB ? 1024 : 2048; }
 size_t smem_topk(const DTask& T, int k, int mode) { return smem_score(T, mode) + align16(topk_state_bytes(topk_buf(k))); }
 
 using ScoreFn = void (*)(const DTask*, const void*, int, int64_t, double*, double*, int32_t*);
