@@ -1271,10 +1271,11 @@ __device__ int eval_space(const DTask& T, const int32_t* __restrict__ sdt, uint6
   }
   const W cap = (W)T.cap;
   const bool cpu = T.family == LS_FAMILY_CPU;
-  int64_t P = 1, H = 0;  // product of all extents; Horner sum of the outer prefix products
+  const int wrap = cpu ? -1 : n - 9;  // PTX: no trip for loops 8+ levels above the innermost
+  W P = 1, H = 0;  // product of all extents; Horner sum of the outer prefix products (NARROW: < 2^32 proven)
   for (int p = n - 1; p >= 0; --p) {
     const int v = (int)((chain >> (4 * p)) & 15u);
-    const int64_t E = c.E(v);
+    const int32_t E = c.E(v);
     mall |= T.vb8[v];
     W single = 0;
 #pragma unroll
@@ -1292,7 +1293,7 @@ __device__ int eval_space(const DTask& T, const int32_t* __restrict__ sdt, uint6
       ru[t] = r0 && !(Ff > cap);
       Fb[t] = Ff;
     }
-    const int64_t Ee = (cpu || p + 8 > n - 1) ? E : 1;  // PTX: no trip 8+ levels above the innermost
+    const W Ee = p > wrap ? (W)E : (W)1;
     if (p < n - 1) H = Ee * (1 + H);
     P *= Ee;
   }
@@ -3920,7 +3921,8 @@ int ls_task_set_space(ls_task* t, const ls_space_desc* sp) {
           const double K = std::pow((double)t->host.t_nu[q], (double)t->host.t_rank[q]);
           if (std::max((double)t->host.t_nacc[q], K) * std::pow(prod, (double)m) >= 4294967295.0) fits = false;
         }
-        t->host.sp_narrow = fits && fsum < 4294967295.0;
+        // the Horner sum of the prefix products is <= (chain length) * P
+        t->host.sp_narrow = fits && fsum < 4294967295.0 && prod * (t->host.sp_nchain + 1) < 4294967295.0;
       }
       t->host.sp_chain = dch;
       t->host.sp_pstat = dst;

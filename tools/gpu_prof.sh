@@ -1,6 +1,6 @@
 # ncu --set full (with source) of one fused points kernel; $1 = template args regex, e.g. "3, .int.4, .int.4"
-SEL=${1:-"3, .int.4, .int.4"}
-TAG=${2:-m4}
+SEL=${1:-"3, .int.4, .int.5"}
+TAG=${2:-m5}
 set -x
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
 timeout 600 ncu --set full --import-source on --clock-control none --kernel-name-base demangled \
