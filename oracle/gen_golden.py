@@ -442,8 +442,8 @@ def es_fixture():
     print(f"es: {len(runs)} optimize runs")
 
 
-def random_tree_schedule(rng: random.Random, prog):
-    """A random Tile / Reorder / Parallel list on a tree program, valid or not."""
+def random_tree_schedule(rng: random.Random, prog, inline=False):
+    """A random Tile / Reorder / Parallel (+ Unroll / Vectorize) list on a tree program, valid or not."""
     loops = {lp.var: lp for lp in prog.loops()}
     ext = {v: lp.extent for v, lp in loops.items()}
     kids = {v: [c.var if hasattr(c, "var") else None for c in lp.children] for v, lp in loops.items()}
@@ -477,6 +477,26 @@ def random_tree_schedule(rng: random.Random, prog):
             sched.append({"reorder": seg})
     for v in rng.sample(list(kids), rng.randint(0, min(2, len(kids)))):
         sched.append({"parallel": {"loop": v}})
+    if inline:
+        for v in rng.sample(list(kids), rng.randint(0, min(2, len(kids)))):
+            r = rng.random()
+            if r < 0.5 and ext[v] <= 8:
+                sched.append({"unroll": {"loop": v}})
+            elif r < 0.9:
+                e = ext[v]
+                w = rng.choice([d for d in (1, 2, 4, 8) if e % d == 0] + ([3] if rng.random() < 0.2 else []))
+                if rng.random() < 0.05:
+                    w = 0
+                sched.append({"vectorize": {"loop": v, "width": w}})
+                inner = v + "_i"
+                while inner in kids:
+                    inner += "_"
+                kids[inner] = kids[v]
+                kids[v] = [inner]
+                ext[inner] = max(w, 1)
+                ext[v] = math.ceil(e / max(w, 1))
+            else:
+                sched.append({"unroll": {"loop": v}})
     return sched
 
 
@@ -522,6 +542,35 @@ def tree_rank_fixture(n_per=60, seed=77):
             r["errors"] = [o[2] for o in outs]
     (OUT / "tree_rank.json").write_text(json.dumps({"programs": progs, "cases": cases}, separators=(",", ":")))
     print(f"tree_rank: {len(jobs)} evaluations")
+    # Unroll / Vectorize on trees (inlined loops: the emission replay path), incl. unrolled base loops
+    small = {k: v for k, v in progs.items() if k in ("two_mm_16_4", "interposed", "trace_layout", "mixed_levels",
+                                                    "deep_branch") or k in ("random_nest_0", "random_nest_1",
+                                                                             "random_nest_2", "random_nest_3")}
+    ub = H.build([H.tensor("A", [8, 8]), H.tensor("B", [8])],
+                 [H.loop("i", 4, [H.acc("B", "load", ["i"]),
+                                  H.loop("j", 2, [H.acc("A", "load", ["i", "j"]),
+                                                  H.loop("k", 3, [H.acc("A", "store", ["k", "j"])])],
+                                         attrs=("unroll",)),
+                                  H.loop("m", 4, [H.acc("B", "store", ["m"])])])])
+    small["unrolled_base"] = json.loads(serialize_program(ub))
+    cases2, jobs2 = [], []
+    for pname, spec in small.items():
+        prog = L.parse_program(json.dumps(spec))
+        scheds = [[]] + [random_tree_schedule(rng, prog, inline=True) for _ in range(n_per)]
+        cases2.append({"program": pname, "schedules": scheds, "results": {a: {} for a in arches}})
+        for a in arches:
+            jobs2.extend((json.dumps(spec), sch, a) for sch in scheds)
+    res = run_pool(jobs2)
+    k = 0
+    for c in cases2:
+        for a, r in c["results"].items():
+            outs = res[k:k + len(c["schedules"])]
+            k += len(c["schedules"])
+            r["scores"] = [o[0] for o in outs]
+            r["features"] = [o[1] for o in outs]
+            r["errors"] = [o[2] for o in outs]
+    (OUT / "tree_inline.json").write_text(json.dumps({"programs": small, "cases": cases2}, separators=(",", ":")))
+    print(f"tree_inline: {len(jobs2)} evaluations")
 
 
 def cli_fixture():

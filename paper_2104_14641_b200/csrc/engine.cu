@@ -183,6 +183,9 @@ struct __align__(16) DTask {
   // ---- general trees: unified node ids, accesses 0..tr_na-1 (preorder), loops
   //      tr_na + j for base loop j (preorder; header j = base_slot/ext/step/flags[j]), tile loops after
   int32_t tree, tr_nl, tr_na, tr_root_first;
+  int32_t tr_inline, tr_target, tr_dialect, tr_issue;  // inlined (unrolled / vector) loops possible: emulated emission
+  int32_t tr_lat[LS_I_COUNT], tr_klass[LS_I_COUNT], tr_ucap[LS_I_COUNT];  // schedule_block tables (ls/ilp.py:18-35)
+  uint8_t acc_decl[MAXACC];  // declaration index of each access's tensor (base register)
   int8_t tr_parent[32], tr_first[32], tr_next[32];
   uint8_t tr_nld[MAXCH], tr_nst[MAXCH];  // per base loop: its direct loads / stores (one access group)
   int64_t tr_c_hi[MAXCH], tr_c_hl[MAXCH];  // cycles of [group body + counter init] / [group body + latch]
@@ -1424,10 +1427,14 @@ __device__ int tree_apply(const DTask& T, const ls_record& r, TreeCand& c) {
     const DXform& xf = T.xf[x];
     if (xf.enable_bit >= 0 && !((r.flags >> xf.enable_bit) & 1u)) continue;
     const int j = xf.slot != NOSLOT ? c.nos[xf.slot] : -1;
-    if (xf.kind == LS_XF_TILE) {
+    if (xf.kind == LS_XF_TILE || xf.kind == LS_XF_VECTORIZE) {
       if (j < 0 || xf.new_slot == NOSLOT) return LS_ST_NO_LOOP;
       const int32_t F = xf.param >= 0 ? (int32_t)rparam(r, xf.param) : xf.value;
       const int32_t E = c.he[j];
+      if (xf.kind == LS_XF_VECTORIZE) {  // extent % width (ls/ir.py:463-468)
+        if (F == 0) return LS_ST_VEC_ZERO;
+        if (E % F != 0) return LS_ST_VEC_DIVIDE;
+      }
       if (F < 1 || F > E) return LS_ST_TILE_RANGE;
       if (c.nl >= NSLOT) return LS_ST_OVERFLOW;
       const int u = c.nl++;
@@ -1435,7 +1442,8 @@ __device__ int tree_apply(const DTask& T, const ls_record& r, TreeCand& c) {
       c.hs[u] = xf.new_slot;
       c.he[u] = F;
       c.hst[u] = c.hst[j];
-      c.hf[u] = 0;
+      c.hf[u] = xf.kind == LS_XF_VECTORIZE ? F_VEC : 0;
+      c.hf[j] &= (uint8_t)~F_VEC;  // the outer loop keeps parallel / unrolled only (ls/ir.py:379-380)
       c.grp[u] = c.grp[j];
       c.grp[j] = -1;
       c.nos[xf.new_slot] = (int8_t)u;
@@ -1484,9 +1492,9 @@ __device__ int tree_apply(const DTask& T, const ls_record& r, TreeCand& c) {
         c.hs[j2] = hs[q], c.hf[j2] = hf[q], c.he[j2] = he[q], c.hst[j2] = hst[q];
         c.nos[hs[q]] = (int8_t)j2;
       }
-    } else if (xf.kind == LS_XF_PARALLEL) {
+    } else if (xf.kind == LS_XF_PARALLEL || xf.kind == LS_XF_UNROLL) {
       if (j < 0) return LS_ST_NO_LOOP;
-      c.hf[j] |= F_PAR;
+      c.hf[j] |= xf.kind == LS_XF_PARALLEL ? F_PAR : F_UNR;
     } else {
       return LS_ST_UNSUPPORTED;
     }
@@ -1566,6 +1574,399 @@ __device__ int64_t tree_footprint(const DTask& T, const TreeCand& c, uint32_t fl
   return card;
 }
 
+// ---- emulated emission for trees with inlined (unrolled / vector) loops -------
+// The mock emitter (ls/ir.py:557-659) inlines an unrolled loop `extent` times
+// and a vector loop once, at the same depth; blocks split at labels and after
+// branches (ls/asm.py:155-167).  The CPU features need the greedy loop_map over
+// the emitted label blocks (ls/asm.py:250-294, copies of loops inside unrolled
+// loops included) and schedule_block of every block (ls/ilp.py:131-204), so the
+// emission is replayed block by block and each block is list-scheduled here.
+
+// register / resource ids of the emitted text: vector regs 0..23, base regs
+// 24 + decl % 6, their memory resources 30 + decl % 6, counters 36 + depth % 8,
+// the PTX predicate 44
+struct EInstr {
+  uint8_t shape, nrd, nwr, pad;
+  int8_t rd[6], wr[2];
+};
+
+constexpr int EM_MAXI = 128;   // instructions per block (more: LS_ST_UNSUPPORTED)
+constexpr int EM_MAXE = 1024;  // dependence edges per block (more: LS_ST_UNSUPPORTED)
+
+// reg_effects (ls/ilp.py:82-121) of one emitted instruction: operands as
+// (kind, id) with kind 0 register, 1 memory operand (base register id), 2 immediate
+__device__ void em_effects(int dialect, int shape, bool st_like, bool rmw, bool is_cmp, bool is_branch, bool mov_like,
+                           int nops, const int8_t* okind, const int8_t* oid, int pred, EInstr& o) {
+  o.shape = (uint8_t)shape;
+  o.nrd = o.nwr = 0;
+  if (pred >= 0) o.rd[o.nrd++] = (int8_t)pred;
+  if (nops == 0 || is_branch) return;
+  int mem = -1;
+  for (int i = 0; i < nops; ++i)
+    if (okind[i] == 1) {
+      mem = i;
+      break;
+    }
+  const bool store = st_like || (mem >= 0 && mem == nops - 1 && mov_like);
+  const int dest = dialect == LS_DIALECT_X86_ATT ? nops - 1 : ((st_like && mem >= 0) ? mem : 0);
+  for (int i = 0; i < nops; ++i) {
+    if (okind[i] == 2) continue;
+    if (i == mem) {
+      o.rd[o.nrd++] = oid[i];  // the base register
+      const int8_t res = (int8_t)(oid[i] + 6);
+      if (i == dest && store)
+        o.wr[o.nwr++] = res;
+      else
+        o.rd[o.nrd++] = res;
+      continue;
+    }
+    if (i == dest && !is_cmp) {
+      o.wr[o.nwr++] = oid[i];
+      if (rmw) o.rd[o.nrd++] = oid[i];
+    } else {
+      o.rd[o.nrd++] = oid[i];
+    }
+  }
+}
+
+struct Emu {
+  const DTask* T;
+  const TreeCand* c;
+  EInstr blk[EM_MAXI];
+  int n;              // instructions in the open block
+  int label;          // the open block starts at a label: loop node id (else -1)
+  int nld, nst, nfma; // significant instructions in the open block
+  int vreg;
+  int cursor;         // loop_map cursor into the preorder non-inlined loops
+  int nfor;
+  int8_t forl[NSLOT];         // preorder non-inlined loops (loop index)
+  int64_t trip[NSLOT];        // enclosing trip product of each of them
+  int64_t ilp, n_ld, n_st, n_fma;
+  int err;
+};
+
+__device__ void em_push(Emu& e, int shape, bool st_like, bool rmw, bool is_cmp, bool is_branch, bool mov_like, int nops,
+                        const int8_t* ok, const int8_t* oi, int pred = -1) {
+  if (e.n >= EM_MAXI) {
+    e.err = LS_ST_UNSUPPORTED;
+    return;
+  }
+  em_effects(e.T->tr_dialect, shape, st_like, rmw, is_cmp, is_branch, mov_like, nops, ok, oi, pred, e.blk[e.n++]);
+}
+
+// schedule_block (ls/ilp.py:131-204): RAW edges with latencies, WAR / WAW order edges, greedy issue
+__device__ int64_t em_schedule(const Emu& e, int& err) {
+  const DTask& T = *e.T;
+  const int n = e.n;
+  int16_t last_w[48];
+  int16_t rhead[48];
+  int16_t rnext[EM_MAXI * 6];
+  int16_t rnode[EM_MAXI * 6];
+  int nr = 0;
+  for (int q = 0; q < 48; ++q) last_w[q] = rhead[q] = -1;
+  int16_t eoff[EM_MAXI + 1], raw_end[EM_MAXI];
+  int16_t edge[EM_MAXE];
+  int ne = 0;
+  for (int k = 0; k < n; ++k) {
+    const EInstr& in = e.blk[k];
+    eoff[k] = (int16_t)ne;
+    for (int q = 0; q < in.nrd; ++q) {  // RAW: last writer of each read resource
+      const int w = last_w[in.rd[q]];
+      if (w < 0) continue;
+      bool dup = false;
+      for (int z = eoff[k]; z < ne; ++z) dup |= edge[z] == w;
+      if (!dup) {
+        if (ne >= EM_MAXE) {
+          err = LS_ST_UNSUPPORTED;
+          return 0;
+        }
+        edge[ne++] = (int16_t)w;
+      }
+    }
+    raw_end[k] = (int16_t)ne;
+    for (int q = 0; q < in.nwr; ++q) {  // WAW + WAR, minus the RAW predecessors
+      const int res = in.wr[q];
+      for (int z = -1; z < 0 || z >= 0;) {
+        int pred;
+        if (z == -1) {  // the last writer first, then the readers since it
+          pred = last_w[res];
+          z = rhead[res] >= 0 ? rhead[res] : -2;
+        } else {
+          pred = rnode[z] != k ? rnode[z] : -1;
+          z = rnext[z] >= 0 ? rnext[z] : -2;
+        }
+        if (pred >= 0) {
+          bool dup = false;
+          for (int y = eoff[k]; y < ne; ++y) dup |= edge[y] == pred;
+          if (!dup) {
+            if (ne >= EM_MAXE) {
+              err = LS_ST_UNSUPPORTED;
+              return 0;
+            }
+            edge[ne++] = (int16_t)pred;
+          }
+        }
+        if (z == -2) break;
+      }
+    }
+    for (int q = 0; q < in.nwr; ++q) {
+      last_w[in.wr[q]] = (int16_t)k;
+      rhead[in.wr[q]] = -1;
+    }
+    for (int q = 0; q < in.nrd; ++q) {
+      rnode[nr] = (int16_t)k;
+      rnext[nr] = rhead[in.rd[q]];
+      rhead[in.rd[q]] = (int16_t)nr;
+      ++nr;
+    }
+  }
+  eoff[n] = (int16_t)ne;
+  int64_t issue[EM_MAXI];
+  for (int k = 0; k < n; ++k) issue[k] = -1;
+  int done = 0, first = 0;
+  int64_t cycle = 0;
+  while (done < n) {
+    int issued = 0;
+    int used[LS_I_COUNT] = {0};
+    while (first < n && issue[first] >= 0) ++first;
+    for (int i = first; i < n && issued < T.tr_issue; ++i) {
+      if (issue[i] >= 0) continue;
+      int64_t ready = 0;
+      bool ok = true;
+      for (int z = eoff[i]; z < eoff[i + 1] && ok; ++z) {
+        const int p = edge[z];
+        if (issue[p] < 0)
+          ok = false;
+        else
+          ready = max(ready, issue[p] + (z < raw_end[i] ? (int64_t)T.tr_lat[e.blk[p].shape] : 1));
+      }
+      if (!ok || ready > cycle) continue;
+      const int cls = T.tr_klass[e.blk[i].shape];
+      const int cap = T.tr_ucap[cls];
+      if (cap > 0 && used[cls] >= cap) continue;
+      issue[i] = cycle;
+      ++used[cls];
+      ++issued;
+      ++done;
+    }
+    ++cycle;
+  }
+  int64_t fin = 0;
+  for (int k = 0; k < n; ++k) fin = max(fin, issue[k] + (int64_t)T.tr_lat[e.blk[k].shape]);
+  return fin;
+}
+
+__device__ void em_end_block(Emu& e) {
+  if (e.n == 0 || e.err) {
+    e.n = 0;
+    e.label = -1;
+    return;
+  }
+  int64_t w = 1;
+  if (e.label >= 0 && e.cursor < e.nfor) {  // greedy in-order loop_map (ls/asm.py:270-292)
+    const int lp = e.forl[e.cursor];
+    const int64_t bound = e.c->he[e.label - e.T->tr_na];
+    if (bound == e.c->he[lp] || bound == (int64_t)e.c->he[lp] * e.c->hst[lp]) {
+      w = e.trip[e.cursor];
+      e.n_ld += (int64_t)e.nld * w;
+      e.n_st += (int64_t)e.nst * w;
+      e.n_fma += (int64_t)e.nfma * w;
+      ++e.cursor;
+    }
+  }
+  int err = 0;
+  const int64_t cyc = em_schedule(e, err);
+  if (err) e.err = err;
+  e.ilp += cyc * w;
+  e.n = 0;
+  e.label = -1;
+  e.nld = e.nst = e.nfma = 0;
+}
+
+// emit_body (ls/ir.py:584-612): loads, then fma + store per store
+__device__ void em_body(Emu& e, int node) {
+  const DTask& T = *e.T;
+  const TreeCand& c = *e.c;
+  const int tg = T.tr_target;
+  int8_t lregs[MAXACC];
+  int L = 0;
+  for (int ch = c.first[node]; ch >= 0; ch = c.nxt[ch]) {
+    if (ch >= T.tr_na || T.acc_store[ch]) continue;
+    const int r = e.vreg++ % 16;
+    lregs[L++] = (int8_t)r;
+    const int8_t base = (int8_t)(24 + T.acc_decl[ch] % 6);
+    if (tg == LS_TARGET_X86) {  // vmovups (B), %zmmR
+      const int8_t ok[2] = {1, 0}, oi[2] = {base, (int8_t)r};
+      em_push(e, LS_I_LOAD, false, false, false, false, true, 2, ok, oi);
+    } else {  // ld1 {vR}, [B]  /  ld.global.f32 %fR, [B]
+      const int8_t ok[2] = {0, 1}, oi[2] = {(int8_t)r, base};
+      em_push(e, LS_I_LOAD, false, false, false, false, false, 2, ok, oi);
+    }
+    ++e.nld;
+  }
+  int j = 0;
+  for (int ch = c.first[node]; ch >= 0; ch = c.nxt[ch]) {
+    if (ch >= T.tr_na || !T.acc_store[ch]) continue;
+    const int8_t acc = (int8_t)(16 + j % 8);
+    const int8_t s1 = L ? lregs[(2 * j) % L] : 0, s2 = L ? lregs[(2 * j + 1) % L] : 1;
+    const int8_t base = (int8_t)(24 + T.acc_decl[ch] % 6);
+    if (tg == LS_TARGET_X86) {
+      const int8_t ok[3] = {0, 0, 0}, oi[3] = {s1, s2, acc};  // vfmadd231ps S1, S2, A
+      em_push(e, LS_I_FMA, false, true, false, false, false, 3, ok, oi);
+      const int8_t sk[2] = {0, 1}, si[2] = {acc, base};        // vmovups A, (B)
+      em_push(e, LS_I_STORE, false, false, false, false, true, 2, sk, si);
+    } else if (tg == LS_TARGET_AARCH64) {
+      const int8_t ok[3] = {0, 0, 0}, oi[3] = {acc, s1, s2};  // fmla A, S1, S2
+      em_push(e, LS_I_FMA, false, true, false, false, false, 3, ok, oi);
+      const int8_t sk[2] = {0, 1}, si[2] = {acc, base};        // st1 {A}, [B]
+      em_push(e, LS_I_STORE, true, false, false, false, false, 2, sk, si);
+    } else {
+      const int8_t ok[4] = {0, 0, 0, 0}, oi[4] = {acc, s1, s2, acc};  // fma.rn.f32 A, S1, S2, A
+      em_push(e, LS_I_FMA, false, true, false, false, false, 4, ok, oi);
+      const int8_t sk[2] = {1, 0}, si[2] = {base, acc};                // st.global.f32 [B], A
+      em_push(e, LS_I_STORE, true, false, false, false, false, 2, sk, si);
+    }
+    ++e.nfma;
+    ++e.nst;
+    ++j;
+  }
+}
+
+__device__ void em_node(Emu& e, int node, int depth) {
+  if (e.err) return;
+  const DTask& T = *e.T;
+  const TreeCand& c = *e.c;
+  const int j = node - T.tr_na;
+  const uint8_t fl = c.hf[j];
+  const int tg = T.tr_target;
+  if (fl & (F_UNR | F_VEC)) {  // inlined: extent copies (vector: one) at the same depth
+    const int copies = (fl & F_VEC) ? 1 : c.he[j];
+    for (int q = 0; q < copies && !e.err; ++q) {
+      em_body(e, node);
+      for (int ch = c.first[node]; ch >= 0; ch = c.nxt[ch])
+        if (ch >= T.tr_na) em_node(e, ch, depth);
+    }
+    return;
+  }
+  const int8_t ctr = (int8_t)(36 + depth % 8);
+  {  // counter init in the open block
+    const int8_t ok[2] = {2, 0}, oi[2] = {0, ctr}, dk[2] = {0, 2}, di[2] = {ctr, 0};
+    if (tg == LS_TARGET_X86)
+      em_push(e, LS_I_INIT, false, false, false, false, true, 2, ok, oi);  // movq $0, C
+    else
+      em_push(e, LS_I_INIT, false, false, false, false, true, 2, dk, di);  // mov C, #0 / mov.u32 C, 0
+  }
+  em_end_block(e);  // the label starts a block
+  e.label = node;
+  em_body(e, node);
+  for (int ch = c.first[node]; ch >= 0; ch = c.nxt[ch])
+    if (ch >= T.tr_na) em_node(e, ch, depth + 1);
+  if (tg == LS_TARGET_X86) {
+    const int8_t ak[2] = {2, 0}, ai[2] = {0, ctr};
+    em_push(e, LS_I_ADD, false, true, false, false, false, 2, ak, ai);    // addq $1, C
+    em_push(e, LS_I_CMP, false, false, true, false, false, 2, ak, ai);    // cmpq $E, C
+    em_push(e, LS_I_BRANCH, false, false, false, true, false, 1, ak, ai); // jne
+  } else if (tg == LS_TARGET_AARCH64) {
+    const int8_t ak[3] = {0, 0, 2}, ai[3] = {ctr, ctr, 0}, ck[2] = {0, 2}, ci[2] = {ctr, 0};
+    em_push(e, LS_I_ADD, false, true, false, false, false, 3, ak, ai);    // add C, C, #1
+    em_push(e, LS_I_CMP, false, false, true, false, false, 2, ck, ci);    // cmp C, #E
+    em_push(e, LS_I_BRANCH, false, false, false, true, false, 1, ck, ci); // b.ne
+  } else {
+    const int8_t ak[3] = {0, 0, 2}, ai[3] = {ctr, ctr, 0}, sk[3] = {0, 0, 2}, si[3] = {44, ctr, 0};
+    em_push(e, LS_I_ADD, false, true, false, false, false, 3, ak, ai);    // add.s32 C, C, 1
+    em_push(e, LS_I_CMP, false, false, false, false, false, 3, sk, si);   // setp.lt.s32 P, C, E
+    em_push(e, LS_I_BRANCH, false, false, false, true, false, 1, sk, si, 44);  // @P bra
+  }
+  em_end_block(e);  // a branch ends the block
+}
+
+// CPU features of a tree with inlined loops: n_fma, n_vload, n_vstore (count_simd over the
+// matched label blocks) and ilp (every block scheduled, times its matched trip product)
+__device__ int em_cpu_features(const DTask& T, const TreeCand& c, int64_t& nfma, int64_t& nld, int64_t& nst,
+                               int64_t& ilp) {
+  Emu e;
+  e.T = &T;
+  e.c = &c;
+  e.n = 0;
+  e.label = -1;
+  e.nld = e.nst = e.nfma = 0;
+  e.vreg = 0;
+  e.cursor = 0;
+  e.nfor = 0;
+  e.ilp = e.n_ld = e.n_st = e.n_fma = 0;
+  e.err = 0;
+  // preorder non-inlined loops and their trip products over non-inlined ancestors (ls/asm.py:261-272)
+  int64_t tp[NSLOT];
+  for (int q = 0; q < c.nn; ++q) {
+    const int L = c.ord[q];
+    if (L < T.tr_na) continue;
+    const int j = L - T.tr_na, p = c.par[L];
+    const int64_t up = p >= 0 ? tp[p - T.tr_na] : 1;
+    const bool inl = c.hf[j] & (F_UNR | F_VEC);
+    tp[j] = inl ? up : up * c.he[j];
+    if (!inl) {
+      e.forl[e.nfor] = (int8_t)j;
+      e.trip[e.nfor++] = tp[j];
+    }
+  }
+  for (int n = c.root; n >= 0; n = c.nxt[n])
+    if (n >= T.tr_na) em_node(e, n, 0);
+  {
+    const int8_t ok[1] = {2}, oi[1] = {0};
+    em_push(e, LS_I_RET, false, false, false, true, false, 0, ok, oi);  // ret
+  }
+  em_end_block(e);
+  if (e.err) return e.err;
+  nfma = e.n_fma;
+  nld = e.n_ld;
+  nst = e.n_st;
+  ilp = e.ilp;
+  return LS_OK;
+}
+
+// thread_cycles in emission line order (ls/ptx.py:225-235) for a tree: inlined loops
+// replay their body `copies` times at the same depth; a branching loop's init line
+// weighs W' of its parent, its body and latch lines its own W'
+__device__ double tree_ptx_node(const DTask& T, const TreeCand& c, const int64_t* Wp, int node, double work) {
+  const double* pc = T.ptx_cost;
+  const int na = T.tr_na, j = node - na, p = c.par[node];
+  const uint8_t fl = c.hf[j];
+  auto body = [&](double w) {
+    const int g = c.grp[j];
+    if (g < 0) return;
+    for (int a = 0; a < T.tr_nld[g]; ++a) work = rn_add(work, rn_mul(pc[LS_I_LOAD], w));
+    for (int a = 0; a < T.tr_nst[g]; ++a) {
+      work = rn_add(work, rn_mul(pc[LS_I_FMA], w));
+      work = rn_add(work, rn_mul(pc[LS_I_STORE], w));
+    }
+  };
+  if (fl & (F_UNR | F_VEC)) {
+    const int copies = (fl & F_VEC) ? 1 : c.he[j];
+    for (int q = 0; q < copies; ++q) {
+      body((double)Wp[j]);
+      for (int ch = c.first[node]; ch >= 0; ch = c.nxt[ch])
+        if (ch >= na) work = tree_ptx_node(T, c, Wp, ch, work);
+    }
+    return work;
+  }
+  work = rn_add(work, rn_mul(pc[LS_I_INIT], (double)(p >= 0 ? Wp[p - na] : 1)));
+  body((double)Wp[j]);
+  for (int ch = c.first[node]; ch >= 0; ch = c.nxt[ch])
+    if (ch >= na) work = tree_ptx_node(T, c, Wp, ch, work);
+  const double w = (double)Wp[j];
+  work = rn_add(work, rn_mul(pc[LS_I_ADD], w));
+  work = rn_add(work, rn_mul(pc[LS_I_CMP], w));
+  work = rn_add(work, rn_mul(pc[LS_I_BRANCH], w));
+  return work;
+}
+
+__device__ double tree_ptx_ordered(const DTask& T, const TreeCand& c, const int64_t* Wp) {
+  double work = 0.0;
+  for (int n = c.root; n >= 0; n = c.nxt[n])
+    if (n >= T.tr_na) work = tree_ptx_node(T, c, Wp, n, work);
+  return rn_add(work, T.ptx_cost[LS_I_RET]);
+}
+
 __device__ int eval_tree(const DTask& T, const ls_record& r, double* f, double* score) {
   TreeCand c;
   const int st = tree_apply(T, r, c);
@@ -1633,15 +2034,18 @@ __device__ int eval_tree(const DTask& T, const ls_record& r, double* f, double* 
         if ((pres[n - na] >> t) & 1u) dmov += dm[n - na][t];
     }
   }
-  // ---- emitted code (ls/ir.py:557-659): every loop branches; W = trips of the enclosing loops
-  int64_t W[NSLOT], Wp[NSLOT];
+  // ---- emitted code (ls/ir.py:557-659).  Per loop: W = trips of the enclosing branching
+  // loops (inlined = unrolled or vector loops do not branch), W' the same with the PTX
+  // counter-register wrap, copies = how often its code is emitted (unrolled ancestors),
+  // Wv = product of enclosing extents with vector loops counting 1 (smem volume)
+  int64_t W[NSLOT], Wp[NSLOT], cp[NSLOT], Wv[NSLOT];
   uint8_t height[NSLOT];
-  for (int q = c.nn - 1; q >= 0; --q) {  // subtree heights: PTX counter registers repeat every 8 depths
+  for (int q = c.nn - 1; q >= 0; --q) {  // branching levels below: counter registers repeat every 8 depths
     const int L = c.ord[q];
     if (L < na) continue;
     int h = 0;
     for (int ch = c.first[L]; ch >= 0; ch = c.nxt[ch])
-      if (ch >= na) h = max(h, height[ch - na] + 1);
+      if (ch >= na) h = max(h, height[ch - na] + ((c.hf[ch - na] & (F_UNR | F_VEC)) ? 0 : 1));
     height[L - na] = (uint8_t)h;
   }
   int64_t nld = 0, nst = 0, ilp = 0, ptx_loops = 0, wld = 0, wst = 0;
@@ -1651,16 +2055,23 @@ __device__ int eval_tree(const DTask& T, const ls_record& r, double* f, double* 
     const int L = c.ord[q];
     if (L < na) continue;
     const int j = L - na, p = c.par[L];
+    const bool inl = c.hf[j] & (F_UNR | F_VEC);
     const int64_t Wpar = p >= 0 ? W[p - na] : 1, Wppar = p >= 0 ? Wp[p - na] : 1;
-    W[j] = Wpar * c.he[j];
-    Wp[j] = Wppar * (height[j] >= 8 ? 1 : c.he[j]);  // no trip when a loop sits 8 deeper (ls/ptx.py:163-169)
-    if (p < 0) ++ntop;
+    const int64_t cpar = p >= 0 ? cp[p - na] * ((c.hf[p - na] & F_UNR) ? c.he[p - na] : 1) : 1;
+    cp[j] = cpar;
+    Wv[j] = (p >= 0 ? Wv[p - na] : 1) * ((c.hf[j] & F_VEC) ? 1 : c.he[j]);
+    W[j] = inl ? Wpar : Wpar * c.he[j];
+    Wp[j] = inl ? Wppar : Wppar * (height[j] >= 8 ? 1 : c.he[j]);  // no trip 8+ levels deep (ls/ptx.py:163-169)
     const int g = c.grp[j];
     const int64_t gl = g >= 0 ? T.tr_nld[g] : 0, gs = g >= 0 ? T.tr_nst[g] : 0;
+    // the loop's own accesses are emitted copies(L) x (its extent if unrolled) times
+    const int64_t acopies = cp[j] * ((c.hf[j] & F_UNR) ? c.he[j] : 1);
+    wld += gl * acopies * Wp[j];
+    wst += gs * acopies * Wp[j];
+    if (inl) continue;
+    if (p < 0) ++ntop;
     nld += gl * W[j];
     nst += gs * W[j];
-    wld += gl * Wp[j];
-    wst += gs * Wp[j];
     int nch = 0;
     for (int ch = c.first[L]; ch >= 0; ch = c.nxt[ch]) nch += ch >= na;
     if (T.family == LS_FAMILY_CPU) {
@@ -1670,13 +2081,20 @@ __device__ int eval_tree(const DTask& T, const ls_record& r, double* f, double* 
       ilp += hdr * W[j];
       if (nch) ilp += T.c_init * (nch - 1) + T.c_latch;
     } else {
-      ptx_loops += ic[LS_I_INIT] * Wppar + (ic[LS_I_ADD] + ic[LS_I_CMP] + ic[LS_I_BRANCH]) * Wp[j];
+      ptx_loops += cp[j] * (ic[LS_I_INIT] * Wppar + (ic[LS_I_ADD] + ic[LS_I_CMP] + ic[LS_I_BRANCH]) * Wp[j]);
     }
   }
   int nf;
   if (T.family == LS_FAMILY_CPU) {
-    ilp += T.c_init * ntop + T.c_ret;  // the top-level init blocks and `ret`
-    f[0] = (double)nst;
+    if (T.tr_inline) {  // inlined loops: replay the emission (greedy loop_map, every block scheduled)
+      int64_t nfma;
+      const int est = em_cpu_features(T, c, nfma, nld, nst, ilp);
+      if (est) return est;
+      f[0] = (double)nfma;
+    } else {
+      ilp += T.c_init * ntop + T.c_ret;  // the top-level init blocks and `ret`
+      f[0] = (double)nst;
+    }
     f[1] = (double)nld;
     f[2] = (double)nst;
     f[3] = (double)dmov;
@@ -1686,48 +2104,8 @@ __device__ int eval_tree(const DTask& T, const ls_record& r, double* f, double* 
     double work;
     if (T.costs_integral) {
       work = (double)(ptx_loops + wld * ic[LS_I_LOAD] + wst * (ic[LS_I_FMA] + ic[LS_I_STORE]) + ic[LS_I_RET]);
-    } else {  // thread_cycles in line order (ls/ptx.py:225-235): enter / exit events of a DFS
-      const double* pc = T.ptx_cost;
-      work = 0.0;
-      int n = c.root;
-      while (n >= 0) {
-        if (n >= na) {
-          const int j = n - na, p = c.par[n];
-          work = rn_add(work, rn_mul(pc[LS_I_INIT], (double)(p >= 0 ? Wp[p - na] : 1)));
-          const int g = c.grp[j];
-          const double w = (double)Wp[j];
-          if (g >= 0) {
-            for (int a = 0; a < T.tr_nld[g]; ++a) work = rn_add(work, rn_mul(pc[LS_I_LOAD], w));
-            for (int a = 0; a < T.tr_nst[g]; ++a) {
-              work = rn_add(work, rn_mul(pc[LS_I_FMA], w));
-              work = rn_add(work, rn_mul(pc[LS_I_STORE], w));
-            }
-          }
-          int ch = c.first[n];
-          while (ch >= 0 && ch < na) ch = c.nxt[ch];  // first child loop
-          if (ch >= 0) {
-            n = ch;
-            continue;
-          }
-        }
-        // leave n (its latch) and climb until a next sibling loop exists
-        while (n >= 0) {
-          if (n >= na) {
-            const double w = (double)Wp[n - na];
-            work = rn_add(work, rn_mul(pc[LS_I_ADD], w));
-            work = rn_add(work, rn_mul(pc[LS_I_CMP], w));
-            work = rn_add(work, rn_mul(pc[LS_I_BRANCH], w));
-          }
-          int s2 = c.nxt[n];
-          while (s2 >= 0 && s2 < na) s2 = c.nxt[s2];
-          if (s2 >= 0) {
-            n = s2;
-            break;
-          }
-          n = c.par[n];
-        }
-      }
-      work = rn_add(work, pc[LS_I_RET]);
+    } else {  // thread_cycles in line order (ls/ptx.py:225-235): the emission replayed with its copies
+      work = tree_ptx_ordered(T, c, Wp);
     }
     double smem = 0.0;
     if (T.has_shared) {  // smem_ops_feature (ls/ptx.py:310-327): vol = product of the enclosing extents
@@ -1735,7 +2113,7 @@ __device__ int eval_tree(const DTask& T, const ls_record& r, double* f, double* 
         const int a = c.ord[q];
         if (a >= na || !T.t_shared[T.acc_tensor[a]]) continue;
         const int p = c.par[a];
-        const int64_t vol = p >= 0 ? W[p - na] : 1;
+        const int64_t vol = p >= 0 ? Wv[p - na] : 1;
         // tid: `tid`, else the last preorder parallel loop indexing the access (ls/ptx.py:298-307)
         uint32_t used = 0;
         const int t = T.acc_tensor[a];
@@ -3057,13 +3435,11 @@ int build_task(const ls_task_desc& d, DTask& T, std::vector<int>& load_t, std::v
   T.tree = chain ? 0 : 1;
   if (nl == 0 || nl > MAXCH) return fail(LS_E_UNSUPPORTED, "program must have 1..16 loops");
   if (na < 1 || na > MAXACC) return fail(LS_E_UNSUPPORTED, "program must hold 1..16 accesses");
-  if (T.tree) {
+  if (T.tree) {  // inlined loops: the emission is emulated per candidate
     for (int p = 0; p < nl; ++p)
-      if (d.nodes[loop_nodes[p]].unrolled || d.nodes[loop_nodes[p]].vector_width)
-        return fail(LS_E_UNSUPPORTED, "tree programs with unrolled or vector loops are outside the device class");
+      if (d.nodes[loop_nodes[p]].unrolled || d.nodes[loop_nodes[p]].vector_width) T.tr_inline = 1;
     for (int x = 0; x < d.n_xforms; ++x)
-      if (d.xforms[x].kind == LS_XF_UNROLL || d.xforms[x].kind == LS_XF_VECTORIZE)
-        return fail(LS_E_UNSUPPORTED, "Unroll / Vectorize on a tree program are outside the device class");
+      if (d.xforms[x].kind == LS_XF_UNROLL || d.xforms[x].kind == LS_XF_VECTORIZE) T.tr_inline = 1;
   }
   for (int x = 0; x < d.n_xforms; ++x) {
     const ls_xform& s = d.xforms[x];
@@ -3340,6 +3716,15 @@ int build_task(const ls_task_desc& d, DTask& T, std::vector<int>& load_t, std::v
     }
     T.tr_nl = nl;
     T.tr_na = na;
+    for (int a = 0; a < na; ++a) T.acc_decl[a] = (uint8_t)d.nodes[acc_nodes[a]].tensor;
+    T.tr_target = d.target;
+    T.tr_dialect = d.dialect;
+    T.tr_issue = d.issue_width;
+    for (int q = 0; q < LS_I_COUNT; ++q) {
+      T.tr_lat[q] = d.lat[q];
+      T.tr_klass[q] = d.klass[q];
+      T.tr_ucap[q] = d.unit_cap[q];
+    }
     for (int p = 0; p < nl; ++p) {  // the group of base loop p: its direct accesses, loads then stores
       std::vector<int> lt, st;
       for (int a = 0; a < na; ++a)
@@ -3539,6 +3924,11 @@ int ls_task_create(const ls_task_desc* desc, int device, ls_task** out) {
     return rc;
   }
   cudaDeviceGetAttribute(&t->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (t->host.tree) {  // the tree kernels recurse (emission replay, line-order PTX) and list-schedule in local memory
+    size_t lim = 0;
+    cudaDeviceGetLimit(&lim, cudaLimitStackSize);
+    if (lim < 20480) CUDA_TRY(cudaDeviceSetLimit(cudaLimitStackSize, 20480));
+  }
   {  // keep stream-ordered workspace allocations cached across calls
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {

@@ -209,13 +209,14 @@ def test_failure_messages_match_reference_errors():
                 assert (None if m is None else f"{m[0]}: {m[1]}") == e
                 n += e is not None
     assert n == 2350
-    tr = json.loads((Path(__file__).resolve().parent / "golden" / "tree_rank.json").read_text())
     m2 = 0
-    for c in tr["cases"]:
-        prog = ir.parse_program(json.dumps(tr["programs"][c["program"]]))
-        msgs = [ir.failure_message(prog, ir.Schedule.from_json(s)) for s in c["schedules"]]
-        for res in c["results"].values():
-            for m, e in zip(msgs, res["errors"]):
-                assert (None if m is None else f"{m[0]}: {m[1]}") == e
-                m2 += e is not None
-    assert m2 == 1065
+    for fx in ("tree_rank.json", "tree_inline.json"):
+        tr = json.loads((Path(__file__).resolve().parent / "golden" / fx).read_text())
+        for c in tr["cases"]:
+            prog = ir.parse_program(json.dumps(tr["programs"][c["program"]]))
+            msgs = [ir.failure_message(prog, ir.Schedule.from_json(s)) for s in c["schedules"]]
+            for res in c["results"].values():
+                for m, e in zip(msgs, res["errors"]):
+                    assert (None if m is None else f"{m[0]}: {m[1]}") == e
+                    m2 += e is not None
+    assert m2 == 1065 + 615

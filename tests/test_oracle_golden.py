@@ -121,13 +121,14 @@ def test_emit_text_byte_identical():
         assert pyoracle.emit_text(d, g.records[0], tgt) == c["text"], (c["program"], c["schedule"])
 
 
-def test_oracle_scheduled_trees():
-    """The C oracle on scheduled tree programs == the reference (tests/golden/tree_rank.json)."""
+@pytest.mark.parametrize("fixture", ["tree_rank.json", "tree_inline.json"])
+def test_oracle_scheduled_trees(fixture):
+    """The C oracle on scheduled tree programs == the reference (tests/golden/tree_*.json)."""
     import json
     from golden_util import GOLDEN, arch_named, launch, status_of_error
     from paper_2104_14641_b200 import ir
     from paper_2104_14641_b200.pack import pack_schedules
-    tr = json.loads((GOLDEN / "tree_rank.json").read_text())
+    tr = json.loads((GOLDEN / fixture).read_text())
     for case in tr["cases"]:
         prog = ir.parse_program(json.dumps(tr["programs"][case["program"]]))
         scheds = [ir.Schedule.from_json(s) for s in case["schedules"]]

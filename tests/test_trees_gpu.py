@@ -12,6 +12,7 @@ from golden_util import GOLDEN, arch_named, launch, status_of_error
 pytestmark = pytest.mark.gpu
 
 TREE_RANK = json.loads((GOLDEN / "tree_rank.json").read_text())
+TREE_INLINE = json.loads((GOLDEN / "tree_inline.json").read_text())
 TREES = json.loads((GOLDEN / "trees.json").read_text())
 
 
@@ -21,11 +22,16 @@ def torch():
     return t
 
 
-@pytest.mark.parametrize("case", TREE_RANK["cases"], ids=[c["program"] for c in TREE_RANK["cases"]])
-def test_scheduled_trees_match_reference(torch, case):
+CASES = [(TREE_RANK, c) for c in TREE_RANK["cases"]] + [(TREE_INLINE, c) for c in TREE_INLINE["cases"]]
+
+
+@pytest.mark.parametrize("fx,case", CASES, ids=[("inline-" if f is TREE_INLINE else "") + c["program"] for f, c in CASES])
+def test_scheduled_trees_match_reference(torch, fx, case):
+    """Tile / Reorder / Parallel (tree_rank) and + Unroll / Vectorize with unrolled base loops
+    (tree_inline: the emission replay + device list scheduler)."""
     from paper_2104_14641_b200 import ir
     from paper_2104_14641_b200.cost import score_batch
-    prog = ir.parse_program(json.dumps(TREE_RANK["programs"][case["program"]]))
+    prog = ir.parse_program(json.dumps(fx["programs"][case["program"]]))
     scheds = [ir.Schedule.from_json(s) for s in case["schedules"]]
     for a, res in case["results"].items():
         out = score_batch(prog, scheds, arch_named(a), launch())
