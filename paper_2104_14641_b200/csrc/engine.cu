@@ -208,6 +208,10 @@ struct ls_task {
   unsigned char* stage = nullptr;  // pinned staging of the host-buffer calls' results
   size_t stage_bytes = 0;
   bool stage_busy = false;
+  unsigned char* ws = nullptr;     // cached top-k workspace (counters self-reset), tied to one stream
+  size_t ws_bytes = 0;
+  cudaStream_t ws_stream = nullptr;
+  bool ws_busy = false;
 };
 
 // ---------------------------------------------------------------------------
@@ -2814,7 +2818,8 @@ __global__ void __launch_bounds__(TPB) merge_filter_kernel(const Key* __restrict
                                                            const Key* __restrict__ mins, int nblk, int k,
                                                            Key* __restrict__ surv, unsigned int* __restrict__ ctr,
                                                            double* __restrict__ out_s, int64_t* __restrict__ out_i,
-                                                           int cap) {
+                                                           int cap, unsigned long long* __restrict__ n_valid,
+                                                           unsigned long long* __restrict__ wvalid) {
   extern __shared__ __align__(16) unsigned char raw[];
   __shared__ unsigned int s_ticket;
   __shared__ Key s_T;
@@ -2877,6 +2882,12 @@ __global__ void __launch_bounds__(TPB) merge_filter_kernel(const Key* __restrict
   } else {
     write_sorted(S, merge_into(S, surv, c, k, false), k, out_s, out_i);
   }
+  if (threadIdx.x == 0) {  // the count out; the counters back to zero for the next launch
+    const unsigned long long v = atomicExch(wvalid, 0ull);
+    if (n_valid) *n_valid = v;
+    ctr[0] = 0;
+    ctr[1] = 0;
+  }
   trace_mark(7);
 }
 
@@ -2889,7 +2900,7 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kern
     const DTask* __restrict__ gtask, const void* __restrict__ src, int pbytes, int64_t n, int64_t base_index, int k,
     Key* __restrict__ block_out, Key* __restrict__ group_out, unsigned int* __restrict__ tickets,
     double* __restrict__ out_s, int64_t* __restrict__ out_i, unsigned long long* __restrict__ n_valid, int cap,
-    Key* __restrict__ mins) {
+    Key* __restrict__ mins, unsigned long long* __restrict__ wvalid) {
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ unsigned int s_ticket;
   DTask& T = *reinterpret_cast<DTask*>(dyn);
@@ -2941,7 +2952,7 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kern
     topk_offer(S, has, key, k, safe);
   }
   for (int off = 16; off > 0; off >>= 1) valid += __shfl_down_sync(0xffffffffu, valid, off);
-  if ((threadIdx.x & 31) == 0 && valid) atomicAdd(n_valid, (unsigned long long)valid);
+  if ((threadIdx.x & 31) == 0 && valid) atomicAdd(wvalid, (unsigned long long)valid);
   __syncthreads();
   trace_mark(2);
   const int kept0 = topk_select(S, k);
@@ -2975,6 +2986,11 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kern
   __threadfence();
   kept = merge_into(S, group_out, (int64_t)ngroups * k, k, false);
   write_sorted(S, kept, k, out_s, out_i);
+  if (threadIdx.x == 0) {  // the count out; every counter back to zero for the next launch
+    const unsigned long long v = atomicExch(wvalid, 0ull);
+    if (n_valid) *n_valid = v;
+    for (int q = 0; q <= ngroups; ++q) tickets[q] = 0;
+  }
   trace_mark(5);
 }
 
@@ -3807,7 +3823,7 @@ size_t smem_topk(const DTask& T, int k, int mode) { return smem_score(T, mode) +
 
 using ScoreFn = void (*)(const DTask*, const void*, int, int64_t, double*, double*, int32_t*);
 using TopkFn = void (*)(const DTask*, const void*, int, int64_t, int64_t, int, Key*, Key*, unsigned int*, double*,
-                       int64_t*, unsigned long long*, int, Key*);
+                       int64_t*, unsigned long long*, int, Key*, unsigned long long*);
 
 template <int SRC>
 ScoreFn score_fn_src(const DTask& T, int mode) {
@@ -3990,6 +4006,7 @@ int ls_task_destroy(ls_task* t) {
   if (t->d_task) cudaFree(t->d_task);
   if (t->d_tab) cudaFree(t->d_tab);
   if (t->stage) cudaFreeHost(t->stage);
+  if (t->ws) cudaFree(t->ws);
   delete t;
   return LS_E_OK;
 }
@@ -4070,8 +4087,13 @@ int ls_score_points(ls_task* t, const void* d_points, int32_t pbytes, int64_t n,
   return score_device(t, d_points, pbytes, n, d_scores, d_features, d_status, (cudaStream_t)stream);
 }
 
-// h_out != null: the top-k scores, indices and the valid count live in the
-// workspace and come back in one copy to h_out ([k] f64, [k] i64, u64).
+// Workspace: [4 KiB of self-resetting counters (tickets) | the valid count] [key lists]
+// [outputs when h_out].  The launch leaves every counter at zero, so a workspace cached
+// on the task is reused on the same stream without a memset.  h_out != null: the top-k
+// scores, indices and the valid count come back in one copy to h_out (count in a 16-byte
+// slot, then [k] f64, [k] i64).
+constexpr size_t WS_CTR_BYTES = 4096 + 16;
+
 static int topk_device(ls_task* t, const void* d_src, int pbytes, int64_t n, int64_t base_index, int32_t k,
                        double* d_top_scores, int64_t* d_top_index, unsigned long long* d_valid, cudaStream_t s,
                        void* h_out = nullptr) {
@@ -4083,23 +4105,43 @@ static int topk_device(ls_task* t, const void* d_src, int pbytes, int64_t n, int
   // two-stage merge (block-minima bound, merge_filter_kernel) when the grid has plenty of
   // blocks per answer key; else the in-kernel merge tree
   const bool two = 4 * k <= grid && grid <= topk_buf(k);
-  const size_t ws_keys = sizeof(Key) * (two ? (size_t)grid * (2 * k + 1) : ((size_t)grid + ngroups) * k);
-  const int nctr = two ? 2 : ngroups + 1;
-  const size_t ctr_bytes = align16(sizeof(unsigned int) * nctr) + (h_out ? 16 : 0);  // + the valid count
-  const size_t out_bytes = h_out ? 16 * (size_t)k : 0;
-  const size_t ws_bytes = ws_keys + ctr_bytes + out_bytes;
+  const size_t keys_bytes = sizeof(Key) * (two ? (size_t)grid * (2 * k + 1) : ((size_t)grid + ngroups) * k);
+  const size_t out_bytes = h_out ? 16 + 16 * (size_t)k : 0;
+  const size_t ws_bytes = WS_CTR_BYTES + keys_bytes + out_bytes;
   unsigned char* ws = nullptr;
-  CUDA_TRY(cudaMallocAsync(&ws, ws_bytes, s));
-  Key* block_out = reinterpret_cast<Key*>(ws);
+  bool cached = false;
+  {
+    std::lock_guard<std::mutex> g(t->mu);
+    if (!t->ws_busy && (!t->ws || t->ws_stream == s)) {
+      if (t->ws_bytes < ws_bytes) {  // grow (the old block is freed in its stream's order)
+        if (t->ws) cudaFreeAsync(t->ws, t->ws_stream);
+        t->ws = nullptr;
+        t->ws_bytes = 0;
+        CUDA_TRY(cudaMallocAsync(&t->ws, ws_bytes, s));
+        CUDA_TRY(cudaMemsetAsync(t->ws, 0, WS_CTR_BYTES, s));
+        t->ws_bytes = ws_bytes;
+        t->ws_stream = s;
+      }
+      t->ws_busy = true;
+      ws = t->ws;
+      cached = true;
+    }
+  }
+  if (!cached) {  // concurrent call or another stream: a private workspace
+    CUDA_TRY(cudaMallocAsync(&ws, ws_bytes, s));
+    CUDA_TRY(cudaMemsetAsync(ws, 0, WS_CTR_BYTES, s));
+  }
+  unsigned int* tickets = reinterpret_cast<unsigned int*>(ws);
+  unsigned long long* wvalid = reinterpret_cast<unsigned long long*>(ws + 4096);
+  Key* block_out = reinterpret_cast<Key*>(ws + WS_CTR_BYTES);
   Key* group_out = block_out + (size_t)grid * k;   // tree: group lists; two-stage: survivors
   Key* mins = two ? group_out + (size_t)grid * k : nullptr;
-  unsigned int* tickets = reinterpret_cast<unsigned int*>(ws + ws_keys);
-  if (h_out) {  // outputs in the workspace: [k] scores, [k] indices, then the count (zeroed with the tickets)
-    d_valid = reinterpret_cast<unsigned long long*>(ws + ws_keys + ctr_bytes - 16);
-    d_top_scores = reinterpret_cast<double*>(ws + ws_keys + ctr_bytes);
+  unsigned char* out = ws + WS_CTR_BYTES + keys_bytes;
+  if (h_out) {
+    d_valid = reinterpret_cast<unsigned long long*>(out);
+    d_top_scores = reinterpret_cast<double*>(out + 16);
     d_top_index = reinterpret_cast<int64_t*>(d_top_scores + k);
   }
-  CUDA_TRY(cudaMemsetAsync(tickets, 0, ctr_bytes, s));
   unsigned long long* tr = nullptr;
   const char* tr_env = getenv("LS_TRACE");
   if (tr_env && tr_env[0] == '1') {  // phase timestamps to stderr (profiling aid)
@@ -4108,7 +4150,7 @@ static int topk_device(ls_task* t, const void* d_src, int pbytes, int64_t n, int
     CUDA_TRY(cudaMemcpyToSymbol(g_trace, &tr, sizeof(tr)));
   }
   fn<<<grid, TPB, sm, s>>>(t->d_task, d_src, pbytes, n, base_index, k, block_out, group_out, tickets, d_top_scores,
-                           d_top_index, d_valid, topk_buf(k), mins);
+                           d_top_index, d_valid, topk_buf(k), mins, wvalid);
   CUDA_TRY(cudaGetLastError());
   if (two) {
     const size_t msm = topk_state_bytes(topk_buf(k));
@@ -4120,13 +4162,16 @@ static int topk_device(ls_task* t, const void* d_src, int pbytes, int64_t n, int
     }
     const int g2 = (int)std::max<int64_t>(1, std::min<int64_t>(4 * t->num_sms, ((int64_t)grid * k + TPB - 1) / TPB));
     merge_filter_kernel<<<g2, TPB, msm, s>>>(block_out, mins, grid, k, group_out, tickets, d_top_scores, d_top_index,
-                                             topk_buf(k));
+                                             topk_buf(k), d_valid, wvalid);
     CUDA_TRY(cudaGetLastError());
   }
-  if (h_out) {  // scores | indices | count, contiguous from d_valid's 16-byte slot onwards
-    CUDA_TRY(cudaMemcpyAsync(h_out, ws + ws_keys + ctr_bytes - 16, 16 + out_bytes, cudaMemcpyDeviceToHost, s));
+  if (h_out) CUDA_TRY(cudaMemcpyAsync(h_out, out, out_bytes, cudaMemcpyDeviceToHost, s));
+  if (cached) {
+    std::lock_guard<std::mutex> g(t->mu);
+    t->ws_busy = false;
+  } else {
+    CUDA_TRY(cudaFreeAsync(ws, s));
   }
-  CUDA_TRY(cudaFreeAsync(ws, s));
   if (tr) {
     std::vector<unsigned long long> h((size_t)8 * grid);
     CUDA_TRY(cudaStreamSynchronize(s));
@@ -4159,16 +4204,9 @@ static int topk_device(ls_task* t, const void* d_src, int pbytes, int64_t n, int
 static int score_topk_any(ls_task* t, const void* d_src, int pbytes, int64_t n, int64_t base_index, int32_t k,
                           double* d_top_scores, int64_t* d_top_index, int64_t* d_n_valid, cudaStream_t s) {
   CUDA_TRY(cudaSetDevice(t->device));
-  unsigned long long* valid = reinterpret_cast<unsigned long long*>(d_n_valid);
-  unsigned long long* tmp = nullptr;
-  if (!valid) {
-    CUDA_TRY(cudaMallocAsync(&tmp, sizeof(unsigned long long), s));
-    valid = tmp;
-  }
-  CUDA_TRY(cudaMemsetAsync(valid, 0, sizeof(unsigned long long), s));
-  int rc = topk_device(t, d_src, pbytes, n, base_index, k, d_top_scores, d_top_index, valid, s);
-  if (tmp) cudaFreeAsync(tmp, s);
-  return rc;
+  // the launch writes the count (no memset): d_n_valid may be null
+  return topk_device(t, d_src, pbytes, n, base_index, k, d_top_scores, d_top_index,
+                     reinterpret_cast<unsigned long long*>(d_n_valid), s);
 }
 
 int ls_score_topk(ls_task* t, const ls_record* d_records, int64_t n, int64_t base_index, int32_t k,
@@ -4427,10 +4465,9 @@ static int score_topk_host_any(ls_task* t, const void* h_src, int pbytes, int64_
     CUDA_TRY(cudaMallocAsync(&buf[b], esz * (size_t)std::min(CH, std::max<int64_t>(n, 1)), s));
   CUDA_TRY(cudaMallocAsync(&ls, sizeof(double) * nch * k, s));
   CUDA_TRY(cudaMallocAsync(&li, sizeof(int64_t) * nch * k, s));
-  CUDA_TRY(cudaMallocAsync(&valid, sizeof(unsigned long long), s));
+  CUDA_TRY(cudaMallocAsync(&valid, sizeof(unsigned long long) * nch, s));  // one count per chunk
   CUDA_TRY(cudaMallocAsync(&out_s, sizeof(double) * k, s));
   CUDA_TRY(cudaMallocAsync(&out_i, sizeof(int64_t) * k, s));
-  CUDA_TRY(cudaMemsetAsync(valid, 0, sizeof(unsigned long long), s));
   CUDA_TRY(cudaEventRecord(ev_start, s));
   CUDA_TRY(cudaStreamWaitEvent(cp, ev_start, 0));
   const unsigned char* src = reinterpret_cast<const unsigned char*>(h_src);
@@ -4441,15 +4478,15 @@ static int score_topk_host_any(ls_task* t, const void* h_src, int pbytes, int64_
     if (m > 0) CUDA_TRY(cudaMemcpyAsync(buf[b], src + off * esz, esz * m, cudaMemcpyHostToDevice, cp));
     CUDA_TRY(cudaEventRecord(ready[b], cp));
     CUDA_TRY(cudaStreamWaitEvent(s, ready[b], 0));
-    rc = topk_device(t, buf[b], pbytes, std::max<int64_t>(m, 0), base_index + off, k, ls + c * k, li + c * k, valid,
+    rc = topk_device(t, buf[b], pbytes, std::max<int64_t>(m, 0), base_index + off, k, ls + c * k, li + c * k, valid + c,
                      s);
     CUDA_TRY(cudaEventRecord(freed[b], s));
   }
   if (rc == LS_E_OK) rc = ls_topk_merge(ls, li, (int32_t)nch, k, k, out_s, out_i, s);
   CUDA_TRY(cudaMemcpyAsync(h_top_scores, out_s, sizeof(double) * k, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaMemcpyAsync(h_top_index, out_i, sizeof(int64_t) * k, cudaMemcpyDeviceToHost, s));
-  unsigned long long hv = 0;
-  CUDA_TRY(cudaMemcpyAsync(&hv, valid, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  std::vector<unsigned long long> hvs((size_t)nch, 0);
+  CUDA_TRY(cudaMemcpyAsync(hvs.data(), valid, sizeof(unsigned long long) * nch, cudaMemcpyDeviceToHost, s));
   for (int b = 0; b < 2; ++b) cudaFreeAsync(buf[b], s);
   cudaFreeAsync(ls, s);
   cudaFreeAsync(li, s);
@@ -4464,6 +4501,8 @@ static int score_topk_host_any(ls_task* t, const void* h_src, int pbytes, int64_
     cudaEventDestroy(ready[b]);
     cudaEventDestroy(freed[b]);
   }
+  unsigned long long hv = 0;
+  for (unsigned long long v : hvs) hv += v;
   if (h_n_valid) *h_n_valid = (int64_t)hv;
   return rc;
 }

@@ -168,7 +168,7 @@ class Task:
         if out is None:
             out = (torch.empty(k, dtype=torch.float64, device=dev),
                    torch.empty(k, dtype=torch.int64, device=dev),
-                   torch.zeros(1, dtype=torch.int64, device=dev))
+                   torch.empty(1, dtype=torch.int64, device=dev))  # written by the launch
         s, i, nv = out
         _check(lib().ls_score_topk(self._h, _dptr(d_records), d_records.shape[0], int(base_index), int(k),
                                    _dptr(s), _dptr(i), _dptr(nv), _stream(torch, stream)), "ls_score_topk")
@@ -214,7 +214,7 @@ class Task:
         if out is None:
             out = (torch.empty(k, dtype=torch.float64, device=dev),
                    torch.empty(k, dtype=torch.int64, device=dev),
-                   torch.zeros(1, dtype=torch.int64, device=dev))
+                   torch.empty(1, dtype=torch.int64, device=dev))  # written by the launch
         s, i, nv = out
         _check(lib().ls_score_topk_points(self._h, _dptr(d_points), d_points.element_size(), d_points.shape[0],
                                           int(base_index), int(k), _dptr(s), _dptr(i), _dptr(nv),
