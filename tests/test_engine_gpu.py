@@ -365,3 +365,26 @@ def test_topk_selection_ties(torch, k):
     assert (ti.cpu().numpy() - 11).tolist() == want.tolist()
     assert np.array_equal(ts.cpu().numpy(), sc[want])
     task.close()
+
+
+@pytest.mark.parametrize("n", [97, 100_003, 1 << 20])
+def test_pinned_host_points_mapped(torch, n):
+    """Pinned host points (read zero-copy through the mapping by the scoring kernel) == the
+    device-resident call: identical top-k and valid count, repeatedly (cached staging reuse)."""
+    E = _engine()
+    from paper_2104_14641_b200 import workloads as W
+    from paper_2104_14641_b200.pack import SpaceTemplate
+    st = SpaceTemplate(W.program(W.conv2d_json()), W.conv_space(4096, 1))
+    from paper_2104_14641_b200.arch import KernelLaunch, load_arch
+    task = E.Task(st.template.desc(load_arch("x86-avx2"), KernelLaunch.from_json(W.KERNEL_LAUNCH)), 0)
+    task.set_space(st.space_desc())
+    assert task.points_path == 3
+    pts = st.points_from_indices(W.distinct_indices(st.sizes, n, 31))
+    dev = torch.from_numpy(pts.view(np.int32)).cuda()
+    pin = torch.from_numpy(pts.view(np.int32)).pin_memory()
+    ds, di, dn = task.score_topk_points(dev, 64, base_index=5)
+    torch.cuda.synchronize()
+    for _ in range(3):
+        hs, hi, hn = task.score_topk_points_host(pin, 64, base_index=5)
+        assert hi.tolist() == di.cpu().tolist() and np.array_equal(hs, ds.cpu().numpy()) and hn == int(dn.item())
+    task.close()

@@ -12,7 +12,7 @@ timeout 900 python bench.py --workload resnet50-es --steps 3 --warmup 3 > gpurun
 timeout 900 python bench.py --workload sweep --steps 8 > gpurun_out/bench_sweep.log 2>&1; echo sweep=$?
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-baseline > gpurun_out/ncu_launch.log 2>&1; echo ncu1=$?
 timeout 600 ncu --set full --import-source on --clock-control none --kernel-name-base demangled \
-  -k "regex:score_topk_kernel<.int.3, .int.4, .int.4, .int.1>" -s 2 -c 1 -o gpurun_out/pts_full_r01 \
+  -k "regex:score_topk_kernel<.int.3, .int.4, .int.5, .int.1>" -s 2 -c 1 -o gpurun_out/pts_full_r01 \
   python bench.py --steps 2 --warmup 1 --no-baseline > gpurun_out/ncu_full.log 2>&1; echo ncu2=$?
 ncu -i gpurun_out/pts_full_r01.ncu-rep --page source --csv --print-source cuda,sass > gpurun_out/pts_src_r01.csv 2>/dev/null
 for f in bench bench_ref bench_volta bench_bert bench_res bench_sweep; do tail -n 1 gpurun_out/$f.log | cut -c1-300; done
