@@ -35,7 +35,7 @@ UNIT = "candidates/s"
 REORDERS = 4096  # 3136 tile points x 4096 chain orders = 12.8M distinct candidates (>= 8 x 2^20)
 RECORD_BYTES = 32
 POINT_BYTES = 4
-PROFILE_JSON = "ncu_score_topk_r01.json"
+PROFILE_JSON = "ncu_score_topk_r01_space.json"
 
 
 def parse():
@@ -370,7 +370,7 @@ def b200_arm(args):
                              "topk_equals_points_path": same_paths and e2e_rtop.tolist() == top_i.tolist()},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "score_topk_kernel<3,4,4,1> (space path: point decode + fused walk/closed forms + "
+                         "kernel": "score_topk_kernel<3,4,5,1> (space path: point decode + fused 32-bit walk/closed forms + "
                                    "block radix-select top-k) + merge_filter_kernel (minima-bound merge); one "
                                    "ls_score_topk_points call",
                          "kernel_ms": kavg * 1e3, "algorithmic_bytes_per_launch": alg_bytes,

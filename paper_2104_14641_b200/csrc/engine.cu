@@ -2667,15 +2667,22 @@ __device__ __forceinline__ void topk_offer(TopkState& S, bool has, const Key& ke
 }
 
 constexpr int TK_GROUP = 16;  // blocks per first-level merge group
+constexpr int TK_DYN_CTR = 1023;  // tickets[] slot of the dynamic round counter
 
 // Phase timestamps of the fused kernel (LS_TRACE=1, tools/ only): per block
 // [start, staged, main loop done, block list written, group merged, final written].
+constexpr int TR_SLOTS = 9;  // 8 timestamps + the SM id
 __device__ unsigned long long* g_trace = nullptr;
 __device__ __forceinline__ void trace_mark(int slot) {
   if (g_trace && threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    g_trace[blockIdx.x * 8 + slot] = t;
+    g_trace[blockIdx.x * TR_SLOTS + slot] = t;
+    if (slot == 0) {
+      unsigned sm;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      g_trace[blockIdx.x * TR_SLOTS + 8] = sm;
+    }
   }
 }
 
@@ -2824,8 +2831,9 @@ __global__ void __launch_bounds__(TPB) merge_filter_kernel(const Key* __restrict
   __shared__ unsigned int s_ticket;
   __shared__ Key s_T;
   TopkState& S = *reinterpret_cast<TopkState*>(raw);
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the scoring grid is complete and visible
   trace_mark(4);
-  // T: the k-th smallest block minimum (bitonic sort of the minima in shared memory)
+  // T: the k-th smallest block minimum
   Key* B = S.buf();
   __shared__ int s_n;
   if (threadIdx.x == 0) {
@@ -2840,12 +2848,14 @@ __global__ void __launch_bounds__(TPB) merge_filter_kernel(const Key* __restrict
   }
   __syncthreads();
   const int nm = s_n;
-  if (nm >= k) {
-    bitonic_sort(B, nm);
-    if (threadIdx.x == 0) s_T = B[k - 1];
+  if (nm > k) {  // radix selection of the k-th minimum (the block buffer's select, no sort)
+    if (threadIdx.x == 0) S.cnt = nm;
+    __syncthreads();
+    topk_select(S, k);
+    if (threadIdx.x == 0) s_T = S.thr;
   }
   __syncthreads();
-  const Key T = s_T;  // +inf (no filtering) when there are fewer than k minima
+  const Key T = s_T;  // +inf (no filtering) when there are at most k minima
   trace_mark(5);
   const int64_t m = (int64_t)nblk * k;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
@@ -2860,7 +2870,7 @@ __global__ void __launch_bounds__(TPB) merge_filter_kernel(const Key* __restrict
   if (s_ticket != gridDim.x - 1) return;
   __threadfence();
   const int c = (int)__ldcg(&ctr[0]);
-  if (g_trace && threadIdx.x == 0) g_trace[blockIdx.x * 8 + 3] = 1000000000000ull + (unsigned long long)c;
+  if (g_trace && threadIdx.x == 0) g_trace[blockIdx.x * TR_SLOTS + 3] = (1ull << 63) | (unsigned long long)c;
   Key* buf = S.buf();
   if (c <= (int)blockDim.x) {  // rank the survivors directly; the k smallest land at their rank
     __syncthreads();
@@ -2887,6 +2897,7 @@ __global__ void __launch_bounds__(TPB) merge_filter_kernel(const Key* __restrict
     if (n_valid) *n_valid = v;
     ctr[0] = 0;
     ctr[1] = 0;
+    ctr[TK_DYN_CTR] = 0;
   }
   trace_mark(7);
 }
@@ -2915,32 +2926,51 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kern
   trace_mark(1);
   unsigned int valid = 0;
   int safe = 1;
-  // every block takes a contiguous range of ceil(n / grid) candidates, so all
-  // blocks run the same number of rounds and the work per SM is balanced
-  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
-  const int64_t b0 = min(n, (int64_t)blockIdx.x * per), b1 = min(n, b0 + per);
-  const int64_t stride = TPB;
-  uint64_t xn = 0;  // space path: the next point, loaded one iteration ahead
+  // Rounds of TPB candidates.  Each block owns a contiguous static share of
+  // 3/4 of all rounds; the rest are handed out one round at a time from a
+  // global counter (tickets[TK_DYN_CTR]), so blocks the SM's warp scheduler
+  // favours take more of them and every SM finishes together.  The round after
+  // next is known one round ahead (block-uniform), so the next round's points
+  // are prefetched; a dynamic round's base is published through s_nb at a
+  // barrier.
+  __shared__ int64_t s_nb[2], s_first[2];
+  unsigned int* const dyn_ctr = tickets + TK_DYN_CTR;
+  const int64_t rounds = (n + TPB - 1) / TPB;
+  const int64_t st_rounds = rounds * 3 / 4 / gridDim.x;  // static rounds per block
+  const int64_t dyn0 = st_rounds * gridDim.x * TPB;     // first dynamically distributed candidate
+  const int64_t sb0 = (int64_t)blockIdx.x * st_rounds * TPB;
+  auto round_base = [&](int64_t r) -> int64_t {  // thread 0: base of the block's round r
+    return r < st_rounds ? sb0 + r * TPB : dyn0 + (int64_t)atomicAdd(dyn_ctr, 1u) * TPB;
+  };
+  if (threadIdx.x == 0) {
+    s_first[0] = round_base(0);
+    s_first[1] = round_base(1);
+  }
+  __syncthreads();
+  int64_t base = s_first[0], nb = s_first[1];
+  uint64_t xn = 0;  // space path: the next point, loaded one round ahead
   if constexpr (MODE == 4 || MODE == 5)
-    if (b0 + threadIdx.x < b1) xn = load_point(src, pbytes, b0 + threadIdx.x);
-  for (int64_t base = b0; base < b0 + per; base += stride) {
+    if (base + threadIdx.x < n) xn = load_point(src, pbytes, base + threadIdx.x);
+  for (int64_t r = 0; base < n; ++r) {
+    const bool dyn = r + 2 >= st_rounds;  // block-uniform: round r + 2 is dynamic
+    if (dyn && threadIdx.x == 0) s_nb[r & 1] = round_base(r + 2);
     const int64_t i = base + threadIdx.x;
     bool has = false;
     Key key;
-    if (i < b1) {
-      ls_record r;
+    if (i < n) {
+      ls_record r_;
       uint32_t kt[4];
       double f[LS_NFEAT_GPU];
       double s;
       int st;
       if constexpr (MODE == 4 || MODE == 5) {
         const uint64_t x = xn;
-        if (i + stride < b1) xn = load_point(src, pbytes, i + stride);
+        if (nb + threadIdx.x < n) xn = load_point(src, pbytes, nb + threadIdx.x);
         st = eval_space<TM, MODE == 5>(T, tab, x, ev.fc, f, &s);
       } else {
         uint32_t pch = 0;
-        st = load_cand<SRC, MODE == 3>(T, src, pbytes, i, r, kt, pch);
-        if (st == LS_OK) st = ev(T, r, kt, pch, f, &s);
+        st = load_cand<SRC, MODE == 3>(T, src, pbytes, i, r_, kt, pch);
+        if (st == LS_OK) st = ev(T, r_, kt, pch, f, &s);
       }
       if (st == LS_OK) {
         key.s = order_bits(s);
@@ -2950,11 +2980,19 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kern
       }
     }
     topk_offer(S, has, key, k, safe);
+    base = nb;
+    if (dyn) {
+      __syncthreads();
+      nb = s_nb[r & 1];
+    } else {
+      nb = sb0 + (r + 2) * TPB;
+    }
   }
   for (int off = 16; off > 0; off >>= 1) valid += __shfl_down_sync(0xffffffffu, valid, off);
   if ((threadIdx.x & 31) == 0 && valid) atomicAdd(wvalid, (unsigned long long)valid);
   __syncthreads();
   trace_mark(2);
+  if (mins) asm volatile("griddepcontrol.launch_dependents;");  // the merge launch may be scheduled now
   const int kept0 = topk_select(S, k);
   write_keys(S, kept0, k, block_out + (int64_t)blockIdx.x * k);
   if (mins) {  // second stage: merge_filter_kernel
@@ -2990,6 +3028,7 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kern
     const unsigned long long v = atomicExch(wvalid, 0ull);
     if (n_valid) *n_valid = v;
     for (int q = 0; q <= ngroups; ++q) tickets[q] = 0;
+    tickets[TK_DYN_CTR] = 0;
   }
   trace_mark(5);
 }
@@ -4145,8 +4184,8 @@ static int topk_device(ls_task* t, const void* d_src, int pbytes, int64_t n, int
   unsigned long long* tr = nullptr;
   const char* tr_env = getenv("LS_TRACE");
   if (tr_env && tr_env[0] == '1') {  // phase timestamps to stderr (profiling aid)
-    CUDA_TRY(cudaMalloc(&tr, sizeof(unsigned long long) * 8 * grid));
-    CUDA_TRY(cudaMemset(tr, 0, sizeof(unsigned long long) * 8 * grid));
+    CUDA_TRY(cudaMalloc(&tr, sizeof(unsigned long long) * TR_SLOTS * grid));
+    CUDA_TRY(cudaMemset(tr, 0, sizeof(unsigned long long) * TR_SLOTS * grid));
     CUDA_TRY(cudaMemcpyToSymbol(g_trace, &tr, sizeof(tr)));
   }
   fn<<<grid, TPB, sm, s>>>(t->d_task, d_src, pbytes, n, base_index, k, block_out, group_out, tickets, d_top_scores,
@@ -4161,9 +4200,23 @@ static int topk_device(ls_task* t, const void* d_src, int pbytes, int64_t n, int
       attr = true;
     }
     const int g2 = (int)std::max<int64_t>(1, std::min<int64_t>(4 * t->num_sms, ((int64_t)grid * k + TPB - 1) / TPB));
-    merge_filter_kernel<<<g2, TPB, msm, s>>>(block_out, mins, grid, k, group_out, tickets, d_top_scores, d_top_index,
-                                             topk_buf(k), d_valid, wvalid);
-    CUDA_TRY(cudaGetLastError());
+    // programmatic dependent launch: the merge is queued behind the scoring
+    // launch's tail (its blocks wait in griddepcontrol.wait for the scoring
+    // grid's completion and memory), not behind a full kernel boundary
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)g2);
+    cfg.blockDim = dim3(TPB);
+    cfg.dynamicSmemBytes = msm;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const Key* cbo = block_out;
+    const Key* cmins = mins;
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, merge_filter_kernel, cbo, cmins, grid, k, group_out, tickets, d_top_scores,
+                                d_top_index, topk_buf(k), d_valid, wvalid));
   }
   if (h_out) CUDA_TRY(cudaMemcpyAsync(h_out, out, out_bytes, cudaMemcpyDeviceToHost, s));
   if (cached) {
@@ -4173,22 +4226,22 @@ static int topk_device(ls_task* t, const void* d_src, int pbytes, int64_t n, int
     CUDA_TRY(cudaFreeAsync(ws, s));
   }
   if (tr) {
-    std::vector<unsigned long long> h((size_t)8 * grid);
+    std::vector<unsigned long long> h((size_t)TR_SLOTS * grid);
     CUDA_TRY(cudaStreamSynchronize(s));
     CUDA_TRY(cudaMemcpy(h.data(), tr, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost));
     unsigned long long* nul = nullptr;
     CUDA_TRY(cudaMemcpyToSymbol(g_trace, &nul, sizeof(nul)));
     cudaFree(tr);
     unsigned long long t0 = ~0ull, surv = 0;
-    for (int b = 0; b < grid; ++b) t0 = std::min(t0, h[b * 8]);
+    for (int b = 0; b < grid; ++b) t0 = std::min(t0, h[b * TR_SLOTS]);
     for (int b = 0; b < grid; ++b)
-      if (h[b * 8 + 3] >= 1000000000000ull) surv = h[b * 8 + 3] - 1000000000000ull, h[b * 8 + 3] = 0;
+      if (h[b * TR_SLOTS + 3] >> 63) surv = h[b * TR_SLOTS + 3] & ~(1ull << 63), h[b * TR_SLOTS + 3] = 0;
     double avg[8] = {0}, mx[8] = {0};
     for (int q = 0; q < 8; ++q) {
       int cnt = 0;
       for (int b = 0; b < grid; ++b)
-        if (h[b * 8 + q] > t0) {
-          const double v = (double)(h[b * 8 + q] - t0) / 1e3;
+        if (h[b * TR_SLOTS + q] > t0) {
+          const double v = (double)(h[b * TR_SLOTS + q] - t0) / 1e3;
           avg[q] += v, mx[q] = std::max(mx[q], v), ++cnt;
         }
       if (cnt) avg[q] /= cnt;
@@ -4197,6 +4250,23 @@ static int topk_device(ls_task* t, const void* d_src, int pbytes, int64_t n, int
             "tree group %.1f final %.1f | two-stage start %.1f T %.1f filtered %.1f final %.1f survivors %llu\n",
             (long long)n, grid, avg[1], mx[1], avg[2], mx[2], avg[3], mx[3], mx[4], mx[5], mx[4], mx[5], mx[6],
             mx[7], surv);
+    if (getenv("LS_TRACE_BLOCKS")) {  // per-block main-loop ends
+      std::vector<std::pair<double, int>> e;
+      for (int b = 0; b < grid; ++b)
+        if (h[b * TR_SLOTS + 2] > t0) e.push_back({(double)(h[b * TR_SLOTS + 2] - t0) / 1e3, b});
+      std::sort(e.begin(), e.end());
+      fprintf(stderr, "LS_TRACE blocks (main end us, block, sm, start us):");
+      for (size_t q = 0; q < e.size(); q += std::max<size_t>(1, e.size() / 24)) {
+        const int b = e[q].second;
+        fprintf(stderr, " %.1f/%d/%llu/%.1f", e[q].first, b, h[b * TR_SLOTS + 8], (double)(h[b * TR_SLOTS] - t0) / 1e3);
+      }
+      if (!e.empty()) {
+        const int b = e.back().second;
+        fprintf(stderr, " | max %.1f/%d/%llu/%.1f", e.back().first, b, h[b * TR_SLOTS + 8],
+                (double)(h[b * TR_SLOTS] - t0) / 1e3);
+      }
+      fprintf(stderr, "\n");
+    }
   }
   return LS_E_OK;
 }

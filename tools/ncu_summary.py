@@ -1,6 +1,8 @@
 """Summarise an ncu --set full report of the scoring kernel into profiles/*.json.
 
-    python tools/ncu_summary.py gpurun_out/prof.ncu-rep profiles/ncu_score_topk_r01.json [n_candidates]
+    python tools/ncu_summary.py gpurun_out/prof.ncu-rep profiles/ncu_score_topk_r01.json [n_candidates [bytes_per_candidate]]
+
+bytes_per_candidate: 4 for space points (the bench headline), 32 for ls_record (default).
 
 Reads the report here (no GPU needed): duration, DRAM bytes per launch (the
 `traffic` of bench.py's roofline), issue/occupancy/divergence counters and
@@ -36,6 +38,7 @@ def to_bytes(v, u):
 def main():
     rep, out = sys.argv[1], sys.argv[2]
     n = int(sys.argv[3]) if len(sys.argv) > 3 else None
+    bpc = int(sys.argv[4]) if len(sys.argv) > 4 else 32
     m = raw(rep)
     g = lambda k: num(m[k][0]) if k in m else None  # noqa: E731
     rd = to_bytes(g("dram__bytes_read.sum"), m["dram__bytes_read.sum"][1])
@@ -67,7 +70,7 @@ def main():
     }
     if n:
         summary["candidates_per_launch"] = n
-        summary["algorithmic_bytes_per_launch"] = 32 * n
+        summary["algorithmic_bytes_per_launch"] = bpc * n
         wi = (g("smsp__inst_executed.sum") or 0) / n
         summary["warp_issue_slots_per_candidate"] = wi
         summary["thread_instructions_per_candidate"] = (g("thread_inst_executed") or 0) / n
