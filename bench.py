@@ -79,7 +79,9 @@ def config_dict(args, n):
                         f"per step, score + top-{args.k} by (score, index)",
             "config": "BASELINE.json configs[1]", "arch": args.arch, "candidates_per_gpu": n, "k": args.k,
             "candidate_encoding": "space point (uint32 mixed-radix choice indices, 4 B)",
-            "l2": "flushed between timed steps (256 MiB write)"}
+            "l2": "flushed between timed steps (256 MiB write)",
+            "step": "one Task.score_topk_points call (Python API -> C-ABI, launch latency inside the timed region) "
+                    "writing the k best + count into preallocated output tensors (out=)"}
 
 
 # -- CPU baseline (the oracle port of the reference algorithm) ---------------------------------
@@ -242,13 +244,17 @@ def b200_arm(args):
     stream = torch.cuda.current_stream()
 
     def make_step(points: bool):
+        # steady-state caller: the k best + count land in the same output tensors every step (out=)
+        out = (torch.empty(k, dtype=torch.float64, device=dev), torch.empty(k, dtype=torch.int64, device=dev),
+               torch.empty(1, dtype=torch.int64, device=dev))
+
         def step(kev=None):
             if kev:
                 kev[0].record(stream)
             if points:
-                s, i, nv = task.score_topk_points(d_pts, k, base_index=base)
+                s, i, nv = task.score_topk_points(d_pts, k, base_index=base, out=out)
             else:
-                s, i, nv = task.score_topk(d_rec, k, base_index=base)
+                s, i, nv = task.score_topk(d_rec, k, base_index=base, out=out)
             if kev:
                 kev[1].record(stream)
             if world > 1:

@@ -2499,6 +2499,19 @@ __device__ __forceinline__ unsigned long long warp_or64(unsigned long long x) {
          __reduce_or_sync(0xffffffffu, (unsigned)x);
 }
 
+// Warp-aggregated append: one atomic per warp for the lanes with pred set;
+// returns the lane's slot (or -1).  All 32 lanes of the warp must call it.
+template <typename C>
+__device__ __forceinline__ int warp_append(C* ctr, bool pred) {
+  const unsigned m = __ballot_sync(0xffffffffu, pred);
+  if (!m) return -1;
+  const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+  C b = 0;
+  if (lane == leader) b = atomicAdd(ctr, (C)__popc(m));
+  b = __shfl_sync(0xffffffffu, b, leader);
+  return pred ? (int)b + __popc(m & ((1u << lane) - 1u)) : -1;
+}
+
 __device__ int topk_select(TopkState& S, int k) {
   const int c = S.cnt;
   if (c <= k) return c;
@@ -2629,8 +2642,10 @@ __device__ int topk_select(TopkState& S, int k) {
     }
     __syncthreads();
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (kp[q]) W[atomicAdd(&S.cnt2, 1)] = keep[q];
+    for (int q = 0; q < 4; ++q) {
+      const int slot = warp_append(&S.cnt2, kp[q]);
+      if (slot >= 0) W[slot] = keep[q];
+    }
     __syncthreads();
   }
   if (threadIdx.x == 0) S.cnt = S.cnt2;
@@ -2651,7 +2666,7 @@ __device__ __forceinline__ void topk_init(TopkState& S, int cap) {
 // Insert-if-better without a barrier; the block synchronises only when the
 // buffer could overflow within the next round (`safe` rounds are free).
 __device__ __forceinline__ void topk_offer(TopkState& S, bool has, const Key& key, int k, int& safe) {
-  if (has && kless(key, S.thr)) {
+  if (has && kless(key, S.thr)) {  // rare after the first rounds: a plain atomic beats a warp vote
     const int slot = atomicAdd(&S.cnt, 1);
     S.buf()[slot] = key;
   }
@@ -2672,8 +2687,8 @@ constexpr int TK_DYN_CTR = 1023;  // tickets[] slot of the dynamic round counter
 // Phase timestamps of the fused kernel (LS_TRACE=1, tools/ only): per block
 // [start, staged, main loop done, block list written, group merged, final written].
 constexpr int TR_SLOTS = 9;  // 8 timestamps + the SM id
-__device__ unsigned long long* g_trace = nullptr;
-__device__ __forceinline__ void trace_mark(int slot) {
+// (the trace buffer is a kernel parameter: no global load at kernel start when off)
+__device__ __forceinline__ void trace_mark(unsigned long long* g_trace, int slot) {
   if (g_trace && threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -2713,9 +2728,11 @@ __device__ int merge_into(TopkState& S, const Key* src, int64_t m, int k, bool s
       }
       const Key thr = S.thr;
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (has[q] && !(key[q].s == KEY_INF_S && key[q].i == KEY_INF_I) && kless(key[q], thr))
-          S.buf()[atomicAdd(&S.cnt, 1)] = key[q];
+      for (int q = 0; q < 4; ++q) {
+        const int slot =
+            warp_append(&S.cnt, has[q] && !(key[q].s == KEY_INF_S && key[q].i == KEY_INF_I) && kless(key[q], thr));
+        if (slot >= 0) S.buf()[slot] = key[q];
+      }
     }
     __syncthreads();
     topk_select(S, k);
@@ -2826,13 +2843,14 @@ __global__ void __launch_bounds__(TPB) merge_filter_kernel(const Key* __restrict
                                                            Key* __restrict__ surv, unsigned int* __restrict__ ctr,
                                                            double* __restrict__ out_s, int64_t* __restrict__ out_i,
                                                            int cap, unsigned long long* __restrict__ n_valid,
-                                                           unsigned long long* __restrict__ wvalid) {
+                                                           unsigned long long* __restrict__ wvalid,
+                                                           unsigned long long* __restrict__ g_trace) {
   extern __shared__ __align__(16) unsigned char raw[];
   __shared__ unsigned int s_ticket;
   __shared__ Key s_T;
   TopkState& S = *reinterpret_cast<TopkState*>(raw);
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the scoring grid is complete and visible
-  trace_mark(4);
+  trace_mark(g_trace, 4);
   // T: the k-th smallest block minimum
   Key* B = S.buf();
   __shared__ int s_n;
@@ -2842,9 +2860,14 @@ __global__ void __launch_bounds__(TPB) merge_filter_kernel(const Key* __restrict
     s_T.i = KEY_INF_I;
   }
   __syncthreads();
-  for (int j = threadIdx.x; j < nblk; j += blockDim.x) {
-    const Key x = ld_key_cg(mins + j);
-    if (!(x.s == KEY_INF_S && x.i == KEY_INF_I)) B[atomicAdd(&s_n, 1)] = x;
+  for (int j0 = 0; j0 < nblk; j0 += blockDim.x) {  // block-uniform trip count (warp appends)
+    const int j = j0 + threadIdx.x;
+    Key x;
+    x.s = KEY_INF_S;
+    x.i = KEY_INF_I;
+    if (j < nblk) x = ld_key_cg(mins + j);
+    const int slot = warp_append(&s_n, !(x.s == KEY_INF_S && x.i == KEY_INF_I));
+    if (slot >= 0) B[slot] = x;
   }
   __syncthreads();
   const int nm = s_n;
@@ -2856,17 +2879,26 @@ __global__ void __launch_bounds__(TPB) merge_filter_kernel(const Key* __restrict
   }
   __syncthreads();
   const Key T = s_T;  // +inf (no filtering) when there are at most k minima
-  trace_mark(5);
-  const int64_t m = (int64_t)nblk * k;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
-    const Key x = ld_key_cg(block_out + i);
-    if (!(x.s == KEY_INF_S && x.i == KEY_INF_I) && !kless(T, x)) surv[atomicAdd(&ctr[0], 1u)] = x;
+  trace_mark(g_trace, 5);
+  const unsigned int* cnts = reinterpret_cast<const unsigned int*>(mins + nblk);
+  for (int b = blockIdx.x; b < nblk; b += gridDim.x) {  // block b's list: cnts[b] keys at b * cap
+    const int cb = (int)__ldcg(cnts + b);
+    const Key* lst = block_out + (int64_t)b * cap;
+    for (int j0 = 0; j0 < cb; j0 += blockDim.x) {
+      const int j = j0 + threadIdx.x;
+      Key x;
+      x.s = KEY_INF_S;
+      x.i = KEY_INF_I;
+      if (j < cb) x = ld_key_cg(lst + j);
+      const int slot = warp_append(&ctr[0], j < cb && !kless(T, x));
+      if (slot >= 0) surv[slot] = x;
+    }
   }
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) s_ticket = atomicAdd(&ctr[1], 1u);
   __syncthreads();
-  trace_mark(6);
+  trace_mark(g_trace, 6);
   if (s_ticket != gridDim.x - 1) return;
   __threadfence();
   const int c = (int)__ldcg(&ctr[0]);
@@ -2899,7 +2931,7 @@ __global__ void __launch_bounds__(TPB) merge_filter_kernel(const Key* __restrict
     ctr[1] = 0;
     ctr[TK_DYN_CTR] = 0;
   }
-  trace_mark(7);
+  trace_mark(g_trace, 7);
 }
 
 // Fused pass: score every record, keep the block's k best, then merge the
@@ -2911,11 +2943,11 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kern
     const DTask* __restrict__ gtask, const void* __restrict__ src, int pbytes, int64_t n, int64_t base_index, int k,
     Key* __restrict__ block_out, Key* __restrict__ group_out, unsigned int* __restrict__ tickets,
     double* __restrict__ out_s, int64_t* __restrict__ out_i, unsigned long long* __restrict__ n_valid, int cap,
-    Key* __restrict__ mins, unsigned long long* __restrict__ wvalid) {
+    Key* __restrict__ mins, unsigned long long* __restrict__ wvalid, unsigned long long* __restrict__ g_trace) {
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ unsigned int s_ticket;
   DTask& T = *reinterpret_cast<DTask*>(dyn);
-  trace_mark(0);
+  trace_mark(g_trace, 0);
   stage_task(T, gtask);
   unsigned char* p = dyn + T.task_bytes;
   const int32_t* tab = stage_tab<MODE>(p, T);
@@ -2923,7 +2955,7 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kern
   TopkState& S = *reinterpret_cast<TopkState*>(p);
   Evaluator<TM, RM, MODE> ev(T, p + align16(topk_state_bytes(cap)), tab);
   topk_init(S, cap);
-  trace_mark(1);
+  trace_mark(g_trace, 1);
   unsigned int valid = 0;
   int safe = 1;
   // Rounds of TPB candidates.  Each block owns a contiguous static share of
@@ -2991,16 +3023,21 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kern
   for (int off = 16; off > 0; off >>= 1) valid += __shfl_down_sync(0xffffffffu, valid, off);
   if ((threadIdx.x & 31) == 0 && valid) atomicAdd(wvalid, (unsigned long long)valid);
   __syncthreads();
-  trace_mark(2);
-  if (mins) asm volatile("griddepcontrol.launch_dependents;");  // the merge launch may be scheduled now
-  const int kept0 = topk_select(S, k);
-  write_keys(S, kept0, k, block_out + (int64_t)blockIdx.x * k);
-  if (mins) {  // second stage: merge_filter_kernel
-    write_block_min(S, kept0, mins + blockIdx.x);
-    trace_mark(3);
+  trace_mark(g_trace, 2);
+  if (mins) {  // second stage (merge_filter_kernel): the whole buffer, a superset of the
+               // block's k best (a key leaves it only below k smaller ones), its count and minimum
+    asm volatile("griddepcontrol.launch_dependents;");  // the merge launch may be scheduled now
+    const int cnt = S.cnt;
+    Key* dst = block_out + (int64_t)blockIdx.x * cap;
+    for (int j = threadIdx.x; j < cnt; j += blockDim.x) dst[j] = S.buf()[j];
+    if (threadIdx.x == 0) reinterpret_cast<unsigned int*>(mins + gridDim.x)[blockIdx.x] = (unsigned)cnt;
+    write_block_min(S, cnt, mins + blockIdx.x);
+    trace_mark(g_trace, 3);
     return;
   }
-  trace_mark(3);
+  const int kept0 = topk_select(S, k);
+  write_keys(S, kept0, k, block_out + (int64_t)blockIdx.x * k);
+  trace_mark(g_trace, 3);
 
   // ---- level 1: last block of the group merges the group's lists
   const int g = blockIdx.x / TK_GROUP;
@@ -3014,7 +3051,7 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kern
   __threadfence();
   int kept = merge_into(S, block_out + (int64_t)g * TK_GROUP * k, (int64_t)gsize * k, k, false);
   write_keys(S, kept, k, group_out + (int64_t)g * k);
-  trace_mark(4);
+  trace_mark(g_trace, 4);
   // ---- level 2: last group merger writes the final list
   __threadfence();
   __syncthreads();
@@ -3030,7 +3067,7 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kern
     for (int q = 0; q <= ngroups; ++q) tickets[q] = 0;
     tickets[TK_DYN_CTR] = 0;
   }
-  trace_mark(5);
+  trace_mark(g_trace, 5);
 }
 
 // Merge m keys (any order, +inf padded) into the k best, written as (score, index).
@@ -3862,7 +3899,7 @@ size_t smem_topk(const DTask& T, int k, int mode) { return smem_score(T, mode) +
 
 using ScoreFn = void (*)(const DTask*, const void*, int, int64_t, double*, double*, int32_t*);
 using TopkFn = void (*)(const DTask*, const void*, int, int64_t, int64_t, int, Key*, Key*, unsigned int*, double*,
-                       int64_t*, unsigned long long*, int, Key*, unsigned long long*);
+                       int64_t*, unsigned long long*, int, Key*, unsigned long long*, unsigned long long*);
 
 template <int SRC>
 ScoreFn score_fn_src(const DTask& T, int mode) {
@@ -4144,7 +4181,9 @@ static int topk_device(ls_task* t, const void* d_src, int pbytes, int64_t n, int
   // two-stage merge (block-minima bound, merge_filter_kernel) when the grid has plenty of
   // blocks per answer key; else the in-kernel merge tree
   const bool two = 4 * k <= grid && grid <= topk_buf(k);
-  const size_t keys_bytes = sizeof(Key) * (two ? (size_t)grid * (2 * k + 1) : ((size_t)grid + ngroups) * k);
+  // two-stage: [grid] buffers of topk_buf(k) keys, as many survivor slots, [grid] minima, [grid] counts
+  const size_t keys_bytes =
+      sizeof(Key) * (two ? (size_t)grid * (2 * (size_t)topk_buf(k) + 2) : ((size_t)grid + ngroups) * k);
   const size_t out_bytes = h_out ? 16 + 16 * (size_t)k : 0;
   const size_t ws_bytes = WS_CTR_BYTES + keys_bytes + out_bytes;
   unsigned char* ws = nullptr;
@@ -4173,8 +4212,8 @@ static int topk_device(ls_task* t, const void* d_src, int pbytes, int64_t n, int
   unsigned int* tickets = reinterpret_cast<unsigned int*>(ws);
   unsigned long long* wvalid = reinterpret_cast<unsigned long long*>(ws + 4096);
   Key* block_out = reinterpret_cast<Key*>(ws + WS_CTR_BYTES);
-  Key* group_out = block_out + (size_t)grid * k;   // tree: group lists; two-stage: survivors
-  Key* mins = two ? group_out + (size_t)grid * k : nullptr;
+  Key* group_out = block_out + (size_t)grid * (two ? topk_buf(k) : k);  // tree: group lists; two-stage: survivors
+  Key* mins = two ? group_out + (size_t)grid * topk_buf(k) : nullptr;
   unsigned char* out = ws + WS_CTR_BYTES + keys_bytes;
   if (h_out) {
     d_valid = reinterpret_cast<unsigned long long*>(out);
@@ -4186,10 +4225,9 @@ static int topk_device(ls_task* t, const void* d_src, int pbytes, int64_t n, int
   if (tr_env && tr_env[0] == '1') {  // phase timestamps to stderr (profiling aid)
     CUDA_TRY(cudaMalloc(&tr, sizeof(unsigned long long) * TR_SLOTS * grid));
     CUDA_TRY(cudaMemset(tr, 0, sizeof(unsigned long long) * TR_SLOTS * grid));
-    CUDA_TRY(cudaMemcpyToSymbol(g_trace, &tr, sizeof(tr)));
   }
   fn<<<grid, TPB, sm, s>>>(t->d_task, d_src, pbytes, n, base_index, k, block_out, group_out, tickets, d_top_scores,
-                           d_top_index, d_valid, topk_buf(k), mins, wvalid);
+                           d_top_index, d_valid, topk_buf(k), mins, wvalid, tr);
   CUDA_TRY(cudaGetLastError());
   if (two) {
     const size_t msm = topk_state_bytes(topk_buf(k));
@@ -4199,7 +4237,7 @@ static int topk_device(ls_task* t, const void* d_src, int pbytes, int64_t n, int
                            (int)topk_state_bytes(2048));
       attr = true;
     }
-    const int g2 = (int)std::max<int64_t>(1, std::min<int64_t>(4 * t->num_sms, ((int64_t)grid * k + TPB - 1) / TPB));
+    const int g2 = grid;  // one block list each
     // programmatic dependent launch: the merge is queued behind the scoring
     // launch's tail (its blocks wait in griddepcontrol.wait for the scoring
     // grid's completion and memory), not behind a full kernel boundary
@@ -4216,7 +4254,7 @@ static int topk_device(ls_task* t, const void* d_src, int pbytes, int64_t n, int
     const Key* cbo = block_out;
     const Key* cmins = mins;
     CUDA_TRY(cudaLaunchKernelEx(&cfg, merge_filter_kernel, cbo, cmins, grid, k, group_out, tickets, d_top_scores,
-                                d_top_index, topk_buf(k), d_valid, wvalid));
+                                d_top_index, topk_buf(k), d_valid, wvalid, tr));
   }
   if (h_out) CUDA_TRY(cudaMemcpyAsync(h_out, out, out_bytes, cudaMemcpyDeviceToHost, s));
   if (cached) {
@@ -4229,8 +4267,6 @@ static int topk_device(ls_task* t, const void* d_src, int pbytes, int64_t n, int
     std::vector<unsigned long long> h((size_t)TR_SLOTS * grid);
     CUDA_TRY(cudaStreamSynchronize(s));
     CUDA_TRY(cudaMemcpy(h.data(), tr, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost));
-    unsigned long long* nul = nullptr;
-    CUDA_TRY(cudaMemcpyToSymbol(g_trace, &nul, sizeof(nul)));
     cudaFree(tr);
     unsigned long long t0 = ~0ull, surv = 0;
     for (int b = 0; b < grid; ++b) t0 = std::min(t0, h[b * TR_SLOTS]);

@@ -68,15 +68,33 @@ def _check(rc: int, what: str):
         raise EngineError(f"{what} failed ({rc}): {lib().ls_last_error().decode()}")
 
 
+_cuda_ok = False
+
+
 def _torch():
+    global _cuda_ok
     import torch
-    if not torch.cuda.is_available():
-        raise EngineError("no CUDA device visible (there is no CPU fallback)")
+    if not _cuda_ok:  # checked once: the per-call wrappers stay a few microseconds
+        if not torch.cuda.is_available():
+            raise EngineError("no CUDA device visible (there is no CPU fallback)")
+        _cuda_ok = True
     return torch
 
 
-def _stream(torch, stream):
-    return (stream or torch.cuda.current_stream()).cuda_stream
+def _stream(torch, stream, device=None):
+    """Raw cudaStream_t: `stream`, else the current stream of `device` (default: current device)."""
+    if stream is not None:
+        return stream.cuda_stream
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    if raw is not None:
+        return raw(torch.cuda.current_device() if device is None else device)
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _outputs(torch, k, device):
+    """Fresh (scores f64[k], indices i64[k], count i64[1]); pass out= to reuse buffers across calls."""
+    return (torch.empty(k, dtype=torch.float64, device=device), torch.empty(k, dtype=torch.int64, device=device),
+            torch.empty(1, dtype=torch.int64, device=device))
 
 
 def _dptr(t):
@@ -165,13 +183,10 @@ class Task:
         """k best (score, global index) ascending + number of valid candidates (CUDA tensors)."""
         torch = _torch()
         dev = d_records.device
-        if out is None:
-            out = (torch.empty(k, dtype=torch.float64, device=dev),
-                   torch.empty(k, dtype=torch.int64, device=dev),
-                   torch.empty(1, dtype=torch.int64, device=dev))  # written by the launch
-        s, i, nv = out
+        s, i, nv = out if out is not None else _outputs(torch, k, dev)  # the count is written by the launch
         _check(lib().ls_score_topk(self._h, _dptr(d_records), d_records.shape[0], int(base_index), int(k),
-                                   _dptr(s), _dptr(i), _dptr(nv), _stream(torch, stream)), "ls_score_topk")
+                                   _dptr(s), _dptr(i), _dptr(nv), _stream(torch, stream, dev.index)),
+               "ls_score_topk")
         return s, i, nv
 
     def score_topk_host(self, h_records, k: int, base_index: int = 0, stream=None):
@@ -184,10 +199,9 @@ class Task:
         s = np.empty(k, np.float64)
         i = np.empty(k, np.int64)
         nv = np.zeros(1, np.int64)
-        with torch.cuda.device(self.device):
-            _check(lib().ls_score_topk_host(self._h, ptr, n, int(base_index), int(k), s.ctypes.data,
-                                            i.ctypes.data, nv.ctypes.data, _stream(torch, stream)),
-                   "ls_score_topk_host")
+        _check(lib().ls_score_topk_host(self._h, ptr, n, int(base_index), int(k), s.ctypes.data,
+                                        i.ctypes.data, nv.ctypes.data, _stream(torch, stream, self.device)),
+               "ls_score_topk_host")
         return s, i, int(nv[0])
 
 
@@ -211,14 +225,10 @@ class Task:
     def score_topk_points(self, d_points, k: int, base_index: int = 0, stream=None, out=None):
         torch = _torch()
         dev = d_points.device
-        if out is None:
-            out = (torch.empty(k, dtype=torch.float64, device=dev),
-                   torch.empty(k, dtype=torch.int64, device=dev),
-                   torch.empty(1, dtype=torch.int64, device=dev))  # written by the launch
-        s, i, nv = out
+        s, i, nv = out if out is not None else _outputs(torch, k, dev)  # the count is written by the launch
         _check(lib().ls_score_topk_points(self._h, _dptr(d_points), d_points.element_size(), d_points.shape[0],
                                           int(base_index), int(k), _dptr(s), _dptr(i), _dptr(nv),
-                                          _stream(torch, stream)), "ls_score_topk_points")
+                                          _stream(torch, stream, dev.index)), "ls_score_topk_points")
         return s, i, nv
 
     def score_topk_points_host(self, h_points, k: int, base_index: int = 0, stream=None):
@@ -232,10 +242,9 @@ class Task:
         s = np.empty(k, np.float64)
         i = np.empty(k, np.int64)
         nv = np.zeros(1, np.int64)
-        with torch.cuda.device(self.device):
-            _check(lib().ls_score_topk_points_host(self._h, ptr, eb, n, int(base_index), int(k), s.ctypes.data,
-                                                   i.ctypes.data, nv.ctypes.data, _stream(torch, stream)),
-                   "ls_score_topk_points_host")
+        _check(lib().ls_score_topk_points_host(self._h, ptr, eb, n, int(base_index), int(k), s.ctypes.data,
+                                               i.ctypes.data, nv.ctypes.data, _stream(torch, stream, self.device)),
+               "ls_score_topk_points_host")
         return s, i, int(nv[0])
 
 
