@@ -2683,6 +2683,8 @@ __device__ __forceinline__ void topk_offer(TopkState& S, bool has, const Key& ke
 
 constexpr int TK_GROUP = 16;  // blocks per first-level merge group
 constexpr int TK_DYN_CTR = 1023;  // tickets[] slot of the dynamic round counter
+constexpr int TK_FIN_CTR = 1022;  // tickets[] slot of the two-stage finish ticket
+constexpr int TK_MAXGRID = 2048;  // two-stage minima slots (grid <= topk_buf(k) <= 2048); slot TK_MAXGRID = T
 
 // Phase timestamps of the fused kernel (LS_TRACE=1, tools/ only): per block
 // [start, staged, main loop done, block list written, group merged, final written].
@@ -2851,36 +2853,38 @@ __global__ void __launch_bounds__(TPB) merge_filter_kernel(const Key* __restrict
   TopkState& S = *reinterpret_cast<TopkState*>(raw);
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the scoring grid is complete and visible
   trace_mark(g_trace, 4);
-  // T: the k-th smallest block minimum
+  // T: published by the scoring grid's (3/4 grid)-th finisher; else the k-th smallest block minimum
   Key* B = S.buf();
   __shared__ int s_n;
   if (threadIdx.x == 0) {
+    S.cap = cap;  // merge_into (many survivors) streams in chunks of cap - k
     s_n = 0;
-    s_T.s = KEY_INF_S;
-    s_T.i = KEY_INF_I;
+    s_T = ld_key_cg(mins + TK_MAXGRID);
+    if (s_T.s == KEY_INF_S) s_T.i = KEY_INF_I;
   }
   __syncthreads();
-  for (int j0 = 0; j0 < nblk; j0 += blockDim.x) {  // block-uniform trip count (warp appends)
-    const int j = j0 + threadIdx.x;
-    Key x;
-    x.s = KEY_INF_S;
-    x.i = KEY_INF_I;
-    if (j < nblk) x = ld_key_cg(mins + j);
-    const int slot = warp_append(&s_n, !(x.s == KEY_INF_S && x.i == KEY_INF_I));
-    if (slot >= 0) B[slot] = x;
-  }
-  __syncthreads();
-  const int nm = s_n;
-  if (nm > k) {  // radix selection of the k-th minimum (the block buffer's select, no sort)
-    if (threadIdx.x == 0) S.cnt = nm;
+  if (s_T.s == KEY_INF_S) {
+    for (int j0 = 0; j0 < nblk; j0 += blockDim.x) {  // block-uniform trip count (warp appends)
+      const int j = j0 + threadIdx.x;
+      Key x;
+      x.s = KEY_INF_S;
+      if (j < nblk) x = ld_key_cg(mins + j);
+      const int slot = warp_append(&s_n, x.s != KEY_INF_S);
+      if (slot >= 0) B[slot] = x;
+    }
     __syncthreads();
-    topk_select(S, k);
-    if (threadIdx.x == 0) s_T = S.thr;
+    const int nm = s_n;
+    if (nm > k) {  // radix selection of the k-th minimum (the block buffer's select, no sort)
+      if (threadIdx.x == 0) S.cnt = nm;
+      __syncthreads();
+      topk_select(S, k);
+      if (threadIdx.x == 0) s_T = S.thr;
+    }
+    __syncthreads();
   }
-  __syncthreads();
   const Key T = s_T;  // +inf (no filtering) when there are at most k minima
   trace_mark(g_trace, 5);
-  const unsigned int* cnts = reinterpret_cast<const unsigned int*>(mins + nblk);
+  const unsigned int* cnts = reinterpret_cast<const unsigned int*>(mins + TK_MAXGRID + 1);
   for (int b = blockIdx.x; b < nblk; b += gridDim.x) {  // block b's list: cnts[b] keys at b * cap
     const int cb = (int)__ldcg(cnts + b);
     const Key* lst = block_out + (int64_t)b * cap;
@@ -2930,6 +2934,12 @@ __global__ void __launch_bounds__(TPB) merge_filter_kernel(const Key* __restrict
     ctr[0] = 0;
     ctr[1] = 0;
     ctr[TK_DYN_CTR] = 0;
+    ctr[TK_FIN_CTR] = 0;
+  }
+  for (int j = threadIdx.x; j <= nblk; j += blockDim.x) {  // minima slots (and T) back to +inf
+    Key* m = const_cast<Key*>(mins) + (j < nblk ? j : TK_MAXGRID);
+    m->s = KEY_INF_S;
+    m->i = KEY_INF_I;
   }
   trace_mark(g_trace, 7);
 }
@@ -3030,8 +3040,39 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kern
     const int cnt = S.cnt;
     Key* dst = block_out + (int64_t)blockIdx.x * cap;
     for (int j = threadIdx.x; j < cnt; j += blockDim.x) dst[j] = S.buf()[j];
-    if (threadIdx.x == 0) reinterpret_cast<unsigned int*>(mins + gridDim.x)[blockIdx.x] = (unsigned)cnt;
+    if (threadIdx.x == 0) reinterpret_cast<unsigned int*>(mins + TK_MAXGRID + 1)[blockIdx.x] = (unsigned)cnt;
     write_block_min(S, cnt, mins + blockIdx.x);
+    // The (3/4 grid)-th block to get here bounds the merge early, while the rest
+    // still score: T = the k-th smallest minimum present in the slots (>= 3/4 grid
+    // >= 3k are, fenced before their tickets).  Slots are +inf (absent) or a finished
+    // block's minimum -- a torn read of one still lies at or above a real key of
+    // that block -- so T has k real keys at or below it: an upper bound of the
+    // global k-th key.  The merge kernel resets every slot after use.
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_ticket = atomicAdd(&tickets[TK_FIN_CTR], 1u);
+    __syncthreads();
+    if (s_ticket == gridDim.x * 3 / 4 - 1) {
+      Key* B = S.buf();
+      if (threadIdx.x == 0) S.cnt = 0;
+      __syncthreads();
+      for (int j0 = 0; j0 < (int)gridDim.x; j0 += blockDim.x) {
+        const int j = j0 + threadIdx.x;
+        Key x;
+        x.s = KEY_INF_S;
+        if (j < (int)gridDim.x) x = ld_key_cg(mins + j);
+        const int slot = warp_append(&S.cnt, x.s != KEY_INF_S);
+        if (slot >= 0) B[slot] = x;
+      }
+      __syncthreads();
+      if (S.cnt > k) {
+        topk_select(S, k);
+        if (threadIdx.x == 0) {
+          mins[TK_MAXGRID].i = S.thr.i;
+          mins[TK_MAXGRID].s = S.thr.s;
+        }
+      }
+    }
     trace_mark(g_trace, 3);
     return;
   }
@@ -4169,6 +4210,14 @@ int ls_score_points(ls_task* t, const void* d_points, int32_t pbytes, int64_t n,
 // scores, indices and the valid count come back in one copy to h_out (count in a 16-byte
 // slot, then [k] f64, [k] i64).
 constexpr size_t WS_CTR_BYTES = 4096 + 16;
+// then the two-stage minima slots + T (+inf between launches: 0xFF fill, reset by the merge)
+// and the block-list counts, at a fixed offset so no other layout ever overlaps them
+constexpr size_t WS_MIN_KEYS = TK_MAXGRID + 1;
+constexpr size_t WS_FIXED_BYTES = WS_CTR_BYTES + 16 * WS_MIN_KEYS + 4 * TK_MAXGRID;
+static cudaError_t ws_init(unsigned char* ws, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(ws, 0, WS_CTR_BYTES, s);
+  return e != cudaSuccess ? e : cudaMemsetAsync(ws + WS_CTR_BYTES, 0xFF, 16 * WS_MIN_KEYS, s);
+}
 
 static int topk_device(ls_task* t, const void* d_src, int pbytes, int64_t n, int64_t base_index, int32_t k,
                        double* d_top_scores, int64_t* d_top_index, unsigned long long* d_valid, cudaStream_t s,
@@ -4180,12 +4229,11 @@ static int topk_device(ls_task* t, const void* d_src, int pbytes, int64_t n, int
   const int ngroups = (grid + TK_GROUP - 1) / TK_GROUP;
   // two-stage merge (block-minima bound, merge_filter_kernel) when the grid has plenty of
   // blocks per answer key; else the in-kernel merge tree
-  const bool two = 4 * k <= grid && grid <= topk_buf(k);
-  // two-stage: [grid] buffers of topk_buf(k) keys, as many survivor slots, [grid] minima, [grid] counts
-  const size_t keys_bytes =
-      sizeof(Key) * (two ? (size_t)grid * (2 * (size_t)topk_buf(k) + 2) : ((size_t)grid + ngroups) * k);
+  const bool two = 4 * k <= grid && grid <= topk_buf(k) && grid <= TK_MAXGRID;
+  // two-stage: [grid] buffers of topk_buf(k) keys and as many survivor slots
+  const size_t keys_bytes = sizeof(Key) * (two ? (size_t)grid * 2 * topk_buf(k) : ((size_t)grid + ngroups) * k);
   const size_t out_bytes = h_out ? 16 + 16 * (size_t)k : 0;
-  const size_t ws_bytes = WS_CTR_BYTES + keys_bytes + out_bytes;
+  const size_t ws_bytes = WS_FIXED_BYTES + keys_bytes + out_bytes;
   unsigned char* ws = nullptr;
   bool cached = false;
   {
@@ -4196,7 +4244,7 @@ static int topk_device(ls_task* t, const void* d_src, int pbytes, int64_t n, int
         t->ws = nullptr;
         t->ws_bytes = 0;
         CUDA_TRY(cudaMallocAsync(&t->ws, ws_bytes, s));
-        CUDA_TRY(cudaMemsetAsync(t->ws, 0, WS_CTR_BYTES, s));
+        CUDA_TRY(ws_init(t->ws, s));
         t->ws_bytes = ws_bytes;
         t->ws_stream = s;
       }
@@ -4207,14 +4255,14 @@ static int topk_device(ls_task* t, const void* d_src, int pbytes, int64_t n, int
   }
   if (!cached) {  // concurrent call or another stream: a private workspace
     CUDA_TRY(cudaMallocAsync(&ws, ws_bytes, s));
-    CUDA_TRY(cudaMemsetAsync(ws, 0, WS_CTR_BYTES, s));
+    CUDA_TRY(ws_init(ws, s));
   }
   unsigned int* tickets = reinterpret_cast<unsigned int*>(ws);
   unsigned long long* wvalid = reinterpret_cast<unsigned long long*>(ws + 4096);
-  Key* block_out = reinterpret_cast<Key*>(ws + WS_CTR_BYTES);
+  Key* block_out = reinterpret_cast<Key*>(ws + WS_FIXED_BYTES);
   Key* group_out = block_out + (size_t)grid * (two ? topk_buf(k) : k);  // tree: group lists; two-stage: survivors
-  Key* mins = two ? group_out + (size_t)grid * topk_buf(k) : nullptr;
-  unsigned char* out = ws + WS_CTR_BYTES + keys_bytes;
+  Key* mins = two ? reinterpret_cast<Key*>(ws + WS_CTR_BYTES) : nullptr;
+  unsigned char* out = ws + WS_FIXED_BYTES + keys_bytes;
   if (h_out) {
     d_valid = reinterpret_cast<unsigned long long*>(out);
     d_top_scores = reinterpret_cast<double*>(out + 16);

@@ -388,3 +388,30 @@ def test_pinned_host_points_mapped(torch, n):
         hs, hi, hn = task.score_topk_points_host(pin, 64, base_index=5)
         assert hi.tolist() == di.cpu().tolist() and np.array_equal(hs, ds.cpu().numpy()) and hn == int(dn.item())
     task.close()
+
+
+@pytest.mark.gpu
+def test_topk_workspace_reuse_across_layouts(torch):
+    """One task, one cached workspace: calls alternating k, n (two-stage merge vs merge tree)
+    and the records / points entry points each equal a stable sort (self-resetting counters,
+    minima slots and published bound survive every layout change)."""
+    E = _engine()
+    from paper_2104_14641_b200 import workloads as W
+    from paper_2104_14641_b200.pack import SpaceTemplate
+    st = SpaceTemplate(W.program(W.conv2d_json()), W.conv_space(4096, 1))
+    task = E.Task(st.template.desc(arch_named("x86-avx2"), launch()), 0)
+    task.set_space(st.space_desc())
+    pts_all = st.points_from_indices(W.distinct_indices(st.sizes, 1 << 20, 17))
+    for n, k in [(1 << 20, 64), (5000, 16), (1 << 20, 1), (300_000, 200), (1 << 20, 64), (1 << 19, 1024),
+                 (77, 5), (1 << 20, 111), (100_003, 97), (1 << 20, 64)]:  # k ~ grid/4: > 256 survivors
+        dp = torch.from_numpy(pts_all[:n].view(np.int32)).cuda()
+        s, _, stt = task.score_points(dp, features=False)
+        ts, ti, nv = task.score_topk_points(dp, k, base_index=3)
+        torch.cuda.synchronize()
+        sc, ok = s.cpu().numpy(), stt.cpu().numpy() == 0
+        ids = np.flatnonzero(ok)
+        want = ids[np.lexsort((ids, sc[ids]))][:k]
+        assert (ti.cpu().numpy()[:len(want)] - 3).tolist() == want.tolist(), (n, k)
+        assert np.array_equal(ts.cpu().numpy()[:len(want)], sc[want]), (n, k)
+        assert int(nv.item()) == int(ok.sum())
+    task.close()
