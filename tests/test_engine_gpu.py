@@ -415,3 +415,27 @@ def test_topk_workspace_reuse_across_layouts(torch):
         assert np.array_equal(ts.cpu().numpy()[:len(want)], sc[want]), (n, k)
         assert int(nv.item()) == int(ok.sum())
     task.close()
+
+
+def test_topk_two_stage_many_survivors(torch):
+    """Points ordered by score put a block's whole buffer under the merge bound (hundreds of
+    survivors: the streamed merge path of merge_filter_kernel); still equal to a stable sort."""
+    E = _engine()
+    from paper_2104_14641_b200 import workloads as W
+    from paper_2104_14641_b200.pack import SpaceTemplate
+    st = SpaceTemplate(W.program(W.conv2d_json()), W.conv_space(4096, 1))
+    task = E.Task(st.template.desc(arch_named("x86-avx2"), launch()), 0)
+    task.set_space(st.space_desc())
+    pts = st.points_from_indices(W.distinct_indices(st.sizes, 1 << 20, 23))
+    dp = torch.from_numpy(pts.view(np.int32)).cuda()
+    s, _, stt = task.score_points(dp, features=False)
+    sc, ok = s.cpu().numpy(), stt.cpu().numpy() == 0
+    order = np.lexsort((np.arange(len(sc)), np.where(ok, sc, np.inf)))  # best first, failures last
+    dq = torch.from_numpy(pts[order].view(np.int32)).cuda()
+    for k in (64, 111):
+        ts, ti, nv = task.score_topk_points(dq, k)
+        torch.cuda.synchronize()
+        assert ti.cpu().tolist() == list(range(k))
+        assert np.array_equal(ts.cpu().numpy(), sc[order[:k]])
+        assert int(nv.item()) == int(ok.sum())
+    task.close()

@@ -16,3 +16,5 @@ timeout 600 ncu --set full --import-source on --clock-control none --kernel-name
   python bench.py --steps 2 --warmup 1 --no-baseline > gpurun_out/ncu_full.log 2>&1; echo ncu2=$?
 ncu -i gpurun_out/pts_full_r01.ncu-rep --page source --csv --print-source cuda,sass > gpurun_out/pts_src_r01.csv 2>/dev/null
 for f in bench bench_ref bench_volta bench_bert bench_res bench_sweep; do tail -n 1 gpurun_out/$f.log | cut -c1-300; done
+LS_TRACE=1 timeout 100 python -m pytest tests/test_engine_gpu.py -q -s -k workspace_reuse 2>&1 | grep -o "LS_TRACE n=[0-9]* grid=[0-9]*\|survivors [0-9]*" | paste - - > gpurun_out/reuse_survivors.txt
+timeout 120 python tools/host_probe.py > gpurun_out/host_probe.txt 2>&1
