@@ -2294,6 +2294,23 @@ __device__ __forceinline__ void stage_task(DTask& s, const DTask* __restrict__ g
   __syncthreads();
 }
 
+// Space path: the task header and its group tables staged together -- both
+// sources addressed from global memory (no wait for the staged header), 16-byte
+// loads, several in flight per thread, one barrier.  The table allocation is
+// padded to 16 bytes.
+__device__ __forceinline__ const int32_t* stage_space(unsigned char* dyn, const DTask* __restrict__ g) {
+  const int tb = __ldg(&g->task_bytes);
+  const int len = __ldg(&g->sd_len);
+  const int4* ts = reinterpret_cast<const int4*>(__ldg(reinterpret_cast<const unsigned long long*>(&g->sd_tab)));
+  const int n16 = tb / 16, tot = n16 + (len + 3) / 4;
+  const int4* gs = reinterpret_cast<const int4*>(g);
+  int4* d = reinterpret_cast<int4*>(dyn);  // header, then the tables at dyn + tb (tb % 16 == 0)
+#pragma unroll 4
+  for (int i = threadIdx.x; i < tot; i += blockDim.x) d[i] = __ldg(i < n16 ? gs + i : ts + (i - n16));
+  __syncthreads();
+  return reinterpret_cast<const int32_t*>(dyn + tb);
+}
+
 // Path selector of the scoring kernels: 0 generic, 1 tabulated with the table
 // in global memory (L1/L2 resident), 2 tabulated with the table in shared memory.
 template <int MODE>
@@ -2958,10 +2975,14 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kern
   __shared__ unsigned int s_ticket;
   DTask& T = *reinterpret_cast<DTask*>(dyn);
   trace_mark(g_trace, 0);
-  stage_task(T, gtask);
-  unsigned char* p = dyn + T.task_bytes;
-  const int32_t* tab = stage_tab<MODE>(p, T);
-  p += tab_smem_bytes(MODE, T);
+  const int32_t* tab;
+  if constexpr (MODE == 4 || MODE == 5) {
+    tab = stage_space(dyn, gtask);
+  } else {
+    stage_task(T, gtask);
+    tab = stage_tab<MODE>(dyn + T.task_bytes, T);
+  }
+  unsigned char* p = dyn + T.task_bytes + tab_smem_bytes(MODE, T);
   TopkState& S = *reinterpret_cast<TopkState*>(p);
   Evaluator<TM, RM, MODE> ev(T, p + align16(topk_state_bytes(cap)), tab);
   topk_init(S, cap);
@@ -4451,7 +4472,7 @@ int ls_task_set_space(ls_task* t, const ls_space_desc* sp) {
       t->retired.push_back(dch);
       CUDA_TRY(cudaMalloc(&dst, sizeof(int32_t) * np));
       t->retired.push_back(dst);
-      CUDA_TRY(cudaMalloc(&dsd, sizeof(int32_t) * t->host.sd_len));
+      CUDA_TRY(cudaMalloc(&dsd, sizeof(int32_t) * ((t->host.sd_len + 3) & ~3)));  // 16-byte staging loads
       t->retired.push_back(dsd);
       CUDA_TRY(cudaMalloc(&drows, sizeof(rows) + sizeof(int32_t) * 9));
       t->retired.push_back(drows);
