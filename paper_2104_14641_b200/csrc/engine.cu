@@ -1204,9 +1204,14 @@ __device__ int eval_space(const DTask& T, const int32_t* __restrict__ sdt, uint6
       ch = (uint32_t)x;
     } else if (ax.n == 1) {
       ch = 0;
-    } else {
-      const uint64_t q = (x >> 32) ? x / ax.n : __umul64hi(x, ax.magic);
+    } else if (x >> 32) {
+      const uint64_t q = x / ax.n;
       ch = (uint32_t)(x - q * ax.n);
+      x = q;
+    } else {  // umulhi(x, magic) for x < 2^32: x * magic_hi + umulhi(x, magic_lo), top word
+      const uint32_t x32 = (uint32_t)x;
+      const uint32_t q = (uint32_t)(((uint64_t)x32 * (uint32_t)(ax.magic >> 32) + __umulhi(x32, (uint32_t)ax.magic)) >> 32);
+      ch = x32 - q * (uint32_t)ax.n;
       x = q;
     }
     if (ax.kind == LS_AX_PERM) {
