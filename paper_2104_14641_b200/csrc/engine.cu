@@ -239,12 +239,12 @@ struct Cand {
 // per nibble), loop flags are slot masks, only the extents stay in shared
 // memory (they are indexed by a data-dependent slot).
 struct FastCand {
-  int32_t* ext;  // [NSLOT][TPB]
+  int32_t* ext;  // this thread's column of [NSLOT][TPB] (base + threadIdx.x)
   uint64_t chain;
   uint32_t unr, vec, par, exist;
   int n;
   uint32_t flags;
-  __device__ __forceinline__ int32_t& E(int v) { return ext[v * TPB + threadIdx.x]; }
+  __device__ __forceinline__ int32_t& E(int v) { return ext[v * TPB]; }
   __device__ __forceinline__ int C(int p) const { return (int)((chain >> (4 * p)) & 15u); }
   __device__ __forceinline__ uint8_t Fl(int v) const {
     return (uint8_t)((((par >> v) & 1u) ? 1 : 0) | (((unr >> v) & 1u) ? 2 : 0) | (((vec >> v) & 1u) ? 4 : 0));
@@ -2199,7 +2199,7 @@ __global__ void build_pchain_kernel(const DTask* __restrict__ g, int32_t pax, ui
   const int pc = blockIdx.x * blockDim.x + threadIdx.x;
   const int n = pax >= 0 ? (int)T.sp_ax[pax].n : 1;
   FastCand c;
-  c.ext = reinterpret_cast<int32_t*>(dyn);
+  c.ext = reinterpret_cast<int32_t*>(dyn) + threadIdx.x;
   if (pc >= n) return;
   ls_record r;
   memset(&r, 0, sizeof(r));
@@ -2351,7 +2351,7 @@ struct Evaluator {
     if constexpr (MODE == 0)
       c = carve(state, T);
     else
-      fc.ext = reinterpret_cast<int32_t*>(state);
+      fc.ext = reinterpret_cast<int32_t*>(state) + threadIdx.x;
   }
   __device__ __forceinline__ int operator()(const DTask& T, const ls_record& r, const uint32_t* kt, uint32_t pch,
                                             double* f, double* s) {
