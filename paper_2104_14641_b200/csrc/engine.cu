@@ -2875,6 +2875,13 @@ __global__ void __launch_bounds__(TPB) merge_filter_kernel(const Key* __restrict
   TopkState& S = *reinterpret_cast<TopkState*>(raw);
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the scoring grid is complete and visible
   trace_mark(g_trace, 4);
+  // the first chunk of this block's list is loaded while T is read (independent loads)
+  const unsigned int* cnts = reinterpret_cast<const unsigned int*>(mins + TK_MAXGRID + 1);
+  int cb0 = (int)blockIdx.x < nblk ? (int)__ldcg(cnts + blockIdx.x) : 0;
+  Key x0;
+  x0.s = KEY_INF_S;
+  x0.i = KEY_INF_I;
+  if ((int)threadIdx.x < cb0) x0 = ld_key_cg(block_out + (int64_t)blockIdx.x * cap + threadIdx.x);
   // T: published by the scoring grid's (3/4 grid)-th finisher; else the k-th smallest block minimum
   Key* B = S.buf();
   __shared__ int s_n;
@@ -2906,16 +2913,16 @@ __global__ void __launch_bounds__(TPB) merge_filter_kernel(const Key* __restrict
   }
   const Key T = s_T;  // +inf (no filtering) when there are at most k minima
   trace_mark(g_trace, 5);
-  const unsigned int* cnts = reinterpret_cast<const unsigned int*>(mins + TK_MAXGRID + 1);
   for (int b = blockIdx.x; b < nblk; b += gridDim.x) {  // block b's list: cnts[b] keys at b * cap
-    const int cb = (int)__ldcg(cnts + b);
+    const int cb = b == (int)blockIdx.x ? cb0 : (int)__ldcg(cnts + b);
     const Key* lst = block_out + (int64_t)b * cap;
     for (int j0 = 0; j0 < cb; j0 += blockDim.x) {
       const int j = j0 + threadIdx.x;
       Key x;
       x.s = KEY_INF_S;
       x.i = KEY_INF_I;
-      if (j < cb) x = ld_key_cg(lst + j);
+      if (j0 == 0 && b == (int)blockIdx.x) x = x0;
+      else if (j < cb) x = ld_key_cg(lst + j);
       const int slot = warp_append(&ctr[0], j < cb && !kless(T, x));
       if (slot >= 0) surv[slot] = x;
     }
@@ -2928,6 +2935,8 @@ __global__ void __launch_bounds__(TPB) merge_filter_kernel(const Key* __restrict
   if (s_ticket != gridDim.x - 1) return;
   __threadfence();
   const int c = (int)__ldcg(&ctr[0]);
+  // every scoring block is done: the valid count is final (read now, off the tail's critical path)
+  const unsigned long long v_final = threadIdx.x == 0 ? __ldcg(wvalid) : 0ull;
   if (g_trace && threadIdx.x == 0) g_trace[blockIdx.x * TR_SLOTS + 3] = (1ull << 63) | (unsigned long long)c;
   Key* buf = S.buf();
   if (c <= (int)blockDim.x) {  // rank the survivors directly; the k smallest land at their rank
@@ -2951,8 +2960,8 @@ __global__ void __launch_bounds__(TPB) merge_filter_kernel(const Key* __restrict
     write_sorted(S, merge_into(S, surv, c, k, false), k, out_s, out_i);
   }
   if (threadIdx.x == 0) {  // the count out; the counters back to zero for the next launch
-    const unsigned long long v = atomicExch(wvalid, 0ull);
-    if (n_valid) *n_valid = v;
+    if (n_valid) *n_valid = v_final;
+    *wvalid = 0ull;
     ctr[0] = 0;
     ctr[1] = 0;
     ctr[TK_DYN_CTR] = 0;
