@@ -628,7 +628,8 @@ def main():
     OUT.mkdir(parents=True, exist_ok=True)
     for name in CUSTOM_ARCHS:  # write the TOMLs before the pool forks (no write races)
         ref_arch(name)
-    which = set(sys.argv[1:]) or {"gemm", "conv", "bert", "rank", "trees", "emit", "es", "cli", "tree_rank"}
+    which = set(sys.argv[1:]) or {"gemm", "conv", "bert", "rank", "trees", "emit", "es", "cli", "tree_rank",
+                                  "resnet", "bertbench"}
     if "gemm" in which:
         space_fixture("gemm1024", W.matmul_json(1024), W.gemm_space(1024), 4096, 0,
                       ["x86-avx2", "aarch64-neon", "nvidia-volta"])
@@ -646,6 +647,14 @@ def main():
                   "reorder": W.random_perms(W.tiled_chain(["b", "i", "j", "k"], ["b", "i", "j", "k"]), 120, 10)}
             space_fixture(f"bmm_{b}_{m}_{n}_{k}", W.batch_matmul_json(b, m, n, k), sp, 256, 2,
                           ["x86-avx2", "nvidia-volta"])
+    if "resnet" in which:
+        # configs[2]: every ResNet-50 task space exactly as bench.py builds it (workloads.resnet50_tasks)
+        for name, spec, space in W.resnet50_tasks():
+            space_fixture(f"resnet_{name}", spec, space, 1024, 3, ["x86-avx2", "aarch64-neon", "nvidia-volta"])
+    if "bertbench" in which:
+        # configs[3]: the BERT spaces exactly as bench.py builds them (workloads.bert_tasks)
+        for name, spec, space in W.bert_tasks():
+            space_fixture(f"bert_{name}", spec, space, 1024, 4, ["x86-avx2", "aarch64-neon", "nvidia-volta"])
     if "rank" in which:
         rank_fixture()
     if "trees" in which:

@@ -63,6 +63,11 @@ def space_case(name: str):
 
 SPACE_FIXTURES = ["gemm1024", "conv56", "dense_1024_768_768", "dense_1024_3072_768",
                   "dense_1024_768_3072", "bmm_96_128_128_64", "bmm_96_128_64_128"]
+# configs[2] / configs[3] exactly as bench.py builds them (workloads.resnet50_tasks / bert_tasks)
+RESNET_FIXTURES = sorted(p.stem for p in GOLDEN.glob("resnet_*.npz"))
+BERT_FIXTURES = sorted(p.stem for p in GOLDEN.glob("bert_*.npz"))
+BENCH_FIXTURES = RESNET_FIXTURES + BERT_FIXTURES
+ALL_SPACE_FIXTURES = SPACE_FIXTURES + BENCH_FIXTURES
 
 
 def rank_groups(case):

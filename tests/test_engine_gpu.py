@@ -7,7 +7,7 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-from golden_util import (GOLDEN, SPACE_FIXTURES, arch_named, launch, rank_cases, rank_groups, space_case,
+from golden_util import (ALL_SPACE_FIXTURES, GOLDEN, SPACE_FIXTURES, arch_named, launch, rank_cases, rank_groups, space_case,
                          status_of_error)
 
 
@@ -37,7 +37,7 @@ POINT_PATHS = [1, 2, 3]  # + LS_PATH_SPACE (points calls only)
 
 
 @pytest.mark.parametrize("path", PATHS)
-@pytest.mark.parametrize("name", SPACE_FIXTURES)
+@pytest.mark.parametrize("name", ALL_SPACE_FIXTURES)
 def test_space_fixtures_bit_exact(torch, name, path):
     E = _engine()
     st, recs, z = space_case(name)
@@ -293,7 +293,7 @@ def test_points_out_of_range(torch):
 
 
 @pytest.mark.parametrize("path", POINT_PATHS)
-@pytest.mark.parametrize("name", SPACE_FIXTURES)
+@pytest.mark.parametrize("name", ALL_SPACE_FIXTURES)
 def test_space_fixtures_points_bit_exact(torch, name, path):
     """Every BASELINE space through the points API on every points path == the reference's outputs."""
     E = _engine()

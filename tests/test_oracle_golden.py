@@ -11,7 +11,7 @@ import numpy as np
 import pytest
 
 import pyoracle
-from golden_util import (SPACE_FIXTURES, arch_named, launch, rank_cases, rank_groups, space_case,
+from golden_util import (ALL_SPACE_FIXTURES, SPACE_FIXTURES, arch_named, launch, rank_cases, rank_groups, space_case,
                          status_of_error, GOLDEN)
 from paper_2104_14641_b200 import abi, ir
 from paper_2104_14641_b200.pack import pack_schedules
@@ -22,7 +22,7 @@ def test_descriptor_layout_matches_c():
     assert pyoracle.sizeof_desc() == ctypes.sizeof(abi.TaskDesc)
 
 
-@pytest.mark.parametrize("name", SPACE_FIXTURES)
+@pytest.mark.parametrize("name", ALL_SPACE_FIXTURES)
 def test_space_fixtures_bit_exact(name):
     st, recs, z = space_case(name)
     for a in z["arches"]:
