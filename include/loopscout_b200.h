@@ -104,7 +104,9 @@ enum {
   LS_ST_REORDER_CHAIN = 6,   /* reorder: not a perfect nest chain ls/ir.py:398-399   */
   LS_ST_BAD_FEATURE = 7,     /* CostModelError non-finite/negative ls/cost.py:43-45  */
   LS_ST_UNSUPPORTED = 16,    /* transformed tree outside the device class            */
-  LS_ST_UNROLL_TABLE = 17,   /* unroll product not prepared (ls_task_prepare_unroll) */
+  LS_ST_UNROLL_TABLE = 17,   /* unroll product not prepared (ls_task_prepare_unroll) or
+                                above 65536 (its block is scheduled on the host: outside
+                                the device class; the reference has no limit)       */
   LS_ST_OVERFLOW = 18,       /* intermediate exceeded the device integer range       */
   LS_ST_POINT_RANGE = 19     /* space point outside the attached space (points API)  */
 };
@@ -230,9 +232,10 @@ int ls_task_points_path(const ls_task* task);
 int ls_task_prepare_unroll(ls_task* task, const int64_t* u_values, int32_t n);
 
 /* Distinct innermost-unroll products U needed by the structurally supported
- * records (device pass), sorted, at most `cap`; feed them to
- * ls_task_prepare_unroll before scoring.  Only needed when the template or
- * program marks loops `unroll`. */
+ * records (device pass), sorted; feed them to ls_task_prepare_unroll before
+ * scoring.  Only needed when the template or program marks loops `unroll`.
+ * LS_E_UNSUPPORTED when a batch needs more than 16384 distinct products,
+ * LS_E_ARG when they do not fit `cap`. */
 int ls_collect_unroll(ls_task* task, const ls_record* d_records, int64_t n, int64_t* h_values,
                       int32_t cap, int32_t* h_count, void* stream);
 
@@ -252,11 +255,32 @@ int ls_score_topk(ls_task* task, const ls_record* d_records, int64_t n, int64_t 
                   int32_t k, double* d_top_scores, int64_t* d_top_index, int64_t* d_n_valid,
                   void* stream);
 
-/* Merge n_lists sorted top-k lists (k_in entries each, contiguous) into the
- * k_out best by (score, index).  Used after an NCCL all-gather of per-GPU
- * lists; no reference equivalent (the reference is single-process). */
+/* ---- multi-GPU top-k merge (no reference equivalent: the
+ * reference is single-process, its order is cmd_rank's (score, index) sort,
+ * ls/cli.py:124-126) ----
+ * A top-k entry as one 16-byte key: the float64 score mapped to order-preserving
+ * unsigned bits (negative scores bit-inverted, others with the sign bit set) and
+ * the global index; (order, index) compare lexicographically.  An empty slot is
+ * order = UINT64_MAX, index = INT64_MAX.  One all-gather of k keys per rank
+ * (ncclAllGather of 16k bytes, or torch.distributed.all_gather_into_tensor)
+ * followed by ls_topk_merge_keys on every rank gives the single-GPU answer. */
+typedef struct ls_topk_key {
+  uint64_t order;
+  int64_t index;
+} ls_topk_key;
+
+/* Merge n_lists top-k lists (k_in entries each, contiguous, any order; index
+ * < 0 marks an empty slot) into the k_out best by (score, index).  No
+ * temporary allocation. */
 int ls_topk_merge(const double* d_scores, const int64_t* d_index, int32_t n_lists, int32_t k_in,
                   int32_t k_out, double* d_out_scores, int64_t* d_out_index, void* stream);
+/* Merge m gathered keys (any order, empty slots allowed) into the k_out best,
+ * written as (score, index) ascending; unfilled slots +inf / -1. */
+int ls_topk_merge_keys(const ls_topk_key* d_keys, int64_t m, int32_t k_out, double* d_out_scores,
+                       int64_t* d_out_index, void* stream);
+/* Pack m (score, index) entries into keys (index < 0 -> empty key). */
+int ls_topk_to_keys(const double* d_scores, const int64_t* d_index, int64_t m, ls_topk_key* d_keys,
+                    void* stream);
 
 /* Host-buffer variant of ls_score_topk: records in host memory (pinned or
  * pageable), results written to host memory.  Mapped page-locked buffers
@@ -308,10 +332,33 @@ typedef struct {
 typedef struct ls_es ls_es;
 
 /* Allocate a run (memo table sized for min(space, population*iterations+1)
- * distinct schedules).  h_theta0: start vector (NULL: ThetaEncoding.initial). */
+ * distinct schedules, at most 2^28: LS_E_UNSUPPORTED above).  h_theta0: start
+ * vector (NULL: ThetaEncoding.initial). */
 int ls_es_create(ls_task* task, const ls_es_params* params, const double* h_theta0, ls_es** out);
 /* Enqueue the start point and every generation (one CUDA graph per generation) on `stream`. */
 int ls_es_run(ls_es* es, void* stream);
+
+/* ---- the same search sharded over `world` ranks (one GPU each) ----
+ * Rank r evaluates members [r P/world, (r+1) P/world) (population P a multiple
+ * of world).  Per generation the caller enqueues, on one stream:
+ *   ls_es_step(es, 0)   decode + memoised scoring of the local members, their F keys
+ *   all-gather in place of the keys buffer (keys_per_rank uint64 per rank, rank
+ *                       slices in rank order; ncclAllGather with sendbuff =
+ *                       keys + r * keys_per_rank)
+ *   ls_es_step(es, 1)   global stable ranks (sort of all P keys) and this rank's
+ *                       chunk partials of sum_i w_i eps_i
+ *   all-gather in place of the partials buffer (partials_per_rank float64 per rank)
+ *   ls_es_step(es, 2)   theta update from every chunk in chunk order, trace, generation
+ * after ls_es_begin (the start point).  Chunking and summation order do not
+ * depend on world, so theta is bit-identical for any world; the distinct count
+ * is the size of the union of the ranks' ls_es_evaluated lists and the trace is
+ * the per-generation minimum over ranks.  world = 1 needs no exchange. */
+int ls_es_create_shard(ls_task* task, const ls_es_params* params, const double* h_theta0, int32_t rank,
+                       int32_t world, ls_es** out);
+int ls_es_begin(ls_es* es, void* stream);
+int ls_es_step(ls_es* es, int32_t stage, void* stream);
+int ls_es_shard_buffers(ls_es* es, void** d_keys, int64_t* keys_per_rank, void** d_partials,
+                        int64_t* partials_per_rank);
 /* After ls_es_run: theta history [iterations+1][dim], trace [iterations] (best score after
  * each generation), distinct evaluations, first failure (0 none; else generation+1 (0: the
  * start point) << 40 | member << 8 | LS_ST_*) and best score.  Any pointer may be NULL.  Synchronous. */

@@ -30,7 +30,7 @@ STATUS = {
     6: "reorder: loops do not form a perfect nest chain",
     7: "feature must be finite and >= 0",
     16: "unsupported transformed structure",
-    17: "unroll product not prepared",
+    17: "unroll product above 65536 or not prepared (outside the device class)",
     18: "integer range exceeded",
     19: "space point outside the space",
 }

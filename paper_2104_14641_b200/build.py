@@ -8,8 +8,10 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 SRC = [PKG / "csrc" / "engine.cu", PKG / "csrc" / "blocksched.cpp"]
-HDR = [PKG.parent / "include" / "loopscout_b200.h"]
+# every header the translation units include (csrc/*.cuh, *.h) and the public header
+HDR = sorted(PKG.glob("csrc/*.cuh")) + sorted(PKG.glob("csrc/*.h")) + [PKG.parent / "include" / "loopscout_b200.h"]
 OUT = PKG / "libloopscout_b200.so"
+PACKER_SRC = PKG / "csrc" / "packer.cpp"
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
@@ -25,7 +27,27 @@ def nvcc() -> str:
     return str(p) if p.exists() else "nvcc"
 
 
+def packer_path() -> Path:
+    import sysconfig
+    return PKG / ("_packer" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+
+def build_packer(force: bool = False) -> Path:
+    """The host schedule-list packer (CPython extension, g++)."""
+    import sysconfig
+    out = packer_path()
+    if not force and out.exists() and out.stat().st_mtime >= PACKER_SRC.stat().st_mtime:
+        return out
+    cmd = ["g++", "-O2", "-std=c++17", "-shared", "-fPIC", f"-I{sysconfig.get_paths()['include']}",
+           "-o", str(out), str(PACKER_SRC)]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"g++ failed:\n{r.stdout}\n{r.stderr}")
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
+    build_packer(force)
     newest = max(p.stat().st_mtime for p in SRC + HDR)
     if not force and OUT.exists() and OUT.stat().st_mtime >= newest:
         return OUT

@@ -11,12 +11,13 @@ candidates are reported as (index, message) like evaluate_population's
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+from collections import OrderedDict
+from dataclasses import dataclass, field
 
 import numpy as np
 
 from . import abi
-from .arch import CPU_FEATURES, GPU_FEATURES, FeatureVector
+from .arch import CPU_FEATURES, GPU_FEATURES, CostModelError, FeatureVector
 from .engine import EngineError, Task, to_device_records
 from .pack import PackError, pack_schedules
 
@@ -35,28 +36,55 @@ class BatchResult:
     features: "np.ndarray | None"  # f64[n, F]
     status: np.ndarray          # i32[n], 0 = ok (include/loopscout_b200.h)
     feature_names: tuple
+    messages: dict = field(default_factory=dict)  # index -> (exception type, text) raised on the host
 
     @property
     def errors(self) -> list:
-        return [(int(i), CandidateError(int(self.status[i]))) for i in np.nonzero(self.status)[0]]
+        return [(int(i), self.exception(int(i))) for i in np.nonzero(self.status)[0]]
+
+    def exception(self, i: int) -> Exception:
+        """The failure of candidate i: the host-side exception when one was recorded, else the
+        device status as a CandidateError."""
+        if i in self.messages and self.messages[i][0] == "CostModelError":
+            return CostModelError(self.messages[i][1])
+        return CandidateError(int(self.status[i]))
 
     def feature_vector(self, i: int) -> FeatureVector:
         return FeatureVector(tuple(zip(self.feature_names, map(float, self.features[i]))))
 
 
-_TASKS: dict = {}
+class _TaskCache:
+    """Device tasks per (template, arch, launch, device), LRU-bounded: a task is built once
+    (descriptor upload + per-task tables, ~0.1 ms) and reused by every later batch of the shape."""
+
+    def __init__(self, cap: int = 64):
+        self.cap = cap
+        self.d: "OrderedDict" = OrderedDict()
+
+    def get(self, template, arch, launch, device):
+        key = (id(template), id(arch), id(launch), device)
+        hit = self.d.get(key)
+        if hit is not None and hit[1] is template and hit[2] is arch and hit[3] is launch:
+            self.d.move_to_end(key)
+            return hit[0]
+        task = Task(template.desc(arch, launch), device)
+        self.d[key] = (task, template, arch, launch)
+        while len(self.d) > self.cap:
+            old = self.d.popitem(last=False)[1][0]
+            old.close()
+        return task
 
 
-def _task_for(template, arch, launch, device):
-    key = (id(template), arch, launch, device)
-    t = _TASKS.get(key)
-    if t is None:
-        t = (Task(template.desc(arch, launch), device), template)
-        _TASKS[key] = t
-    return t[0]
+_TASKS = _TaskCache()
 
 
 def score_batch(program, schedules, arch, launch=None, device: int = 0, features: bool = True) -> BatchResult:
+    """Score every schedule on the device (groups by shape, one fused launch per group).
+
+    Per-candidate failures never abort the batch: device status codes for the reference's
+    ProgramError/CostModelError classes, and host-side failures of a whole group (a GPU arch
+    without a launch record, a shape outside the device class) recorded per candidate with the
+    reference's message, like evaluate_population's `errors` (ls/es.py:96-116)."""
     import torch
 
     n = len(schedules)
@@ -64,14 +92,19 @@ def score_batch(program, schedules, arch, launch=None, device: int = 0, features
     scores = np.full(n, np.nan)
     feats = np.full((n, len(names)), np.nan) if features else None
     status = np.zeros(n, np.int32)
+    messages: dict = {}
     for g in pack_schedules(program, schedules):
         if g.template is None:
             status[g.index] = abi.ST_UNSUPPORTED
             continue
         try:
-            task = Task(g.template.desc(arch, launch), device)
-        except EngineError as e:
-            if "(-3)" not in str(e):  # LS_E_UNSUPPORTED: outside the device class, per candidate
+            task = _TASKS.get(g.template, arch, launch, device)
+        except CostModelError as e:  # e.g. a GPU arch without a launch record (ls/cost.py:137-138)
+            status[g.index] = abi.ST_UNSUPPORTED
+            messages.update({int(i): ("CostModelError", str(e)) for i in g.index})
+            continue
+        except (EngineError, PackError) as e:
+            if isinstance(e, EngineError) and "(-3)" not in str(e):  # only LS_E_UNSUPPORTED is per candidate
                 raise
             status[g.index] = abi.ST_UNSUPPORTED
             continue
@@ -86,22 +119,56 @@ def score_batch(program, schedules, arch, launch=None, device: int = 0, features
         scores[g.index[ok]] = s.cpu().numpy()[ok]
         if features:
             feats[g.index[ok]] = f.cpu().numpy()[ok]
-        task.close()
-    return BatchResult(scores, feats, status, names)
+    return BatchResult(scores, feats, status, names, messages)
 
 
 def rank_schedules(program, schedules, arch, launch=None, device: int = 0):
     """cmd_rank's core: [(index, score, FeatureVector)] ascending by (score, index) + errors."""
-    import torch
-
     res = score_batch(program, schedules, arch, launch, device)
     ok = np.nonzero(res.status == 0)[0]
-    if len(ok):
-        s = torch.from_numpy(res.scores[ok]).cuda(device)
-        order = torch.sort(s, stable=True).indices.cpu().numpy()  # ties keep input order
-        ok = ok[order]
+    ok = ok[np.lexsort((ok, res.scores[ok]))]  # ties keep input order (ls/cli.py:124-126)
     rows = [(int(i), float(res.scores[i]), res.feature_vector(int(i))) for i in ok]
     return rows, res.errors
+
+
+def rank_topk(program, schedules, arch, k: int, launch=None, device: int = 0):
+    """The k best of a schedule list by (score, input index) -- cmd_rank's order (ls/cli.py:124-126)
+    cut at k -- with the fused score + top-k launch per shape group and the library merge across
+    groups.  Returns (scores f64[k], indices i64[k] (+inf / -1 padded), valid count)."""
+    import torch
+
+    from .engine import topk_merge
+
+    lists = []
+    n_valid = 0
+    for g in pack_schedules(program, schedules):
+        if g.template is None or (g.host_status != 0).any():
+            ok = g.host_status == 0 if g.template is not None else np.zeros(len(g.index), bool)
+            if not ok.any():
+                continue
+            g = type(g)(g.template, g.index[ok], g.records[ok], g.host_status[ok])
+        try:
+            task = _TASKS.get(g.template, arch, launch, device)
+        except (CostModelError, EngineError, PackError) as e:
+            if isinstance(e, EngineError) and "(-3)" not in str(e):
+                raise
+            continue
+        d_rec = to_device_records(g.records, device)
+        task.prepare_unroll_for(d_rec)
+        # group-local indices ranked by the fused kernel, mapped to input positions: the group's
+        # positions ascend, so (score, local) order == (score, input index) order
+        s, i, nv = task.score_topk(d_rec, k)
+        loc = i.cpu().numpy()
+        glob = np.where(loc >= 0, g.index[np.clip(loc, 0, None)], -1)
+        lists.append((s, torch.from_numpy(glob).to(s.device)))
+        n_valid += int(nv.item())
+    if not lists:
+        return np.full(k, np.inf), np.full(k, -1, np.int64), 0
+    if len(lists) == 1:
+        s, i = lists[0]
+    else:
+        s, i = topk_merge(torch.cat([x[0] for x in lists]), torch.cat([x[1] for x in lists]), len(lists), k, k)
+    return s.cpu().numpy(), i.cpu().numpy(), n_valid
 
 
 def score(fv, arch) -> float:

@@ -212,6 +212,7 @@ struct ls_task {
   size_t ws_bytes = 0;
   cudaStream_t ws_stream = nullptr;
   bool ws_busy = false;
+  bool ws_dirty = false;           // a call failed after its first launch: re-initialise before reuse
 };
 
 // ---------------------------------------------------------------------------
@@ -3147,7 +3148,10 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kern
 }
 
 // Merge m keys (any order, +inf padded) into the k best, written as (score, index).
-__global__ void __launch_bounds__(TPB) merge_keys_kernel(const Key* __restrict__ in, int64_t m, int k,
+// Input either packed keys (in) or parallel (score, index) lists (idx < 0 = empty slot),
+// converted on the fly: no staging buffer.
+__global__ void __launch_bounds__(TPB) merge_keys_kernel(const Key* __restrict__ in, const double* __restrict__ in_s,
+                                                         const int64_t* __restrict__ in_i, int64_t m, int k,
                                                          double* __restrict__ out_s, int64_t* __restrict__ out_i,
                                                          int cap) {
   extern __shared__ __align__(16) unsigned char raw[];
@@ -3159,8 +3163,14 @@ __global__ void __launch_bounds__(TPB) merge_keys_kernel(const Key* __restrict__
     bool has = false;
     Key key;
     if (i < m) {
-      key = in[i];
-      has = !(key.s == KEY_INF_S && key.i == KEY_INF_I);
+      if (in) {
+        key = in[i];
+        has = !(key.s == KEY_INF_S && key.i == KEY_INF_I);
+      } else {
+        key.i = in_i[i];
+        has = key.i >= 0;
+        key.s = has ? order_bits(in_s[i]) : KEY_INF_S;
+      }
     }
     topk_offer(S, has, key, k, safe);
   }
@@ -3170,7 +3180,7 @@ __global__ void __launch_bounds__(TPB) merge_keys_kernel(const Key* __restrict__
 
 __global__ void lists_to_keys_kernel(const double* __restrict__ s, const int64_t* __restrict__ idx, int64_t m,
                                      Key* __restrict__ out) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= m) return;
   Key k;
   if (idx[i] < 0) {
@@ -3210,11 +3220,13 @@ __global__ void __launch_bounds__(TPB) collect_unroll_kernel(const DTask* __rest
     }
     const unsigned long long key = (unsigned long long)(k ? Uin : R);
     unsigned int h = (unsigned int)((key * 0x9E3779B97F4A7C15ull) >> 40) % (unsigned)cap;
-    for (int probe = 0; probe < cap; ++probe) {
+    int probe = 0;
+    for (; probe < cap; ++probe) {
       const unsigned long long prev = atomicCAS(&set[h], 0ull, key);
       if (prev == 0ull || prev == key) break;
       h = (h + 1) % (unsigned)cap;
     }
+    if (probe == cap) atomicExch(&set[cap], 1ull);  // set full: reported, never dropped silently
   }
 }
 
@@ -3926,11 +3938,15 @@ int upload(ls_task* t) {
   return LS_E_OK;
 }
 
+// Body-replication products above this are outside the device class: their candidates report
+// LS_ST_UNROLL_TABLE (the block of U body copies is list-scheduled on the host, O(U) instructions).
+constexpr int64_t LS_UNROLL_MAX = 65536;
+
 int add_unroll(ls_task* t, const int64_t* us, int n) {
   bool changed = false;
   for (int i = 0; i < n; ++i) {
     int64_t U = us[i];
-    if (U < 1 || U > 4096) continue;
+    if (U < 1 || U > LS_UNROLL_MAX) continue;
     bool have = false;
     for (auto& e : t->utab) have |= e.u == U;
     if (have) continue;
@@ -4036,37 +4052,63 @@ TopkFn topk_fn(const DTask& T, int mode, int pbytes) {
   return pbytes ? topk_fn_src<1>(T, mode) : topk_fn_src<0>(T, mode);
 }
 
-// Resident blocks per SM of a kernel at a dynamic shared-memory size (cached:
-// the attribute and occupancy queries cost host time on every scoring call).
-// The kernel's dynamic shared-memory limit only ever grows, so a cached launch
-// at a smaller size stays valid after a larger one.
+// Dynamic shared-memory limit and resident blocks per SM of a kernel on the
+// current device (cached per (device, kernel): the attribute and occupancy
+// queries cost host time on every scoring call).  cudaFuncSetAttribute acts on
+// the current device only, so each device gets its own entry.  The limit only
+// ever grows, so a cached launch at a smaller size stays valid after a larger
+// one.  Returns -1 (with ls_last_error set) when the attribute cannot be set.
+struct KernAttr {
+  int device;
+  const void* fn;
+  size_t limit;                                  // MaxDynamicSharedMemorySize set so far
+  std::vector<std::pair<size_t, int>> occ;       // (dynamic smem, blocks per SM)
+};
 template <typename K>
-int blocks_per_sm(K kernel, size_t smem) {
+int kernel_prepare(K kernel, size_t smem, bool want_occupancy) {
   static std::mutex mu;
-  static std::vector<std::pair<std::pair<const void*, size_t>, int>> cache;
-  static std::vector<std::pair<const void*, size_t>> limit;
+  static std::vector<KernAttr> cache;
   const void* f = reinterpret_cast<const void*>(kernel);
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return fail(LS_E_CUDA, "cudaGetDevice failed"), -1;
   std::lock_guard<std::mutex> g(mu);
-  bool raise = true;
-  for (auto& e : limit)
-    if (e.first == f) {
-      raise = smem > e.second;
-      if (raise) e.second = smem;
-    }
-  if (raise) {
-    bool known = false;
-    for (auto& e : limit) known |= e.first == f;
-    if (!known) limit.push_back({f, smem});
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  KernAttr* e = nullptr;
+  for (auto& c : cache)
+    if (c.device == dev && c.fn == f) e = &c;
+  if (!e) {
+    cache.push_back({dev, f, 0, {}});
+    e = &cache.back();
   }
-  for (auto& e : cache)
-    if (e.first.first == f && e.first.second == smem) return e.second;
+  if (smem > e->limit) {
+    const cudaError_t r = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (r != cudaSuccess) {
+      cudaGetLastError();
+      return fail(LS_E_CUDA, std::string("cudaFuncSetAttribute(MaxDynamicSharedMemorySize=") + std::to_string(smem) +
+                                 "): " + cudaGetErrorString(r)),
+             -1;
+    }
+    e->limit = smem;
+  }
+  if (!want_occupancy) return 1;
+  for (auto& o : e->occ)
+    if (o.first == smem) return o.second;
   int b = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, TPB, smem);
+  const cudaError_t r = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, TPB, smem);
+  if (r != cudaSuccess) {
+    cudaGetLastError();
+    return fail(LS_E_CUDA, std::string("cudaOccupancyMaxActiveBlocksPerMultiprocessor: ") + cudaGetErrorString(r)), -1;
+  }
   b = std::max(b, 1);
-  cache.push_back({{f, smem}, b});
+  e->occ.push_back({smem, b});
   return b;
 }
+template <typename K>
+int blocks_per_sm(K kernel, size_t smem) {
+  return kernel_prepare(kernel, smem, true);
+}
+#define BPS_TRY(var, kernel, smem)           \
+  const int var = blocks_per_sm(kernel, smem); \
+  if (var < 0) return LS_E_CUDA
 
 }  // namespace
 
@@ -4183,23 +4225,29 @@ int ls_collect_unroll(ls_task* t, const ls_record* d_records, int64_t n, int64_t
   }
   CUDA_TRY(cudaSetDevice(t->device));
   cudaStream_t s = (cudaStream_t)stream;
-  const int slots = 4096;
+  const int slots = 16384;  // distinct products per batch; one more slot flags a full set
   unsigned long long* set = nullptr;
-  CUDA_TRY(cudaMallocAsync(&set, sizeof(unsigned long long) * slots, s));
-  CUDA_TRY(cudaMemsetAsync(set, 0, sizeof(unsigned long long) * slots, s));
+  CUDA_TRY(cudaMallocAsync(&set, sizeof(unsigned long long) * (slots + 1), s));
+  CUDA_TRY(cudaMemsetAsync(set, 0, sizeof(unsigned long long) * (slots + 1), s));
   if (n > 0) {
     const size_t sm = smem_score(t->host, 0);
-    collect_unroll_kernel<<<grid_for(t, n, blocks_per_sm(collect_unroll_kernel, sm)), TPB, sm, s>>>(
+    BPS_TRY(bps, collect_unroll_kernel, sm);
+    collect_unroll_kernel<<<grid_for(t, n, bps), TPB, sm, s>>>(
         t->d_task, d_records, n, set, slots);
     CUDA_TRY(cudaGetLastError());
   }
-  std::vector<unsigned long long> h(slots);
-  CUDA_TRY(cudaMemcpyAsync(h.data(), set, sizeof(unsigned long long) * slots, cudaMemcpyDeviceToHost, s));
+  std::vector<unsigned long long> h(slots + 1);
+  CUDA_TRY(cudaMemcpyAsync(h.data(), set, sizeof(unsigned long long) * (slots + 1), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaFreeAsync(set, s));
   CUDA_TRY(cudaStreamSynchronize(s));
-  int c = 0;
-  for (auto v : h)
-    if (v && c < cap) h_values[c++] = (int64_t)v;
+  if (h[slots]) return fail(LS_E_UNSUPPORTED, "more than 16384 distinct unroll products in one batch");
+  int c = 0, distinct = 0;
+  for (int q = 0; q < slots; ++q)
+    if (h[q]) {
+      ++distinct;
+      if (c < cap) h_values[c++] = (int64_t)h[q];
+    }
+  if (distinct > cap) return fail(LS_E_ARG, "h_values holds fewer entries than the distinct unroll products");
   std::sort(h_values, h_values + c);
   *h_count = c;
   return LS_E_OK;
@@ -4210,7 +4258,8 @@ static int score_device(ls_task* t, const void* d_src, int pbytes, int64_t n, do
   const int mode = mode_of(t, pbytes != 0);
   const ScoreFn fn = score_fn(t->host, mode, pbytes);
   const size_t sm = smem_score(t->host, mode);
-  fn<<<grid_for(t, n, blocks_per_sm(fn, sm)), TPB, sm, s>>>(t->d_task, d_src, pbytes, n, d_scores, d_features,
+  BPS_TRY(bps, fn, sm);
+  fn<<<grid_for(t, n, bps), TPB, sm, s>>>(t->d_task, d_src, pbytes, n, d_scores, d_features,
                                                             d_status);
   CUDA_TRY(cudaGetLastError());
   return LS_E_OK;
@@ -4260,7 +4309,8 @@ static int topk_device(ls_task* t, const void* d_src, int pbytes, int64_t n, int
   const int mode = mode_of(t, pbytes != 0);
   const TopkFn fn = topk_fn(t->host, mode, pbytes);
   const size_t sm = smem_topk(t->host, k, mode);
-  const int grid = n > 0 ? grid_for(t, n, blocks_per_sm(fn, sm)) : 1;
+  BPS_TRY(bps, fn, sm);
+  const int grid = n > 0 ? grid_for(t, n, bps) : 1;
   const int ngroups = (grid + TK_GROUP - 1) / TK_GROUP;
   // two-stage merge (block-minima bound, merge_filter_kernel) when the grid has plenty of
   // blocks per answer key; else the in-kernel merge tree
@@ -4269,8 +4319,27 @@ static int topk_device(ls_task* t, const void* d_src, int pbytes, int64_t n, int
   const size_t keys_bytes = sizeof(Key) * (two ? (size_t)grid * 2 * topk_buf(k) : ((size_t)grid + ngroups) * k);
   const size_t out_bytes = h_out ? 16 + 16 * (size_t)k : 0;
   const size_t ws_bytes = WS_FIXED_BYTES + keys_bytes + out_bytes;
-  unsigned char* ws = nullptr;
-  bool cached = false;
+  // The workspace lease: the task's cached block (grown on demand) unless another call holds it
+  // or it belongs to another stream, else a private block.  Released on every exit path; a call
+  // that fails after its first launch leaves the cached block marked for re-initialisation (its
+  // self-resetting counters may not have been reset).
+  struct Lease {
+    ls_task* t;
+    cudaStream_t s;
+    unsigned char* ws = nullptr;
+    unsigned long long* tr = nullptr;
+    bool cached = false, launched = false, ok = false;
+    ~Lease() {
+      if (tr) cudaFree(tr);
+      if (cached) {
+        std::lock_guard<std::mutex> g(t->mu);
+        t->ws_busy = false;
+        if (launched && !ok) t->ws_dirty = true;
+      } else if (ws) {
+        cudaFreeAsync(ws, s);
+      }
+    }
+  } L{t, s};
   {
     std::lock_guard<std::mutex> g(t->mu);
     if (!t->ws_busy && (!t->ws || t->ws_stream == s)) {
@@ -4279,19 +4348,24 @@ static int topk_device(ls_task* t, const void* d_src, int pbytes, int64_t n, int
         t->ws = nullptr;
         t->ws_bytes = 0;
         CUDA_TRY(cudaMallocAsync(&t->ws, ws_bytes, s));
-        CUDA_TRY(ws_init(t->ws, s));
         t->ws_bytes = ws_bytes;
         t->ws_stream = s;
+        t->ws_dirty = true;
+      }
+      if (t->ws_dirty) {
+        CUDA_TRY(ws_init(t->ws, s));
+        t->ws_dirty = false;
       }
       t->ws_busy = true;
-      ws = t->ws;
-      cached = true;
+      L.ws = t->ws;
+      L.cached = true;
     }
   }
-  if (!cached) {  // concurrent call or another stream: a private workspace
-    CUDA_TRY(cudaMallocAsync(&ws, ws_bytes, s));
-    CUDA_TRY(ws_init(ws, s));
+  if (!L.cached) {  // concurrent call or another stream: a private workspace
+    CUDA_TRY(cudaMallocAsync(&L.ws, ws_bytes, s));
+    CUDA_TRY(ws_init(L.ws, s));
   }
+  unsigned char* const ws = L.ws;
   unsigned int* tickets = reinterpret_cast<unsigned int*>(ws);
   unsigned long long* wvalid = reinterpret_cast<unsigned long long*>(ws + 4096);
   Key* block_out = reinterpret_cast<Key*>(ws + WS_FIXED_BYTES);
@@ -4303,23 +4377,19 @@ static int topk_device(ls_task* t, const void* d_src, int pbytes, int64_t n, int
     d_top_scores = reinterpret_cast<double*>(out + 16);
     d_top_index = reinterpret_cast<int64_t*>(d_top_scores + k);
   }
-  unsigned long long* tr = nullptr;
   const char* tr_env = getenv("LS_TRACE");
   if (tr_env && tr_env[0] == '1') {  // phase timestamps to stderr (profiling aid)
-    CUDA_TRY(cudaMalloc(&tr, sizeof(unsigned long long) * TR_SLOTS * grid));
-    CUDA_TRY(cudaMemset(tr, 0, sizeof(unsigned long long) * TR_SLOTS * grid));
+    CUDA_TRY(cudaMalloc(&L.tr, sizeof(unsigned long long) * TR_SLOTS * grid));
+    CUDA_TRY(cudaMemset(L.tr, 0, sizeof(unsigned long long) * TR_SLOTS * grid));
   }
+  unsigned long long* const tr = L.tr;
+  L.launched = true;
   fn<<<grid, TPB, sm, s>>>(t->d_task, d_src, pbytes, n, base_index, k, block_out, group_out, tickets, d_top_scores,
                            d_top_index, d_valid, topk_buf(k), mins, wvalid, tr);
   CUDA_TRY(cudaGetLastError());
   if (two) {
     const size_t msm = topk_state_bytes(topk_buf(k));
-    static thread_local bool attr = false;
-    if (!attr) {  // the largest state this kernel is launched with
-      cudaFuncSetAttribute(merge_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)topk_state_bytes(2048));
-      attr = true;
-    }
+    if (kernel_prepare(merge_filter_kernel, msm, false) < 0) return LS_E_CUDA;
     const int g2 = grid;  // one block list each
     // programmatic dependent launch: the merge is queued behind the scoring
     // launch's tail (its blocks wait in griddepcontrol.wait for the scoring
@@ -4340,17 +4410,11 @@ static int topk_device(ls_task* t, const void* d_src, int pbytes, int64_t n, int
                                 d_top_index, topk_buf(k), d_valid, wvalid, tr));
   }
   if (h_out) CUDA_TRY(cudaMemcpyAsync(h_out, out, out_bytes, cudaMemcpyDeviceToHost, s));
-  if (cached) {
-    std::lock_guard<std::mutex> g(t->mu);
-    t->ws_busy = false;
-  } else {
-    CUDA_TRY(cudaFreeAsync(ws, s));
-  }
+  L.ok = true;
   if (tr) {
     std::vector<unsigned long long> h((size_t)TR_SLOTS * grid);
     CUDA_TRY(cudaStreamSynchronize(s));
     CUDA_TRY(cudaMemcpy(h.data(), tr, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost));
-    cudaFree(tr);
     unsigned long long t0 = ~0ull, surv = 0;
     for (int b = 0; b < grid; ++b) t0 = std::min(t0, h[b * TR_SLOTS]);
     for (int b = 0; b < grid; ++b)
@@ -4551,24 +4615,39 @@ int ls_task_set_space(ls_task* t, const ls_space_desc* sp) {
   return LS_E_OK;
 }
 
+static int merge_launch(const Key* keys, const double* d_scores, const int64_t* d_index, int64_t m, int32_t k_out,
+                        double* d_out_scores, int64_t* d_out_index, cudaStream_t s) {
+  const size_t msm = topk_state_bytes(topk_buf(k_out));
+  if (kernel_prepare(merge_keys_kernel, msm, false) < 0) return LS_E_CUDA;
+  merge_keys_kernel<<<1, TPB, msm, s>>>(keys, d_scores, d_index, m, k_out, d_out_scores, d_out_index, topk_buf(k_out));
+  CUDA_TRY(cudaGetLastError());
+  return LS_E_OK;
+}
+
 int ls_topk_merge(const double* d_scores, const int64_t* d_index, int32_t n_lists, int32_t k_in, int32_t k_out,
                   double* d_out_scores, int64_t* d_out_index, void* stream) {
   if (!d_scores || !d_index || n_lists < 0 || k_in < 0 || k_out < 1 || k_out > TK_MAXK || !d_out_scores ||
       !d_out_index)
     return fail(LS_E_ARG, "bad argument");
-  cudaStream_t s = (cudaStream_t)stream;
-  int64_t m = (int64_t)n_lists * k_in;
-  Key* keys = nullptr;
-  CUDA_TRY(cudaMallocAsync(&keys, sizeof(Key) * std::max<int64_t>(1, m), s));
-  if (m > 0) {
-    lists_to_keys_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(d_scores, d_index, m, keys);
-    CUDA_TRY(cudaGetLastError());
-  }
-  const size_t msm = topk_state_bytes(topk_buf(k_out));
-  cudaFuncSetAttribute(merge_keys_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm);
-  merge_keys_kernel<<<1, TPB, msm, s>>>(keys, m, k_out, d_out_scores, d_out_index, topk_buf(k_out));
+  return merge_launch(nullptr, d_scores, d_index, (int64_t)n_lists * k_in, k_out, d_out_scores, d_out_index,
+                      (cudaStream_t)stream);
+}
+
+int ls_topk_merge_keys(const ls_topk_key* d_keys, int64_t m, int32_t k_out, double* d_out_scores,
+                       int64_t* d_out_index, void* stream) {
+  if ((m > 0 && !d_keys) || m < 0 || k_out < 1 || k_out > TK_MAXK || !d_out_scores || !d_out_index)
+    return fail(LS_E_ARG, "bad argument");
+  static_assert(sizeof(ls_topk_key) == sizeof(Key), "ls_topk_key layout");
+  return merge_launch(reinterpret_cast<const Key*>(d_keys), nullptr, nullptr, m, k_out, d_out_scores, d_out_index,
+                      (cudaStream_t)stream);
+}
+
+int ls_topk_to_keys(const double* d_scores, const int64_t* d_index, int64_t m, ls_topk_key* d_keys, void* stream) {
+  if (m < 0 || (m > 0 && (!d_scores || !d_index || !d_keys))) return fail(LS_E_ARG, "bad argument");
+  if (m == 0) return LS_E_OK;
+  lists_to_keys_kernel<<<(unsigned)((m + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      d_scores, d_index, m, reinterpret_cast<Key*>(d_keys));
   CUDA_TRY(cudaGetLastError());
-  CUDA_TRY(cudaFreeAsync(keys, s));
   return LS_E_OK;
 }
 
@@ -4586,8 +4665,21 @@ static const void* mapped_alias(const void* h) {
 
 static int score_topk_mapped(ls_task* t, const void* d_alias, int pbytes, int64_t n, int64_t base_index, int32_t k,
                              double* h_top_scores, int64_t* h_top_index, int64_t* h_n_valid, cudaStream_t s) {
-  // pinned staging block: count (16 B slot) | scores | indices, filled by one D2H copy
-  unsigned char* stage = nullptr;
+  // pinned staging block: count (16 B slot) | scores | indices, filled by one D2H copy; the task's
+  // cached block unless another host call holds it (then a private one), released on every path
+  struct Stage {
+    ls_task* t;
+    unsigned char* p = nullptr;
+    bool own = false;
+    ~Stage() {
+      if (own) {
+        if (p) cudaFreeHost(p);
+      } else if (p) {
+        std::lock_guard<std::mutex> g(t->mu);
+        t->stage_busy = false;
+      }
+    }
+  } S{t};
   const size_t need = 16 + 16 * (size_t)k;
   {
     std::lock_guard<std::mutex> g(t->mu);
@@ -4600,32 +4692,29 @@ static int score_topk_mapped(ls_task* t, const void* d_alias, int pbytes, int64_
         t->stage_bytes = need;
       }
       t->stage_busy = true;
-      stage = t->stage;
+      S.p = t->stage;
     }
   }
-  bool own = false;
-  if (!stage) {  // concurrent host call on this task: a private staging block
-    CUDA_TRY(cudaMallocHost(&stage, need));
-    own = true;
+  if (!S.p) {  // concurrent host call on this task: a private staging block
+    S.own = true;
+    CUDA_TRY(cudaMallocHost(&S.p, need));
   }
-  int rc = topk_device(t, d_alias, pbytes, n, base_index, k, nullptr, nullptr, nullptr, s, stage);
-  if (rc == LS_E_OK) {
-    CUDA_TRY(cudaStreamSynchronize(s));
-    unsigned long long hv = 0;
-    memcpy(&hv, stage, 8);
-    memcpy(h_top_scores, stage + 16, sizeof(double) * k);
-    memcpy(h_top_index, stage + 16 + 8 * (size_t)k, sizeof(int64_t) * k);
-    if (h_n_valid) *h_n_valid = (int64_t)hv;
-  }
-  if (own) {
-    cudaFreeHost(stage);
-  } else {
-    std::lock_guard<std::mutex> g(t->mu);
-    t->stage_busy = false;
-  }
-  return rc;
+  const int rc = topk_device(t, d_alias, pbytes, n, base_index, k, nullptr, nullptr, nullptr, s, S.p);
+  if (rc != LS_E_OK) return rc;
+  CUDA_TRY(cudaStreamSynchronize(s));
+  unsigned long long hv = 0;
+  memcpy(&hv, S.p, 8);
+  memcpy(h_top_scores, S.p + 16, sizeof(double) * k);
+  memcpy(h_top_index, S.p + 16 + 8 * (size_t)k, sizeof(int64_t) * k);
+  if (h_n_valid) *h_n_valid = (int64_t)hv;
+  return LS_E_OK;
 }
 
+// Host buffers that are not mapped: chunks are copied on a side stream into two
+// device buffers (the copy of chunk c+1 overlaps the scoring of chunk c), every
+// chunk gets its own fused top-k, and the chunk lists are merged.  Every stream,
+// event and buffer is owned by `R` and released (after the work it backs has
+// drained) on every exit path.
 static int score_topk_host_any(ls_task* t, const void* h_src, int pbytes, int64_t n, int64_t base_index, int32_t k,
                                double* h_top_scores, int64_t* h_top_index, int64_t* h_n_valid, cudaStream_t s) {
   CUDA_TRY(cudaSetDevice(t->device));
@@ -4633,67 +4722,65 @@ static int score_topk_host_any(ls_task* t, const void* h_src, int pbytes, int64_
     if (const void* alias = mapped_alias(h_src))
       return score_topk_mapped(t, alias, pbytes, n, base_index, k, h_top_scores, h_top_index, h_n_valid, s);
   const size_t esz = pbytes ? (size_t)pbytes : sizeof(ls_record);
-  const int64_t CH = (int64_t)((8u << 20) / esz);  // 8 MiB chunks: copy of chunk c+1 overlaps scoring of chunk c
+  const int64_t CH = (int64_t)((8u << 20) / esz);  // 8 MiB chunks
   const int64_t nch = std::max<int64_t>(1, (n + CH - 1) / CH);
-  cudaStream_t cp;
-  CUDA_TRY(cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking));
-  cudaEvent_t ev_start, ready[2], freed[2];
-  CUDA_TRY(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
-  for (int b = 0; b < 2; ++b) {
-    CUDA_TRY(cudaEventCreateWithFlags(&ready[b], cudaEventDisableTiming));
-    CUDA_TRY(cudaEventCreateWithFlags(&freed[b], cudaEventDisableTiming));
-  }
+  struct Res {
+    cudaStream_t s, cp = nullptr;
+    cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // start, ready[2], freed[2]
+    std::vector<void*> bufs;
+    ~Res() {
+      cudaStreamSynchronize(s);  // the queued work that uses the buffers has drained
+      if (cp) cudaStreamSynchronize(cp);
+      for (void* p : bufs) cudaFree(p);
+      for (cudaEvent_t e : ev)
+        if (e) cudaEventDestroy(e);
+      if (cp) cudaStreamDestroy(cp);
+    }
+    cudaError_t alloc(void** p, size_t bytes) {
+      const cudaError_t e = cudaMallocAsync(p, std::max<size_t>(bytes, 16), s);
+      if (e == cudaSuccess) bufs.push_back(*p);
+      return e;
+    }
+  } R{s};
+  CUDA_TRY(cudaStreamCreateWithFlags(&R.cp, cudaStreamNonBlocking));
+  for (auto& e : R.ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  cudaEvent_t ev_start = R.ev[0], *ready = R.ev + 1, *freed = R.ev + 3;
   unsigned char* buf[2] = {nullptr, nullptr};
-  double* ls = nullptr;
-  int64_t* li = nullptr;
+  double *ls = nullptr, *out_s = nullptr;
+  int64_t *li = nullptr, *out_i = nullptr;
   unsigned long long* valid = nullptr;
-  double* out_s = nullptr;
-  int64_t* out_i = nullptr;
-  int rc = LS_E_OK;
   for (int b = 0; b < 2; ++b)
-    CUDA_TRY(cudaMallocAsync(&buf[b], esz * (size_t)std::min(CH, std::max<int64_t>(n, 1)), s));
-  CUDA_TRY(cudaMallocAsync(&ls, sizeof(double) * nch * k, s));
-  CUDA_TRY(cudaMallocAsync(&li, sizeof(int64_t) * nch * k, s));
-  CUDA_TRY(cudaMallocAsync(&valid, sizeof(unsigned long long) * nch, s));  // one count per chunk
-  CUDA_TRY(cudaMallocAsync(&out_s, sizeof(double) * k, s));
-  CUDA_TRY(cudaMallocAsync(&out_i, sizeof(int64_t) * k, s));
+    CUDA_TRY(R.alloc((void**)&buf[b], esz * (size_t)std::min(CH, std::max<int64_t>(n, 1))));
+  CUDA_TRY(R.alloc((void**)&ls, sizeof(double) * nch * k));
+  CUDA_TRY(R.alloc((void**)&li, sizeof(int64_t) * nch * k));
+  CUDA_TRY(R.alloc((void**)&valid, sizeof(unsigned long long) * nch));  // one count per chunk
+  CUDA_TRY(R.alloc((void**)&out_s, sizeof(double) * k));
+  CUDA_TRY(R.alloc((void**)&out_i, sizeof(int64_t) * k));
   CUDA_TRY(cudaEventRecord(ev_start, s));
-  CUDA_TRY(cudaStreamWaitEvent(cp, ev_start, 0));
+  CUDA_TRY(cudaStreamWaitEvent(R.cp, ev_start, 0));
   const unsigned char* src = reinterpret_cast<const unsigned char*>(h_src);
-  for (int64_t c = 0; c < nch && rc == LS_E_OK; ++c) {
+  for (int64_t c = 0; c < nch; ++c) {
     const int b = (int)(c & 1);
     const int64_t off = c * CH, m = std::min(CH, n - off);
-    if (c >= 2) CUDA_TRY(cudaStreamWaitEvent(cp, freed[b], 0));
-    if (m > 0) CUDA_TRY(cudaMemcpyAsync(buf[b], src + off * esz, esz * m, cudaMemcpyHostToDevice, cp));
-    CUDA_TRY(cudaEventRecord(ready[b], cp));
+    if (c >= 2) CUDA_TRY(cudaStreamWaitEvent(R.cp, freed[b], 0));
+    if (m > 0) CUDA_TRY(cudaMemcpyAsync(buf[b], src + off * esz, esz * m, cudaMemcpyHostToDevice, R.cp));
+    CUDA_TRY(cudaEventRecord(ready[b], R.cp));
     CUDA_TRY(cudaStreamWaitEvent(s, ready[b], 0));
-    rc = topk_device(t, buf[b], pbytes, std::max<int64_t>(m, 0), base_index + off, k, ls + c * k, li + c * k, valid + c,
-                     s);
+    if (int rc = topk_device(t, buf[b], pbytes, std::max<int64_t>(m, 0), base_index + off, k, ls + c * k, li + c * k,
+                             valid + c, s))
+      return rc;
     CUDA_TRY(cudaEventRecord(freed[b], s));
   }
-  if (rc == LS_E_OK) rc = ls_topk_merge(ls, li, (int32_t)nch, k, k, out_s, out_i, s);
+  if (int rc = ls_topk_merge(ls, li, (int32_t)nch, k, k, out_s, out_i, s)) return rc;
   CUDA_TRY(cudaMemcpyAsync(h_top_scores, out_s, sizeof(double) * k, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaMemcpyAsync(h_top_index, out_i, sizeof(int64_t) * k, cudaMemcpyDeviceToHost, s));
   std::vector<unsigned long long> hvs((size_t)nch, 0);
   CUDA_TRY(cudaMemcpyAsync(hvs.data(), valid, sizeof(unsigned long long) * nch, cudaMemcpyDeviceToHost, s));
-  for (int b = 0; b < 2; ++b) cudaFreeAsync(buf[b], s);
-  cudaFreeAsync(ls, s);
-  cudaFreeAsync(li, s);
-  cudaFreeAsync(valid, s);
-  cudaFreeAsync(out_s, s);
-  cudaFreeAsync(out_i, s);
   CUDA_TRY(cudaStreamSynchronize(s));
-  CUDA_TRY(cudaStreamSynchronize(cp));
-  cudaStreamDestroy(cp);
-  cudaEventDestroy(ev_start);
-  for (int b = 0; b < 2; ++b) {
-    cudaEventDestroy(ready[b]);
-    cudaEventDestroy(freed[b]);
-  }
   unsigned long long hv = 0;
   for (unsigned long long v : hvs) hv += v;
   if (h_n_valid) *h_n_valid = (int64_t)hv;
-  return rc;
+  return LS_E_OK;
 }
 
 int ls_score_topk_host(ls_task* t, const ls_record* h_records, int64_t n, int64_t base_index, int32_t k,

@@ -24,6 +24,18 @@
 // trajectories differ from the reference's optimize; es.optimize keeps the
 // reference's exact trajectory with host noise (parity mode).  Everything
 // downstream of the noise follows the reference's arithmetic.
+//
+// Sharded over G ranks: rank r evaluates members [r P/G,
+// (r+1) P/G) (their noise depends on the global member index only), the F keys
+// are all-gathered in place (every rank then holds the whole population's keys
+// and sorts them: global stable ranks, ls/es.py:65-71), rank r sums its share
+// of the fixed 1024-position chunks, the chunk partials are all-gathered in
+// place and every rank adds all of them in chunk order.  Chunk boundaries and
+// the order of every float64 addition are independent of G, so theta, the
+// trace and the evaluated set are bit-identical for G = 1, 2, 4, 8.  The memo
+// is per rank; the distinct count is the size of the union of the ranks'
+// evaluated lists and the trace the per-generation minimum over ranks (both
+// computed by the caller after the run).
 
 #include <cub/device/device_radix_sort.cuh>
 
@@ -36,16 +48,20 @@ struct EsDev {
   uint64_t seed;
   int32_t pop, iters, dim, rank_normalize;
   int32_t gen, pad;
+  int32_t lo, hi;                      // this rank's members [lo, hi)
+  int32_t c0, c1;                      // this rank's chunks [c0, c1) of sum_i w_i eps_i
+  int32_t chunks, pad2;                // all chunks
   uint32_t n_ax[ES_MAXDIM];            // choices per axis
   unsigned long long best;             // order bits of the best score so far
   unsigned long long evaluations;      // distinct schedules scored
-  long long err;                       // first failure: (generation+1 | 0 start) << 40 | member << 8 | status
+  unsigned long long err;              // first failure (atomicMin; ~0 none): (generation+1 | 0 start) << 40 | member << 8 | status
   unsigned long long* keys;            // memo: flat point + 1 (0 = empty)
   unsigned long long* vals;            // memo: order bits of the score (0 = being scored)
   unsigned long long cap_mask;
   unsigned long long* list_p;          // evaluated points in discovery order
   double* list_s;                      // their scores
   unsigned long long list_cap;
+  unsigned long long full;             // memo probes exhausted (table full): reported as a failure
   unsigned long long* sort_in;         // per member: order bits of F = -score
   unsigned long long* sort_out;
   uint32_t* idx_in;
@@ -117,7 +133,7 @@ __device__ int es_memo_score(const DTask& T, const int32_t* tab, Evaluator<TM, R
                              double* s) {
   const unsigned long long key = x + 1;
   unsigned long long h = (key * 0x9E3779B97F4A7C15ull) >> 17;
-  for (;;) {
+  for (unsigned long long probe = 0; probe <= E.cap_mask; ++probe, ++h) {
     h &= E.cap_mask;
     const unsigned long long k = atomicCAS(&E.keys[h], 0ull, key);
     if (k == 0ull) {  // claimed: a new distinct schedule
@@ -140,8 +156,9 @@ __device__ int es_memo_score(const DTask& T, const int32_t* tab, Evaluator<TM, R
       }
       return score_point<TM, RM, MODE>(T, tab, ev, x, s);
     }
-    ++h;
   }
+  atomicExch(&E.full, 1ull);  // cannot happen within the sizing of ls_es_create
+  return LS_ST_OVERFLOW;
 }
 
 // One generation (start = true: the decode of theta alone, ls/es.py:183-186).
@@ -157,8 +174,8 @@ __global__ void __launch_bounds__(TPB, 2) es_gen_kernel(const DTask* __restrict_
   Evaluator<TM, RM, MODE> ev(T, p, tab);
   EsDev& E = *ges;
   const int g = E.gen;
-  const int n = start ? 1 : E.pop;
-  for (int i = blockIdx.x * TPB + threadIdx.x; i < n; i += gridDim.x * TPB) {
+  const int lo = start ? 0 : E.lo, hi = start ? 1 : E.hi;
+  for (int i = lo + blockIdx.x * TPB + threadIdx.x; i < hi; i += gridDim.x * TPB) {
     uint64_t x = 0;
     for (int d = 0; d < E.dim; d += 2) {
       double z0 = 0.0, z1 = 0.0;
@@ -173,14 +190,12 @@ __global__ void __launch_bounds__(TPB, 2) es_gen_kernel(const DTask* __restrict_
     double s = 0.0;
     const int st = es_memo_score<TM, RM, MODE>(T, tab, ev, E, x, &s);
     if (st) {  // generation field 0: the start point
-      atomicCAS(reinterpret_cast<unsigned long long*>(&E.err), 0ull,
-                ((unsigned long long)(start ? 0 : g + 1) << 40) | ((unsigned long long)i << 8) |
-                    (unsigned long long)st);
+      atomicMin(&E.err, ((unsigned long long)(start ? 0 : g + 1) << 40) | ((unsigned long long)i << 8) |
+                            (unsigned long long)st);
       s = 0.0;
     }
     if (!start) {
-      E.sort_in[i] = order_bits(-s);  // F = -score, maximised (ls/es.py:176)
-      E.idx_in[i] = (uint32_t)i;
+      E.sort_in[i] = order_bits(-s);  // F = -score, maximised (ls/es.py:176); idx_in is the identity
     }
   }
 }
@@ -192,7 +207,8 @@ __global__ void __launch_bounds__(TPB) es_partial_kernel(EsDev* __restrict__ ges
   EsDev& E = *ges;
   const int n = E.pop, dim = E.dim, g = E.gen;
   const bool flat = E.rank_normalize && E.sort_out[0] == E.sort_out[n - 1];  // np.ptp(values) == 0
-  const int j0 = blockIdx.x * ES_CHUNK;
+  const int chunk = E.c0 + blockIdx.x;
+  const int j0 = chunk * ES_CHUNK;
   double acc[ES_MAXDIM];
   for (int d = 0; d < dim; ++d) acc[d] = 0.0;
   for (int j = j0 + threadIdx.x; j < min(n, j0 + ES_CHUNK); j += TPB) {
@@ -216,13 +232,14 @@ __global__ void __launch_bounds__(TPB) es_partial_kernel(EsDev* __restrict__ ges
       if (threadIdx.x < w) red[threadIdx.x] = __dadd_rn(red[threadIdx.x], red[threadIdx.x + w]);
       __syncthreads();
     }
-    if (threadIdx.x == 0) E.partial[(size_t)blockIdx.x * dim + d] = red[0];
+    if (threadIdx.x == 0) E.partial[(size_t)chunk * dim + d] = red[0];
     __syncthreads();
   }
 }
 
-__global__ void es_update_kernel(EsDev* __restrict__ ges, int chunks) {
+__global__ void es_update_kernel(EsDev* __restrict__ ges) {
   EsDev& E = *ges;
+  const int chunks = E.chunks;
   const int d = threadIdx.x;
   const int g = E.gen;
   if (d < E.dim) {
@@ -253,6 +270,7 @@ struct ls_es {
   void* sort_tmp;
   size_t sort_tmp_bytes;
   int chunks, mode;
+  int rank, world, cpr;  // shard: rank of world, chunks per rank (the partials' gather slice)
   cudaGraphExec_t graph;
   std::vector<void*> owned;
 };
@@ -289,39 +307,58 @@ int es_launch_gen(ls_es* es, int start, cudaStream_t s) {
   const ls_task* t = es->task;
   const EsGenFn fn = es_gen_fn(t->host, es->mode);
   const size_t sm = smem_score(t->host, es->mode);
-  const int64_t n = start ? 1 : es->host.pop;
-  fn<<<grid_for(t, n, blocks_per_sm(fn, sm)), TPB, sm, s>>>(t->d_task, es->dev, start);
+  const int64_t n = start ? 1 : es->host.hi - es->host.lo;
+  BPS_TRY(bps, fn, sm);
+  fn<<<grid_for(t, n, bps), TPB, sm, s>>>(t->d_task, es->dev, start);
+  CUDA_TRY(cudaGetLastError());
+  return LS_E_OK;
+}
+
+// after the F keys of the whole population are present: global stable ranks and this
+// rank's chunk partials
+int es_launch_rank(ls_es* es, cudaStream_t s) {
+  size_t bytes = es->sort_tmp_bytes;
+  CUDA_TRY(cub::DeviceRadixSort::SortPairs(es->sort_tmp, bytes, es->host.sort_in, es->host.sort_out, es->host.idx_in,
+                                           es->host.idx_out, es->host.pop, 0, 64, s));
+  if (es->host.c1 > es->host.c0) {
+    es_partial_kernel<<<es->host.c1 - es->host.c0, TPB, 0, s>>>(es->dev);
+    CUDA_TRY(cudaGetLastError());
+  }
+  return LS_E_OK;
+}
+
+int es_launch_update(ls_es* es, cudaStream_t s) {
+  es_update_kernel<<<1, 32, 0, s>>>(es->dev);
   CUDA_TRY(cudaGetLastError());
   return LS_E_OK;
 }
 
 int es_enqueue_generation(ls_es* es, cudaStream_t s) {
   if (int rc = es_launch_gen(es, 0, s)) return rc;
-  size_t bytes = es->sort_tmp_bytes;
-  CUDA_TRY(cub::DeviceRadixSort::SortPairs(es->sort_tmp, bytes, es->host.sort_in, es->host.sort_out, es->host.idx_in,
-                                           es->host.idx_out, es->host.pop, 0, 64, s));
-  es_partial_kernel<<<es->chunks, TPB, 0, s>>>(es->dev);
-  CUDA_TRY(cudaGetLastError());
-  es_update_kernel<<<1, 32, 0, s>>>(es->dev, es->chunks);
-  CUDA_TRY(cudaGetLastError());
-  return LS_E_OK;
+  if (int rc = es_launch_rank(es, s)) return rc;
+  return es_launch_update(es, s);
 }
 
 }  // namespace
 
 extern "C" {
 
-int ls_es_create(ls_task* t, const ls_es_params* p, const double* h_theta0, ls_es** out) {
+int ls_es_create_shard(ls_task* t, const ls_es_params* p, const double* h_theta0, int32_t rank, int32_t world,
+                       ls_es** out) {
   if (!t || !p || !out) return fail(LS_E_ARG, "null argument");
   *out = nullptr;
   if (t->host.sp_n < 1) return fail(LS_E_ARG, "no schedule space attached (ls_task_set_space)");
   if (!(p->alpha > 0) || !(p->sigma > 0)) return fail(LS_E_ARG, "alpha and sigma must be positive");
   if (p->population < 2 || p->iterations < 1) return fail(LS_E_ARG, "population >= 2 and iterations >= 1");
+  if (world < 1 || rank < 0 || rank >= world) return fail(LS_E_ARG, "bad rank / world");
+  if (p->population % world) return fail(LS_E_ARG, "population must be a multiple of the number of ranks");
   CUDA_TRY(cudaSetDevice(t->device));
   ls_es* es = new ls_es();
   es->task = t;
   es->graph = nullptr;
   es->sort_tmp = nullptr;
+  es->rank = rank;
+  es->world = world;
   EsDev& H = es->host;
   memset(&H, 0, sizeof(H));
   H.dim = t->host.sp_n;
@@ -343,12 +380,27 @@ int ls_es_create(ls_task* t, const ls_es_params* p, const double* h_theta0, ls_e
   H.iters = p->iterations;
   H.rank_normalize = p->rank_normalize ? 1 : 0;
   H.best = ~0ull;
-  const double distinct = std::min(space, (double)p->population * p->iterations + 1.0);
-  unsigned long long cap = 1024;
-  while ((double)cap < 2.0 * distinct && cap < (1ull << 27)) cap <<= 1;
-  H.cap_mask = cap - 1;
-  H.list_cap = (unsigned long long)std::min(distinct, (double)(1ull << 27));
+  H.err = ~0ull;
+  const int per = p->population / world;
+  H.lo = rank * per;
+  H.hi = H.lo + per;
   es->chunks = (H.pop + ES_CHUNK - 1) / ES_CHUNK;
+  es->cpr = (es->chunks + world - 1) / world;
+  H.chunks = es->chunks;
+  H.c0 = std::min(es->chunks, rank * es->cpr);
+  H.c1 = std::min(es->chunks, (rank + 1) * es->cpr);
+  // memo sized for this rank's distinct schedules at load <= 1/2; the probe is bounded
+  const double distinct = std::min(space, (double)per * p->iterations + 1.0);
+  constexpr double ES_MAX_DISTINCT = (double)(1ull << 28);
+  if (distinct > ES_MAX_DISTINCT) {
+    delete es;
+    return fail(LS_E_UNSUPPORTED, "more than 2^28 distinct schedules per rank (population x iterations); "
+                                  "shard the population over more ranks or run fewer iterations per call");
+  }
+  unsigned long long cap = 1024;
+  while ((double)cap < 2.0 * distinct) cap <<= 1;
+  H.cap_mask = cap - 1;
+  H.list_cap = (unsigned long long)distinct;
   es->mode = mode_of(t, true);
   auto alloc = [&](void** ptr, size_t bytes) -> int {
     if (cudaMalloc(ptr, std::max<size_t>(bytes, 16)) != cudaSuccess) return fail(LS_E_NOMEM, "ES buffer allocation");
@@ -364,7 +416,7 @@ int ls_es_create(ls_task* t, const ls_es_params* p, const double* h_theta0, ls_e
   rc = rc ? rc : alloc((void**)&H.sort_out, sizeof(unsigned long long) * H.pop);
   rc = rc ? rc : alloc((void**)&H.idx_in, sizeof(uint32_t) * H.pop);
   rc = rc ? rc : alloc((void**)&H.idx_out, sizeof(uint32_t) * H.pop);
-  rc = rc ? rc : alloc((void**)&H.partial, sizeof(double) * es->chunks * H.dim);
+  rc = rc ? rc : alloc((void**)&H.partial, sizeof(double) * (size_t)es->cpr * world * H.dim);
   rc = rc ? rc : alloc((void**)&H.theta_hist, sizeof(double) * (H.iters + 1) * H.dim);
   rc = rc ? rc : alloc((void**)&H.trace, sizeof(double) * H.iters);
   rc = rc ? rc : alloc((void**)&es->dev, sizeof(EsDev));
@@ -374,6 +426,12 @@ int ls_es_create(ls_task* t, const ls_es_params* p, const double* h_theta0, ls_e
     es->sort_tmp_bytes = bytes;
     rc = alloc(&es->sort_tmp, bytes);
   }
+  if (rc == LS_E_OK) {  // member indices of the gathered keys: the identity (rank slices in rank order)
+    std::vector<uint32_t> iota((size_t)H.pop);
+    for (int i = 0; i < H.pop; ++i) iota[i] = (uint32_t)i;
+    if (cudaMemcpy(H.idx_in, iota.data(), sizeof(uint32_t) * H.pop, cudaMemcpyHostToDevice) != cudaSuccess)
+      rc = fail(LS_E_CUDA, "ES index upload");
+  }
   if (rc) {
     ls_es_destroy(es);
     return rc;
@@ -382,7 +440,11 @@ int ls_es_create(ls_task* t, const ls_es_params* p, const double* h_theta0, ls_e
   return LS_E_OK;
 }
 
-int ls_es_run(ls_es* es, void* stream) {
+int ls_es_create(ls_task* t, const ls_es_params* p, const double* h_theta0, ls_es** out) {
+  return ls_es_create_shard(t, p, h_theta0, 0, 1, out);
+}
+
+int ls_es_begin(ls_es* es, void* stream) {
   if (!es) return fail(LS_E_ARG, "null argument");
   ls_task* t = es->task;
   CUDA_TRY(cudaSetDevice(t->device));
@@ -393,7 +455,32 @@ int ls_es_run(ls_es* es, void* stream) {
   CUDA_TRY(cudaMemsetAsync(H.vals, 0, sizeof(unsigned long long) * (H.cap_mask + 1), s));
   CUDA_TRY(cudaMemcpyAsync(es->dev, &H, sizeof(EsDev), cudaMemcpyHostToDevice, s));
   CUDA_TRY(cudaMemcpyAsync(H.theta_hist, H.theta, sizeof(double) * H.dim, cudaMemcpyHostToDevice, s));
-  if (int rc = es_launch_gen(es, 1, s)) return rc;  // the start point (ls/es.py:183-186)
+  return es_launch_gen(es, 1, s);  // the start point (ls/es.py:183-186), on every rank
+}
+
+int ls_es_step(ls_es* es, int32_t stage, void* stream) {
+  if (!es || stage < 0 || stage > 2) return fail(LS_E_ARG, "bad argument");
+  CUDA_TRY(cudaSetDevice(es->task->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  return stage == 0 ? es_launch_gen(es, 0, s) : stage == 1 ? es_launch_rank(es, s) : es_launch_update(es, s);
+}
+
+int ls_es_shard_buffers(ls_es* es, void** d_keys, int64_t* keys_per_rank, void** d_partials,
+                        int64_t* partials_per_rank) {
+  if (!es) return fail(LS_E_ARG, "null argument");
+  if (d_keys) *d_keys = es->host.sort_in;
+  if (keys_per_rank) *keys_per_rank = es->host.hi - es->host.lo;
+  if (d_partials) *d_partials = es->host.partial;
+  if (partials_per_rank) *partials_per_rank = (int64_t)es->cpr * es->host.dim;
+  return LS_E_OK;
+}
+
+int ls_es_run(ls_es* es, void* stream) {
+  if (!es) return fail(LS_E_ARG, "null argument");
+  if (es->world != 1) return fail(LS_E_ARG, "a sharded run is driven generation by generation (ls_es_step)");
+  if (int rc = ls_es_begin(es, stream)) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  EsDev& H = es->host;
   bool single = true;
   for (int a = 0; a < H.dim; ++a) single &= H.n_ax[a] == 1;
   if (single) return LS_E_OK;  // a 1-schedule space needs no generation (ls/es.py:187-188)
@@ -405,10 +492,17 @@ int ls_es_run(ls_es* es, void* stream) {
     const int rc = es_enqueue_generation(es, cs);
     const cudaError_t ce = cudaStreamEndCapture(cs, &g);
     cudaStreamDestroy(cs);
-    if (rc) return rc;
+    if (rc) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
     if (ce != cudaSuccess) return fail(LS_E_CUDA, std::string("ES graph capture: ") + cudaGetErrorString(ce));
-    CUDA_TRY(cudaGraphInstantiate(&es->graph, g, 0));
+    const cudaError_t ie = cudaGraphInstantiate(&es->graph, g, 0);
     cudaGraphDestroy(g);
+    if (ie != cudaSuccess) {
+      es->graph = nullptr;
+      return fail(LS_E_CUDA, std::string("ES graph instantiate: ") + cudaGetErrorString(ie));
+    }
   }
   for (int it = 0; it < H.iters; ++it) CUDA_TRY(cudaGraphLaunch(es->graph, s));
   return LS_E_OK;
@@ -428,7 +522,7 @@ int ls_es_result(ls_es* es, double* h_theta_hist, double* h_trace, int64_t* h_ev
   if (h_trace) CUDA_TRY(cudaMemcpyAsync(h_trace, H.trace, sizeof(double) * H.iters, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
   if (h_evaluations) *h_evaluations = (int64_t)D.evaluations;
-  if (h_error) *h_error = D.err;
+  if (h_error) *h_error = D.err == ~0ull ? 0 : (int64_t)D.err;
   if (h_best_score) *h_best_score = D.best == ~0ull ? 0.0 : [](unsigned long long o) {
     unsigned long long b = (o >> 63) ? (o & 0x7fffffffffffffffull) : ~o;
     double x;

@@ -43,6 +43,8 @@ def lib():
     L.ls_score.argtypes = [vp, vp, i64, vp, vp, vp, vp]
     L.ls_score_topk.argtypes = [vp, vp, i64, i64, i32, vp, vp, vp, vp]
     L.ls_topk_merge.argtypes = [vp, vp, i32, i32, i32, vp, vp, vp]
+    L.ls_topk_merge_keys.argtypes = [vp, i64, i32, vp, vp, vp]
+    L.ls_topk_to_keys.argtypes = [vp, vp, i64, vp, vp]
     L.ls_score_topk_host.argtypes = [vp, vp, i64, i64, i32, vp, vp, vp, vp]
     L.ls_task_set_path.argtypes = [vp, i32]
     L.ls_task_set_space.argtypes = [vp, vp]
@@ -52,6 +54,10 @@ def lib():
     L.ls_task_path.argtypes = [vp]
     L.ls_task_points_path.argtypes = [vp]
     L.ls_es_create.argtypes = [vp, vp, vp, C.POINTER(vp)]
+    L.ls_es_create_shard.argtypes = [vp, vp, vp, i32, i32, C.POINTER(vp)]
+    L.ls_es_begin.argtypes = [vp, vp]
+    L.ls_es_step.argtypes = [vp, i32, vp]
+    L.ls_es_shard_buffers.argtypes = [vp, vp, vp, vp, vp]
     L.ls_es_run.argtypes = [vp, vp]
     L.ls_es_result.argtypes = [vp, vp, vp, vp, vp, vp, vp]
     L.ls_es_evaluated.argtypes = [vp, vp, vp, i64, vp, vp]
@@ -99,6 +105,16 @@ def _outputs(torch, k, device):
 
 def _dptr(t):
     return None if t is None else t.data_ptr()
+
+
+def _device_view(torch, ptr: int, n: int, dtype, device):
+    """A CUDA tensor aliasing library-owned device memory (no copy; valid while the owner lives)."""
+    class _Arr:  # __cuda_array_interface__ shim
+        def __init__(self):
+            typestr = {torch.int64: "<i8", torch.float64: "<f8"}[dtype]
+            self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": typestr, "data": (int(ptr), False),
+                                             "version": 3, "strides": None}
+    return torch.as_tensor(_Arr(), device=device)
 
 
 def to_device_records(records: np.ndarray, device=0):
@@ -158,7 +174,7 @@ class Task:
             return
         torch = _torch()
         n = d_records.shape[0]
-        vals = np.zeros(4096, np.int64)
+        vals = np.zeros(16384, np.int64)
         cnt = np.zeros(1, np.int32)
         _check(lib().ls_collect_unroll(self._h, _dptr(d_records), n, vals.ctypes.data, len(vals),
                                        cnt.ctypes.data, _stream(torch, stream)), "ls_collect_unroll")
@@ -249,7 +265,7 @@ class Task:
 
 
 def topk_merge(scores, index, n_lists: int, k_in: int, k_out: int, stream=None):
-    """Merge n_lists sorted (score, index) lists of k_in each into the k_out best (CUDA tensors)."""
+    """Merge n_lists (score, index) lists of k_in each into the k_out best (CUDA tensors)."""
     torch = _torch()
     out_s = torch.empty(k_out, dtype=torch.float64, device=scores.device)
     out_i = torch.empty(k_out, dtype=torch.int64, device=scores.device)
@@ -258,13 +274,37 @@ def topk_merge(scores, index, n_lists: int, k_in: int, k_out: int, stream=None):
     return out_s, out_i
 
 
+def topk_to_keys(scores, index, out, stream=None):
+    """Pack (score, index) lists into 16-byte ls_topk_key rows of `out` (int64 CUDA tensor [m, 2])."""
+    torch = _torch()
+    m = scores.shape[0]
+    assert out.dtype == torch.int64 and out.shape[0] >= m and out.is_contiguous()
+    _check(lib().ls_topk_to_keys(_dptr(scores), _dptr(index), m, _dptr(out), _stream(torch, stream)),
+           "ls_topk_to_keys")
+    return out
+
+
+def topk_merge_keys(keys, k_out: int, out=None, stream=None):
+    """Merge gathered ls_topk_key rows (int64 CUDA tensor [m, 2]) into the k_out best (score, index)."""
+    torch = _torch()
+    if out is None:
+        out = (torch.empty(k_out, dtype=torch.float64, device=keys.device),
+               torch.empty(k_out, dtype=torch.int64, device=keys.device))
+    _check(lib().ls_topk_merge_keys(_dptr(keys), keys.shape[0], int(k_out), _dptr(out[0]), _dptr(out[1]),
+                                    _stream(torch, stream)), "ls_topk_merge_keys")
+    return out
+
+
 class EsRun:
-    """A device ES run over a task's attached space (ls_es_* in include/loopscout_b200.h)."""
+    """A device ES run over a task's attached space (ls_es_* in include/loopscout_b200.h).
+
+    rank/world shard the population (ls_es_create_shard): drive it with run_sharded."""
 
     def __init__(self, task: Task, alpha: float, sigma: float, population: int, iterations: int, seed: int,
-                 rank_normalize: bool = True, theta0=None):
+                 rank_normalize: bool = True, theta0=None, rank: int = 0, world: int = 1):
         self.task = task
         self.dim = None
+        self.rank, self.world = int(rank), int(world)
         p = abi.EsParams(alpha=float(alpha), sigma=float(sigma), population=int(population),
                          iterations=int(iterations), seed=int(seed) & (2 ** 64 - 1),
                          rank_normalize=1 if rank_normalize else 0)
@@ -272,14 +312,54 @@ class EsRun:
         th = None if theta0 is None else np.ascontiguousarray(theta0, np.float64)
         h = C.c_void_p()
         with _torch().cuda.device(task.device):
-            _check(lib().ls_es_create(task._h, C.addressof(p), None if th is None else th.ctypes.data,
-                                      C.byref(h)), "ls_es_create")
+            _check(lib().ls_es_create_shard(task._h, C.addressof(p), None if th is None else th.ctypes.data,
+                                            self.rank, self.world, C.byref(h)), "ls_es_create_shard")
         self._h = h
 
     def run(self, stream=None):
         torch = _torch()
         with torch.cuda.device(self.task.device):
             _check(lib().ls_es_run(self._h, _stream(torch, stream)), "ls_es_run")
+
+    def shard_buffers(self):
+        """(keys u64 [world * keys_per_rank], partials f64 [world * partials_per_rank]) as CUDA tensors
+        aliasing the run's exchange buffers (zero-copy views), plus the per-rank slice lengths."""
+        torch = _torch()
+        kp, pp = C.c_void_p(), C.c_void_p()
+        kn, pn = C.c_int64(), C.c_int64()
+        _check(lib().ls_es_shard_buffers(self._h, C.byref(kp), C.byref(kn), C.byref(pp), C.byref(pn)),
+               "ls_es_shard_buffers")
+        dev = f"cuda:{self.task.device}"
+        keys = _device_view(torch, kp.value, kn.value * self.world, torch.int64, dev)
+        parts = _device_view(torch, pp.value, pn.value * self.world, torch.float64, dev)
+        return keys, parts, kn.value, pn.value
+
+    def begin(self, stream=None):
+        """Fresh state and the start point (ls_es_begin)."""
+        torch = _torch()
+        with torch.cuda.device(self.task.device):
+            _check(lib().ls_es_begin(self._h, _stream(torch, stream)), "ls_es_begin")
+
+    def step(self, stage: int, stream=None):
+        """One stage of a generation (ls_es_step): 0 local members, 1 ranks + local chunks, 2 update."""
+        torch = _torch()
+        with torch.cuda.device(self.task.device):
+            _check(lib().ls_es_step(self._h, int(stage), _stream(torch, stream)), "ls_es_step")
+
+    def run_sharded(self, exchange, stream=None, generations: "int | None" = None):
+        """Every generation stage by stage, with exchange(full_tensor, per_rank) an in-place all-gather
+        of the rank slices between stages 0/1 and 1/2 (not called for world 1).  generations=0 for a
+        one-schedule space (only the start point, ls/es.py:187-188)."""
+        keys, parts, kn, pn = self.shard_buffers()
+        self.begin(stream)
+        for _ in range(self.params.iterations if generations is None else generations):
+            self.step(0, stream)
+            if self.world > 1:
+                exchange(keys, kn)
+            self.step(1, stream)
+            if self.world > 1:
+                exchange(parts, pn)
+            self.step(2, stream)
 
     def result(self, dim: int, stream=None):
         """(theta history [iters+1, dim], trace [iters], evaluations, error code, best score)."""

@@ -13,7 +13,6 @@ so the theta trajectory, trace and evaluated table are too.
 from __future__ import annotations
 
 import json
-from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 
 import numpy as np
@@ -89,39 +88,6 @@ def es_update(theta: np.ndarray, params: EsParams, values: np.ndarray, noise: np
         values = np.where(bad, fill, values)
     weights = shape_fitness(values) if params.rank_normalize else values
     return theta + (params.alpha / (params.population * params.sigma)) * (weights @ noise)
-
-
-def es_step(theta, params: EsParams, objective, rng=None, noise=None, diagnostics=None):
-    """Generic host ES step over a Python objective (ls/es.py:74-93)."""
-    theta = np.asarray(theta, dtype=float)
-    if rng is None:
-        rng = np.random.default_rng(params.seed)
-    if noise is None:
-        noise = rng.standard_normal((params.population, theta.shape[0]))
-    values = np.array([objective(theta + params.sigma * eps) for eps in noise], dtype=float)
-    return es_update(theta, params, values, noise, diagnostics)
-
-
-def evaluate_population(thetas, objective, jobs=None, errors=None) -> list:
-    """Order-preserving evaluation of a Python objective (ls/es.py:96-116).
-
-    Generic callables cannot run on the device; the batched device path is
-    cost.score_batch / optimize below.
-    """
-    def safe(item):
-        i, th = item
-        try:
-            return objective(th)
-        except Exception as e:  # noqa: BLE001 - recorded like the reference
-            if errors is not None:
-                errors.append((i, e))
-            return None
-
-    items = list(enumerate(thetas))
-    if jobs is not None and jobs <= 1:
-        return [safe(it) for it in items]
-    with ThreadPoolExecutor(max_workers=jobs) as pool:
-        return list(pool.map(safe, items))
 
 
 @dataclass
@@ -226,7 +192,7 @@ def _error_text(err: int) -> str:
 
 
 def optimize_device(program, space: dict, arch, params: EsParams, jobs=None, launch=None, device: int = 0,
-                    materialize: bool = True) -> OptimizeResult:
+                    materialize: bool = True, group=None) -> OptimizeResult:
     """ES search with every generation on the device (throughput mode, include/loopscout_b200.h ls_es_*).
 
     Same API, EsParams, centroid start, decode, memo of distinct schedules,
@@ -235,6 +201,8 @@ def optimize_device(program, space: dict, arch, params: EsParams, jobs=None, lau
     numpy's PCG64, so the trajectory is not the reference's (optimize above is
     the exact-trajectory mode).  `jobs` is accepted for API parity and unused.
     materialize=False skips building the evaluated dict (JSON keys) for large runs.
+    Under torch.distributed (world > 1 in `group`) the population is sharded over the ranks
+    (one GPU each, dist.py); every rank returns the same result, bit-identical to one rank.
     """
     axes = tuple(space_axes(program, space))
     if not axes:
@@ -248,17 +216,32 @@ def optimize_device(program, space: dict, arch, params: EsParams, jobs=None, lau
                 raise SearchError("device ES: unroll axes over a space above 2^22 points are not supported")
             idx = st.indices_from_points(np.arange(st.size, dtype=np.uint64))
             task.prepare_unroll_for(to_device_records(st.records_from_indices(idx), device))
-        run = EsRun(task, params.alpha, params.sigma, params.population, params.iterations, params.seed,
-                    params.rank_normalize)
+        world, rank = 1, 0
         try:
-            run.run()
+            import torch.distributed as dist
+            if dist.is_available() and dist.is_initialized():
+                world, rank = dist.get_world_size(group), dist.get_rank(group)
+        except ImportError:
+            pass
+        single = all(len(ax.choices) == 1 for ax in axes)
+        run = EsRun(task, params.alpha, params.sigma, params.population, params.iterations, params.seed,
+                    params.rank_normalize, rank=rank, world=world)
+        try:
+            if world == 1:
+                run.run()
+            else:
+                from .dist import es_exchange
+                run.run_sharded(es_exchange(group), generations=0 if single else None)
             hist, trace, evaluations, err, best = run.result(st.dim)
-            if err:
-                raise SearchError(_error_text(err))
             pts, scores = run.evaluated()
         finally:
             run.close()
-        single = all(len(ax.choices) == 1 for ax in axes)
+        if world > 1:
+            from .dist import es_merge_results
+            trace, pts, scores, err, best = es_merge_results(trace, pts, scores, err, best, group)
+            evaluations = len(pts)
+        if err:
+            raise SearchError(_error_text(err))
         key_of = lambda p: json.dumps(st.schedule_of(st.indices_from_points(np.array([p]))[0]).to_json())  # noqa: E731
         # incumbent: min over distinct schedules by (score, JSON key) (ls/es.py:189, 197)
         ties = [int(p) for p, s in zip(pts, scores) if s == best]

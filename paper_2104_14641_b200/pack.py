@@ -301,16 +301,77 @@ class PackedGroup:
     host_status: np.ndarray    # int32, nonzero = not sent to the device
 
 
+_TEMPLATES: dict = {}  # (id(program), shape key) -> (program, Template | PackError)
+
+
+def _template_cached(program, key: tuple):
+    """template_for_shape, memoised per (program object, shape); PackError is cached too."""
+    ck = (id(program), key)
+    hit = _TEMPLATES.get(ck)
+    if hit is not None and hit[0] is program:
+        if isinstance(hit[1], PackError):
+            raise hit[1]
+        return hit[1]
+    if len(_TEMPLATES) > 4096:
+        _TEMPLATES.clear()
+    try:
+        t = template_for_shape(program, key)
+    except PackError as e:
+        _TEMPLATES[ck] = (program, e)
+        raise
+    _TEMPLATES[ck] = (program, t)
+    return t
+
+
+def _fast_packer():
+    try:
+        from . import _packer  # csrc/packer.cpp (built by build.py)
+        return _packer
+    except ImportError:
+        return None
+
+
 def pack_schedules(program, schedules) -> list:
-    """Group schedules by shape and pack each group into records."""
+    """Group schedules by shape and pack each group into records (groups in first-appearance
+    order, indices ascending).  The native packer (csrc/packer.cpp) reads the Schedule objects
+    in one pass; schedules it cannot read go through the Python path, which raises the
+    reference's exception."""
     max_extent = max([lp.extent for lp in _loops(program)] + [1])
+    fp = _fast_packer()
+    n = len(schedules)
+    if fp is not None and n:
+        sid = np.empty(n, np.int32)
+        prm = np.empty((n, abi.MAX_PARAMS), np.uint16)
+        perm = np.empty(n, np.uint64)
+        hst = np.empty(n, np.int32)
+        keys = fp.pack(schedules, int(max_extent), sid, prm, perm, hst)
+        if keys is not None:
+            order = np.argsort(sid, kind="stable")
+            bounds = np.searchsorted(sid[order], np.arange(len(keys) + 1))
+            out = []
+            for g, key in enumerate(keys):
+                idx = order[bounds[g]:bounds[g + 1]]
+                recs = np.zeros(len(idx), abi.RECORD_DTYPE)
+                try:
+                    tmpl = _template_cached(program, key)
+                except PackError:
+                    out.append(PackedGroup(None, idx, recs, np.full(len(idx), abi.ST_UNSUPPORTED, np.int32)))
+                    continue
+                recs["param"] = prm[idx]
+                recs["perm"] = perm[idx]
+                out.append(PackedGroup(tmpl, idx, recs, hst[idx]))
+            return out
+    return _pack_schedules_py(program, schedules, max_extent)
+
+
+def _pack_schedules_py(program, schedules, max_extent) -> list:
     by_key: dict = {}
     for i, s in enumerate(schedules):
         by_key.setdefault(shape_key(s), []).append(i)
     out = []
     for key, idxs in by_key.items():
         try:
-            tmpl = template_for_shape(program, key)
+            tmpl = _template_cached(program, key)
         except PackError:
             recs = np.zeros(len(idxs), abi.RECORD_DTYPE)
             out.append(PackedGroup(None, np.array(idxs), recs,

@@ -71,7 +71,17 @@ def test_shard_ranges_cover_exactly():
             assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
 
 
+def _order_bits(x: np.ndarray) -> np.ndarray:
+    """ls_topk_key.order of float64 scores (include/loopscout_b200.h)."""
+    b = x.view(np.uint64)
+    return np.where(b >> np.uint64(63), ~b, b | np.uint64(1 << 63))
+
+
 def _worker(rank, world, port, q):
+    """One rank of the CPU multi-rank check: the exchange layer of dist.py (in-place all-gather of
+    rank slices over gloo) with the packed ls_topk_key layout, and the sharded-ES result merge.  The
+    per-rank top-k comes from the oracle here (no GPU on this box); tests/test_dist_gpu.py runs the
+    same exchange with the device kernels and the library merge."""
     import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -80,32 +90,40 @@ def _worker(rank, world, port, q):
     import pyoracle
     from paper_2104_14641_b200 import workloads as W
     from paper_2104_14641_b200.arch import KernelLaunch, load_arch
-    from paper_2104_14641_b200.dist import gather_topk, shard_range
+    from paper_2104_14641_b200.dist import all_gather_inplace, es_merge_results, shard_range
     from paper_2104_14641_b200.pack import SpaceTemplate
     st = SpaceTemplate(W.program(W.matmul_json(64)), W.gemm_space(64))
     desc = st.template.desc(load_arch("x86-avx2"), KernelLaunch.from_json(W.KERNEL_LAUNCH))
     n, k = 3000, 50
     recs = st.records_from_indices(W.distinct_indices(st.sizes, n, 9))
     lo, hi = shard_range(n, rank, world)
-    # per-rank local top-k (oracle stands in for the device kernel on this CPU-only box)
     s, _, _ = pyoracle.evaluate(desc, recs[lo:hi])
     order = sorted(range(hi - lo), key=lambda i: (s[i], i))[:k]
-    ls = torch.tensor([s[i] for i in order], dtype=torch.float64)
-    li = torch.tensor([lo + i for i in order], dtype=torch.int64)
-
-    def cpu_merge(gs, gi, nl, kin, kout):
-        pairs = sorted(zip(gs.tolist(), gi.tolist()))[:kout]
-        return (torch.tensor([p[0] for p in pairs], dtype=torch.float64),
-                torch.tensor([p[1] for p in pairs], dtype=torch.int64))
-
-    gs, gi = gather_topk(ls, li, k, merge=cpu_merge)
-    full, _, _ = pyoracle.evaluate(desc, recs)
-    want = sorted(range(n), key=lambda i: (full[i], i))[:k]
-    q.put((rank, gi.tolist() == want))
+    full = torch.full((world * k, 2), -1, dtype=torch.int64)
+    mine = np.stack([_order_bits(np.array([s[i] for i in order])).view(np.int64),
+                     np.array([lo + i for i in order], np.int64)], 1)
+    full[rank * k:rank * k + len(order)] = torch.from_numpy(mine)
+    all_gather_inplace(full, k)
+    keys = full.numpy()
+    keys = keys[keys[:, 1] >= 0]
+    merged = keys[np.lexsort((keys[:, 1], keys[:, 0].view(np.uint64)))][:k, 1]
+    ref, _, _ = pyoracle.evaluate(desc, recs)
+    want = sorted(range(n), key=lambda i: (ref[i], i))[:k]
+    ok_topk = merged.tolist() == want
+    # sharded ES results: per-generation trace minimum, union of distinct lists, earliest failure
+    tr = np.array([5.0 + rank, 3.0 - rank, 1.0])
+    pts = np.array([rank, 100, 7 + rank], np.uint64)
+    sc = np.array([float(rank), 1.0, 2.0 + rank])
+    err = 0 if rank == 0 else (2 << 40) | (rank << 8) | 3
+    t2, p2, s2, e2, b2 = es_merge_results(tr, pts, sc, err, float(rank))
+    ok_es = (t2.tolist() == [5.0, 3.0 - (world - 1), 1.0] and sorted(p2.tolist()) ==
+             sorted(set(range(world)) | {100} | {7 + r for r in range(world)}) and
+             e2 == (0 if world == 1 else (2 << 40) | (1 << 8) | 3) and b2 == 0.0)
+    q.put((rank, ok_topk and ok_es))
     dist.destroy_process_group()
 
 
-def test_gloo_two_rank_topk_merge():
+def _spawn(world, target):
     import multiprocessing as mp
     import socket
     with socket.socket() as so:
@@ -113,13 +131,18 @@ def test_gloo_two_rank_topk_merge():
         port = so.getsockname()[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    ps = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    ps = [ctx.Process(target=target, args=(r, world, port, q)) for r in range(world)]
     for p in ps:
         p.start()
     res = dict(q.get(timeout=240) for _ in ps)
     for p in ps:
         p.join(60)
-    assert res == {0: True, 1: True}
+    return res
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_gloo_multi_rank_exchange(world):
+    assert _spawn(world, _worker) == {r: True for r in range(world)}
 
 
 REF = Path("/root/reference/pkg/src")
@@ -220,3 +243,34 @@ def test_failure_messages_match_reference_errors():
                     assert (None if m is None else f"{m[0]}: {m[1]}") == e
                     m2 += e is not None
     assert m2 == 1065 + 615
+
+
+def test_native_packer_equals_python_path():
+    """csrc/packer.cpp (one pass over the Schedule objects) == the Python packer: same groups (first
+    appearance order), indices, records and host statuses, on mixed shapes incl. unencodable factors."""
+    import itertools
+    import random
+    from paper_2104_14641_b200 import ir, workloads as W
+    from paper_2104_14641_b200.build import build_packer
+    from paper_2104_14641_b200.pack import _loops, _pack_schedules_py, pack_schedules
+    build_packer()
+    from paper_2104_14641_b200 import _packer  # noqa: F401  (the fast path must be the one tested)
+    prog = W.program(W.matmul_json(1024))
+    rng = random.Random(5)
+    perms = list(itertools.permutations(W.tiled_chain(["i", "j", "k"], ["i", "j", "k"])))
+    sch = []
+    for q in range(3000):
+        t = [ir.Tile(v, rng.choice(W.divisors(1024) + [0, -3, 70000, 2000])) for v in rng.sample("ijk", rng.randint(0, 3))]
+        if rng.random() < 0.7:
+            t.append(ir.Reorder(rng.choice(perms)[: rng.randint(0, 6)]))
+        if rng.random() < 0.2:
+            t.append(ir.Vectorize(rng.choice("ijk"), rng.choice([1, 4, 8, 3])))
+        if rng.random() < 0.2:
+            t.append(rng.choice([ir.Unroll, ir.Parallel])(rng.choice("ijkq")))
+        sch.append(ir.Schedule(tuple(t)))
+    me = max([lp.extent for lp in _loops(prog)] + [1])
+    a, b = pack_schedules(prog, sch), _pack_schedules_py(prog, sch, me)
+    assert len(a) == len(b) > 10
+    for x, y in zip(a, b):
+        assert (x.template is None) == (y.template is None) and np.array_equal(x.index, y.index)
+        assert x.records.tobytes() == y.records.tobytes() and np.array_equal(x.host_status, y.host_status)
