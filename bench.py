@@ -80,8 +80,9 @@ def config_dict(args, n):
             "config": "BASELINE.json configs[1]", "arch": args.arch, "candidates_per_gpu": n, "k": args.k,
             "candidate_encoding": "space point (uint32 mixed-radix choice indices, 4 B)",
             "l2": "flushed between timed steps (256 MiB write)",
-            "step": "one Task.score_topk_points call (Python API -> C-ABI, launch latency inside the timed region) "
-                    "writing the k best + count into preallocated output tensors (out=)"}
+            "step": "one Task.score_topk_points call (Python API -> C-ABI) writing the k best + count into "
+                    "preallocated output tensors (out=); steps enqueued back to back, each bracketed by its own "
+                    "CUDA events after an L2 flush (device time; see sync_step_ms for host-synchronous calls)"}
 
 
 # -- CPU baseline (the oracle port of the reference algorithm) ---------------------------------
@@ -185,20 +186,26 @@ class ClockSampler:
 # -- B200 arm ------------------------------------------------------------------------------------
 
 
-def _timed(step, steps, flush, stream, torch, kern=None):
-    """Device time of `steps` calls of step() (L2 flushed before each), kernel-only events around kern()."""
+def _timed(step, steps, flush, stream, torch, sync_each: bool = False):
+    """Device time of `steps` calls of step(), each preceded by an L2 flush (outside its events).
+
+    The steps are enqueued back to back (the host runs ahead, as a pipelined caller does), so
+    each step's events bracket its device work only; sync_each=True synchronises the host
+    before every step instead, exposing the per-call host/launch latency too."""
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    torch.cuda.synchronize()
     for j in range(steps):
         flush.zero_()
-        torch.cuda.synchronize()
+        if sync_each:
+            torch.cuda.synchronize()
         ev[j][0].record(stream)
         step(kev[j])
         ev[j][1].record(stream)
     torch.cuda.synchronize()
     try:
         kms = [a.elapsed_time(b) for a, b in kev]
-    except ValueError:  # the step does not bracket a single kernel
+    except (ValueError, RuntimeError):  # the step does not bracket a single kernel
         kms = None
     return [a.elapsed_time(b) for a, b in ev], kms
 
@@ -284,9 +291,11 @@ def b200_arm(args):
             torch.cuda.synchronize()
         step_ms, kern_ms = _timed(step_p, args.steps, flush, stream, torch)
         rstep_ms, rkern_ms = _timed(step_r, args.steps, flush, stream, torch)
+        sync_ms, _ = _timed(step_p, args.steps, flush, stream, torch, sync_each=True)
     if world > 1:
         dist.barrier()
     total_s = max_over_ranks(sum(step_ms)) / 1e3
+    sync_step_ms = max_over_ranks(sum(sync_ms)) / args.steps  # host-synchronous call (launch latency exposed)
     value = world * n * args.steps / total_s
     value_rec = world * n * args.steps / (max_over_ranks(sum(rstep_ms)) / 1e3)
     top_i = step_p.out[1].cpu().numpy()
@@ -377,17 +386,18 @@ def b200_arm(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": "score_topk_kernel<3,4,5,1> (space path: point decode + fused 32-bit walk/closed forms + "
-                                   "block radix-select top-k) + merge_filter_kernel (minima-bound merge); one "
-                                   "ls_score_topk_points call",
+                                   "block radix-select top-k + in-kernel minima-bound merge); one ls_score_topk_points "
+                                   "call, one launch",
                          "kernel_ms": kavg * 1e3, "algorithmic_bytes_per_launch": alg_bytes,
                          "note": "instruction-issue bound by design (4 B read per candidate vs thousands of "
                                  "integer ops): see issue_roofline"},
             "issue_roofline": issue,
             "cpu_baseline": cpu, "parity": parity,
             "clocks": clk.summary(),
-            # per step: the fused kernel + the minima-bound merge (k <= grid / 4), and for N > 1 the
+            # per step: the fused kernel (score + top-k + merge in one launch), and for N > 1 the
             # all-gathered lists' lists_to_keys + merge_keys kernels (the memsets are not ours)
-            "gpu_launches": args.steps * (1 + (1 if 4 * args.k <= 3 * 148 else 0) + (2 if world > 1 else 0)),
+            "gpu_launches": args.steps * (1 + (2 if world > 1 else 0)),
+            "sync_step_ms": sync_step_ms,
             "n_valid_per_gpu": n_valid, "path": task.path, "points_path": task.points_path,
         }
         print(json.dumps(line), flush=True)

@@ -1,0 +1,229 @@
+// Device part of the ES search (see es.cuh for the design notes): the device
+// state, Philox noise, the memoised scoring step and the generation kernels.
+#pragma once
+
+constexpr int ES_CHUNK = 1024;  // sorted positions per partial sum (independent of the grid)
+constexpr int ES_MAXDIM = LS_MAX_AXES;
+
+struct EsDev {
+  double theta[ES_MAXDIM];
+  double alpha, sigma, coef;           // coef = alpha / (population * sigma)
+  uint64_t seed;
+  int32_t pop, iters, dim, rank_normalize;
+  int32_t gen, pad;
+  int32_t lo, hi;                      // this rank's members [lo, hi)
+  int32_t c0, c1;                      // this rank's chunks [c0, c1) of sum_i w_i eps_i
+  int32_t chunks, pad2;                // all chunks
+  uint32_t n_ax[ES_MAXDIM];            // choices per axis
+  unsigned long long best;             // order bits of the best score so far
+  unsigned long long evaluations;      // distinct schedules scored
+  unsigned long long err;              // first failure (atomicMin; ~0 none): (generation+1 | 0 start) << 40 | member << 8 | status
+  unsigned long long* keys;            // memo: flat point + 1 (0 = empty)
+  unsigned long long* vals;            // memo: order bits of the score (0 = being scored)
+  unsigned long long cap_mask;
+  unsigned long long* list_p;          // evaluated points in discovery order
+  double* list_s;                      // their scores
+  unsigned long long list_cap;
+  unsigned long long full;             // memo probes exhausted (table full): reported as a failure
+  unsigned long long* sort_in;         // per member: order bits of F = -score
+  unsigned long long* sort_out;
+  uint32_t* idx_in;
+  uint32_t* idx_out;
+  double* partial;                     // [chunks][dim]
+  double* theta_hist;                  // [iters + 1][dim]
+  double* trace;                       // [iters]
+};
+
+// ---- Philox4x32-10 (Salmon et al., SC'11) ---------------------------------------
+__host__ __device__ inline void philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {
+  for (int r = 0; r < 10; ++r) {
+    if (r) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c[0];
+    const uint64_t p1 = (uint64_t)0xCD9E8D57u * c[2];
+    const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c[1] ^ k0;
+    const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c[3] ^ k1;
+    c[0] = n0;
+    c[1] = (uint32_t)p1;
+    c[2] = n2;
+    c[3] = (uint32_t)p0;
+  }
+}
+
+// Standard normals eps[2q], eps[2q+1] of member i in generation g: one Philox
+// block per pair, Box-Muller on two 53-bit uniforms (u1 in (0, 1], u2 in [0, 1)).
+__device__ __forceinline__ void es_normal_pair(uint64_t seed, int g, uint32_t i, int q, double& z0, double& z1) {
+  uint32_t c[4] = {i, (uint32_t)q, (uint32_t)g, 0u};
+  philox4x32_10(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+  const uint64_t a = ((uint64_t)c[1] << 32 | c[0]) >> 11, b = ((uint64_t)c[3] << 32 | c[2]) >> 11;
+  const double u1 = (double)(a + 1) * 0x1.0p-53, u2 = (double)b * 0x1.0p-53;
+  const double rad = sqrt(-2.0 * log(u1));
+  const double ang = 6.283185307179586 * u2;
+  z0 = rad * cos(ang);
+  z1 = rad * sin(ang);
+}
+
+__device__ __forceinline__ double es_eps(const EsDev& E, int g, uint32_t i, int d) {
+  double z0, z1;
+  es_normal_pair(E.seed, g, i, d >> 1, z0, z1);
+  return (d & 1) ? z1 : z0;
+}
+
+// Score of space point x through the task's points kernel code (status != 0: failure).
+template <int TM, int RM, int MODE>
+__device__ __forceinline__ int score_point(const DTask& T, const int32_t* tab, Evaluator<TM, RM, MODE>& ev,
+                                           uint64_t x, double* s) {
+  double f[LS_NFEAT_GPU];
+  if constexpr (MODE == 4 || MODE == 5) {
+    return eval_space<TM, MODE == 5>(T, tab, x, ev.fc, f, s);
+  } else {
+    ls_record r;
+    uint32_t kt[4];
+    uint32_t pch = 0;
+    int st = point_record<MODE == 3>(T, x, r, kt, pch);
+    if (st == LS_OK) st = ev(T, r, kt, pch, f, s);
+    return st;
+  }
+}
+
+// Memoised score of point x (ls/es.py:139-160): the first thread to claim the
+// key scores it and counts a distinct evaluation; others reuse the value (or
+// rescore it themselves while it is being written: scores are pure).
+template <int TM, int RM, int MODE>
+__device__ int es_memo_score(const DTask& T, const int32_t* tab, Evaluator<TM, RM, MODE>& ev, EsDev& E, uint64_t x,
+                             double* s) {
+  const unsigned long long key = x + 1;
+  unsigned long long h = (key * 0x9E3779B97F4A7C15ull) >> 17;
+  for (unsigned long long probe = 0; probe <= E.cap_mask; ++probe, ++h) {
+    h &= E.cap_mask;
+    const unsigned long long k = atomicCAS(&E.keys[h], 0ull, key);
+    if (k == 0ull) {  // claimed: a new distinct schedule
+      const int st = score_point<TM, RM, MODE>(T, tab, ev, x, s);
+      if (st) return st;
+      const unsigned long long pos = atomicAdd(&E.evaluations, 1ull);
+      if (pos < E.list_cap) {
+        E.list_p[pos] = x;
+        E.list_s[pos] = *s;
+      }
+      atomicMin(&E.best, order_bits(*s));
+      atomicExch(&E.vals[h], order_bits(*s));
+      return LS_OK;
+    }
+    if (k == key) {
+      const unsigned long long v = __ldcg(&E.vals[h]);
+      if (v) {
+        *s = from_order_bits(v);
+        return LS_OK;
+      }
+      return score_point<TM, RM, MODE>(T, tab, ev, x, s);
+    }
+  }
+  atomicExch(&E.full, 1ull);  // cannot happen within the sizing of ls_es_create
+  return LS_ST_OVERFLOW;
+}
+
+// One generation (start = true: the decode of theta alone, ls/es.py:183-186).
+template <int TM, int RM, int MODE>
+__global__ void __launch_bounds__(TPB, 2) es_gen_kernel(const DTask* __restrict__ gtask, EsDev* __restrict__ ges,
+                                                       int start) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  DTask& T = *reinterpret_cast<DTask*>(dyn);
+  stage_task(T, gtask);
+  unsigned char* p = dyn + T.task_bytes;
+  const int32_t* tab = stage_tab<MODE>(p, T);
+  p += tab_smem_bytes(MODE, T);
+  Evaluator<TM, RM, MODE> ev(T, p, tab);
+  EsDev& E = *ges;
+  const int g = E.gen;
+  const int lo = start ? 0 : E.lo, hi = start ? 1 : E.hi;
+  for (int i = lo + blockIdx.x * TPB + threadIdx.x; i < hi; i += gridDim.x * TPB) {
+    uint64_t x = 0;
+    for (int d = 0; d < E.dim; d += 2) {
+      double z0 = 0.0, z1 = 0.0;
+      if (!start) es_normal_pair(E.seed, g, (uint32_t)i, d >> 1, z0, z1);
+      for (int q = d; q < d + 2 && q < E.dim; ++q) {
+        const double pt = __dadd_rn(E.theta[q], __dmul_rn(E.sigma, q == d ? z0 : z1));
+        const double m = (double)(E.n_ax[q] - 1);
+        const double c = fmin(fmax(rint(pt), 0.0), m);  // np.clip(round(x), 0, n - 1)
+        x = x * E.n_ax[q] + (uint64_t)c;
+      }
+    }
+    double s = 0.0;
+    const int st = es_memo_score<TM, RM, MODE>(T, tab, ev, E, x, &s);
+    if (st) {  // generation field 0: the start point
+      atomicMin(&E.err, ((unsigned long long)(start ? 0 : g + 1) << 40) | ((unsigned long long)i << 8) |
+                            (unsigned long long)st);
+      s = 0.0;
+    }
+    if (!start) {
+      E.sort_in[i] = order_bits(-s);  // F = -score, maximised (ls/es.py:176); idx_in is the identity
+    }
+  }
+}
+
+// sum over fixed chunks of sorted positions of w_j * eps[member_j]; w_j = the
+// centred rank j/(n-1) - 0.5 (rank_normalize) or F itself (ls/es.py:65-71, 90).
+#ifdef LS_MAIN_TU
+__global__ void __launch_bounds__(TPB) es_partial_kernel(EsDev* __restrict__ ges) {
+  __shared__ double red[TPB];
+  EsDev& E = *ges;
+  const int n = E.pop, dim = E.dim, g = E.gen;
+  const bool flat = E.rank_normalize && E.sort_out[0] == E.sort_out[n - 1];  // np.ptp(values) == 0
+  const int chunk = E.c0 + blockIdx.x;
+  const int j0 = chunk * ES_CHUNK;
+  double acc[ES_MAXDIM];
+  for (int d = 0; d < dim; ++d) acc[d] = 0.0;
+  for (int j = j0 + threadIdx.x; j < min(n, j0 + ES_CHUNK); j += TPB) {
+    double w;
+    if (E.rank_normalize)
+      w = flat ? 0.0 : __dadd_rn(__ddiv_rn((double)j, (double)(n - 1)), -0.5);
+    else
+      w = from_order_bits(E.sort_out[j]);
+    const uint32_t i = E.idx_out[j];
+    for (int d = 0; d < dim; d += 2) {
+      double z0, z1;
+      es_normal_pair(E.seed, g, i, d >> 1, z0, z1);
+      acc[d] = __dadd_rn(acc[d], __dmul_rn(w, z0));
+      if (d + 1 < dim) acc[d + 1] = __dadd_rn(acc[d + 1], __dmul_rn(w, z1));
+    }
+  }
+  for (int d = 0; d < dim; ++d) {
+    red[threadIdx.x] = acc[d];
+    __syncthreads();
+    for (int w = TPB / 2; w > 0; w >>= 1) {
+      if (threadIdx.x < w) red[threadIdx.x] = __dadd_rn(red[threadIdx.x], red[threadIdx.x + w]);
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) E.partial[(size_t)chunk * dim + d] = red[0];
+    __syncthreads();
+  }
+}
+
+__global__ void es_update_kernel(EsDev* __restrict__ ges) {
+  EsDev& E = *ges;
+  const int chunks = E.chunks;
+  const int d = threadIdx.x;
+  const int g = E.gen;
+  if (d < E.dim) {
+    double sum = 0.0;
+    for (int b = 0; b < chunks; ++b) sum = __dadd_rn(sum, E.partial[(size_t)b * E.dim + d]);
+    E.theta[d] = __dadd_rn(E.theta[d], __dmul_rn(E.coef, sum));
+    E.theta_hist[(size_t)(g + 1) * E.dim + d] = E.theta[d];
+  }
+  __syncthreads();
+  if (d == 0) {
+    E.trace[g] = from_order_bits(E.best);
+    E.gen = g + 1;
+  }
+}
+
+// Diagnostic: the Gaussian noise of generation g, [pop][dim].
+__global__ void es_noise_kernel(const EsDev* __restrict__ ges, int g, double* __restrict__ out) {
+  const EsDev& E = *ges;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= E.pop) return;
+  for (int d = 0; d < E.dim; ++d) out[(size_t)i * E.dim + d] = es_eps(E, g, (uint32_t)i, d);
+}
+#endif  // LS_MAIN_TU

@@ -439,3 +439,18 @@ def test_topk_two_stage_many_survivors(torch):
         assert np.array_equal(ts.cpu().numpy(), sc[order[:k]])
         assert int(nv.item()) == int(ok.sum())
     task.close()
+
+
+@pytest.mark.parametrize("mode", ["bound", "tree"])
+def test_topk_merge_modes_forced(mode):
+    """The bound merge ranked by the scoring grid's last block (forced even where blocks end
+    before the bound is out: the last block filters the lists left) and the in-kernel merge tree
+    (forced for small k), at several (n, k): each equals a stable sort."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    env = dict(os.environ, LS_MERGE=mode)
+    r = subprocess.run([sys.executable, str(Path(__file__).with_name("merge_modes_check.py"))], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr

@@ -15,7 +15,7 @@ from paper_2104_14641_b200.engine import Task  # noqa: E402
 st, desc = bench.workload("x86-avx2")
 task = Task(desc, 0)
 task.set_space(st.space_desc())
-for n in (1 << 20, 1 << 22):
+for n in [int(x) for x in os.environ.get("TRACE_N", str((1 << 20)) + "," + str(1 << 22)).split(",")]:
     pts = st.points_from_indices(W.distinct_indices(st.sizes, n, 2104))
     d = torch.from_numpy(pts.view(np.int32)).cuda()
     for _ in range(3):
