@@ -181,6 +181,15 @@ struct __align__(16) DTask {
   uint8_t sp_tslot[LS_MAX_AXES], sp_tnew[LS_MAX_AXES];
   int32_t sp_n_untiled, pad8;            // static tiles: base loops no tile splits
   uint8_t sp_untiled[MAXCH], sp_untiled_pos[MAXCH];
+  // packed walk (MODE 5): a tensor's two group offsets in one word (group 2t in
+  // the low half, 2t + 1 in the high half; every table offset < 2^16), advanced per loop level
+  // by one add of the level's packed stage bytes
+  int32_t sp_pack, pad9;
+  uint32_t sd_offp[4];                   // packed first-row offsets per tensor
+  uint32_t sd_Sp[LS_MAX_AXES][4];        // packed byte stride of one choice of each tile axis
+  uint32_t sp_vbp[NSLOT][4];             // per loop slot: packed stage bytes of tensors 0..2, tensor-use bits
+  uint32_t sp_vbp3[NSLOT];               // per loop slot: packed stage bytes of tensor 3
+  const uint64_t* sp_rchain;             // per reorder choice: the chain innermost loop first
   // ---- general trees: unified node ids, accesses 0..tr_na-1 (preorder), loops
   //      tr_na + j for base loop j (preorder; header j = base_slot/ext/step/flags[j]), tile loops after
   int32_t tree, tr_nl, tr_na, tr_root_first;
@@ -193,6 +202,14 @@ struct __align__(16) DTask {
   int32_t n_terms;
   DTerm term[MAXTERM];
 };
+
+// Entries per group-table row: the 2^nb stage masks plus LS_SD_PAD padding
+// entries, so rows start on different banks and lanes reading the same stage mask of different
+// rows (the common case within a warp) do not conflict.
+#ifndef LS_SD_PAD
+#define LS_SD_PAD 1
+#endif
+__host__ __device__ inline int sd_row_len(int nb) { return (1 << nb) + LS_SD_PAD; }
 
 struct ls_task {
   ls_task_desc desc;
@@ -1184,6 +1201,9 @@ __device__ __forceinline__ uint64_t load_point(const void* __restrict__ src, int
                      : (uint64_t)__ldg(reinterpret_cast<const unsigned long long*>(src) + i);
 }
 
+__device__ __forceinline__ int space_score(const DTask& T, int n, int64_t P, int64_t H, int64_t dmov, double* f,
+                                           double* score);
+
 template <int TM, bool NARROW>
 __device__ int eval_space(const DTask& T, const int32_t* __restrict__ sdt, uint64_t x, FastCand& c, double* f,
                           double* score) {
@@ -1314,6 +1334,14 @@ __device__ int eval_space(const DTask& T, const int32_t* __restrict__ sdt, uint6
   int64_t dmov = 0;
 #pragma unroll
   for (int t = 0; t < TM; ++t) dmov += (int64_t)dm[t];
+  return space_score(T, n, (int64_t)P, (int64_t)H, dmov, f, score);
+}
+
+// Features and score of a space-path candidate from the walk's products (ls/cost.py:132-161;
+// closed forms of DESIGN.md §3.6).
+__device__ __forceinline__ int space_score(const DTask& T, int n, int64_t P, int64_t H, int64_t dmov, double* f,
+                                           double* score) {
+  const bool cpu = T.family == LS_FAMILY_CPU;
   const int64_t L = T.L, S = T.S;
   double total = 0.0;
   if (cpu) {
@@ -1348,6 +1376,133 @@ __device__ int eval_space(const DTask& T, const int32_t* __restrict__ sdt, uint6
   return LS_OK;
 }
 
+// MODE 5 with packed group offsets (T.sp_pack): the same decode, walk and closed forms as
+// eval_space<TM, true> with the per-level work cut down --
+//   * a tensor's two group-table offsets live in one register (16 bits each) and advance by one
+//     add of the level's packed stage bytes (a variable's stage bits are disjoint from every
+//     other's, so the OR of eval_space is an add); each half is a shared-memory address;
+//   * the chain is stored innermost-first and the walk is unrolled over chain positions (the
+//     chain length is uniform across the launch), so nibble extraction uses constant shifts,
+//     the PTX counter-register wrap is a constant condition and the reuse flags stay predicates;
+//   * the tensors using the level's variable come with the packed stage bytes (one 16-byte
+//     shared load per level);
+//   * the extents of untiled base loops are written once per thread (Evaluator).
+// Bit-identical to eval_space<TM, true> (tests: every BASELINE space on the points paths).
+template <int TM>
+__device__ __forceinline__ int eval_space_packed(const DTask& T, const int32_t* __restrict__ sdt, uint64_t x,
+                                                 FastCand& c, double* f, double* score) {
+  uint32_t kp[TM];
+#pragma unroll
+  for (int t = 0; t < TM; ++t) kp[t] = T.sd_offp[t];
+  uint32_t pch = 0;
+  for (int a = T.sp_n - 1; a >= 0; --a) {
+    const DAxis& ax = T.sp_ax[a];
+    uint32_t ch;
+    if (a == 0) {
+      if (x >= ax.n) return LS_ST_POINT_RANGE;
+      ch = (uint32_t)x;
+    } else if (ax.n == 1) {
+      ch = 0;
+    } else if (x >> 32) {
+      const uint64_t q = x / ax.n;
+      ch = (uint32_t)(x - q * ax.n);
+      x = q;
+    } else {  // umulhi(x, magic) for x < 2^32: x * magic_hi + umulhi(x, magic_lo), top word
+      const uint32_t x32 = (uint32_t)x;
+      const uint32_t q = (uint32_t)(((uint64_t)x32 * (uint32_t)(ax.magic >> 32) + __umulhi(x32, (uint32_t)ax.magic)) >> 32);
+      ch = x32 - q * (uint32_t)ax.n;
+      x = q;
+    }
+    if (ax.kind == LS_AX_PERM) {
+      pch = ch;
+      continue;
+    }
+#pragma unroll
+    for (int t = 0; t < TM; ++t) kp[t] += ch * T.sd_Sp[a][t];
+    // Tile (ls/ir.py:361-382) of a base loop: F and ceil(E/F) per choice
+    const uint64_t e = __ldg(reinterpret_cast<const unsigned long long*>(T.sp_ext) + ax.voff + ch);
+    if (e >> 63) return LS_ST_TILE_RANGE;
+    c.E(T.sp_tnew[a]) = (int32_t)(e & 0xFFFFu);
+    c.E(T.sp_tslot[a]) = (int32_t)((e >> 16) & 0x7FFFFFFFu);
+  }
+  const int pst = __ldg(T.sp_pstat + pch);
+  if (pst) return pst;
+  const uint64_t rchain = __ldg(reinterpret_cast<const unsigned long long*>(T.sp_rchain) + pch);
+  const int n = T.sp_nchain;
+  const char* tb = reinterpret_cast<const char*>(sdt);
+  auto fp = [&](uint32_t o) -> uint32_t {
+    return *reinterpret_cast<const uint32_t*>(tb + (o & 0xFFFFu)) * *reinterpret_cast<const uint32_t*>(tb + (o >> 16));
+  };
+  uint32_t Fb[TM], dm[TM];
+  bool ru[TM];
+#pragma unroll
+  for (int t = 0; t < TM; ++t) {
+    Fb[t] = fp(kp[t]);
+    dm[t] = (uint32_t)T.t_nacc[t];
+    ru[t] = true;
+  }
+  const uint32_t cap = (uint32_t)T.cap;
+  const bool cpu = T.family == LS_FAMILY_CPU;
+  const uint32_t* const vbp = &T.sp_vbp[0][0];
+  uint32_t P = 1, H = 0;  // product of the extents; Horner sum of the outer prefix products (< 2^32 proven)
+#ifdef LS_WALK_PIPE
+  int vn = (int)(rchain & 15u);
+  uint32_t En = (uint32_t)c.E(vn);
+  uint4 rown = *reinterpret_cast<const uint4*>(vbp + 4 * vn);
+#endif
+#pragma unroll
+  for (int q = 0; q < LS_MAX_CHAIN; ++q) {  // chain position p = n - 1 - q, innermost first
+    if (q >= n) break;                        // uniform
+#ifdef LS_WALK_PIPE
+    const int v = vn;
+    const uint32_t E = En;
+    const uint4 row = rown;
+    if (q + 1 < n) {  // the next level's extent and stage bytes, one level ahead
+      vn = (int)((rchain >> (4 * (q + 1))) & 15u);
+      En = (uint32_t)c.E(vn);
+      rown = *reinterpret_cast<const uint4*>(vbp + 4 * vn);
+    }
+#else
+    const int v = (int)((rchain >> (4 * q)) & 15u);
+    const uint32_t E = (uint32_t)c.E(v);
+    const uint4 row = *reinterpret_cast<const uint4*>(vbp + 4 * v);
+#endif
+    const uint32_t use = row.w;
+    uint32_t single = 0;
+#pragma unroll
+    for (int t = 0; t < TM; ++t) single += Fb[t];
+    const bool over = single > cap;
+#pragma unroll
+    for (int t = 0; t < TM; ++t) {
+      const uint32_t add = t == 0 ? row.x : t == 1 ? row.y : t == 2 ? row.z : T.sp_vbp3[v];
+      kp[t] += add;
+      const uint32_t Ff = fp(kp[t]);
+      const bool r0 = ru[t] && (!over || ((use >> t) & 1u));
+      dm[t] = (!over || r0) ? Ff : dm[t] * E;
+      ru[t] = r0 && Ff <= cap;
+      Fb[t] = Ff;
+    }
+    const uint32_t Ee = (cpu || q < 8) ? E : 1u;  // PTX: no trip for loops 8+ levels above the innermost
+    if (q > 0) H = Ee * (1 + H);
+    P *= Ee;
+  }
+  int64_t dmov = 0;
+#pragma unroll
+  for (int t = 0; t < TM; ++t) dmov += (int64_t)dm[t];
+  return space_score(T, n, (int64_t)P, (int64_t)H, dmov, f, score);
+}
+
+// The space kernels' evaluator: MODE 5 takes the packed walk (LS_WALK_OLD: the reference
+// formulation, for A/B runs).
+template <int TM, int MODE>
+__device__ __forceinline__ int eval_space_mode(const DTask& T, const int32_t* __restrict__ sdt, uint64_t x,
+                                               FastCand& c, double* f, double* s) {
+#ifndef LS_WALK_OLD
+  if constexpr (MODE == 5) return eval_space_packed<TM>(T, sdt, x, c, f, s);
+#endif
+  return eval_space<TM, MODE == 5>(T, sdt, x, c, f, s);
+}
+
 // One group-table entry per thread: decode (group slot, tile-axis choices, stage
 // mask); the entry is the product of the group's dimension counts (same fold as
 // build_tab_kernel).  Products that do not fit 32 bits raise *overflow.
@@ -1364,15 +1519,20 @@ __global__ void build_sdt_kernel(const DTask* __restrict__ g, const int32_t* __r
   }
   int G = -1;
   for (int q = 0; q < 8; ++q)
-    if (rows[q] && e >= (int)T.sd_off[q] / 4 && e < (int)T.sd_off[q] / 4 + (rows[q] << T.sd_nb[q])) G = q;
+    if (rows[q] && e >= (int)T.sd_off[q] / 4 && e < (int)T.sd_off[q] / 4 + rows[q] * sd_row_len(T.sd_nb[q])) G = q;
   if (G < 0) return;
   const int loc = e - (int)T.sd_off[G] / 4;
-  const uint32_t mask = (uint32_t)loc & ((1u << T.sd_nb[G]) - 1u);
-  const uint32_t key = (uint32_t)loc >> T.sd_nb[G];
+  const int rl = sd_row_len(T.sd_nb[G]);
+  const uint32_t mask = (uint32_t)(loc % rl);
+  const uint32_t key = (uint32_t)(loc / rl);
+  if (mask >> T.sd_nb[G]) {  // the row's padding entry (never read)
+    tab[e] = 0;
+    return;
+  }
   int32_t prm[LS_MAX_PARAMS];
   for (int q = 0; q < LS_MAX_PARAMS; ++q) prm[q] = 1;
   for (int a = 0; a < T.sp_n; ++a) {
-    const uint32_t stride = T.sd_S[a][G] >> (2 + T.sd_nb[G]);
+    const uint32_t stride = T.sd_S[a][G] / (4u * (uint32_t)rl);
     if (!stride) continue;
     const DAxis& ax = T.sp_ax[a];
     const uint32_t ch = (key / stride) % ax.n;
@@ -2198,7 +2358,7 @@ static __device__ int eval_tree(const DTask& T, const ls_record& r, double* f, d
 // every tile factor 1 (always in range), i.e. what the reorder alone decides.
 #ifdef LS_MAIN_TU
 __global__ void build_pchain_kernel(const DTask* __restrict__ g, int32_t pax, uint64_t* __restrict__ chain,
-                                    int32_t* __restrict__ pst) {
+                                    int32_t* __restrict__ pst, uint64_t* __restrict__ rchain) {
   extern __shared__ __align__(16) unsigned char dyn[];
   const DTask& T = *g;
   const int pc = blockIdx.x * blockDim.x + threadIdx.x;
@@ -2213,6 +2373,9 @@ __global__ void build_pchain_kernel(const DTask* __restrict__ g, int32_t pax, ui
   const int st = apply_fast(T, r, c);
   pst[pc] = st;
   chain[pc] = st ? 0 : c.chain;
+  uint64_t rc = 0;  // innermost loop first
+  for (int q = 0; q < c.n && !st; ++q) rc |= ((c.chain >> (4 * (c.n - 1 - q))) & 15ull) << (4 * q);
+  rchain[pc] = rc;
 }
 #endif  // LS_MAIN_TU
 
@@ -2362,6 +2525,8 @@ struct Evaluator {
       c = carve(state, T);
     else
       fc.ext = reinterpret_cast<int32_t*>(state) + threadIdx.x;
+    if constexpr (MODE == 5)  // base loops no tile splits: their extents never change
+      for (int q = 0; q < T.sp_n_untiled; ++q) fc.E(T.sp_untiled[q]) = T.base_ext[T.sp_untiled_pos[q]];
   }
   __device__ __forceinline__ int operator()(const DTask& T, const ls_record& r, const uint32_t* kt, uint32_t pch,
                                             double* f, double* s) {
@@ -2398,7 +2563,12 @@ __device__ __forceinline__ int load_cand(const DTask& T, const void* __restrict_
   }
 }
 
-constexpr int min_blocks(int tm, int rm, int mode) { return mode == 6 ? 1 : mode ? 3 : (tm * rm <= 16 ? 3 : 1); }
+#ifndef LS_MB5
+#define LS_MB5 3  // resident blocks per SM the MODE 5 kernels are compiled for (register budget)
+#endif
+constexpr int min_blocks(int tm, int rm, int mode) {
+  return mode == 6 ? 1 : mode == 5 ? LS_MB5 : mode ? 3 : (tm * rm <= 16 ? 3 : 1);
+}
 
 template <int TM, int RM, int MODE, int SRC>
 __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE))
@@ -2419,7 +2589,7 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE))
     double s = 0.0;
     int st;
     if constexpr (MODE == 4 || MODE == 5) {
-      st = eval_space<TM, MODE == 5>(T, tab, load_point(src, pbytes, i), ev.fc, f, &s);
+      st = eval_space_mode<TM, MODE>(T, tab, load_point(src, pbytes, i), ev.fc, f, &s);
     } else {
       uint32_t pch = 0;
       st = load_cand<SRC, MODE == 3>(T, src, pbytes, i, r, kt, pch);
@@ -3310,7 +3480,7 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kern
       if constexpr (MODE == 4 || MODE == 5) {
         const uint64_t x = xn;
         if (nb + threadIdx.x < n) xn = load_point(src, pbytes, nb + threadIdx.x);
-        st = eval_space<TM, MODE == 5>(T, tab, x, ev.fc, f, &s);
+        st = eval_space_mode<TM, MODE>(T, tab, x, ev.fc, f, &s);
       } else {
         uint32_t pch = 0;
         st = load_cand<SRC, MODE == 3>(T, src, pbytes, i, r_, kt, pch);

@@ -271,7 +271,7 @@ bool plan_space_groups(DTask& T, int32_t* rows) {
         int64_t keys = 1;
         for (int a = 0; a < T.sp_n && ok; ++a)
           if (T.sp_ax[a].kind == LS_AX_PARAM && ((pm >> T.sp_ax[a].param) & 1u)) keys *= T.sp_ax[a].n;
-        total += keys << nb;
+        total += keys * sd_row_len(nb);
         if (total > SD_MAX_ENTRIES) ok = false;
       }
       if (ok && (best < 0 || total < best)) best = total, best_sel = sel;
@@ -297,16 +297,38 @@ bool plan_space_groups(DTask& T, int32_t* rows) {
       for (int a = T.sp_n - 1; a >= 0; --a) {
         const DAxis& ax = T.sp_ax[a];
         if (ax.kind != LS_AX_PARAM || !((pm >> ax.param) & 1u)) continue;
-        T.sd_S[a][G] = (uint32_t)((keys << nb) * 4);
+        T.sd_S[a][G] = (uint32_t)(keys * sd_row_len(nb) * 4);
         keys *= ax.n;
       }
-      if (off + (keys << nb) > SD_MAX_ENTRIES) return false;
+      if (off + keys * sd_row_len(nb) > SD_MAX_ENTRIES) return false;
       T.sd_off[G] = (uint32_t)(off * 4);
       rows[G] = (int32_t)keys;
-      off += keys << nb;
+      off += keys * sd_row_len(nb);
     }
   }
   T.sd_len = (int32_t)off;
+  // packed walk (MODE 5): both group offsets of a tensor in one word when every offset fits 16 bits
+  memset(T.sd_offp, 0, sizeof(T.sd_offp));
+  memset(T.sd_Sp, 0, sizeof(T.sd_Sp));
+  memset(T.sp_vbp, 0, sizeof(T.sp_vbp));
+  memset(T.sp_vbp3, 0, sizeof(T.sp_vbp3));
+  T.sp_pack = off * 4 <= 0xFFFF;
+  for (int t = 0; t < 4; ++t) {
+    T.sd_offp[t] = T.sd_off[2 * t] | (T.sd_off[2 * t + 1] << 16);
+    for (int a = 0; a < T.sp_n; ++a) T.sd_Sp[a][t] = T.sd_S[a][2 * t] | (T.sd_S[a][2 * t + 1] << 16);
+  }
+  for (int v = 0; v < NSLOT; ++v) {
+    uint32_t pk[4];
+    for (int t = 0; t < 4; ++t)
+      pk[t] = (uint32_t)((T.vb8[v] >> (16 * t)) & 0xFFu) | ((uint32_t)((T.vb8[v] >> (16 * t + 8)) & 0xFFu) << 16);
+    T.sp_vbp[v][0] = pk[0];
+    T.sp_vbp[v][1] = pk[1];
+    T.sp_vbp[v][2] = pk[2];
+    T.sp_vbp3[v] = pk[3];
+    uint32_t use = 0;
+    for (int t = 0; t < T.n_tensors; ++t) use |= ((T.t_vmask[t] >> v) & 1u) << t;
+    T.sp_vbp[v][3] = use;
+  }
   return true;
 }
 
@@ -1297,8 +1319,11 @@ int ls_task_set_space(ls_task* t, const ls_space_desc* sp) {
       uint64_t* dch = nullptr;
       int32_t *dst = nullptr, *drows = nullptr, *dovf = nullptr;
       uint32_t* dsd = nullptr;
+      uint64_t* drch = nullptr;
       CUDA_TRY(cudaMalloc(&dch, sizeof(uint64_t) * np));
       t->retired.push_back(dch);
+      CUDA_TRY(cudaMalloc(&drch, sizeof(uint64_t) * np));
+      t->retired.push_back(drch);
       CUDA_TRY(cudaMalloc(&dst, sizeof(int32_t) * np));
       t->retired.push_back(dst);
       CUDA_TRY(cudaMalloc(&dsd, sizeof(int32_t) * ((t->host.sd_len + 3) & ~3)));  // 16-byte staging loads
@@ -1310,7 +1335,7 @@ int ls_task_set_space(ls_task* t, const ls_space_desc* sp) {
       CUDA_TRY(cudaMemset(dovf, 0, sizeof(int32_t) * 9));  // overflow flag + per-group maxima
       if (int rc = upload(t)) return rc;
       const size_t sm = sizeof(int32_t) * NSLOT * TPB;
-      build_pchain_kernel<<<(np + TPB - 1) / TPB, TPB, sm>>>(t->d_task, pax, dch, dst);
+      build_pchain_kernel<<<(np + TPB - 1) / TPB, TPB, sm>>>(t->d_task, pax, dch, dst, drch);
       CUDA_TRY(cudaGetLastError());
       build_sdt_kernel<<<(t->host.sd_len + 255) / 256, 256>>>(t->d_task, drows, dsd, dovf,
                                                               reinterpret_cast<unsigned int*>(dovf + 1));
@@ -1354,9 +1379,12 @@ int ls_task_set_space(ls_task* t, const ls_space_desc* sp) {
           if (std::max((double)t->host.t_nacc[q], K) * std::pow(prod, (double)m) >= 4294967295.0) fits = false;
         }
         // the Horner sum of the prefix products is <= (chain length) * P
-        t->host.sp_narrow = fits && fsum < 4294967295.0 && prod * (t->host.sp_nchain + 1) < 4294967295.0;
+        // (MODE 5 also packs both group offsets of a tensor into one word: every offset < 2^16)
+        t->host.sp_narrow = fits && fsum < 4294967295.0 && prod * (t->host.sp_nchain + 1) < 4294967295.0 &&
+                            t->host.sp_pack;
       }
       t->host.sp_chain = dch;
+      t->host.sp_rchain = drch;
       t->host.sp_pstat = dst;
       t->host.sd_tab = reinterpret_cast<const int32_t*>(dsd);
       t->host.sp_ok = ovf ? 0 : 1;  // a group product beyond 32 bits: keep the tensor-table path

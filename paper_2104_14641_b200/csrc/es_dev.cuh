@@ -77,7 +77,7 @@ __device__ __forceinline__ int score_point(const DTask& T, const int32_t* tab, E
                                            uint64_t x, double* s) {
   double f[LS_NFEAT_GPU];
   if constexpr (MODE == 4 || MODE == 5) {
-    return eval_space<TM, MODE == 5>(T, tab, x, ev.fc, f, s);
+    return eval_space_mode<TM, MODE>(T, tab, x, ev.fc, f, s);
   } else {
     ls_record r;
     uint32_t kt[4];
