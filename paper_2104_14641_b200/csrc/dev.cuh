@@ -190,6 +190,14 @@ struct __align__(16) DTask {
   uint32_t sp_vbp[NSLOT][4];             // per loop slot: packed stage bytes of tensors 0..2, tensor-use bits
   uint32_t sp_vbp3[NSLOT];               // per loop slot: packed stage bytes of tensor 3
   const uint64_t* sp_rchain;             // per reorder choice: the chain innermost loop first
+  // tile-point rows (MODE 5): the reorder axis is the last axis, so a point is tile point * choices
+  // + reorder choice; one 32-byte row per tile point holds the tiled extents (F | ceil(E/F) << 16
+  // per tile axis; 0 = a factor out of range) and the packed first-row offsets per tensor
+  int32_t sp_tp_ok, sp_ntile;
+  uint32_t sp_total;                     // points in the space (< 2^32)
+  int32_t sp_pax;                        // the reorder axis (the last one) or -1
+  uint8_t sp_tj_new[4], sp_tj_slot[4];   // slots the j-th tile axis writes (inner F, outer ceil(E/F))
+  const uint4* sp_tp;                    // [tile points][2]
   // ---- general trees: unified node ids, accesses 0..tr_na-1 (preorder), loops
   //      tr_na + j for base loop j (preorder; header j = base_slot/ext/step/flags[j]), tile loops after
   int32_t tree, tr_nl, tr_na, tr_root_first;
@@ -1392,9 +1400,36 @@ template <int TM>
 __device__ __forceinline__ int eval_space_packed(const DTask& T, const int32_t* __restrict__ sdt, uint64_t x,
                                                  FastCand& c, double* f, double* score) {
   uint32_t kp[TM];
+  uint32_t pch = 0;
+  if (T.sp_tp_ok) {  // tile-point row: one division, two 16-byte loads
+    if (x >= T.sp_total) return LS_ST_POINT_RANGE;
+    const uint32_t x32 = (uint32_t)x;
+    uint32_t tp = x32;
+    if (T.sp_pax >= 0) {
+      const DAxis& ax = T.sp_ax[T.sp_pax];
+      if (ax.n > 1) {
+        tp = (uint32_t)(((uint64_t)x32 * (uint32_t)(ax.magic >> 32) + __umulhi(x32, (uint32_t)ax.magic)) >> 32);
+        pch = x32 - tp * (uint32_t)ax.n;
+      } else {
+        tp = x32;
+      }
+    }
+    const uint4 w = __ldg(T.sp_tp + 2 * (size_t)tp);
+    const uint4 kw = __ldg(T.sp_tp + 2 * (size_t)tp + 1);
+    if (w.x == 0u) return LS_ST_TILE_RANGE;
+    const int nt = T.sp_ntile;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (j >= nt) break;  // uniform
+      const uint32_t wj = j == 0 ? w.x : j == 1 ? w.y : j == 2 ? w.z : w.w;
+      c.E(T.sp_tj_new[j]) = (int32_t)(wj & 0xFFFFu);
+      c.E(T.sp_tj_slot[j]) = (int32_t)(wj >> 16);
+    }
+#pragma unroll
+    for (int t = 0; t < TM; ++t) kp[t] = t == 0 ? kw.x : t == 1 ? kw.y : t == 2 ? kw.z : kw.w;
+  } else {
 #pragma unroll
   for (int t = 0; t < TM; ++t) kp[t] = T.sd_offp[t];
-  uint32_t pch = 0;
   for (int a = T.sp_n - 1; a >= 0; --a) {
     const DAxis& ax = T.sp_ax[a];
     uint32_t ch;
@@ -1425,13 +1460,19 @@ __device__ __forceinline__ int eval_space_packed(const DTask& T, const int32_t* 
     c.E(T.sp_tnew[a]) = (int32_t)(e & 0xFFFFu);
     c.E(T.sp_tslot[a]) = (int32_t)((e >> 16) & 0x7FFFFFFFu);
   }
+  }
   const int pst = __ldg(T.sp_pstat + pch);
   if (pst) return pst;
   const uint64_t rchain = __ldg(reinterpret_cast<const unsigned long long*>(T.sp_rchain) + pch);
   const int n = T.sp_nchain;
-  const char* tb = reinterpret_cast<const char*>(sdt);
+  // offsets relative to the dynamic shared memory base (the tables sit at dyn + task_bytes,
+  // DESIGN.md §3.6): a lookup is one mask/shift and one shared load
+  extern __shared__ __align__(16) unsigned char dyn[];
+  const uint32_t tbo = (uint32_t)(reinterpret_cast<const unsigned char*>(sdt) - dyn);
+#pragma unroll
+  for (int t = 0; t < TM; ++t) kp[t] += tbo | (tbo << 16);
   auto fp = [&](uint32_t o) -> uint32_t {
-    return *reinterpret_cast<const uint32_t*>(tb + (o & 0xFFFFu)) * *reinterpret_cast<const uint32_t*>(tb + (o >> 16));
+    return *reinterpret_cast<const uint32_t*>(dyn + (o & 0xFFFFu)) * *reinterpret_cast<const uint32_t*>(dyn + (o >> 16));
   };
   uint32_t Fb[TM], dm[TM];
   bool ru[TM];
@@ -1477,9 +1518,12 @@ __device__ __forceinline__ int eval_space_packed(const DTask& T, const int32_t* 
       const uint32_t add = t == 0 ? row.x : t == 1 ? row.y : t == 2 ? row.z : T.sp_vbp3[v];
       kp[t] += add;
       const uint32_t Ff = fp(kp[t]);
-      const bool r0 = ru[t] && (!over || ((use >> t) & 1u));
-      dm[t] = (!over || r0) ? Ff : dm[t] * E;
-      ru[t] = r0 && Ff <= cap;
+      // r0 = ru && (!over || uses); keep Ff when !over || r0 == !over || (ru && uses);
+      // ru' = r0 && Ff <= cap (bitwise on predicates: no short-circuit branches)
+      const bool ub = (use & (1u << t)) != 0u;
+      const bool keep = !over | (ru[t] & ub);
+      dm[t] = keep ? Ff : dm[t] * E;
+      ru[t] = ru[t] & (!over | ub) & (Ff <= cap);
       Fb[t] = Ff;
     }
     const uint32_t Ee = (cpu || q < 8) ? E : 1u;  // PTX: no trip for loops 8+ levels above the innermost

@@ -175,6 +175,65 @@ constexpr int64_t SD_MAX_ENTRIES = 8192;  // 32 KiB of shared memory
 // inner extent F and the outer extent ceil(E/F) (ls/ir.py:361-382) and whether
 // F is out of range.  ext[voff + c] per choice of the tile axes (indexed like
 // sp_vals; other axes' entries unused).
+// Tile-point rows of the packed walk (MODE 5): eligible when the reorder
+// axis (if any) is the last axis, there are at most 4 tile axes and 2^16 tile points, the
+// space has fewer than 2^32 points and every outer extent fits 16 bits.  Row = 8 words:
+// F | ceil(E/F) << 16 per tile axis (all zero when a factor is out of range), then the packed
+// first-row group offsets per tensor.
+bool plan_tile_points(DTask& T, const std::vector<uint64_t>& ext, std::vector<uint32_t>& rows) {
+  T.sp_tp_ok = 0;
+  if (!T.sp_static || !T.sp_pack) return false;
+  int tile[LS_MAX_AXES], nt = 0, pax = -1;
+  double total = 1;
+  for (int a = 0; a < T.sp_n; ++a) {
+    total *= T.sp_ax[a].n;
+    if (T.sp_ax[a].kind == LS_AX_PERM) {
+      if (a != T.sp_n - 1) return false;
+      pax = a;
+    } else if (T.sp_ax[a].kind == LS_AX_PARAM) {
+      tile[nt++] = a;
+    } else {
+      return false;
+    }
+  }
+  if (nt < 1 || nt > 4 || total >= 4294967296.0) return false;
+  int64_t ntp = 1;
+  for (int j = 0; j < nt; ++j) ntp *= T.sp_ax[tile[j]].n;
+  if (ntp > 65536) return false;
+  rows.assign((size_t)ntp * 8, 0u);
+  for (int64_t tp = 0; tp < ntp; ++tp) {
+    uint32_t* r = &rows[(size_t)tp * 8];
+    int64_t rest = tp;
+    uint32_t kp[4];
+    for (int t = 0; t < 4; ++t) kp[t] = T.sd_offp[t];
+    bool bad = false;
+    for (int j = nt - 1; j >= 0; --j) {  // the last tile axis is the least significant digit
+      const DAxis& ax = T.sp_ax[tile[j]];
+      const uint32_t ch = (uint32_t)(rest % ax.n);
+      rest /= ax.n;
+      const uint64_t e = ext[ax.voff + ch];
+      if (e >> 63) bad = true;
+      const uint64_t outer = (e >> 16) & 0x7FFFFFFFull;
+      if (!bad && outer > 0xFFFFu) return false;
+      r[j] = (uint32_t)(e & 0xFFFFu) | ((uint32_t)outer << 16);
+      for (int t = 0; t < 4; ++t) kp[t] += ch * T.sd_Sp[tile[j]][t];
+    }
+    if (bad) {
+      for (int q = 0; q < 8; ++q) r[q] = 0;
+      continue;
+    }
+    for (int t = 0; t < 4; ++t) r[4 + t] = kp[t];
+  }
+  for (int j = 0; j < nt; ++j) {
+    T.sp_tj_new[j] = T.sp_tnew[tile[j]];
+    T.sp_tj_slot[j] = T.sp_tslot[tile[j]];
+  }
+  T.sp_ntile = nt;
+  T.sp_pax = pax;
+  T.sp_total = (uint32_t)total;
+  return true;
+}
+
 void plan_static_tiles(DTask& T, const ls_space_desc* sp, std::vector<uint64_t>& ext) {
   T.sp_static = 0;
   int ntile = 0;
@@ -1298,6 +1357,7 @@ int ls_task_set_space(ls_task* t, const ls_space_desc* sp) {
   }
   if (int rc = upload(t)) return rc;
   t->host.sp_ok = 0;
+  t->host.sp_tp_ok = 0;
   if (tables) {
     build_ttab_kernel<<<(unsigned)((t->host.tt_len + 255) / 256), 256>>>(t->d_task, dtt);
     CUDA_TRY(cudaGetLastError());
@@ -1385,6 +1445,15 @@ int ls_task_set_space(ls_task* t, const ls_space_desc* sp) {
       }
       t->host.sp_chain = dch;
       t->host.sp_rchain = drch;
+      std::vector<uint32_t> tprows;
+      if (t->host.sp_narrow && plan_tile_points(t->host, ext, tprows)) {
+        uint4* dtp = nullptr;
+        CUDA_TRY(cudaMalloc(&dtp, sizeof(uint32_t) * tprows.size()));
+        t->retired.push_back(dtp);
+        CUDA_TRY(cudaMemcpy(dtp, tprows.data(), sizeof(uint32_t) * tprows.size(), cudaMemcpyHostToDevice));
+        t->host.sp_tp = dtp;
+        t->host.sp_tp_ok = 1;
+      }
       t->host.sp_pstat = dst;
       t->host.sd_tab = reinterpret_cast<const int32_t*>(dsd);
       t->host.sp_ok = ovf ? 0 : 1;  // a group product beyond 32 bits: keep the tensor-table path
