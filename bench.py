@@ -245,7 +245,12 @@ def b200_arm(args):
     d_rec = to_device_records(recs, dev)
     d_pts = torch.from_numpy(pts.view(np.int32)).to(dev)
     base = rank * n
-    pinned_pts = torch.from_numpy(pts.view(np.int32)).pin_memory()
+    # the host-buffer (e2e) call ships packed 3-byte points when the space has < 2^24 of them
+    # (pack.pack_points; a quarter less over the host link than 4-byte points)
+    from paper_2104_14641_b200.pack import pack_points
+    e2e_pbytes = 3 if int(np.prod(st.sizes)) <= (1 << 24) else 4
+    pinned_pts = (torch.from_numpy(pack_points(pts, 3)) if e2e_pbytes == 3
+                  else torch.from_numpy(pts.view(np.int32))).pin_memory()
     pinned_rec = torch.from_numpy(recs.view(np.uint8).reshape(-1, RECORD_BYTES)).pin_memory()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
@@ -321,7 +326,9 @@ def b200_arm(args):
         return world * n / (max_over_ranks(sum(ms) / len(ms)) / 1e3), hi
 
     reps = max(3, args.steps // 2)
-    e2e_value, e2e_top = e2e(lambda: task.score_topk_points_host(pinned_pts, k, base_index=base), reps)
+    h_out = (np.empty(k, np.float64), np.empty(k, np.int64), np.zeros(1, np.int64))
+    e2e_value, e2e_top = e2e(lambda: task.score_topk_points_host(pinned_pts, k, base_index=base, out=h_out), reps)
+    e2e_top = e2e_top.copy()
     e2e_rec, e2e_rtop = e2e(lambda: task.score_topk_host(pinned_rec, k, base_index=base), reps)
 
     # ---- roofline of the fused launch ----
@@ -374,11 +381,12 @@ def b200_arm(args):
             "warmup": args.warmup, "ms_per_step": total_s * 1e3 / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int64+f64", "data": "synthetic",
             "config": config_dict(args, n),
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n * POINT_BYTES,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n * e2e_pbytes,
                     "d2h_bytes_per_step": k * 16 + 8,
-                    "path": "ls_score_topk_points_host (C-ABI): 4-byte space points in pinned, mapped host memory, read by "
-                            "the scoring kernel over the host link (the H2D transfer inside the kernel, no staging "
-                            "copy); top-k + count copied back",
+                    "path": f"ls_score_topk_points_host (C-ABI): {e2e_pbytes}-byte space points in pinned, mapped "
+                            "host memory, read by the scoring kernel over the host link (the H2D transfer inside the "
+                            "kernel, no staging copy); the k best + count written by the kernel into pinned host "
+                            "memory (no D2H copy)",
                     "topk_equals_device_path": e2e_top.tolist() == top_i.tolist() if world == 1 else None},
             "records_path": {"value": value_rec, "e2e": e2e_rec, "record_bytes": RECORD_BYTES,
                              "path": "ls_score_topk / ls_score_topk_host over 32-byte ls_record (rank path)",

@@ -295,10 +295,10 @@ int ls_score_topk_host(ls_task* task, const ls_record* h_records, int64_t n, int
 /* ---- points API: candidates as space points ----
  * A point is the mixed-radix number of a candidate's per-axis choice indices,
  * axis 0 most significant: the flat index of the choices ThetaEncoding.decode
- * picks (ls/es.py:57-62) over space_axes (ls/ir.py:517-547).  Points are 4- or
- * 8-byte unsigned integers (point_bytes); a 4-byte point is an 8x smaller
- * candidate than an ls_record.  Results are identical to scoring the records
- * the points decode to. */
+ * picks (ls/es.py:57-62) over space_axes (ls/ir.py:517-547).  Points are 3-,
+ * 4- or 8-byte little-endian unsigned integers (point_bytes; 3 = packed, for
+ * spaces below 2^24 points); a 4-byte point is an 8x smaller candidate than an
+ * ls_record.  Results are identical to scoring the records the points decode to. */
 
 /* Attach the task's schedule space (copied; replaces a previous one). */
 int ls_task_set_space(ls_task* task, const ls_space_desc* space);

@@ -1204,9 +1204,39 @@ __device__ int eval_tensor(const DTask& T, const ls_record& r, const uint32_t* k
 //   PTX  W'_j uses extent 1 for loops 8+ above the innermost (counter-register wrap),
 //        sum_j W'_{j-1} = 1 + A, sum_j W'_j = A + W'_{n-1}, A = sum_{j<n-1} W'_j
 // which are the general closed forms of features_score with every R_j = 1.
+// Points are 3-, 4- or 8-byte little-endian unsigned integers (3: packed, for spaces below
+// 2^24 points -- a quarter less to move over the host link than 4-byte points).
 __device__ __forceinline__ uint64_t load_point(const void* __restrict__ src, int pbytes, int64_t i) {
-  return pbytes == 4 ? (uint64_t)__ldg(reinterpret_cast<const unsigned int*>(src) + i)
-                     : (uint64_t)__ldg(reinterpret_cast<const unsigned long long*>(src) + i);
+  if (pbytes == 4) return (uint64_t)__ldg(reinterpret_cast<const unsigned int*>(src) + i);
+  if (pbytes == 3) {
+    const unsigned char* b = reinterpret_cast<const unsigned char*>(src) + 3 * i;
+    return (uint64_t)__ldg(b) | ((uint64_t)__ldg(b + 1) << 8) | ((uint64_t)__ldg(b + 2) << 16);
+  }
+  return (uint64_t)__ldg(reinterpret_cast<const unsigned long long*>(src) + i);
+}
+
+// The point of candidate b + lane of a warp-aligned round base b (b % 32 == 0), or 0 past n.
+// Warp-cooperative (every lane calls it): 3-byte points are read as the warp's 24 aligned
+// words (one coalesced 96-byte request -- over the host link, byte loads would fetch every
+// sector three times) and reassembled with two shuffles.
+__device__ __forceinline__ uint64_t load_point_warp(const void* __restrict__ src, int pbytes, int64_t b, int64_t n) {
+  const int lane = threadIdx.x & 31;
+  const int64_t p0 = b + (threadIdx.x & ~31);  // the warp's first point
+  if (pbytes != 3) return p0 + lane < n ? load_point(src, pbytes, p0 + lane) : 0;
+  const unsigned char* bytes = reinterpret_cast<const unsigned char*>(src);
+  const int64_t B0 = 3 * p0, Bend = 3 * n;  // B0 % 96 == 0: word aligned
+  uint32_t w = 0;
+  const int64_t wb = B0 + 4 * lane;
+  if (lane < 24 && wb < Bend) {
+    if (wb + 4 <= Bend) {
+      w = __ldg(reinterpret_cast<const unsigned int*>(bytes + wb));
+    } else {  // the buffer ends inside this word
+      for (int q = 0; q < (int)(Bend - wb); ++q) w |= (uint32_t)__ldg(bytes + wb + q) << (8 * q);
+    }
+  }
+  const int a = (3 * lane) >> 2, sh = (3 * lane & 3) * 8;
+  const uint32_t lo = __shfl_sync(0xffffffffu, w, a), hi = __shfl_sync(0xffffffffu, w, a + 1);
+  return p0 + lane < n ? (uint64_t)(__funnelshift_r(lo, hi, sh) & 0xFFFFFFu) : 0;
 }
 
 __device__ __forceinline__ int space_score(const DTask& T, int n, int64_t P, int64_t H, int64_t dmov, double* f,
@@ -2601,9 +2631,7 @@ __device__ __forceinline__ int load_cand(const DTask& T, const void* __restrict_
     r = load_record(reinterpret_cast<const ls_record*>(src), i);
     return LS_OK;
   } else {
-    const uint64_t x = pbytes == 4 ? (uint64_t)__ldg(reinterpret_cast<const unsigned int*>(src) + i)
-                                   : (uint64_t)__ldg(reinterpret_cast<const unsigned long long*>(src) + i);
-    return point_record<KEYS>(T, x, r, kt, pch);
+    return point_record<KEYS>(T, load_point(src, pbytes, i), r, kt, pch);
   }
 }
 
@@ -3503,7 +3531,7 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kern
   bool published = false;
   uint64_t xn = 0;  // space path: the next point, loaded one round ahead
   if constexpr (MODE == 4 || MODE == 5)
-    if (base + threadIdx.x < n) xn = load_point(src, pbytes, base + threadIdx.x);
+    xn = load_point_warp(src, pbytes, base, n);
   // two passes over the same loop: rounds [0, R0), the bound publication (no call inside the
   // hot loop: a call's clobbers would spill the loop state), then the rest
   int64_t r = 0;
@@ -3515,6 +3543,11 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kern
     const int64_t i = base + threadIdx.x;
     bool has = false;
     Key key;
+    uint64_t x = 0;
+    if constexpr (MODE == 4 || MODE == 5) {  // every lane (warp-cooperative load)
+      x = xn;
+      xn = load_point_warp(src, pbytes, nb, n);
+    }
     if (i < n) {
       ls_record r_;
       uint32_t kt[4];
@@ -3522,8 +3555,6 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kern
       double s;
       int st;
       if constexpr (MODE == 4 || MODE == 5) {
-        const uint64_t x = xn;
-        if (nb + threadIdx.x < n) xn = load_point(src, pbytes, nb + threadIdx.x);
         st = eval_space_mode<TM, MODE>(T, tab, x, ev.fc, f, &s);
       } else {
         uint32_t pch = 0;

@@ -1095,7 +1095,7 @@ int ls_score(ls_task* t, const ls_record* d_records, int64_t n, double* d_scores
 }
 
 static int check_points(const ls_task* t, int32_t pbytes) {
-  if (pbytes != 4 && pbytes != 8) return fail(LS_E_ARG, "point_bytes must be 4 or 8");
+  if (pbytes != 3 && pbytes != 4 && pbytes != 8) return fail(LS_E_ARG, "point_bytes must be 3, 4 or 8");
   if (t->host.sp_n < 1) return fail(LS_E_ARG, "no schedule space attached (ls_task_set_space)");
   return LS_E_OK;
 }
@@ -1126,7 +1126,7 @@ static cudaError_t ws_init(unsigned char* ws, cudaStream_t s) {
 
 static int topk_device(ls_task* t, const void* d_src, int pbytes, int64_t n, int64_t base_index, int32_t k,
                        double* d_top_scores, int64_t* d_top_index, unsigned long long* d_valid, cudaStream_t s,
-                       void* h_out = nullptr) {
+                       void* h_out = nullptr, void* h_out_dev = nullptr) {
   const int mode = mode_of(t, pbytes != 0);
   const TopkFn fn = topk_fn(t->host, mode, pbytes);
   const size_t sm = smem_topk(t->host, k, mode);
@@ -1201,9 +1201,11 @@ static int topk_device(ls_task* t, const void* d_src, int pbytes, int64_t n, int
   Key* group_out = block_out + (size_t)grid * (two ? topk_buf(k) : k);  // tree: group lists; bound merge: survivors
   Key* mins = two ? reinterpret_cast<Key*>(ws + WS_CTR_BYTES) : nullptr;
   unsigned char* out = ws + WS_FIXED_BYTES + keys_bytes;
-  if (h_out) {
-    d_valid = reinterpret_cast<unsigned long long*>(out);
-    d_top_scores = reinterpret_cast<double*>(out + 16);
+  if (h_out) {  // results to a pinned host block: written by the kernel through its device
+                // alias when it has one (no copy), else staged in the workspace and copied
+    unsigned char* o = h_out_dev ? reinterpret_cast<unsigned char*>(h_out_dev) : out;
+    d_valid = reinterpret_cast<unsigned long long*>(o);
+    d_top_scores = reinterpret_cast<double*>(o + 16);
     d_top_index = reinterpret_cast<int64_t*>(d_top_scores + k);
   }
   const char* tr_env = getenv("LS_TRACE");
@@ -1235,7 +1237,7 @@ static int topk_device(ls_task* t, const void* d_src, int pbytes, int64_t n, int
     CUDA_TRY(cudaLaunchKernelEx(&cfg, bound_merge_kernel, mins, tickets, cbo, grid, k, topk_buf(k), group_out,
                                 d_top_scores, d_top_index, d_valid, wvalid, tr));
   }
-  if (h_out) CUDA_TRY(cudaMemcpyAsync(h_out, out, out_bytes, cudaMemcpyDeviceToHost, s));
+  if (h_out && !h_out_dev) CUDA_TRY(cudaMemcpyAsync(h_out, out, out_bytes, cudaMemcpyDeviceToHost, s));
   L.ok = true;
   if (tr) {
     std::vector<unsigned long long> h((size_t)TR_SLOTS * grid);
@@ -1513,7 +1515,8 @@ static const void* mapped_alias(const void* h) {
 
 static int score_topk_mapped(ls_task* t, const void* d_alias, int pbytes, int64_t n, int64_t base_index, int32_t k,
                              double* h_top_scores, int64_t* h_top_index, int64_t* h_n_valid, cudaStream_t s) {
-  // pinned staging block: count (16 B slot) | scores | indices, filled by one D2H copy; the task's
+  // pinned staging block: count (16 B slot) | scores | indices, written by the kernel through the
+  // block's device alias (else filled by one D2H copy); the task's
   // cached block unless another host call holds it (then a private one), released on every path
   struct Stage {
     ls_task* t;
@@ -1547,7 +1550,8 @@ static int score_topk_mapped(ls_task* t, const void* d_alias, int pbytes, int64_
     S.own = true;
     CUDA_TRY(cudaMallocHost(&S.p, need));
   }
-  const int rc = topk_device(t, d_alias, pbytes, n, base_index, k, nullptr, nullptr, nullptr, s, S.p);
+  const int rc = topk_device(t, d_alias, pbytes, n, base_index, k, nullptr, nullptr, nullptr, s, S.p,
+                             const_cast<void*>(mapped_alias(S.p)));
   if (rc != LS_E_OK) return rc;
   CUDA_TRY(cudaStreamSynchronize(s));
   unsigned long long hv = 0;

@@ -227,41 +227,55 @@ class Task:
         _check(lib().ls_task_set_space(self._h, C.addressof(space)), "ls_task_set_space")
 
     def score_points(self, d_points, features: bool = True, stream=None):
-        """ls_score over a CUDA int32/int64 tensor of space points."""
+        """ls_score over a CUDA tensor of space points: int32 / int64, or uint8 [n, 3] (packed
+        3-byte points, pack.pack_points)."""
         torch = _torch()
-        n = d_points.shape[0]
+        n, eb = _points_shape(d_points)
         dev = d_points.device
         scores = torch.empty(n, dtype=torch.float64, device=dev)
         feats = torch.empty((n, self.nfeat), dtype=torch.float64, device=dev) if features else None
         status = torch.empty(n, dtype=torch.int32, device=dev)
-        _check(lib().ls_score_points(self._h, _dptr(d_points), d_points.element_size(), n, _dptr(scores),
+        _check(lib().ls_score_points(self._h, _dptr(d_points), eb, n, _dptr(scores),
                                      _dptr(feats), _dptr(status), _stream(torch, stream)), "ls_score_points")
         return scores, feats, status
 
     def score_topk_points(self, d_points, k: int, base_index: int = 0, stream=None, out=None):
         torch = _torch()
         dev = d_points.device
+        n, eb = _points_shape(d_points)
         s, i, nv = out if out is not None else _outputs(torch, k, dev)  # the count is written by the launch
-        _check(lib().ls_score_topk_points(self._h, _dptr(d_points), d_points.element_size(), d_points.shape[0],
+        _check(lib().ls_score_topk_points(self._h, _dptr(d_points), eb, n,
                                           int(base_index), int(k), _dptr(s), _dptr(i), _dptr(nv),
                                           _stream(torch, stream, dev.index)), "ls_score_topk_points")
         return s, i, nv
 
-    def score_topk_points_host(self, h_points, k: int, base_index: int = 0, stream=None):
-        """Host points (numpy uint32/uint64 or pinned torch tensor) in, host top-k out."""
-        torch = _torch()
+    def score_topk_points_host(self, h_points, k: int, base_index: int = 0, stream=None, out=None):
+        """Host points (numpy uint32 / uint64 / uint8 [n, 3], or a pinned torch tensor) in, host
+        top-k out; `out` = preallocated (f64[k], i64[k], i64[1]) numpy arrays."""
         if isinstance(h_points, np.ndarray):
-            h_points = np.ascontiguousarray(h_points)
-            ptr, n, eb = h_points.ctypes.data, len(h_points), h_points.itemsize
+            if not h_points.flags.c_contiguous:
+                h_points = np.ascontiguousarray(h_points)
+            ptr = h_points.ctypes.data
         else:
-            ptr, n, eb = h_points.data_ptr(), h_points.shape[0], h_points.element_size()
-        s = np.empty(k, np.float64)
-        i = np.empty(k, np.int64)
-        nv = np.zeros(1, np.int64)
+            ptr = h_points.data_ptr()
+        n, eb = _points_shape(h_points)
+        if out is None:
+            out = (np.empty(k, np.float64), np.empty(k, np.int64), np.zeros(1, np.int64))
+        s, i, nv = out
         _check(lib().ls_score_topk_points_host(self._h, ptr, eb, n, int(base_index), int(k), s.ctypes.data,
-                                               i.ctypes.data, nv.ctypes.data, _stream(torch, stream, self.device)),
+                                               i.ctypes.data, nv.ctypes.data, _stream(_torch(), stream, self.device)),
                "ls_score_topk_points_host")
         return s, i, int(nv[0])
+
+
+def _points_shape(p):
+    """(count, point_bytes) of a points buffer: 1-D 4/8-byte integers, or uint8 [n, 3]."""
+    if len(p.shape) == 2:
+        if p.shape[1] != 3 or (p.dtype != np.uint8 and str(p.dtype) != "torch.uint8"):
+            raise ValueError("2-D points must be packed uint8 [n, 3] (pack.pack_points)")
+        return p.shape[0], 3
+    eb = p.itemsize if isinstance(p, np.ndarray) else p.element_size()
+    return p.shape[0], eb
 
 
 def topk_merge(scores, index, n_lists: int, k_in: int, k_out: int, stream=None):

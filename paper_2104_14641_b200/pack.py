@@ -537,3 +537,13 @@ class SpaceTemplate:
         for ax, i in zip(self.axes, idx_row):
             out.extend(ax.choices[int(i)])
         return Schedule(tuple(out))
+
+
+def pack_points(points: np.ndarray, nbytes: int = 3) -> np.ndarray:
+    """Space points (non-negative integers below 2^(8 nbytes)) as packed little-endian bytes,
+    uint8 [n, nbytes] -- the 3-byte point format of the points API (include/loopscout_b200.h)."""
+    p = np.ascontiguousarray(points).astype("<u8", copy=False)
+    if len(p) and int(p.max()) >> (8 * nbytes):
+        raise ValueError(f"a point does not fit {nbytes} bytes")
+    return np.ascontiguousarray(p.view(np.uint8).reshape(-1, 8)[:, :nbytes])
+

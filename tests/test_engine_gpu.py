@@ -454,3 +454,39 @@ def test_topk_merge_modes_forced(mode):
     r = subprocess.run([sys.executable, str(Path(__file__).with_name("merge_modes_check.py"))], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("n", [1, 97, 100_003, 1 << 20])
+def test_points_3byte_equal_4byte(torch, n):
+    """Packed 3-byte points (pack.pack_points) score and rank exactly like 4-byte points: device
+    buffers (score + top-k) and pinned host buffers (results written by the kernel into pinned
+    host memory)."""
+    E = _engine()
+    from paper_2104_14641_b200 import workloads as W
+    from paper_2104_14641_b200.arch import KernelLaunch, load_arch
+    from paper_2104_14641_b200.pack import SpaceTemplate, pack_points
+    st = SpaceTemplate(W.program(W.conv2d_json()), W.conv_space(4096, 1))
+    task = E.Task(st.template.desc(load_arch("x86-avx2"), KernelLaunch.from_json(W.KERNEL_LAUNCH)), 0)
+    task.set_space(st.space_desc())
+    pts = st.points_from_indices(W.distinct_indices(st.sizes, n, 53))
+    d4 = torch.from_numpy(pts.view(np.int32)).cuda()
+    p3 = pack_points(pts, 3)
+    d3 = torch.from_numpy(p3).cuda()
+    s4, _, st4 = task.score_points(d4, features=False)
+    s3, _, st3 = task.score_points(d3, features=False)
+    torch.cuda.synchronize()
+    assert np.array_equal(s3.cpu().numpy(), s4.cpu().numpy(), equal_nan=True)
+    assert np.array_equal(st3.cpu().numpy(), st4.cpu().numpy())
+    k = min(64, n)
+    a = task.score_topk_points(d4, k, base_index=9)
+    b = task.score_topk_points(d3, k, base_index=9)
+    torch.cuda.synchronize()
+    assert a[1].cpu().tolist() == b[1].cpu().tolist() and int(a[2].item()) == int(b[2].item())
+    pin = torch.from_numpy(p3).pin_memory()
+    for _ in range(2):
+        hs, hi, hn = task.score_topk_points_host(pin, k, base_index=9)
+        assert hi.tolist() == a[1].cpu().tolist() and hn == int(a[2].item())
+        assert np.array_equal(hs, a[0].cpu().numpy())
+    hs, hi, hn = task.score_topk_points_host(p3, k, base_index=9)  # pageable: staged copies
+    assert hi.tolist() == a[1].cpu().tolist() and hn == int(a[2].item())
+    task.close()
