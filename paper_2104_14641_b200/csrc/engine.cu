@@ -17,8 +17,8 @@ ScoreFn k_score_fn(const DTask& T, int mode, int src) {
 TopkFn k_topk_fn(const DTask& T, int mode, int src) {
   switch (mode) {
     case 0: return k_topk_fn_generic(T, src);
-    case 4: return k_topk_fn_space4(T);
-    case 5: return k_topk_fn_space5(T);
+    case 4: return k_topk_fn_space4(T, src);
+    case 5: return k_topk_fn_space5(T, src);
     case 6: return k_topk_fn_tree(src);
     default: return k_topk_fn_tab(T, mode, src);
   }
@@ -1124,11 +1124,62 @@ static cudaError_t ws_init(unsigned char* ws, cudaStream_t s) {
   return e != cudaSuccess ? e : cudaMemsetAsync(ws + WS_CTR_BYTES, 0xFF, 16 * WS_MIN_KEYS, s);
 }
 
+// Phase timestamps of one fused launch to stderr (LS_TRACE=1, profiling aid).
+static int print_trace(unsigned long long* tr, int grid, int64_t n, bool two, cudaStream_t s) {
+    std::vector<unsigned long long> h((size_t)TR_SLOTS * grid);
+    CUDA_TRY(cudaStreamSynchronize(s));
+    CUDA_TRY(cudaMemcpy(h.data(), tr, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost));
+    unsigned long long t0 = ~0ull, surv = 0;
+    for (int b = 0; b < grid; ++b) t0 = std::min(t0, h[b * TR_SLOTS]);
+    for (int b = 0; b < grid; ++b)
+      if (h[b * TR_SLOTS + 7] >> 63) surv = h[b * TR_SLOTS + 7] & ~(1ull << 63), h[b * TR_SLOTS + 7] = 0;
+    double avg[TR_SLOTS] = {0}, mx[TR_SLOTS] = {0};
+    for (int q = 0; q < TR_SLOTS; ++q) {
+      if (q == 8) continue;
+      int cnt = 0;
+      for (int b = 0; b < grid; ++b)
+        if (h[b * TR_SLOTS + q] > t0) {
+          const double v = (double)(h[b * TR_SLOTS + q] - t0) / 1e3;
+          avg[q] += v, mx[q] = std::max(mx[q], v), ++cnt;
+        }
+      if (cnt) avg[q] /= cnt;
+    }
+    if (two)
+      fprintf(stderr, "LS_TRACE n=%lld grid=%d us(avg/max): staged %.1f/%.1f main %.1f/%.1f | bound merge: T out %.1f "
+              "filtered %.1f/%.1f last block %.1f (controls %.1f loaded %.1f ranked %.1f) final %.1f survivors %llu\n",
+              (long long)n, grid, avg[1], mx[1], avg[2], mx[2], mx[4], avg[3], mx[3], mx[5], mx[9], mx[10], mx[11],
+              mx[6], surv);
+    else
+      fprintf(stderr, "LS_TRACE n=%lld grid=%d us(avg/max): staged %.1f/%.1f main %.1f/%.1f listed %.1f/%.1f | "
+              "tree group %.1f final %.1f\n", (long long)n, grid, avg[1], mx[1], avg[2], mx[2], avg[3], mx[3], mx[4],
+              mx[5]);
+    if (getenv("LS_TRACE_BLOCKS")) {  // per-block main-loop ends
+      std::vector<std::pair<double, int>> e;
+      for (int b = 0; b < grid; ++b)
+        if (h[b * TR_SLOTS + 2] > t0) e.push_back({(double)(h[b * TR_SLOTS + 2] - t0) / 1e3, b});
+      std::sort(e.begin(), e.end());
+      fprintf(stderr, "LS_TRACE blocks (main end us, block, sm, start us):");
+      for (size_t q = 0; q < e.size(); q += std::max<size_t>(1, e.size() / 24)) {
+        const int b = e[q].second;
+        fprintf(stderr, " %.1f/%d/%llu/%.1f", e[q].first, b, h[b * TR_SLOTS + 8], (double)(h[b * TR_SLOTS] - t0) / 1e3);
+      }
+      if (!e.empty()) {
+        const int b = e.back().second;
+        fprintf(stderr, " | max %.1f/%d/%llu/%.1f", e.back().first, b, h[b * TR_SLOTS + 8],
+                (double)(h[b * TR_SLOTS] - t0) / 1e3);
+      }
+      fprintf(stderr, "\n");
+    }
+    return LS_E_OK;
+}
+
 static int topk_device(ls_task* t, const void* d_src, int pbytes, int64_t n, int64_t base_index, int32_t k,
                        double* d_top_scores, int64_t* d_top_index, unsigned long long* d_valid, cudaStream_t s,
-                       void* h_out = nullptr, void* h_out_dev = nullptr) {
+                       void* h_out = nullptr, void* h_out_dev = nullptr, bool host_points = false) {
   const int mode = mode_of(t, pbytes != 0);
-  const TopkFn fn = topk_fn(t->host, mode, pbytes);
+  // points in mapped host memory (16-byte aligned) on the space paths: block-cooperative loads
+  const bool coop = host_points && (mode == 4 || mode == 5) && (reinterpret_cast<uintptr_t>(d_src) & 15) == 0;
+  const TopkFn fn = k_topk_fn(t->host, mode, coop ? 2 : pbytes ? 1 : 0);
   const size_t sm = smem_topk(t->host, k, mode);
   BPS_TRY(bps, fn, sm);
   const int grid = n > 0 ? grid_for(t, n, bps) : 1;
@@ -1239,52 +1290,8 @@ static int topk_device(ls_task* t, const void* d_src, int pbytes, int64_t n, int
   }
   if (h_out && !h_out_dev) CUDA_TRY(cudaMemcpyAsync(h_out, out, out_bytes, cudaMemcpyDeviceToHost, s));
   L.ok = true;
-  if (tr) {
-    std::vector<unsigned long long> h((size_t)TR_SLOTS * grid);
-    CUDA_TRY(cudaStreamSynchronize(s));
-    CUDA_TRY(cudaMemcpy(h.data(), tr, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost));
-    unsigned long long t0 = ~0ull, surv = 0;
-    for (int b = 0; b < grid; ++b) t0 = std::min(t0, h[b * TR_SLOTS]);
-    for (int b = 0; b < grid; ++b)
-      if (h[b * TR_SLOTS + 7] >> 63) surv = h[b * TR_SLOTS + 7] & ~(1ull << 63), h[b * TR_SLOTS + 7] = 0;
-    double avg[TR_SLOTS] = {0}, mx[TR_SLOTS] = {0};
-    for (int q = 0; q < TR_SLOTS; ++q) {
-      if (q == 8) continue;
-      int cnt = 0;
-      for (int b = 0; b < grid; ++b)
-        if (h[b * TR_SLOTS + q] > t0) {
-          const double v = (double)(h[b * TR_SLOTS + q] - t0) / 1e3;
-          avg[q] += v, mx[q] = std::max(mx[q], v), ++cnt;
-        }
-      if (cnt) avg[q] /= cnt;
-    }
-    if (two)
-      fprintf(stderr, "LS_TRACE n=%lld grid=%d us(avg/max): staged %.1f/%.1f main %.1f/%.1f | bound merge: T out %.1f "
-              "filtered %.1f/%.1f last block %.1f (controls %.1f loaded %.1f ranked %.1f) final %.1f survivors %llu\n",
-              (long long)n, grid, avg[1], mx[1], avg[2], mx[2], mx[4], avg[3], mx[3], mx[5], mx[9], mx[10], mx[11],
-              mx[6], surv);
-    else
-      fprintf(stderr, "LS_TRACE n=%lld grid=%d us(avg/max): staged %.1f/%.1f main %.1f/%.1f listed %.1f/%.1f | "
-              "tree group %.1f final %.1f\n", (long long)n, grid, avg[1], mx[1], avg[2], mx[2], avg[3], mx[3], mx[4],
-              mx[5]);
-    if (getenv("LS_TRACE_BLOCKS")) {  // per-block main-loop ends
-      std::vector<std::pair<double, int>> e;
-      for (int b = 0; b < grid; ++b)
-        if (h[b * TR_SLOTS + 2] > t0) e.push_back({(double)(h[b * TR_SLOTS + 2] - t0) / 1e3, b});
-      std::sort(e.begin(), e.end());
-      fprintf(stderr, "LS_TRACE blocks (main end us, block, sm, start us):");
-      for (size_t q = 0; q < e.size(); q += std::max<size_t>(1, e.size() / 24)) {
-        const int b = e[q].second;
-        fprintf(stderr, " %.1f/%d/%llu/%.1f", e[q].first, b, h[b * TR_SLOTS + 8], (double)(h[b * TR_SLOTS] - t0) / 1e3);
-      }
-      if (!e.empty()) {
-        const int b = e.back().second;
-        fprintf(stderr, " | max %.1f/%d/%llu/%.1f", e.back().first, b, h[b * TR_SLOTS + 8],
-                (double)(h[b * TR_SLOTS] - t0) / 1e3);
-      }
-      fprintf(stderr, "\n");
-    }
-  }
+  if (tr)
+    if (int rc = print_trace(tr, grid, n, two, s)) return rc;
   return LS_E_OK;
 }
 
@@ -1550,8 +1557,10 @@ static int score_topk_mapped(ls_task* t, const void* d_alias, int pbytes, int64_
     S.own = true;
     CUDA_TRY(cudaMallocHost(&S.p, need));
   }
-  const int rc = topk_device(t, d_alias, pbytes, n, base_index, k, nullptr, nullptr, nullptr, s, S.p,
-                             const_cast<void*>(mapped_alias(S.p)));
+  // cudaMallocHost memory is mapped at the same address under unified addressing (every 64-bit
+  // platform CUDA supports): the kernel writes the results straight into the block
+  const int rc = topk_device(t, d_alias, pbytes, n, base_index, k, nullptr, nullptr, nullptr, s, S.p, S.p,
+                             pbytes != 0);
   if (rc != LS_E_OK) return rc;
   CUDA_TRY(cudaStreamSynchronize(s));
   unsigned long long hv = 0;
@@ -1570,7 +1579,11 @@ static int score_topk_mapped(ls_task* t, const void* d_alias, int pbytes, int64_
 static int score_topk_host_any(ls_task* t, const void* h_src, int pbytes, int64_t n, int64_t base_index, int32_t k,
                                double* h_top_scores, int64_t* h_top_index, int64_t* h_n_valid, cudaStream_t s) {
   CUDA_TRY(cudaSetDevice(t->device));
-  if (n > 0)
+  static const bool staged_env = [] {  // LS_HOST_PATH=staged forces the staged copies (tests / profiling aid)
+    const char* e = getenv("LS_HOST_PATH");
+    return e && e[0] == 's';
+  }();
+  if (n > 0 && !staged_env)
     if (const void* alias = mapped_alias(h_src))
       return score_topk_mapped(t, alias, pbytes, n, base_index, k, h_top_scores, h_top_index, h_n_valid, s);
   const size_t esz = pbytes ? (size_t)pbytes : sizeof(ls_record);

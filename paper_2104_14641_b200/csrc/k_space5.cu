@@ -11,12 +11,12 @@ ScoreFn k_score_fn_space5(const DTask& T) {
     default: return score_kernel<4, 4, 5, 1>;
   }
 }
-TopkFn k_topk_fn_space5(const DTask& T) {
+TopkFn k_topk_fn_space5(const DTask& T, int src) {  // src 2: points in mapped pinned host memory
   switch (T.n_tensors) {
-    case 1: return score_topk_kernel<1, 4, 5, 1>;
-    case 2: return score_topk_kernel<2, 4, 5, 1>;
-    case 3: return score_topk_kernel<3, 4, 5, 1>;
-    default: return score_topk_kernel<4, 4, 5, 1>;
+    case 1: return src == 2 ? score_topk_kernel<1, 4, 5, 2> : score_topk_kernel<1, 4, 5, 1>;
+    case 2: return src == 2 ? score_topk_kernel<2, 4, 5, 2> : score_topk_kernel<2, 4, 5, 1>;
+    case 3: return src == 2 ? score_topk_kernel<3, 4, 5, 2> : score_topk_kernel<3, 4, 5, 1>;
+    default: return src == 2 ? score_topk_kernel<4, 4, 5, 2> : score_topk_kernel<4, 4, 5, 1>;
   }
 }
 EsGenFn k_es_gen_fn_space5(const DTask& T) {

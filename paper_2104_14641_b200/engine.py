@@ -77,13 +77,17 @@ def _check(rc: int, what: str):
 _cuda_ok = False
 
 
+_TORCH = None  # the torch module once CUDA was found usable
+
+
 def _torch():
-    global _cuda_ok
+    global _cuda_ok, _TORCH
     import torch
     if not _cuda_ok:  # checked once: the per-call wrappers stay a few microseconds
         if not torch.cuda.is_available():
             raise EngineError("no CUDA device visible (there is no CPU fallback)")
         _cuda_ok = True
+        _TORCH = torch
     return torch
 
 
@@ -136,6 +140,7 @@ class Task:
         h = C.c_void_p()
         _check(lib().ls_task_create(C.addressof(desc), device, C.byref(h)), "ls_task_create")
         self._h = h
+        self._host_points_fn = None
         self.has_unroll = any(desc.xforms[i].kind == abi.XF_UNROLL for i in range(desc.n_xforms)) or \
             any(desc.nodes[i].kind == abi.NODE_LOOP and desc.nodes[i].unrolled for i in range(desc.n_nodes))
 
@@ -262,9 +267,13 @@ class Task:
         if out is None:
             out = (np.empty(k, np.float64), np.empty(k, np.int64), np.zeros(1, np.int64))
         s, i, nv = out
-        _check(lib().ls_score_topk_points_host(self._h, ptr, eb, n, int(base_index), int(k), s.ctypes.data,
-                                               i.ctypes.data, nv.ctypes.data, _stream(_torch(), stream, self.device)),
-               "ls_score_topk_points_host")
+        fn = self._host_points_fn
+        if fn is None:
+            fn = self._host_points_fn = lib().ls_score_topk_points_host
+        rc = fn(self._h, ptr, eb, n, base_index, k, s.ctypes.data, i.ctypes.data, nv.ctypes.data,
+                _stream(_TORCH or _torch(), stream, self.device))
+        if rc:
+            _check(rc, "ls_score_topk_points_host")
         return s, i, int(nv[0])
 
 

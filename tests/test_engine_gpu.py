@@ -490,3 +490,28 @@ def test_points_3byte_equal_4byte(torch, n):
     hs, hi, hn = task.score_topk_points_host(p3, k, base_index=9)  # pageable: staged copies
     assert hi.tolist() == a[1].cpu().tolist() and hn == int(a[2].item())
     task.close()
+
+
+@pytest.mark.parametrize("path", ["staged"])
+def test_host_points_paths_forced(path):
+    """The host-buffer points call through the staged-copy path (LS_HOST_PATH forces it for
+    pinned buffers too) returns the device call's top-k for 3- and 4-byte points."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    env = dict(os.environ, LS_HOST_PATH=path)
+    r = subprocess.run([sys.executable, str(Path(__file__).with_name("host_paths_check.py"))], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_host_points_default_paths():
+    """Default host paths (pinned: mapped zero-copy with block-cooperative aligned loads; pageable:
+    staged copies) == the device call."""
+    import subprocess
+    import sys
+    from pathlib import Path
+    r = subprocess.run([sys.executable, str(Path(__file__).with_name("host_paths_check.py"))],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
