@@ -49,9 +49,9 @@ def parse():
     ap.add_argument("--arch", default="x86-avx2")
     ap.add_argument("--no-baseline", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--path", type=int, default=0, help="0 auto, 1 generic, 2 tabulated, 3 space-specialised")
-    ap.add_argument("--workload", default="conv", choices=["conv", "bert", "resnet50-es", "sweep"],
-                    help="conv: BASELINE configs[1] (the headline); bert: configs[3]; resnet50-es: configs[2]; "
-                         "sweep: configs[4]")
+    ap.add_argument("--workload", default="conv", choices=["conv", "gemm", "bert", "resnet50-es", "sweep"],
+                    help="conv: BASELINE configs[1] (the headline); gemm: configs[0]; bert: configs[3]; "
+                         "resnet50-es: configs[2]; sweep: configs[4]")
     ap.add_argument("--population", type=int, default=1 << 20, help="resnet50-es: ES population per generation")
     ap.add_argument("--generations", type=int, default=20, help="resnet50-es: generations per task")
     ap.add_argument("--sigma", type=float, default=2.0, help="resnet50-es: ES sigma")
@@ -88,11 +88,15 @@ def config_dict(args, n):
 # -- CPU baseline (the oracle port of the reference algorithm) ---------------------------------
 
 
-def cpu_rate(desc, recs, threads: int):
+def cpu_rate(desc, recs, threads: int, k: int = 64):
+    """Oracle scoring of `recs` plus the cmd_rank ordering cut at k (ls/cli.py:124-126): the
+    (score, index) sort of the valid candidates, timed together."""
     sys.path.insert(0, str(ROOT / "oracle"))
     import pyoracle
     t0 = time.perf_counter()
     s, f, st = pyoracle.evaluate(desc, recs, nthreads=threads)
+    ok = np.nonzero(st == 0)[0]
+    top = ok[np.lexsort((ok, s[ok]))][:k]
     dt = time.perf_counter() - t0
     return len(recs) / dt, dt, s, st
 
@@ -124,14 +128,52 @@ def reference_arm(args):
         times.append(dt)
     value = m * args.steps / sum(times)
     sample = (f"{m} candidates per step of the same conv2d workload, oracle/oracle.c (C restatement of "
-              f"the reference path) on {threads} threads")
+              f"the reference path) on {threads} threads of a {cpu_model()}, scoring + (score, index) "
+              f"sort of the top {args.k}")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64+f64",
             "data": "synthetic", "config": config_dict(args, m),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
+                             "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def points_parity(task, st, desc, pts: np.ndarray, k: int, torch, threads: int) -> dict:
+    """Bit-exact check of the device scores, status and top-k of `pts` (one task) against the
+    oracle (oracle/oracle.c, run after the timed region)."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import pyoracle
+    recs = st.records_from_indices(st.indices_from_points(pts))
+    cs, _, cst = pyoracle.evaluate(desc, recs, nthreads=threads)
+    d = torch.from_numpy(pts.astype(np.uint32).view(np.int32)).to(task.device)
+    gs, _, gst = task.score_points(d, features=False)
+    _, ti, _ = task.score_topk_points(d, k)
+    torch.cuda.synchronize()
+    ok = cst == 0
+    want = np.nonzero(ok)[0][np.lexsort((np.nonzero(ok)[0], cs[ok]))][:k]
+    return {"sample": int(len(pts)),
+            "scores_bit_exact": bool(np.array_equal(np.where(ok, gs.cpu().numpy(), 0.0), np.where(ok, cs, 0.0))),
+            "status_equal": bool(np.array_equal(gst.cpu().numpy(), cst)),
+            "topk_identical": ti.cpu().numpy()[:len(want)].tolist() == want.tolist()}
+
+
+def merge_parity(parts: list) -> dict:
+    return {"sample": sum(p["sample"] for p in parts),
+            "scores_bit_exact": all(p["scores_bit_exact"] for p in parts),
+            "status_equal": all(p["status_equal"] for p in parts),
+            "topk_identical": all(p["topk_identical"] for p in parts), "per_task": len(parts)}
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 # -- clocks -------------------------------------------------------------------------------------
@@ -365,9 +407,10 @@ def b200_arm(args):
             sidx = W.distinct_indices(st.sizes, m, 2104)
             sample = st.records_from_indices(sidx)
             rate, dt, cs, cst = cpu_rate(desc, sample, threads)
-            cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+            cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port", "cpu_model": cpu_model(),
                    "sample": f"{m} candidates of the same workload through oracle/oracle.c (C restatement of "
-                             f"the reference path) on {threads} threads, {dt:.1f} s"}
+                             f"the reference path) on {threads} threads, scoring + (score, index) sort of "
+                             f"the top {k}, {dt:.1f} s"}
             dsp = torch.from_numpy(st.points_from_indices(sidx).view(np.int32)).to(dev)
             gs, _, gst = task.score_points(dsp, features=False)
             ts, ti, _ = task.score_topk_points(dsp, k)
@@ -490,6 +533,15 @@ def bert_arm(args):
         ms, _ = _timed(lambda kev=None: step(), args.steps, flush, stream, torch)
     per_step = sum(n for _, _, _, n, _ in jobs) * world
     tot = _max_ms(torch, dist, world, dev, sum(ms)) / 1e3
+    parity = None
+    if rank == 0 and not args.no_baseline:  # bit-exact vs the oracle on 4096 of each task's points
+        parts = []
+        for j, ((name, spec, space), (_, task, d, n_task, _)) in enumerate(zip(tasks, jobs)):
+            st = SpaceTemplate(W.program(spec), space)
+            desc = st.template.desc(load_arch(args.arch), KernelLaunch.from_json(W.KERNEL_LAUNCH))
+            pts = d[:4096].cpu().numpy().view(np.uint32).astype(np.uint64)
+            parts.append(points_parity(task, st, desc, pts, args.k, torch, cpu_cores()))
+        parity = merge_parity(parts)
     line = {"metric": METRIC, "value": per_step * args.steps / tot, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot * 1e3 / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64+f64",
@@ -501,7 +553,8 @@ def bert_arm(args):
                        "arch": args.arch, "candidates_per_step": per_step, "k": args.k,
                        "tasks": {name: {"candidates_per_gpu": n, "points_path": pp} for name, _, _, n, pp in jobs},
                        "l2": "flushed between timed steps (256 MiB write)"},
-            "clocks": clk.summary(), "gpu_launches": args.steps * len(jobs) * (2 + (2 if world > 1 else 0))}
+            "clocks": clk.summary(), "gpu_launches": args.steps * len(jobs) * (1 + (2 if world > 1 else 0)),
+            "parity": parity}
     for _, task, _, _, _ in jobs:
         task.close()
     _emit(line, world, dist)
@@ -540,11 +593,25 @@ def resnet_es_arm(args):
         ms, _ = _timed(lambda kev=None: step(), args.steps, flush, stream, torch)
     distinct = 0
     paths = {}
+    parts = []
     for name, st, task, run in runs:
         _, trace, ev, err, best = run.result(st.dim)
         assert err == 0, (name, err)
         distinct += ev
         paths[name] = task.points_path
+        if not args.no_baseline:  # the memo's scores (every distinct schedule scored) vs the oracle
+            sys.path.insert(0, str(ROOT / "oracle"))
+            import pyoracle
+            pts, sc = run.evaluated()
+            sel = np.linspace(0, len(pts) - 1, min(len(pts), 1024)).astype(np.int64)
+            desc = task.desc
+            recs = st.records_from_indices(st.indices_from_points(pts[sel]))
+            cs, _, cst = pyoracle.evaluate(desc, recs, nthreads=cpu_cores())
+            parts.append({"sample": int(len(sel)), "scores_bit_exact": bool(np.array_equal(sc[sel], cs)),
+                          "status_equal": bool((cst == 0).all()),
+                          # the incumbent (best score) is the minimum over the evaluated schedules
+                          "topk_identical": bool(len(sc) > 0 and float(np.min(sc)) == float(best))})
+    parity = merge_parity(parts) if parts else None
     dt = torch.tensor([distinct], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(dt)
@@ -562,10 +629,106 @@ def resnet_es_arm(args):
                        "config": "BASELINE.json configs[2]", "arch": args.arch,
                        "distinct_schedules_per_step": float(dt.item()), "points_paths": paths,
                        "l2": "flushed between timed steps (256 MiB write)"},
-            "clocks": clk.summary(), "gpu_launches": args.steps * len(mine) * (1 + 4 * args.generations)}
+            "clocks": clk.summary(), "gpu_launches": args.steps * len(mine) * (1 + 4 * args.generations),
+            "parity": parity}
     for _, _, task, run in runs:
         run.close()
         task.close()
+    _emit(line, world, dist)
+
+
+def gemm_arm(args):
+    """configs[0]: one GEMM 1024^3 task, 4096 random tile/reorder candidates scored and ranked
+    top-64.  `value`: the fused launch over 4096 device-resident points; `e2e`: the reference-facing
+    rank API from the reference's own Schedule objects (cost.rank_topk: host packing, H2D of the
+    packed records, the fused launch, D2H of the k best; cmd_rank's seam ls/cli.py:106-141)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2104_14641_b200 import cost
+    from paper_2104_14641_b200 import workloads as W
+    from paper_2104_14641_b200.arch import KernelLaunch, load_arch
+    from paper_2104_14641_b200.engine import Task
+    from paper_2104_14641_b200.pack import SpaceTemplate
+    world, rank, dev = _dist_setup(torch, dist)
+    prog = W.program(W.matmul_json(1024))
+    st = SpaceTemplate(prog, W.gemm_space(1024))
+    arch, launch = load_arch(args.arch), KernelLaunch.from_json(W.KERNEL_LAUNCH)
+    desc = st.template.desc(arch, launch)
+    task = Task(desc, dev)
+    task.set_space(st.space_desc())
+    n = 4096
+    idx = W.distinct_indices(st.sizes, n, 1024 + rank)
+    schedules = [st.schedule_of(row) for row in idx]
+    pts = st.points_from_indices(idx)
+    d = torch.from_numpy(pts.view(np.int32)).to(dev)
+    out = (torch.empty(args.k, dtype=torch.float64, device=dev), torch.empty(args.k, dtype=torch.int64, device=dev),
+           torch.empty(1, dtype=torch.int64, device=dev))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step(kev=None):
+        task.score_topk_points(d, args.k, out=out)
+    for _ in range(max(3, args.warmup)):
+        step()
+        cost.rank_topk(prog, schedules, arch, args.k, launch, dev)
+    torch.cuda.synchronize()
+    with ClockSampler(dev) as clk:
+        ms, _ = _timed(step, args.steps, flush, stream, torch)
+        e2e_ms = []
+        for _ in range(args.steps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            a.record(stream)
+            rs, ri, rnv = cost.rank_topk(prog, schedules, arch, args.k, launch, dev)
+            b.record(stream)
+            torch.cuda.synchronize()
+            e2e_ms.append(a.elapsed_time(b))
+    tot = _max_ms(torch, dist, world, dev, sum(ms)) / 1e3
+    e2e_tot = _max_ms(torch, dist, world, dev, sum(e2e_ms)) / 1e3
+    # the same rank API over a long list: 2^19 of the space's 958 320 schedules as Schedule objects
+    big = None
+    if rank == 0:
+        bidx = W.distinct_indices(st.sizes, 1 << 19, 77)
+        bsched = [st.schedule_of(row) for row in bidx]
+        cost.rank_topk(prog, bsched[:4096], arch, args.k, launch, dev)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        cost.rank_topk(prog, bsched, arch, args.k, launch, dev)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        big = {"candidates": len(bsched), "value": len(bsched) / dt, "unit": UNIT, "wall_s": dt,
+               "path": "cost.rank_topk over 2^19 Schedule objects (host wall clock: native packer + H2D + fused "
+                       "launch + D2H); the host packer bounds it"}
+        del bsched
+    parity = None
+    if rank == 0 and not args.no_baseline:  # every candidate vs the oracle; the rank API's top-k
+        sys.path.insert(0, str(ROOT / "oracle"))
+        import pyoracle
+        cs, _, cst = pyoracle.evaluate(desc, st.records_from_indices(idx), nthreads=cpu_cores())
+        ok = np.nonzero(cst == 0)[0]
+        want = ok[np.lexsort((ok, cs[ok]))][:args.k]
+        gs, _, gst = task.score_points(d, features=False)
+        torch.cuda.synchronize()
+        parity = {"sample": n, "scores_bit_exact": bool(np.array_equal(gs.cpu().numpy()[ok], cs[ok])),
+                  "status_equal": bool(np.array_equal(gst.cpu().numpy(), cst)),
+                  "topk_identical": out[1].cpu().tolist()[:len(want)] == want.tolist()
+                  and ri.tolist()[:len(want)] == want.tolist()}
+    line = {"metric": METRIC, "value": world * n * args.steps / tot, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot * 1e3 / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64+f64",
+            "data": "synthetic",
+            "config": {"workload": "single GEMM 1024x1024x1024 task: 4096 random tile (divisors of 1024 for i/j/k) "
+                                   "x 720 chain-order candidates scored and top-64 ranked",
+                       "config": "BASELINE.json configs[0]", "arch": args.arch, "candidates_per_gpu": n,
+                       "k": args.k, "l2": "flushed between timed steps (256 MiB write)",
+                       "step": "value: one Task.score_topk_points launch over 4096 device-resident points"},
+            "e2e": {"value": world * n * args.steps / e2e_tot, "unit": UNIT,
+                    "h2d_bytes_per_step": n * RECORD_BYTES, "d2h_bytes_per_step": args.k * 16 + 8,
+                    "path": "cost.rank_topk(program, [Schedule] * 4096, arch, 64): the reference's Schedule "
+                            "objects packed on the host (native packer), 32-byte records H2D, the fused "
+                            "launch, the k best D2H", "ms_per_step": e2e_tot * 1e3 / args.steps},
+            "rank_list": big, "clocks": clk.summary(), "gpu_launches": args.steps, "parity": parity}
+    task.close()
     _emit(line, world, dist)
 
 
@@ -586,6 +749,7 @@ def sweep_arm(args):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
     rows = []
+    sweep_parity = None
     for e in range(20, 27):
         n = (1 << e) // world
         pts = st.points_from_indices(W.distinct_indices(st.sizes, n, 2104, start=rank * n))
@@ -603,6 +767,10 @@ def sweep_arm(args):
         ms, _ = _timed(step, steps, flush, stream, torch)
         tot = _max_ms(torch, dist, world, dev, sum(ms)) / 1e3
         rows.append({"n": 1 << e, "value": (1 << e) * steps / tot, "ms_per_step": tot * 1e3 / steps})
+        if e == 26 and rank == 0 and not args.no_baseline:  # bit-exact vs the oracle on a sample
+            sample = d[: 1 << 12].cpu().numpy().view(np.uint32).astype(np.uint64)
+            desc = st.template.desc(load_arch(args.arch), KernelLaunch.from_json(W.KERNEL_LAUNCH))
+            sweep_parity = points_parity(task, st, desc, sample, args.k, torch, cpu_cores())
         del d
     peak = max(r["value"] for r in rows)
     line = {"metric": METRIC, "value": rows[-1]["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -612,7 +780,8 @@ def sweep_arm(args):
                                    "n = 2^20..2^26 distinct candidates per step sharded over the GPUs, "
                                    f"score + top-{args.k}", "config": "BASELINE.json configs[4]", "arch": args.arch,
                        "l2": "flushed between timed steps (256 MiB write)"},
-            "sweep": rows, "peak_value": peak, "gpu_launches": None}
+            "sweep": rows, "peak_value": peak, "gpu_launches": sum(max(3, args.steps // 4) for _ in rows),
+            "parity": sweep_parity}
     task.close()
     _emit(line, world, dist)
 
@@ -621,6 +790,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         reference_arm(args)
+    elif args.workload == "gemm":
+        gemm_arm(args)
     elif args.workload == "bert":
         bert_arm(args)
     elif args.workload == "resnet50-es":

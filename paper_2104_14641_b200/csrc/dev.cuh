@@ -3162,7 +3162,9 @@ __host__ __device__ inline int64_t bound_rounds(int64_t n, int k, int grid) {
 }
 inline bool bound_inline_rank(int64_t n, int k, int grid) {
   const double per_block = (double)((n + TPB - 1) / TPB) / grid;
-  return per_block >= 6.0 && (double)bound_rounds(n, k, grid) <= 0.6 * per_block;
+  // T comes out ~2 rounds after the (3/4 grid)-th block published (the warp scheduler's age
+  // priority delays the youngest blocks); blocks must still be scoring by then
+  return per_block >= 6.0 && (double)bound_rounds(n, k, grid) + 2.0 <= 0.8 * per_block;
 }
 // Every block publishes the minimum of the keys it has seen after its first R0
 // rounds; the (3/4 grid)-th block to publish sets T = the k-th smallest of the
@@ -3275,11 +3277,13 @@ static __device__ __noinline__ void bound_finish(TopkState& S, int k, Key* __res
       if (slot >= 0) surv[slot] = x;
     }
     if (threadIdx.x == 0) cnts[blockIdx.x] = 0;
-  } else {  // T is not out yet: the list is left for the last block
+  } else {  // T is not out yet: the block's k best (a radix selection of the buffer) are left
+            // for the last block / bound_merge_kernel to filter
+    const int kept = topk_select(S, k);  // block-uniform (every thread reads the same S.cnt)
     Key* dst = block_out + (int64_t)blockIdx.x * cap;
-    for (int j = threadIdx.x; j < cnt; j += blockDim.x) dst[j] = B[j];
+    for (int j = threadIdx.x; j < kept; j += blockDim.x) dst[j] = B[j];
     if (threadIdx.x == 0) {
-      cnts[blockIdx.x] = TK_UNFILTERED | (unsigned)cnt;
+      cnts[blockIdx.x] = TK_UNFILTERED | (unsigned)kept;
       atomicAdd(&ctr[TK_UNF_CTR], 1u);
     }
   }
