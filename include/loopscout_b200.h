@@ -281,6 +281,17 @@ int ls_topk_merge_keys(const ls_topk_key* d_keys, int64_t m, int32_t k_out, doub
 /* Pack m (score, index) entries into keys (index < 0 -> empty key). */
 int ls_topk_to_keys(const double* d_scores, const int64_t* d_index, int64_t m, ls_topk_key* d_keys,
                     void* stream);
+/* The whole multi-GPU step over NCCL: this rank's k best
+ * (d_scores / d_index, from ls_score_topk*) are packed into d_scratch[rank*k ..
+ * (rank+1)*k), one in-place ncclAllGather of 16k bytes per rank fills
+ * d_scratch[world*k], and the merge kernel writes the global k best (identical
+ * on every rank, equal to the single-GPU answer).  nccl_comm is the caller's
+ * ncclComm_t (rank / world of it); the library binds ncclAllGather from the
+ * libnccl.so.2 already loaded in the process (else dlopen), LS_E_UNSUPPORTED
+ * when there is none.  Stream-ordered, no allocation. */
+int ls_topk_allgather_merge(void* nccl_comm, int32_t rank, int32_t world, const double* d_scores,
+                            const int64_t* d_index, int32_t k, ls_topk_key* d_scratch, double* d_out_scores,
+                            int64_t* d_out_index, void* stream);
 
 /* Host-buffer variant of ls_score_topk: records in host memory (pinned or
  * pageable), results written to host memory.  Mapped page-locked buffers

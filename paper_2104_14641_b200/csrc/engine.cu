@@ -5,6 +5,17 @@
 #define LS_MAIN_TU
 #include "dev.cuh"
 
+#include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>
+
+// NVTX range over every public scoring / merge / ES entry point (header-only NVTX3: no cost
+// unless a profiler is attached): ncu / Nsight timelines show the C-ABI calls by name.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+#define LS_NVTX(name) NvtxRange ls_nvtx_range_(name)
+
 ScoreFn k_score_fn(const DTask& T, int mode, int src) {
   switch (mode) {
     case 0: return k_score_fn_generic(T, src);
@@ -942,6 +953,7 @@ const char* ls_last_error(void) { return g_err.c_str(); }
 int ls_abi_version(void) { return LS_ABI_VERSION; }
 
 int ls_task_create(const ls_task_desc* desc, int device, ls_task** out) {
+  LS_NVTX("ls_task_create");
   if (!desc || !out) return fail(LS_E_ARG, "null argument");
   *out = nullptr;
   CUDA_TRY(cudaSetDevice(device));
@@ -1039,6 +1051,7 @@ int ls_task_prepare_unroll(ls_task* t, const int64_t* u, int32_t n) {
 
 int ls_collect_unroll(ls_task* t, const ls_record* d_records, int64_t n, int64_t* h_values, int32_t cap,
                       int32_t* h_count, void* stream) {
+  LS_NVTX("ls_collect_unroll");
   if (!t || !h_values || !h_count || cap < 1) return fail(LS_E_ARG, "bad argument");
   if (t->host.tree) {  // no Unroll on the tree path: nothing to prepare
     *h_count = 0;
@@ -1088,6 +1101,7 @@ static int score_device(ls_task* t, const void* d_src, int pbytes, int64_t n, do
 
 int ls_score(ls_task* t, const ls_record* d_records, int64_t n, double* d_scores, double* d_features,
              int32_t* d_status, void* stream) {
+  LS_NVTX("ls_score");
   if (!t || n < 0 || (n && !d_records)) return fail(LS_E_ARG, "bad argument");
   if (n == 0) return LS_E_OK;
   CUDA_TRY(cudaSetDevice(t->device));
@@ -1102,6 +1116,7 @@ static int check_points(const ls_task* t, int32_t pbytes) {
 
 int ls_score_points(ls_task* t, const void* d_points, int32_t pbytes, int64_t n, double* d_scores,
                     double* d_features, int32_t* d_status, void* stream) {
+  LS_NVTX("ls_score_points");
   if (!t || n < 0 || (n && !d_points)) return fail(LS_E_ARG, "bad argument");
   if (int rc = check_points(t, pbytes)) return rc;
   if (n == 0) return LS_E_OK;
@@ -1305,6 +1320,7 @@ static int score_topk_any(ls_task* t, const void* d_src, int pbytes, int64_t n, 
 
 int ls_score_topk(ls_task* t, const ls_record* d_records, int64_t n, int64_t base_index, int32_t k,
                   double* d_top_scores, int64_t* d_top_index, int64_t* d_n_valid, void* stream) {
+  LS_NVTX("ls_score_topk");
   if (!t || n < 0 || (n && !d_records) || !d_top_scores || !d_top_index) return fail(LS_E_ARG, "bad argument");
   if (k < 1 || k > TK_MAXK) return fail(LS_E_ARG, "k must be in 1..1024");
   return score_topk_any(t, d_records, 0, n, base_index, k, d_top_scores, d_top_index, d_n_valid,
@@ -1313,6 +1329,7 @@ int ls_score_topk(ls_task* t, const ls_record* d_records, int64_t n, int64_t bas
 
 int ls_score_topk_points(ls_task* t, const void* d_points, int32_t pbytes, int64_t n, int64_t base_index, int32_t k,
                          double* d_top_scores, int64_t* d_top_index, int64_t* d_n_valid, void* stream) {
+  LS_NVTX("ls_score_topk_points");
   if (!t || n < 0 || (n && !d_points) || !d_top_scores || !d_top_index) return fail(LS_E_ARG, "bad argument");
   if (k < 1 || k > TK_MAXK) return fail(LS_E_ARG, "k must be in 1..1024");
   if (int rc = check_points(t, pbytes)) return rc;
@@ -1321,6 +1338,7 @@ int ls_score_topk_points(ls_task* t, const void* d_points, int32_t pbytes, int64
 }
 
 int ls_task_set_space(ls_task* t, const ls_space_desc* sp) {
+  LS_NVTX("ls_task_set_space");
   if (!t || !sp || sp->n_axes < 1 || sp->n_axes > LS_MAX_AXES) return fail(LS_E_ARG, "bad space");
   std::vector<uint64_t> vals;
   DAxis ax[LS_MAX_AXES];
@@ -1483,6 +1501,7 @@ static int merge_launch(const Key* keys, const double* d_scores, const int64_t* 
 
 int ls_topk_merge(const double* d_scores, const int64_t* d_index, int32_t n_lists, int32_t k_in, int32_t k_out,
                   double* d_out_scores, int64_t* d_out_index, void* stream) {
+  LS_NVTX("ls_topk_merge");
   if (!d_scores || !d_index || n_lists < 0 || k_in < 0 || k_out < 1 || k_out > TK_MAXK || !d_out_scores ||
       !d_out_index)
     return fail(LS_E_ARG, "bad argument");
@@ -1492,6 +1511,7 @@ int ls_topk_merge(const double* d_scores, const int64_t* d_index, int32_t n_list
 
 int ls_topk_merge_keys(const ls_topk_key* d_keys, int64_t m, int32_t k_out, double* d_out_scores,
                        int64_t* d_out_index, void* stream) {
+  LS_NVTX("ls_topk_merge_keys");
   if ((m > 0 && !d_keys) || m < 0 || k_out < 1 || k_out > TK_MAXK || !d_out_scores || !d_out_index)
     return fail(LS_E_ARG, "bad argument");
   static_assert(sizeof(ls_topk_key) == sizeof(Key), "ls_topk_key layout");
@@ -1499,7 +1519,39 @@ int ls_topk_merge_keys(const ls_topk_key* d_keys, int64_t m, int32_t k_out, doub
                       (cudaStream_t)stream);
 }
 
+// ncclAllGather, bound at run time (no link-time NCCL dependency): the process's libnccl.so.2
+// (torch's, when loaded) or the system one.
+using NcclAllGatherFn = int (*)(const void*, void*, size_t, int, void*, cudaStream_t);
+static NcclAllGatherFn nccl_all_gather() {
+  static NcclAllGatherFn fn = [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    return h ? reinterpret_cast<NcclAllGatherFn>(dlsym(h, "ncclAllGather")) : nullptr;
+  }();
+  return fn;
+}
+
+int ls_topk_allgather_merge(void* nccl_comm, int32_t rank, int32_t world, const double* d_scores,
+                            const int64_t* d_index, int32_t k, ls_topk_key* d_scratch, double* d_out_scores,
+                            int64_t* d_out_index, void* stream) {
+  LS_NVTX("ls_topk_allgather_merge");
+  if (!nccl_comm || world < 1 || rank < 0 || rank >= world || k < 1 || k > TK_MAXK || !d_scores || !d_index ||
+      !d_scratch || !d_out_scores || !d_out_index)
+    return fail(LS_E_ARG, "bad argument");
+  const NcclAllGatherFn ag = nccl_all_gather();
+  if (!ag) return fail(LS_E_UNSUPPORTED, "libnccl.so.2 (ncclAllGather) is not available");
+  const cudaStream_t s = (cudaStream_t)stream;
+  ls_topk_key* mine = d_scratch + (size_t)rank * k;
+  if (int rc = ls_topk_to_keys(d_scores, d_index, k, mine, stream)) return rc;
+  constexpr int kNcclUint8 = 1;  // ncclDataType_t
+  if (int r = ag(mine, d_scratch, sizeof(ls_topk_key) * (size_t)k, kNcclUint8, nccl_comm, s))
+    return fail(LS_E_CUDA, "ncclAllGather failed: ncclResult_t " + std::to_string(r));
+  return ls_topk_merge_keys(d_scratch, (int64_t)world * k, k, d_out_scores, d_out_index, stream);
+}
+
 int ls_topk_to_keys(const double* d_scores, const int64_t* d_index, int64_t m, ls_topk_key* d_keys, void* stream) {
+  LS_NVTX("ls_topk_to_keys");
   if (m < 0 || (m > 0 && (!d_scores || !d_index || !d_keys))) return fail(LS_E_ARG, "bad argument");
   if (m == 0) return LS_E_OK;
   lists_to_keys_kernel<<<(unsigned)((m + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
@@ -1650,6 +1702,7 @@ static int score_topk_host_any(ls_task* t, const void* h_src, int pbytes, int64_
 
 int ls_score_topk_host(ls_task* t, const ls_record* h_records, int64_t n, int64_t base_index, int32_t k,
                        double* h_top_scores, int64_t* h_top_index, int64_t* h_n_valid, void* stream) {
+  LS_NVTX("ls_score_topk_host");
   if (!t || n < 0 || (n && !h_records) || !h_top_scores || !h_top_index) return fail(LS_E_ARG, "bad argument");
   if (k < 1 || k > TK_MAXK) return fail(LS_E_ARG, "k must be in 1..1024");
   return score_topk_host_any(t, h_records, 0, n, base_index, k, h_top_scores, h_top_index, h_n_valid,
@@ -1659,6 +1712,7 @@ int ls_score_topk_host(ls_task* t, const ls_record* h_records, int64_t n, int64_
 int ls_score_topk_points_host(ls_task* t, const void* h_points, int32_t pbytes, int64_t n, int64_t base_index,
                               int32_t k, double* h_top_scores, int64_t* h_top_index, int64_t* h_n_valid,
                               void* stream) {
+  LS_NVTX("ls_score_topk_points_host");
   if (!t || n < 0 || (n && !h_points) || !h_top_scores || !h_top_index) return fail(LS_E_ARG, "bad argument");
   if (k < 1 || k > TK_MAXK) return fail(LS_E_ARG, "k must be in 1..1024");
   if (int rc = check_points(t, pbytes)) return rc;

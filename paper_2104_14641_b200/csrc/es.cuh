@@ -199,6 +199,7 @@ int ls_es_create(ls_task* t, const ls_es_params* p, const double* h_theta0, ls_e
 }
 
 int ls_es_begin(ls_es* es, void* stream) {
+  LS_NVTX("ls_es_begin");
   if (!es) return fail(LS_E_ARG, "null argument");
   ls_task* t = es->task;
   CUDA_TRY(cudaSetDevice(t->device));
@@ -213,6 +214,7 @@ int ls_es_begin(ls_es* es, void* stream) {
 }
 
 int ls_es_step(ls_es* es, int32_t stage, void* stream) {
+  LS_NVTX("ls_es_step");
   if (!es || stage < 0 || stage > 2) return fail(LS_E_ARG, "bad argument");
   CUDA_TRY(cudaSetDevice(es->task->device));
   cudaStream_t s = (cudaStream_t)stream;
@@ -230,6 +232,7 @@ int ls_es_shard_buffers(ls_es* es, void** d_keys, int64_t* keys_per_rank, void**
 }
 
 int ls_es_run(ls_es* es, void* stream) {
+  LS_NVTX("ls_es_run");
   if (!es) return fail(LS_E_ARG, "null argument");
   if (es->world != 1) return fail(LS_E_ARG, "a sharded run is driven generation by generation (ls_es_step)");
   if (int rc = ls_es_begin(es, stream)) return rc;

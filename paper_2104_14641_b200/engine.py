@@ -44,6 +44,7 @@ def lib():
     L.ls_score_topk.argtypes = [vp, vp, i64, i64, i32, vp, vp, vp, vp]
     L.ls_topk_merge.argtypes = [vp, vp, i32, i32, i32, vp, vp, vp]
     L.ls_topk_merge_keys.argtypes = [vp, i64, i32, vp, vp, vp]
+    L.ls_topk_allgather_merge.argtypes = [vp, i32, i32, vp, vp, i32, vp, vp, vp, vp]
     L.ls_topk_to_keys.argtypes = [vp, vp, i64, vp, vp]
     L.ls_score_topk_host.argtypes = [vp, vp, i64, i64, i32, vp, vp, vp, vp]
     L.ls_task_set_path.argtypes = [vp, i32]
@@ -315,6 +316,23 @@ def topk_merge_keys(keys, k_out: int, out=None, stream=None):
                torch.empty(k_out, dtype=torch.int64, device=keys.device))
     _check(lib().ls_topk_merge_keys(_dptr(keys), keys.shape[0], int(k_out), _dptr(out[0]), _dptr(out[1]),
                                     _stream(torch, stream)), "ls_topk_merge_keys")
+    return out
+
+
+def topk_allgather_merge(nccl_comm: int, rank: int, world: int, scores, index, k: int, scratch=None, out=None,
+                         stream=None):
+    """The C-ABI multi-GPU merge over a caller-owned NCCL communicator (ncclComm_t as an int):
+    pack this rank's k best, one in-place ncclAllGather, the merge kernel (ls_topk_allgather_merge).
+    torch.distributed users go through dist.gather_topk (same keys, same merge kernel)."""
+    torch = _torch()
+    dev = scores.device
+    if scratch is None:
+        scratch = torch.empty((world * k, 2), dtype=torch.int64, device=dev)
+    if out is None:
+        out = (torch.empty(k, dtype=torch.float64, device=dev), torch.empty(k, dtype=torch.int64, device=dev))
+    _check(lib().ls_topk_allgather_merge(C.c_void_p(nccl_comm), int(rank), int(world), _dptr(scores), _dptr(index),
+                                         int(k), _dptr(scratch), _dptr(out[0]), _dptr(out[1]),
+                                         _stream(torch, stream, dev.index)), "ls_topk_allgather_merge")
     return out
 
 

@@ -231,3 +231,39 @@ def test_two_devices_in_one_process():
         res.append((s.cpu().numpy(), i.cpu().numpy()))
         task.close()
     assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
+
+
+@pytest.mark.gpu
+def test_topk_allgather_merge_nccl_single_rank():
+    """ls_topk_allgather_merge over a real NCCL communicator (one rank: the all-gather is the
+    local copy) == the rank's own k best; the library binds ncclAllGather from the process's
+    libnccl.so.2 (torch's)."""
+    import ctypes
+    import glob
+    import os
+
+    import torch
+
+    from paper_2104_14641_b200 import engine as E
+    nccl = None
+    cands = ["libnccl.so.2"] + glob.glob(os.path.join(os.path.dirname(torch.__file__), "..", "nvidia", "nccl", "lib",
+                                                      "libnccl.so*"))
+    for name in cands:
+        try:
+            nccl = ctypes.CDLL(name, mode=ctypes.RTLD_GLOBAL)
+            break
+        except OSError:
+            continue
+    if nccl is None:
+        pytest.skip("no libnccl.so.2 in this process")
+    torch.cuda.init()
+    comm = ctypes.c_void_p()
+    devs = (ctypes.c_int * 1)(0)
+    assert nccl.ncclCommInitAll(ctypes.byref(comm), 1, devs) == 0
+    k = 64
+    s = torch.sort(torch.rand(k, dtype=torch.float64, device="cuda")).values
+    i = torch.arange(100, 100 + k, dtype=torch.int64, device="cuda")
+    out_s, out_i = E.topk_allgather_merge(comm.value, 0, 1, s, i, k)
+    torch.cuda.synchronize()
+    assert torch.equal(out_s, s) and torch.equal(out_i, i)
+    nccl.ncclCommDestroy(comm)
