@@ -382,6 +382,57 @@ int ls_es_evaluated(ls_es* es, uint64_t* h_points, double* h_scores, int64_t cap
 int ls_es_noise(ls_es* es, int32_t generation, double* d_out, void* stream);
 int ls_es_destroy(ls_es* es);
 
+/* ---- external code-text analysis (`analyze --code`, ls/cli.py:86) ----
+ * The text-dependent features of extract_features (ls/cost.py:132-152) for a batch of
+ * assembly / PTX texts, parsed on the device (one CUDA block per text): CPU family
+ * n_fma, n_vload, n_vstore, ilp_cycles (parse_asm + loop_map + count_simd + the list
+ * scheduler, ls/asm.py:110-337, ls/ilp.py:82-271); GPU family workload_per_thread,
+ * n_fma, n_ld, n_st (loop_map_ptx + count_ptx + thread_cycles, ls/ptx.py:90-227).  The
+ * IR-side features (cache movement; occupancy, warp slack, shared-memory ops) come from
+ * the scoring path on the program.  Keys of the class / cost tables are ls_code_hash of
+ * the reference's lowercase class names (fma, load, move, store, or a mnemonic root). */
+#define LS_CODE_MAX_CLASSES 32
+#define LS_CODE_MAX_LOOPS 64
+#define LS_CODE_TARGET_X86 0
+#define LS_CODE_TARGET_AARCH64 1
+#define LS_CODE_DIALECT_ATT 0
+#define LS_CODE_DIALECT_DEST_FIRST 1
+/* per-text status: 0 ok; AsmError("empty assembly input") / AsmError("jump to undefined
+ * label ...") (err_info = line, operand offset, length in the text); ValueError (a line
+ * holding only a predicate); a device limit exceeded (operands / resources per
+ * instruction, dependence predecessors, trip products beyond int64). */
+#define LS_CODE_E_EMPTY 1
+#define LS_CODE_E_LABEL 2
+#define LS_CODE_E_VALUE 3
+#define LS_CODE_E_LIMIT 4
+typedef struct {
+  int32_t family;           /* LS_FAMILY_CPU / LS_FAMILY_GPU */
+  int32_t target;           /* CPU: LS_CODE_TARGET_* (count_simd's significant sets) */
+  int32_t dialect;          /* CPU: LS_CODE_DIALECT_* (reg_effects' destination operand) */
+  int32_t issue_width;      /* SchedSpec.issue_width */
+  int32_t default_latency;  /* SchedSpec.default_latency */
+  int32_t n_classes;        /* latency / unit classes (SchedSpec.latency / units keys) */
+  uint64_t cls_hash[LS_CODE_MAX_CLASSES];
+  int32_t cls_latency[LS_CODE_MAX_CLASSES];  /* 0: not in the latency table (default) */
+  int32_t cls_units[LS_CODE_MAX_CLASSES];    /* 0: no unit cap */
+  int32_t n_costs, pad0;    /* GPU: GpuSpec.instr_cost (root -> cycles; 1 otherwise) */
+  uint64_t cost_hash[LS_CODE_MAX_CLASSES];
+  double cost[LS_CODE_MAX_CLASSES];
+  int32_t n_loops, pad1;    /* CPU: the program's branching loops in preorder (loop_map) */
+  int64_t loop_extent[LS_CODE_MAX_LOOPS], loop_step[LS_CODE_MAX_LOOPS];
+  int64_t loop_weight[LS_CODE_MAX_LOOPS];  /* product of its and its branching ancestors' extents */
+} ls_code_desc;
+uint64_t ls_code_hash(const char* s, int32_t n);
+/* Device scratch a text of text_bytes needs (ls_code_features takes the sum over the
+ * batch + a few KiB for the descriptor and offsets). */
+int64_t ls_code_scratch_bytes(int64_t text_bytes);
+/* d_texts: the texts back to back on the device; h_offsets[n_texts + 1] their byte
+ * offsets (host).  d_features[4 * n_texts] (order above), d_status[n_texts],
+ * d_err_info[3 * n_texts].  Stream-ordered. */
+int ls_code_features(const ls_code_desc* desc, const char* d_texts, const int64_t* h_offsets, int32_t n_texts,
+                     void* d_scratch, int64_t scratch_bytes, double* d_features, int32_t* d_status,
+                     int64_t* d_err_info, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -624,12 +624,155 @@ def cli_fixture():
     print(f"cli: {len(manifest)} reference CLI runs")
 
 
+def _mutate(rng: random.Random, text: str, target: str, kind: str) -> str:
+    """A user-style edit of an emitted text (the reference decides what it means)."""
+    lines = text.splitlines()
+    if kind == "comments":
+        out = []
+        for ln in lines:
+            r = rng.random()
+            if r < 0.15:
+                out.append(ln + ("  # note" if target != "gpu-ptx" else "  // note"))
+            elif r < 0.25:
+                out.append("")
+                out.append(ln)
+            elif r < 0.3:
+                out.append("\t" + ln.strip() + "   ")
+            else:
+                out.append(ln)
+        return "\n".join(out) + "\n"
+    if kind == "extra":
+        extra = {"cpu-x86": ["    xorq %rdx, %rdx", "    addq $8, %rsi", "    vmovups %zmm3, (%rdi)",
+                             "    vfmadd231ps %zmm4, %zmm5, %zmm6", "    leaq 16(%rax,%rbx,4), %rcx"],
+                 "cpu-aarch64": ["    add x3, x3, #1", "    ld1 {v4.4s}, [x5]", "    fmla v6.4s, v4.4s, v5.4s",
+                                 "    st1 {v6.4s}, [x7]", "    mul x8, x8, x9"],
+                 "gpu-ptx": ["    mov.u32 %r9, 7;", "    ld.global.f32 %f9, [%rd9];", "    fma.rn.f32 %f9, %f9, %f8, %f9;",
+                             "    st.shared.f32 [%rd8], %f9;", "    mul.lo.s32 %r8, %r8, 3;"]}[target]
+        out = list(lines)
+        for _ in range(rng.randint(1, 6)):
+            out.insert(rng.randint(0, len(out)), rng.choice(extra))
+        return "\n".join(out) + "\n"
+    if kind == "bound":
+        idx = [i for i, ln in enumerate(lines) if ("cmp" in ln or "setp" in ln) and any(c.isdigit() for c in ln)]
+        if idx:
+            i = rng.choice(idx)
+            import re as _re
+            lines[i] = _re.sub(r"(\d+)(?!.*\d)", lambda m: str(int(m.group(1)) + rng.choice((1, 2, -1))), lines[i])
+        return "\n".join(lines) + "\n"
+    if kind == "join":  # a label and its first instruction on one line
+        out, i = [], 0
+        while i < len(lines):
+            if lines[i].rstrip().endswith(":") and i + 1 < len(lines) and rng.random() < 0.5:
+                out.append(lines[i].rstrip() + " " + lines[i + 1].strip())
+                i += 2
+            else:
+                out.append(lines[i])
+                i += 1
+        return "\n".join(out) + "\n"
+    if kind == "upper":
+        out = []
+        for ln in lines:
+            parts = ln.split(None, 1)
+            if parts and not parts[0].endswith(":") and rng.random() < 0.3:
+                ln = ln.replace(parts[0], parts[0].upper(), 1)
+            out.append(ln)
+        return "\n".join(out) + "\n"
+    if kind == "crlf":
+        return "\r\n".join(lines) + "\r\n"
+    if kind == "droplabel":
+        idx = [i for i, ln in enumerate(lines) if ln.rstrip().endswith(":")]
+        if idx:
+            del lines[rng.choice(idx)]
+        return "\n".join(lines) + "\n"
+    return text
+
+
+def code_fixture():
+    """f4: extract_features(program, code, arch, launch) of the reference on emitted texts and on
+    user-style edits of them (comments, blank lines, extra instructions, changed loop bounds,
+    label + instruction lines, upper-case mnemonics, CRLF, a dropped label), plus the
+    reference tests' own hand-written texts."""
+    from loopscout.ir import serialize_program
+    cases = []
+    rng = random.Random(11)
+    launch = L.KernelLaunch.from_json(LAUNCH)
+    progs = dict(RANK_PROGRAMS)
+    arches = {"cpu-x86": ["x86-avx2", "odd-x86"], "cpu-aarch64": ["aarch64-neon"], "gpu-ptx": ["nvidia-volta", "odd-gpu"]}
+    for pname in ("matmul8", "nested4x8", "conv_small", "deep9", "smem_tid"):
+        prog = L.parse_program(json.dumps(progs[pname]))
+        for _ in range(5):
+            s = random_schedule(rng, prog, kinds="TRVUP")
+            try:
+                q = L.apply_schedule(prog, L.Schedule.from_json(s))
+            except Exception:  # noqa: BLE001
+                continue
+            for tgt, anames in arches.items():
+                base = L.emit_mock_asm(q, tgt)
+                if len(base) > 60000:
+                    continue
+                for kind in ("none", "comments", "extra", "bound", "join", "upper", "crlf", "droplabel"):
+                    text = _mutate(rng, base, tgt, kind)
+                    for an in anames:
+                        arch = ref_arch(an)
+                        entry = {"program": json.loads(serialize_program(q)), "arch": an, "kind": kind,
+                                 "text": text}
+                        try:
+                            fv = L.extract_features(q, text, arch, launch)
+                            entry["features"] = [[k, v] for k, v in fv.values]
+                            entry["score"] = L.score(fv, arch)
+                        except Exception as e:  # noqa: BLE001
+                            entry["error"] = [type(e).__name__, str(e)]
+                        cases.append(entry)
+    # hand-written texts in the style of the reference's tests (ls tests/test_ptx.py, test_asm.py)
+    single = L.parse_program(json.dumps({"tensors": [{"name": "A", "dims": [64]}],
+                                         "body": [{"loop": {"var": "i", "extent": 8, "body": [
+                                             {"access": {"tensor": "A", "kind": "load", "idx": ["i"]}}]}}]}))
+
+    def countdown(init, delta, op, bound, body=""):
+        return (f"    mov r1, {init}\n" "back:\n" f"{body}" f"    add r1, r1, {delta}\n"
+                f"    setp.{op} r1, {bound}\n" "    bra back\n")
+    body = "    fma.rn.f32 %f0, %f1, %f2, %f0\n" * 4 + "    ld.global.f32 %f3, [%rd1]\n" * 2
+    hand = [countdown(0, 1, "lt", 8), countdown(4, 2, "lt", 16), countdown(0, 1, "le", 7), countdown(0, 2, "ne", 10),
+            countdown(0, 3, "ne", 10), countdown(0, 1, "lt", 4, body), countdown(10, -1, "gt", 0, body),
+            "    mov r1, 1\nback:\n    mul r1, r1, 2\n    setp.lt r1, 64\n    bra back\n",
+            "back:\n    add r1, r1, 1\n    setp.lt r1, 8\n    bra back\n", "    ret\n", "", "   // only a comment\n",
+            "    mov r1, 0\nback:\n    add r1, r1, 1\n    setp.lt %p1, r1, 8\n    @%p1 bra back\n    ret\n",
+            "    mov r1, 0\nL0: add r1, r1, 1\n    setp.ge r1, 8\n    @!%p1 bra L0\n",
+            "    jmp nowhere\n", "@p\n"]
+    xhand = ["    movq $0, %r8\n.L1:\n    vmovups (%rax), %zmm0\n    vfmadd231ps %zmm0, %zmm1, %zmm2\n"
+             "    vmovups %zmm2, (%rcx)\n    addq $1, %r8\n    cmpq $8, %r8\n    jne .L1\n    ret\n",
+             "    mov x0, #0\n.L1:\n    ld1 {v0.4s}, [x1]\n    fmla v2.4s, v0.4s, v1.4s\n    st1 {v2.4s}, [x2]\n"
+             "    add x0, x0, #1\n    cmp x0, #8\n    b.ne .L1\n    ret\n"]
+    for text in hand:
+        for an in ("nvidia-volta", "odd-gpu"):
+            entry = {"program": json.loads(serialize_program(single)), "arch": an, "kind": "hand", "text": text}
+            try:
+                fv = L.extract_features(single, text, ref_arch(an), launch)
+                entry["features"] = [[k, v] for k, v in fv.values]
+                entry["score"] = L.score(fv, ref_arch(an))
+            except Exception as e:  # noqa: BLE001
+                entry["error"] = [type(e).__name__, str(e)]
+            cases.append(entry)
+    for text, an in ((xhand[0], "x86-avx2"), (xhand[0], "odd-x86"), (xhand[1], "aarch64-neon")):
+        entry = {"program": json.loads(serialize_program(single)), "arch": an, "kind": "hand", "text": text}
+        try:
+            fv = L.extract_features(single, text, ref_arch(an), launch)
+            entry["features"] = [[k, v] for k, v in fv.values]
+            entry["score"] = L.score(fv, ref_arch(an))
+        except Exception as e:  # noqa: BLE001
+            entry["error"] = [type(e).__name__, str(e)]
+        cases.append(entry)
+    (OUT / "code_analysis.json").write_text(json.dumps(cases, separators=(",", ":")))
+    print(f"code: {len(cases)} (program, text, arch) cases, "
+          f"{sum('error' in c for c in cases)} raise in the reference")
+
+
 def main():
     OUT.mkdir(parents=True, exist_ok=True)
     for name in CUSTOM_ARCHS:  # write the TOMLs before the pool forks (no write races)
         ref_arch(name)
     which = set(sys.argv[1:]) or {"gemm", "conv", "bert", "rank", "trees", "emit", "es", "cli", "tree_rank",
-                                  "resnet", "bertbench"}
+                                  "resnet", "bertbench", "code"}
     if "gemm" in which:
         space_fixture("gemm1024", W.matmul_json(1024), W.gemm_space(1024), 4096, 0,
                       ["x86-avx2", "aarch64-neon", "nvidia-volta"])
@@ -667,6 +810,8 @@ def main():
         cli_fixture()
     if "tree_rank" in which:
         tree_rank_fixture()
+    if "code" in which:
+        code_fixture()
 
 
 if __name__ == "__main__":

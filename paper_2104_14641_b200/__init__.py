@@ -11,6 +11,7 @@ no CPU fallback.  The batched seams the reference CLI calls are
 
 from .arch import (ArchSpec, CostModelError, FeatureVector, GpuSpec, KernelLaunch, load_arch)
 from .backend import evaluate_schedules
+from .code import AsmError, code_features, extract_features
 from .cost import analyze, rank, rank_schedules, rank_topk, score, score_batch
 from .es import EsParams, OptimizeResult, SearchError, ThetaEncoding, optimize, optimize_device
 from .ir import (AccessNode, AffineExpr, LoopNode, LoopProgram, Parallel, ProgramError, Reorder, Schedule,
@@ -19,9 +20,9 @@ from .ir import (AccessNode, AffineExpr, LoopNode, LoopProgram, Parallel, Progra
 __version__ = "0.2.0"
 
 __all__ = [
-    "AccessNode", "AffineExpr", "ArchSpec", "CostModelError", "EsParams", "FeatureVector", "GpuSpec",
+    "AccessNode", "AffineExpr", "ArchSpec", "AsmError", "CostModelError", "EsParams", "FeatureVector", "GpuSpec",
     "KernelLaunch", "LoopNode", "LoopProgram", "OptimizeResult", "Parallel", "ProgramError", "Reorder",
     "Schedule", "SearchError", "TensorDecl", "ThetaEncoding", "Tile", "Unroll", "Vectorize", "analyze",
-    "evaluate_schedules", "load_arch", "optimize", "optimize_device", "parse_program", "rank",
+    "code_features", "evaluate_schedules", "extract_features", "load_arch", "optimize", "optimize_device", "parse_program", "rank",
     "rank_schedules", "rank_topk", "score", "score_batch", "space_axes",
 ]

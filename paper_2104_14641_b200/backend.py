@@ -9,6 +9,9 @@ by replacing those two calls:
     results = backend.evaluate_schedules(program, schedules, arch, launch, jobs=args.jobs, errors=errors)
     result = backend.optimize(program, space, arch, params, jobs=args.jobs, launch=launch)
 
+and ``cmd_analyze --code`` (ls/cli.py:89) calls ``backend.extract_features(program, code, arch,
+launch, diagnostics)``: the user's assembly / PTX parsed on the device (code.py, csrc/code.cu).
+
 Everything else in the reference CLI (report assembly, sorting, printing, exit
 codes) stays as it is.  Both functions accept the reference's own objects
 (LoopProgram, Schedule, ArchSpec, KernelLaunch, EsParams) as well as this
@@ -59,3 +62,11 @@ def optimize(program, space, arch, params, jobs=None, launch=None):
     """Drop-in for es_mod.optimize in cmd_search (ls/cli.py:152): the reference's exact trajectory
     with device-scored generations (es.optimize)."""
     return _optimize(program, space, arch, params, jobs=jobs, launch=launch)
+
+
+def extract_features(program, code, arch, launch=None, diagnostics=None):
+    """Drop-in for cost_mod.extract_features in cmd_analyze (ls/cli.py:89, ls/cost.py:132-152): the
+    text-dependent features from the device parser, the IR-side ones from the scoring path."""
+    from .code import extract_features as _extract
+    return _extract(program, code, arch, launch, diagnostics)
+

@@ -8,7 +8,8 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 # one translation unit per scoring path (k_*.cu) + the host side, compiled in parallel
-SRC = sorted(PKG.glob("csrc/k_*.cu")) + [PKG / "csrc" / "engine.cu", PKG / "csrc" / "blocksched.cpp"]
+SRC = sorted(PKG.glob("csrc/k_*.cu")) + [PKG / "csrc" / "engine.cu", PKG / "csrc" / "code.cu",
+                                         PKG / "csrc" / "blocksched.cpp"]
 OBJ_DIR = PKG.parent / "build" / "obj"
 # every header the translation units include (csrc/*.cuh, *.h) and the public header
 HDR = sorted(PKG.glob("csrc/*.cuh")) + sorted(PKG.glob("csrc/*.h")) + [PKG.parent / "include" / "loopscout_b200.h"]

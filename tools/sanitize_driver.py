@@ -44,4 +44,15 @@ E.topk_to_keys(s, i, keys)
 E.topk_merge_keys(keys, 16)
 torch.cuda.synchronize()
 task.close()
+from paper_2104_14641_b200 import code as K  # noqa: E402
+from paper_2104_14641_b200.ir import parse_program  # noqa: E402
+import json  # noqa: E402
+prog = parse_program(json.dumps({"tensors": [{"name": "A", "dims": [8]}], "body": [
+    {"loop": {"var": "i", "extent": 8, "body": [{"access": {"tensor": "A", "kind": "load", "idx": ["i"]}}]}}]}))
+x86 = ("    movq $0, %r8\n.L1:\n    vmovups (%rax), %zmm0\n    vfmadd231ps %zmm0, %zmm1, %zmm2\n"
+       "    vmovups %zmm2, (%rcx)\n    addq $1, %r8\n    cmpq $8, %r8\n    jne .L1\n    ret\n")
+K.code_features(prog, [x86, "", "    jmp nowhere\n"], load_arch("x86-avx2"))
+K.code_features(prog, ["    mov r1, 0\nb:\n    add r1, r1, 1\n    setp.lt r1, 8\n    bra b\n"],
+                load_arch("nvidia-volta"), KernelLaunch.from_json(W.KERNEL_LAUNCH))
+torch.cuda.synchronize()
 print("sanitize driver done")
