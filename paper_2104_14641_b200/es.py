@@ -19,7 +19,7 @@ import numpy as np
 
 from .engine import EsRun, Task, to_device_records
 from .ir import Schedule, space_axes
-from .pack import SpaceTemplate
+from .pack import PackError, SpaceTemplate
 from .arch import CPU_FEATURES, GPU_FEATURES, FeatureVector
 
 
@@ -107,13 +107,26 @@ class _DeviceObjective:
     def __init__(self, program, space, arch, launch, device):
         import torch
         self.torch = torch
-        self.st = SpaceTemplate(program, space)
-        self.task = Task(self.st.template.desc(arch, launch), device)
+        self.program = program
+        self.arch, self.launch = arch, launch
         self.device = device
         self.names = CPU_FEATURES if arch.family == "cpu" else GPU_FEATURES
-        self.sizes = self.st.sizes
+        try:
+            self.st = SpaceTemplate(program, space)
+        except PackError:  # e.g. reorder choices over different loop sets: score the decoded
+            self.st = None  # schedules as lists (one template per shape, cost.score_batch)
+            self.axes = tuple(space_axes(program, space))
+            self.sizes = np.array([len(ax.choices) for ax in self.axes], np.int64)
+        if self.st is not None:
+            self.task = Task(self.st.template.desc(arch, launch), device)
+            self.sizes = self.st.sizes
         self.cache: dict = {}   # flat point index -> (key, score, features)
         self.by_key: dict = {}  # json key -> (score, features)
+
+    def schedule_of(self, row) -> Schedule:
+        if self.st is not None:
+            return self.st.schedule_of(row)
+        return Schedule(tuple(t for a, i in enumerate(row) for t in self.axes[a].choices[int(i)]))
 
     def flat(self, idx: np.ndarray) -> np.ndarray:
         f = np.zeros(len(idx), np.int64)
@@ -131,15 +144,33 @@ class _DeviceObjective:
         new = [int(u) for u in uniq[is_new]]
         if new:
             rows = idx[first[is_new]]
-            recs = self.st.records_from_indices(rows)
-            d_rec = to_device_records(recs, self.device)
-            self.task.prepare_unroll_for(d_rec)
-            s, f, st = self.task.score(d_rec, features=True)
-            s, f, st = s.cpu().numpy(), f.cpu().numpy(), st.cpu().numpy()
+            if self.st is not None:
+                recs = self.st.records_from_indices(rows)
+                d_rec = to_device_records(recs, self.device)
+                self.task.prepare_unroll_for(d_rec)
+                s, f, st = self.task.score(d_rec, features=True)
+                s, f, st = s.cpu().numpy(), f.cpu().numpy(), st.cpu().numpy()
+            else:
+                from .cost import score_batch
+                res = score_batch(self.program, [self.schedule_of(r) for r in rows], self.arch, self.launch,
+                                  self.device)
+                s, f, st = res.scores, res.features, res.status
+            bad = [j for j in range(len(new)) if st[j]]
+            if bad:  # the reference's message: the first failing member in population order
+                failing = {new[j]: j for j in bad}
+                member = next(m for m, u in enumerate(flat) if int(u) in failing)
+                j = failing[int(flat[member])]
+                sched = self.schedule_of(rows[j])
+                key = json.dumps(sched.to_json())
+                from .ir import failure_message
+                fm = failure_message(self.program, sched)
+                text = fm[1] if fm is not None else f"status {int(st[j])}"
+                inner = f"candidate {key} failed: {text}"  # ls/es.py:153-154
+                if where == "start":
+                    raise SearchError(inner)
+                raise SearchError(f"population candidate {member} failed at {where}: {inner}")  # ls/es.py:186-187
             for j, u in enumerate(new):
-                key = json.dumps(self.st.schedule_of(rows[j]).to_json())
-                if st[j]:
-                    raise SearchError(f"{where}: candidate {key} failed: status {int(st[j])}")
+                key = json.dumps(self.schedule_of(rows[j]).to_json())
                 self.cache[u] = (key, float(s[j]), f[j])
                 self.by_key[key] = (float(s[j]), f[j])
         return np.array([self.cache[int(u)][1] for u in flat])

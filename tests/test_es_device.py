@@ -116,3 +116,26 @@ def test_optimize_device_single_schedule_space(torch):
     res = optimize_device(prog, {"tile": {"i": [4]}}, arch_named("x86-avx2"),
                           EsParams(population=8, iterations=3), launch=launch())
     assert res.evaluations == 1 and res.trace == [res.best_score]
+
+
+def test_optimize_failure_messages_match_reference():
+    """es.optimize (exact trajectory) raises the reference's SearchError text when a population
+    member's schedule fails: 'population candidate {i} failed at iteration {t}: candidate {key}
+    failed: {ProgramError text}' (ls/es.py:153-154, 186-187); successful runs find the same best."""
+    import json
+
+    from golden_util import GOLDEN
+    from paper_2104_14641_b200.arch import load_arch
+    from paper_2104_14641_b200.es import EsParams, SearchError, optimize
+    from paper_2104_14641_b200.ir import parse_program
+    g = json.loads((GOLDEN / "es_fail.json").read_text())
+    prog = parse_program(json.dumps(g["program"]))
+    for c in g["cases"]:
+        params = EsParams(seed=c["seed"], **g["params"])
+        if "error" in c:
+            with pytest.raises(SearchError) as ei:
+                optimize(prog, c["space"], load_arch("x86-avx2"), params, jobs=1)
+            assert [type(ei.value).__name__, str(ei.value)] == c["error"]
+        else:
+            r = optimize(prog, c["space"], load_arch("x86-avx2"), params, jobs=1)
+            assert r.best_score == c["best"] and r.evaluations == c["evaluations"]
