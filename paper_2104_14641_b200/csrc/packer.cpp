@@ -321,8 +321,35 @@ PyObject* pack(PyObject*, PyObject* args) {
   return out;
 }
 
+// call(fn, task, points, point_bytes, n, base_index, k, scores, index, n_valid, stream): the
+// host-buffer points call (ls_score_topk_points_host) through its address -- the thinnest
+// binding (one vectorcall, no ctypes argument conversion), used by Task.score_topk_points_host.
+using HostPointsFn = int (*)(void*, const void*, int32_t, int64_t, int64_t, int32_t, double*, int64_t*, int64_t*,
+                             void*);
+PyObject* call_points_host(PyObject*, PyObject* const* args, Py_ssize_t nargs) {
+  if (nargs != 11) {
+    PyErr_SetString(PyExc_TypeError, "call_points_host takes 11 arguments");
+    return nullptr;
+  }
+  unsigned long long v[11];
+  for (int i = 0; i < 11; ++i) {
+    v[i] = PyLong_AsUnsignedLongLongMask(args[i]);
+    if (PyErr_Occurred()) return nullptr;
+  }
+  const auto fn = reinterpret_cast<HostPointsFn>(v[0]);
+  int rc;
+  Py_BEGIN_ALLOW_THREADS
+  rc = fn(reinterpret_cast<void*>(v[1]), reinterpret_cast<const void*>(v[2]), (int32_t)v[3], (int64_t)v[4],
+          (int64_t)v[5], (int32_t)v[6], reinterpret_cast<double*>(v[7]), reinterpret_cast<int64_t*>(v[8]),
+          reinterpret_cast<int64_t*>(v[9]), reinterpret_cast<void*>(v[10]));
+  Py_END_ALLOW_THREADS
+  return PyLong_FromLong(rc);
+}
+
 PyMethodDef methods[] = {
     {"pack", pack, METH_VARARGS, "pack(schedules, max_extent, shape_out, param_out, perm_out, status_out)"},
+    {"call_points_host", reinterpret_cast<PyCFunction>(reinterpret_cast<void (*)()>(call_points_host)), METH_FASTCALL,
+     "call_points_host(fn, task, points, point_bytes, n, base_index, k, scores, index, n_valid, stream) -> rc"},
     {nullptr, nullptr, 0, nullptr}};
 
 PyModuleDef module = {PyModuleDef_HEAD_INIT, "_packer", "Fast packer of schedule lists into ls_record fields",

@@ -142,6 +142,8 @@ class Task:
         _check(lib().ls_task_create(C.addressof(desc), device, C.byref(h)), "ls_task_create")
         self._h = h
         self._host_points_fn = None
+        self._host_out = None
+        self._host_out_ptrs = None
         self.has_unroll = any(desc.xforms[i].kind == abi.XF_UNROLL for i in range(desc.n_xforms)) or \
             any(desc.nodes[i].kind == abi.NODE_LOOP and desc.nodes[i].unrolled for i in range(desc.n_nodes))
 
@@ -268,11 +270,26 @@ class Task:
         if out is None:
             out = (np.empty(k, np.float64), np.empty(k, np.int64), np.zeros(1, np.int64))
         s, i, nv = out
+        if out is self._host_out:  # the caller's preallocated outputs: their addresses are cached
+            sp, ip, nvp = self._host_out_ptrs
+        else:
+            sp, ip, nvp = s.ctypes.data, i.ctypes.data, nv.ctypes.data
+            self._host_out, self._host_out_ptrs = out, (sp, ip, nvp)
         fn = self._host_points_fn
-        if fn is None:
-            fn = self._host_points_fn = lib().ls_score_topk_points_host
-        rc = fn(self._h, ptr, eb, n, base_index, k, s.ctypes.data, i.ctypes.data, nv.ctypes.data,
-                _stream(_TORCH or _torch(), stream, self.device))
+        if fn is None:  # (native call helper, address of the C entry point)
+            try:
+                from . import _packer  # csrc/packer.cpp (built by build.py)
+                call = getattr(_packer, "call_points_host", None)
+            except ImportError:
+                call = None
+            fn = self._host_points_fn = (call, C.cast(lib().ls_score_topk_points_host, C.c_void_p).value,
+                                         self._h.value)
+        call, addr, h = fn
+        st = _stream(_TORCH or _torch(), stream, self.device)
+        if call is not None:
+            rc = call(addr, h, ptr, eb, n, base_index, k, sp, ip, nvp, st or 0)
+        else:
+            rc = lib().ls_score_topk_points_host(self._h, ptr, eb, n, base_index, k, sp, ip, nvp, st)
         if rc:
             _check(rc, "ls_score_topk_points_host")
         return s, i, int(nv[0])
@@ -280,12 +297,13 @@ class Task:
 
 def _points_shape(p):
     """(count, point_bytes) of a points buffer: 1-D 4/8-byte integers, or uint8 [n, 3]."""
-    if len(p.shape) == 2:
-        if p.shape[1] != 3 or (p.dtype != np.uint8 and str(p.dtype) != "torch.uint8"):
+    shape = p.shape
+    if len(shape) == 2:
+        if shape[1] != 3 or p.dtype not in (np.uint8, getattr(_TORCH, "uint8", None)):
             raise ValueError("2-D points must be packed uint8 [n, 3] (pack.pack_points)")
-        return p.shape[0], 3
+        return shape[0], 3
     eb = p.itemsize if isinstance(p, np.ndarray) else p.element_size()
-    return p.shape[0], eb
+    return shape[0], eb
 
 
 def topk_merge(scores, index, n_lists: int, k_in: int, k_out: int, stream=None):
