@@ -13,4 +13,4 @@ for tool in memcheck racecheck synccheck; do
   timeout 900 compute-sanitizer --tool $tool --print-limit 50 python tools/sanitize_driver.py > gpurun_out/sanitizer_$tool.txt 2>&1
   echo "$tool rc=$?" >> gpurun_out/sanitizer_$tool.txt
 done
-tail -2 gpurun_out/pytest_gpu_r02.txt; tail -2 gpurun_out/sanitizer_*.txt
+tail -n 2 gpurun_out/pytest_gpu_r02.txt
