@@ -13,8 +13,8 @@
 //                     as an open-addressing table keyed by the point; a new
 //                     point is scored by the task's points kernel code; the
 //                     sort key of F = -score (ls/es.py:176)
-//   cub radix sort    (F bits, member index): stable ranks, _shape_fitness's
-//                     argsort(argsort(., stable), stable) (ls/es.py:65-71)
+//   rs_* kernels      stable onesweep radix sort of (F bits, member index): stable ranks,
+//                     _shape_fitness's argsort(argsort(., stable), stable) (ls/es.py:65-71)
 //   es_partial_kernel fixed 1024-position chunks of sum_i w_i eps_i (noise
 //                     regenerated, not stored), fixed-order reductions
 //   es_update_kernel  theta += alpha / (population * sigma) * sum (ls/es.py:91-92),
@@ -37,16 +37,13 @@
 // evaluated lists and the trace the per-generation minimum over ranks (both
 // computed by the caller after the run).
 
-#include <cub/device/device_radix_sort.cuh>
-
-// EsDev, the Philox noise and the kernels: es_dev.cuh (included by every TU)
+// EsDev, the Philox noise, the rank sort and the kernels: es_dev.cuh (included by every TU)
 
 struct ls_es {
   ls_task* task;
   EsDev host;
   EsDev* dev;
-  void* sort_tmp;
-  size_t sort_tmp_bytes;
+  RsBufs rs;  // the rank sort's buffers (es_dev.cuh)
   int chunks, mode;
   int rank, world, cpr;  // shard: rank of world, chunks per rank (the partials' gather slice)
   cudaGraphExec_t graph;
@@ -71,9 +68,16 @@ int es_launch_gen(ls_es* es, int start, cudaStream_t s) {
 // after the F keys of the whole population are present: global stable ranks and this
 // rank's chunk partials
 int es_launch_rank(ls_es* es, cudaStream_t s) {
-  size_t bytes = es->sort_tmp_bytes;
-  CUDA_TRY(cub::DeviceRadixSort::SortPairs(es->sort_tmp, bytes, es->host.sort_in, es->host.sort_out, es->host.idx_in,
-                                           es->host.idx_out, es->host.pop, 0, 64, s));
+  const RsBufs& R = es->rs;
+  CUDA_TRY(cudaMemsetAsync(R.andor, 0xFF, sizeof(unsigned long long), s));
+  CUDA_TRY(cudaMemsetAsync(R.andor + 1, 0, sizeof(unsigned long long), s));
+  CUDA_TRY(cudaMemsetAsync(R.count, 0, sizeof(uint32_t) * 8 * 256, s));
+  CUDA_TRY(cudaMemsetAsync(R.ticket, 0, sizeof(uint32_t) * 8, s));
+  CUDA_TRY(cudaMemsetAsync(R.status, 0, sizeof(uint32_t) * 8 * 256 * (size_t)R.nblk, s));
+  rs_upsweep_kernel<<<std::min(R.nblk, 2 * es->task->num_sms), TPB, 0, s>>>(R);
+  rs_plan_kernel<<<1, 256, 0, s>>>(R);
+  for (int d = 0; d < 8; ++d) rs_pass_kernel<<<R.nblk, TPB, 0, s>>>(R, d);
+  CUDA_TRY(cudaGetLastError());
   if (es->host.c1 > es->host.c0) {
     es_partial_kernel<<<es->host.c1 - es->host.c0, TPB, 0, s>>>(es->dev);
     CUDA_TRY(cudaGetLastError());
@@ -110,7 +114,7 @@ int ls_es_create_shard(ls_task* t, const ls_es_params* p, const double* h_theta0
   ls_es* es = new ls_es();
   es->task = t;
   es->graph = nullptr;
-  es->sort_tmp = nullptr;
+  memset(&es->rs, 0, sizeof(es->rs));
   es->rank = rank;
   es->world = world;
   EsDev& H = es->host;
@@ -174,11 +178,21 @@ int ls_es_create_shard(ls_task* t, const ls_es_params* p, const double* h_theta0
   rc = rc ? rc : alloc((void**)&H.theta_hist, sizeof(double) * (H.iters + 1) * H.dim);
   rc = rc ? rc : alloc((void**)&H.trace, sizeof(double) * H.iters);
   rc = rc ? rc : alloc((void**)&es->dev, sizeof(EsDev));
-  if (rc == LS_E_OK) {
-    size_t bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, bytes, H.sort_in, H.sort_out, H.idx_in, H.idx_out, H.pop, 0, 64);
-    es->sort_tmp_bytes = bytes;
-    rc = alloc(&es->sort_tmp, bytes);
+  if (rc == LS_E_OK) {  // the rank sort: ping-pong buffers, tile histograms, plan, AND / OR
+    RsBufs& R = es->rs;
+    R.n = H.pop;
+    R.nblk = (H.pop + RS_TILE - 1) / RS_TILE;
+    R.key[0] = H.sort_in;
+    R.key[1] = H.sort_out;
+    R.idx[0] = H.idx_in;
+    R.idx[1] = H.idx_out;
+    rc = rc ? rc : alloc((void**)&R.key[2], sizeof(unsigned long long) * H.pop);
+    rc = rc ? rc : alloc((void**)&R.idx[2], sizeof(uint32_t) * H.pop);
+    rc = rc ? rc : alloc((void**)&R.count, sizeof(uint32_t) * 8 * 256);
+    rc = rc ? rc : alloc((void**)&R.status, sizeof(uint32_t) * 8 * 256 * (size_t)R.nblk);
+    rc = rc ? rc : alloc((void**)&R.ticket, sizeof(uint32_t) * 8);
+    rc = rc ? rc : alloc((void**)&R.plan, sizeof(int32_t) * 32);
+    rc = rc ? rc : alloc((void**)&R.andor, sizeof(unsigned long long) * 2);
   }
   if (rc == LS_E_OK) {  // member indices of the gathered keys: the identity (rank slices in rank order)
     std::vector<uint32_t> iota((size_t)H.pop);

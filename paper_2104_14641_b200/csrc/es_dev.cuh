@@ -166,6 +166,181 @@ __global__ void __launch_bounds__(TPB, 2) es_gen_kernel(const DTask* __restrict_
 // sum over fixed chunks of sorted positions of w_j * eps[member_j]; w_j = the
 // centred rank j/(n-1) - 0.5 (rank_normalize) or F itself (ls/es.py:65-71, 90).
 #ifdef LS_MAIN_TU
+// ---- stable LSD radix sort of (F order bits, member) pairs: the ranks of _shape_fitness
+// (argsort(argsort(F, stable), stable), ls/es.py:65-71).  Single-pass-per-digit ("onesweep")
+// form, 8-bit digits:
+//   rs_upsweep_kernel  the global counts of all eight digits in one read (order-independent),
+//                      AND / OR of the keys;
+//   rs_plan_kernel     the digits some keys differ in (the others are skipped), their global
+//                      digit bases, the in -> {tmp, out} chain so the last pass writes `out`;
+//   rs_pass_kernel     per active digit: tiles of RS_TILE keys taken in launch order (ticket),
+//                      stable in-tile ranks (sub-rounds of TPB keys: warp ranks by
+//                      __match_any_sync, prefix over warps), the tile's exclusive prefix per
+//                      digit by decoupled look-back over its predecessors' published counts,
+//                      scatter.  A predecessor tile always belongs to a block already running,
+//                      so the look-back never waits on an unscheduled block.
+// Every launch is fixed (inactive passes exit at once): a generation stays one CUDA graph.
+constexpr int RS_TILE = 2048;          // keys per tile
+constexpr int RS_SUB = RS_TILE / TPB;  // sub-rounds of TPB keys
+constexpr uint32_t RS_AGG = 1u << 30, RS_INC = 2u << 30, RS_MASK = (1u << 30) - 1u;
+struct RsBufs {
+  unsigned long long* key[3];  // in, out, tmp
+  uint32_t* idx[3];
+  uint32_t* count;             // [8][256] global digit counts, then (plan) digit bases
+  uint32_t* status;            // [8][nblk][256] look-back words (flag << 30 | count)
+  uint32_t* ticket;            // [8] tile tickets
+  int32_t* plan;               // [8][4]: active, shift, src, dst
+  unsigned long long* andor;   // [2]
+  int32_t n, nblk;
+};
+
+__global__ void __launch_bounds__(TPB) rs_upsweep_kernel(RsBufs R) {
+  __shared__ uint32_t h[8][256];
+  for (int c = threadIdx.x; c < 8 * 256; c += TPB) (&h[0][0])[c] = 0;
+  __syncthreads();
+  unsigned long long a = ~0ull, o = 0ull;
+  for (int64_t i = blockIdx.x * (int64_t)TPB + threadIdx.x; i < R.n; i += (int64_t)gridDim.x * TPB) {
+    const unsigned long long k = R.key[0][i];
+    a &= k;
+    o |= k;
+#pragma unroll
+    for (int d = 0; d < 8; ++d) atomicAdd(&h[d][(k >> (8 * d)) & 0xFFu], 1u);
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    a &= __shfl_xor_sync(0xffffffffu, a, off);
+    o |= __shfl_xor_sync(0xffffffffu, o, off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAnd(&R.andor[0], a);
+    atomicOr(&R.andor[1], o);
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < 8 * 256; c += TPB)
+    if ((&h[0][0])[c]) atomicAdd(&R.count[c], (&h[0][0])[c]);
+}
+
+__global__ void __launch_bounds__(256) rs_plan_kernel(RsBufs R) {
+  __shared__ int act[8];
+  __shared__ uint32_t sc[256];
+  const int t = threadIdx.x;
+  if (t == 0) {
+    const unsigned long long x = R.andor[0] ^ R.andor[1];
+    int m = 0;
+    for (int d = 0; d < 8; ++d) m += act[d] = ((x >> (8 * d)) & 0xFFull) != 0;
+    if (!m) act[0] = 1, m = 1;  // every key equal: one stable copy in -> out
+    int left = m, src = 0;
+    for (int d = 0; d < 8; ++d) {
+      int32_t* p = R.plan + 4 * d;
+      p[0] = act[d];
+      p[1] = 8 * d;
+      if (!act[d]) continue;
+      const int dst = (--left) % 2 == 0 ? 1 : 2;  // the last active pass writes `out`
+      p[2] = src;
+      p[3] = dst;
+      src = dst;
+    }
+  }
+  __syncthreads();
+  for (int d = 0; d < 8; ++d) {  // digit bases: exclusive scan of each digit's global counts
+    const uint32_t c = R.count[d * 256 + t];
+    sc[t] = c;
+    __syncthreads();
+    for (int off = 1; off < 256; off <<= 1) {
+      const uint32_t v = t >= off ? sc[t - off] : 0u;
+      __syncthreads();
+      sc[t] += v;
+      __syncthreads();
+    }
+    R.count[d * 256 + t] = sc[t] - c;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(TPB) rs_pass_kernel(RsBufs R, int d) {
+  const int32_t* p = R.plan + 4 * d;
+  if (!p[0]) return;
+  __shared__ uint32_t lcount[256];       // the tile's keys per digit so far (stable in-tile ranks)
+  __shared__ uint32_t wcnt[TPB / 32][256];
+  __shared__ uint32_t gbase[256];        // global position of the tile's first key of each digit
+  __shared__ int s_tile;
+  const int sh = p[1];
+  const unsigned long long* ks = R.key[p[2]];
+  const uint32_t* is = R.idx[p[2]];
+  unsigned long long* kd = R.key[p[3]];
+  uint32_t* id = R.idx[p[3]];
+  if (threadIdx.x == 0) s_tile = (int)atomicAdd(&R.ticket[d], 1u);
+  lcount[threadIdx.x] = 0;
+  __syncthreads();
+  const int tile = s_tile;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t t0 = (int64_t)tile * RS_TILE;
+  unsigned long long key[RS_SUB];
+  uint32_t val[RS_SUB], pos[RS_SUB];  // pos: in-tile rank among the digit's keys
+#pragma unroll
+  for (int q = 0; q < RS_SUB; ++q) {
+    for (int c = threadIdx.x; c < (TPB / 32) * 256; c += TPB) (&wcnt[0][0])[c] = 0;
+    __syncthreads();
+    const int64_t i = t0 + q * TPB + threadIdx.x;
+    const bool has = i < R.n;
+    uint32_t dig = 0x100u;
+    key[q] = 0;
+    val[q] = 0;
+    if (has) {
+      key[q] = ks[i];
+      val[q] = is[i];
+      dig = (uint32_t)(key[q] >> sh) & 0xFFu;
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, dig);
+    const int rank = __popc(peers & ((1u << lane) - 1u));
+    if (has && rank == 0) wcnt[w][dig] = __popc(peers);
+    __syncthreads();
+    if (has) {
+      uint32_t off = lcount[dig] + rank;
+      for (int u = 0; u < w; ++u) off += wcnt[u][dig];
+      pos[q] = off;
+    }
+    __syncthreads();
+    uint32_t add = 0;
+    for (int u = 0; u < TPB / 32; ++u) add += wcnt[u][threadIdx.x];
+    lcount[threadIdx.x] += add;
+    __syncthreads();
+  }
+  // decoupled look-back: thread t owns digit t
+  {
+    const int t = threadIdx.x;
+    uint32_t* st = R.status + (size_t)d * R.nblk * 256;
+    const uint32_t mine = lcount[t];
+    volatile uint32_t* me = st + (size_t)tile * 256 + t;
+    if (tile == 0) {
+      *me = RS_INC | mine;
+      gbase[t] = R.count[d * 256 + t];
+    } else {
+      *me = RS_AGG | mine;
+      uint32_t excl = 0;
+      for (int pt = tile - 1; pt >= 0; --pt) {
+        const volatile uint32_t* ps = st + (size_t)pt * 256 + t;
+        uint32_t v;
+        while (((v = *ps) >> 30) == 0u) __nanosleep(32);
+        excl += v & RS_MASK;
+        if ((v >> 30) == 2u) break;  // an inclusive prefix ends the walk
+      }
+      __threadfence();
+      *me = RS_INC | (excl + mine);
+      gbase[t] = R.count[d * 256 + t] + excl;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < RS_SUB; ++q) {
+    const int64_t i = t0 + q * TPB + threadIdx.x;
+    if (i >= R.n) continue;
+    const uint32_t dig = (uint32_t)(key[q] >> sh) & 0xFFu;
+    const uint32_t o = gbase[dig] + pos[q];
+    kd[o] = key[q];
+    id[o] = val[q];
+  }
+}
+
 __global__ void __launch_bounds__(TPB) es_partial_kernel(EsDev* __restrict__ ges) {
   __shared__ double red[TPB];
   EsDev& E = *ges;
