@@ -176,6 +176,18 @@ def cpu_model() -> str:
     return "unknown"
 
 
+def init_dist(torch, dist, local: int):
+    """One process per GPU over NCCL.  LS_BENCH_SHARED_GPU=1 (a test hook for the multi-rank code
+    paths on a one-GPU box) puts every rank on GPU 0 and uses gloo (NCCL refuses two ranks on one
+    device); the exchanged top-k lists are staged through host memory (dist.all_gather_inplace)."""
+    if os.environ.get("LS_BENCH_SHARED_GPU") == "1":
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo")
+    else:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+
+
 # -- clocks -------------------------------------------------------------------------------------
 
 
@@ -265,8 +277,7 @@ def b200_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        init_dist(torch, dist, local)
     else:
         torch.cuda.set_device(0)
     if rank == 0:
@@ -466,8 +477,7 @@ def _dist_setup(torch, dist):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        init_dist(torch, dist, local)
     else:
         torch.cuda.set_device(0)
     if rank == 0:
