@@ -311,9 +311,8 @@ bool plan_space_groups(DTask& T, int32_t* rows) {
   for (int g = 0; g < 8; ++g) T.sd_off[g] = 0, rows[g] = 0;
   if (T.n_tensors > 4) return false;
   int64_t off = 4;  // entries 0..3: the ones row
-  for (int t = 0; t < T.n_tensors; ++t) {
-    int dims[4], nd = 0;
-    uint32_t pmask[4];
+  auto collect = [&](int t, int* dims, uint32_t* pmask) {  // the tensor's dimensions whose count varies
+    int nd = 0;
     for (int rr = 0; rr < T.t_rank[t]; ++rr) {
       const int D = t * 4 + rr;
       bool varies = false;
@@ -324,29 +323,64 @@ bool plan_space_groups(DTask& T, int32_t* rows) {
       pmask[nd] = pm;
       dims[nd++] = D;
     }
-    // choose the split (bit j of `sel`: dimension j goes to group 1) with the fewest entries
+    return nd;
+  };
+  // entries of split `sel` (bit j: dimension j goes to group 1), -1 when a group has > 6 bits
+  auto entries = [&](int nd, const int* dims, const uint32_t* pmask, int sel) -> int64_t {
+    int64_t total = 0;
+    for (int j = 0; j < 2; ++j) {
+      uint32_t pm = 0;
+      int nb = 0, members = 0;
+      for (int q = 0; q < nd; ++q)
+        if (((sel >> q) & 1) == j) pm |= pmask[q], nb += T.dim_nv[dims[q]], ++members;
+      if (!members) continue;
+      if (nb > 6) return -1;
+      int64_t keys = 1;
+      for (int a = 0; a < T.sp_n; ++a)
+        if (T.sp_ax[a].kind == LS_AX_PARAM && ((pm >> T.sp_ax[a].param) & 1u)) keys *= T.sp_ax[a].n;
+      total += keys * sd_row_len(nb);
+      if (total > SD_MAX_ENTRIES) return -1;
+    }
+    return total;
+  };
+  // per tensor: the split with the fewest entries.  (LS_SD_SINGLE=1: then, while the whole table
+  // stays within SD_MAX_ENTRIES, single-group splits -- one random lookup per level for that
+  // tensor, the empty group reading the broadcast ones row; measured slower on the BASELINE
+  // spaces: the larger tables cost more than the lookups they save.)
+  int chosen[4] = {0, 0, 0, 0};
+  int64_t cost[4] = {0, 0, 0, 0}, single_cost[4] = {-1, -1, -1, -1};
+  for (int t = 0; t < T.n_tensors; ++t) {
+    int dims[4];
+    uint32_t pmask[4];
+    const int nd = collect(t, dims, pmask);
     int64_t best = -1;
-    int best_sel = 0;
     for (int sel = 0; sel < (1 << nd); ++sel) {
       if (nd && (sel >> (nd - 1)) & 1) continue;  // symmetric splits: the last dimension stays in group 0
-      int64_t total = 0;
-      bool ok = true;
-      for (int j = 0; j < 2 && ok; ++j) {
-        uint32_t pm = 0;
-        int nb = 0, members = 0;
-        for (int q = 0; q < nd; ++q)
-          if (((sel >> q) & 1) == j) pm |= pmask[q], nb += T.dim_nv[dims[q]], ++members;
-        if (!members) continue;
-        if (nb > 6) ok = false;
-        int64_t keys = 1;
-        for (int a = 0; a < T.sp_n && ok; ++a)
-          if (T.sp_ax[a].kind == LS_AX_PARAM && ((pm >> T.sp_ax[a].param) & 1u)) keys *= T.sp_ax[a].n;
-        total += keys * sd_row_len(nb);
-        if (total > SD_MAX_ENTRIES) ok = false;
-      }
-      if (ok && (best < 0 || total < best)) best = total, best_sel = sel;
+      const int64_t total = entries(nd, dims, pmask, sel);
+      if (total >= 0 && (best < 0 || total < best)) best = total, chosen[t] = sel;
     }
     if (best < 0) return false;
+    cost[t] = best;
+    single_cost[t] = entries(nd, dims, pmask, 0);
+  }
+  {
+    static const bool prefer_single = [] {
+      const char* e = getenv("LS_SD_SINGLE");
+      return e && e[0] == '1';
+    }();
+    int64_t total = 4;
+    for (int t = 0; t < T.n_tensors; ++t) total += cost[t];
+    for (int t = 0; t < T.n_tensors && prefer_single; ++t)
+      if (chosen[t] && single_cost[t] >= 0 && total - cost[t] + single_cost[t] <= SD_MAX_ENTRIES) {
+        total += single_cost[t] - cost[t];
+        chosen[t] = 0;
+      }
+  }
+  for (int t = 0; t < T.n_tensors; ++t) {
+    int dims[4];
+    uint32_t pmask[4];
+    const int nd = collect(t, dims, pmask);
+    const int best_sel = chosen[t];
     for (int j = 0; j < 2; ++j) {
       const int G = 2 * t + j;
       uint32_t pm = 0;
