@@ -198,6 +198,7 @@ struct __align__(16) DTask {
   int32_t sp_pax;                        // the reorder axis (the last one) or -1
   uint8_t sp_tj_new[4], sp_tj_slot[4];   // slots the j-th tile axis writes (inner F, outer ceil(E/F))
   const uint4* sp_tp;                    // [tile points][2]
+  const uint4* sp_crow;                  // per reorder choice: {innermost-first chain lo, hi, status, 0}
   // ---- general trees: unified node ids, accesses 0..tr_na-1 (preorder), loops
   //      tr_na + j for base loop j (preorder; header j = base_slot/ext/step/flags[j]), tile loops after
   int32_t tree, tr_nl, tr_na, tr_root_first;
@@ -1456,6 +1457,7 @@ __device__ __forceinline__ int eval_space_packed(const DTask& T, const int32_t* 
                                                  FastCand& c, double* f, double* score) {
   uint32_t kp[TM];
   uint32_t pch = 0;
+  uint4 crow;
   if (T.sp_tp_ok) {  // tile-point row: one division, two 16-byte loads
     if (x >= T.sp_total) return LS_ST_POINT_RANGE;
     const uint32_t x32 = (uint32_t)x;
@@ -1469,8 +1471,10 @@ __device__ __forceinline__ int eval_space_packed(const DTask& T, const int32_t* 
         tp = x32;
       }
     }
+    // the tile-point row and the reorder choice's chain row, issued together (one latency)
     const uint4 w = __ldg(T.sp_tp + 2 * (size_t)tp);
     const uint4 kw = __ldg(T.sp_tp + 2 * (size_t)tp + 1);
+    crow = __ldg(T.sp_crow + pch);
     if (w.x == 0u) return LS_ST_TILE_RANGE;
     const int nt = T.sp_ntile;
 #pragma unroll
@@ -1516,9 +1520,9 @@ __device__ __forceinline__ int eval_space_packed(const DTask& T, const int32_t* 
     c.E(T.sp_tslot[a]) = (int32_t)((e >> 16) & 0x7FFFFFFFu);
   }
   }
-  const int pst = __ldg(T.sp_pstat + pch);
-  if (pst) return pst;
-  const uint64_t rchain = __ldg(reinterpret_cast<const unsigned long long*>(T.sp_rchain) + pch);
+  if (!T.sp_tp_ok) crow = __ldg(T.sp_crow + pch);
+  if (crow.z) return (int)crow.z;
+  const uint64_t rchain = (uint64_t)crow.x | ((uint64_t)crow.y << 32);
   const int n = T.sp_nchain;
   // offsets relative to the dynamic shared memory base (the tables sit at dyn + task_bytes,
   // DESIGN.md §3.6): a lookup is one mask/shift and one shared load
@@ -2457,7 +2461,8 @@ static __device__ int eval_tree(const DTask& T, const ls_record& r, double* f, d
 // every tile factor 1 (always in range), i.e. what the reorder alone decides.
 #ifdef LS_MAIN_TU
 __global__ void build_pchain_kernel(const DTask* __restrict__ g, int32_t pax, uint64_t* __restrict__ chain,
-                                    int32_t* __restrict__ pst, uint64_t* __restrict__ rchain) {
+                                    int32_t* __restrict__ pst, uint64_t* __restrict__ rchain,
+                                    uint4* __restrict__ crow) {
   extern __shared__ __align__(16) unsigned char dyn[];
   const DTask& T = *g;
   const int pc = blockIdx.x * blockDim.x + threadIdx.x;
@@ -2475,6 +2480,7 @@ __global__ void build_pchain_kernel(const DTask* __restrict__ g, int32_t pax, ui
   uint64_t rc = 0;  // innermost loop first
   for (int q = 0; q < c.n && !st; ++q) rc |= ((c.chain >> (4 * (c.n - 1 - q))) & 15ull) << (4 * q);
   rchain[pc] = rc;
+  crow[pc] = make_uint4((uint32_t)rc, (uint32_t)(rc >> 32), (uint32_t)st, 0u);
 }
 #endif  // LS_MAIN_TU
 

@@ -1441,6 +1441,9 @@ int ls_task_set_space(ls_task* t, const ls_space_desc* sp) {
       int32_t *dst = nullptr, *drows = nullptr, *dovf = nullptr;
       uint32_t* dsd = nullptr;
       uint64_t* drch = nullptr;
+      uint4* dcrow = nullptr;
+      CUDA_TRY(cudaMalloc(&dcrow, sizeof(uint4) * np));
+      t->retired.push_back(dcrow);
       CUDA_TRY(cudaMalloc(&dch, sizeof(uint64_t) * np));
       t->retired.push_back(dch);
       CUDA_TRY(cudaMalloc(&drch, sizeof(uint64_t) * np));
@@ -1456,7 +1459,7 @@ int ls_task_set_space(ls_task* t, const ls_space_desc* sp) {
       CUDA_TRY(cudaMemset(dovf, 0, sizeof(int32_t) * 9));  // overflow flag + per-group maxima
       if (int rc = upload(t)) return rc;
       const size_t sm = sizeof(int32_t) * NSLOT * TPB;
-      build_pchain_kernel<<<(np + TPB - 1) / TPB, TPB, sm>>>(t->d_task, pax, dch, dst, drch);
+      build_pchain_kernel<<<(np + TPB - 1) / TPB, TPB, sm>>>(t->d_task, pax, dch, dst, drch, dcrow);
       CUDA_TRY(cudaGetLastError());
       build_sdt_kernel<<<(t->host.sd_len + 255) / 256, 256>>>(t->d_task, drows, dsd, dovf,
                                                               reinterpret_cast<unsigned int*>(dovf + 1));
@@ -1506,6 +1509,7 @@ int ls_task_set_space(ls_task* t, const ls_space_desc* sp) {
       }
       t->host.sp_chain = dch;
       t->host.sp_rchain = drch;
+      t->host.sp_crow = dcrow;
       std::vector<uint32_t> tprows;
       if (t->host.sp_narrow && plan_tile_points(t->host, ext, tprows)) {
         uint4* dtp = nullptr;
