@@ -219,6 +219,8 @@ struct __align__(16) DTask {
 #define LS_SD_PAD 1
 #endif
 __host__ __device__ inline int sd_row_len(int nb) { return (1 << nb) + LS_SD_PAD; }
+// the tabulated path's dimension-count rows, padded the same way
+__host__ __device__ inline int tab_row_len(int nv) { return (1 << nv) + LS_SD_PAD; }
 
 struct ls_task {
   ls_task_desc desc;
@@ -1096,7 +1098,7 @@ __device__ int eval_fast(const DTask& T, const int32_t* __restrict__ tab, const 
       }
       k = k * T.fk_rad[D][q] + val;
     }
-    kb[D] = 4u * (uint32_t)(T.ftab_off[D] + (k << T.dim_nv[D]));
+    kb[D] = 4u * (uint32_t)(T.ftab_off[D] + k * tab_row_len(T.dim_nv[D]));
   }
   uint64_t mall = 0;
   const char* tb = reinterpret_cast<const char*>(tab);
@@ -2499,8 +2501,13 @@ __global__ void build_tab_kernel(const DTask* __restrict__ g, int32_t* __restric
   }
   const int nv = T.dim_nv[D];
   const int loc = e - T.ftab_off[D];
-  const uint32_t mask = (uint32_t)loc & ((1u << nv) - 1u);
-  int32_t key = loc >> nv;
+  const int rl = tab_row_len(nv);
+  const uint32_t mask = (uint32_t)(loc % rl);
+  int32_t key = loc / rl;
+  if (mask >> nv) {  // the row's padding entry (never read)
+    tab[e] = 0;
+    return;
+  }
   int32_t prm[LS_MAX_PARAMS];
   for (int q = 0; q < LS_MAX_PARAMS; ++q) prm[q] = 1;
   uint32_t flags = 0;

@@ -485,7 +485,7 @@ void plan_tabulated(const ls_task_desc& d, DTask& T, int RM, const std::vector<i
       ++nd;
     }
     if (bm >> 24) return;  // enable bits >= 24 do not fit the key encoding
-    len <<= nv;
+    len *= tab_row_len(nv);  // rows of 2^nv stage masks + padding (bank skew, like the group tables)
     if (off + len > TAB_MAX_ENTRIES) return;
     T.fk_n[D] = (int8_t)nd;
     T.ftab_off[D] = (int32_t)off;

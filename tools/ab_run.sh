@@ -8,7 +8,8 @@ for r in $(seq ${ROUNDS:-3}); do
     cp $so $lib
     timeout 300 python bench.py --no-baseline ${BENCH_ARGS} 2>/dev/null | tail -1 | python -c "
 import sys, json; d = json.loads(sys.stdin.read())
-print('$(basename $so .so)', round(d['value'] / 1e9, 3), round(d['e2e']['value'] / 1e9, 3) if isinstance(d.get('e2e'), dict) else None, round(d['ms_per_step'] * 1e3, 1))"
+rp = d.get('records_path') or {}
+print('$(basename $so .so)', round(d['value'] / 1e9, 3), round(d['e2e']['value'] / 1e9, 3) if isinstance(d.get('e2e'), dict) else None, round(d['ms_per_step'] * 1e3, 1), 'records', round(rp.get('value', 0) / 1e9, 3))"
   done
 done
 cp /tmp/ab_orig.so $lib
