@@ -916,7 +916,6 @@ int topk_buf(int k) { return TOPK_CAP_SMALL && k <= 1024 - TPB ? 1024 : 2048; }
 size_t smem_topk(const DTask& T, int k, int mode) { return smem_score(T, mode) + align16(topk_state_bytes(topk_buf(k))); }
 
 ScoreFn score_fn(const DTask& T, int mode, int pbytes) { return k_score_fn(T, mode, pbytes ? 1 : 0); }
-TopkFn topk_fn(const DTask& T, int mode, int pbytes) { return k_topk_fn(T, mode, pbytes ? 1 : 0); }
 
 // Dynamic shared-memory limit and resident blocks per SM of a kernel on the
 // current device (cached per (device, kernel): the attribute and occupancy

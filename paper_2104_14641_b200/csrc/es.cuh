@@ -69,14 +69,10 @@ int es_launch_gen(ls_es* es, int start, cudaStream_t s) {
 // rank's chunk partials
 int es_launch_rank(ls_es* es, cudaStream_t s) {
   const RsBufs& R = es->rs;
-  CUDA_TRY(cudaMemsetAsync(R.andor, 0xFF, sizeof(unsigned long long), s));
-  CUDA_TRY(cudaMemsetAsync(R.andor + 1, 0, sizeof(unsigned long long), s));
-  CUDA_TRY(cudaMemsetAsync(R.count, 0, sizeof(uint32_t) * 8 * 256, s));
-  CUDA_TRY(cudaMemsetAsync(R.ticket, 0, sizeof(uint32_t) * 8, s));
-  CUDA_TRY(cudaMemsetAsync(R.status, 0, sizeof(uint32_t) * 8 * 256 * (size_t)R.nblk, s));
+  CUDA_TRY(cudaMemsetAsync(R.ctl, 0, RS_CTL_RESET, s));  // status words are epoch-tagged: never cleared
   rs_upsweep_kernel<<<std::min(R.nblk, 2 * es->task->num_sms), TPB, 0, s>>>(R);
   rs_plan_kernel<<<1, 256, 0, s>>>(R);
-  for (int d = 0; d < 8; ++d) rs_pass_kernel<<<R.nblk, TPB, 0, s>>>(R, d);
+  for (int d = 0; d < 8; ++d) rs_pass_kernel<<<R.nblk, RS_TPB, 0, s>>>(R, d);
   CUDA_TRY(cudaGetLastError());
   if (es->host.c1 > es->host.c0) {
     es_partial_kernel<<<es->host.c1 - es->host.c0, TPB, 0, s>>>(es->dev);
@@ -86,7 +82,7 @@ int es_launch_rank(ls_es* es, cudaStream_t s) {
 }
 
 int es_launch_update(ls_es* es, cudaStream_t s) {
-  es_update_kernel<<<1, 32, 0, s>>>(es->dev);
+  es_update_kernel<<<1, ES_UPD_TPB, 0, s>>>(es->dev);
   CUDA_TRY(cudaGetLastError());
   return LS_E_OK;
 }
@@ -177,6 +173,12 @@ int ls_es_create_shard(ls_task* t, const ls_es_params* p, const double* h_theta0
   rc = rc ? rc : alloc((void**)&H.partial, sizeof(double) * (size_t)es->cpr * world * H.dim);
   rc = rc ? rc : alloc((void**)&H.theta_hist, sizeof(double) * (H.iters + 1) * H.dim);
   rc = rc ? rc : alloc((void**)&H.trace, sizeof(double) * H.iters);
+  {  // single rank: es_gen keeps the noise for es_partial (a sharded rank's partials need every
+     // member's noise, so they regenerate it; the values are the same function either way)
+    const size_t nb = sizeof(double) * 2 * (size_t)((H.dim + 1) / 2) * (size_t)H.pop;
+    H.noise = nullptr;
+    if (world == 1 && nb <= ((size_t)1 << 31)) rc = rc ? rc : alloc((void**)&H.noise, nb);
+  }
   rc = rc ? rc : alloc((void**)&es->dev, sizeof(EsDev));
   if (rc == LS_E_OK) {  // the rank sort: ping-pong buffers, tile histograms, plan, AND / OR
     RsBufs& R = es->rs;
@@ -188,11 +190,12 @@ int ls_es_create_shard(ls_task* t, const ls_es_params* p, const double* h_theta0
     R.idx[1] = H.idx_out;
     rc = rc ? rc : alloc((void**)&R.key[2], sizeof(unsigned long long) * H.pop);
     rc = rc ? rc : alloc((void**)&R.idx[2], sizeof(uint32_t) * H.pop);
-    rc = rc ? rc : alloc((void**)&R.count, sizeof(uint32_t) * 8 * 256);
-    rc = rc ? rc : alloc((void**)&R.status, sizeof(uint32_t) * 8 * 256 * (size_t)R.nblk);
-    rc = rc ? rc : alloc((void**)&R.ticket, sizeof(uint32_t) * 8);
+    const size_t st_bytes = sizeof(unsigned long long) * 8 * 256 * (size_t)R.nblk;
+    rc = rc ? rc : alloc((void**)&R.ctl, sizeof(RsCtl));
+    rc = rc ? rc : alloc((void**)&R.status, st_bytes);
     rc = rc ? rc : alloc((void**)&R.plan, sizeof(int32_t) * 32);
-    rc = rc ? rc : alloc((void**)&R.andor, sizeof(unsigned long long) * 2);
+    if (rc == LS_E_OK && (cudaMemset(R.ctl, 0, sizeof(RsCtl)) != cudaSuccess || cudaMemset(R.status, 0, st_bytes) != cudaSuccess))
+      rc = fail(LS_E_CUDA, "ES sort buffer initialisation");
   }
   if (rc == LS_E_OK) {  // member indices of the gathered keys: the identity (rank slices in rank order)
     std::vector<uint32_t> iota((size_t)H.pop);

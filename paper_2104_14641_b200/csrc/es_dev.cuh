@@ -32,6 +32,8 @@ struct EsDev {
   double* partial;                     // [chunks][dim]
   double* theta_hist;                  // [iters + 1][dim]
   double* trace;                       // [iters]
+  double* noise;                       // [pop][dim rounded up to pairs]: the generation's noise kept by
+                                       // es_gen for es_partial (single-rank runs), or null (regenerated)
 };
 
 // ---- Philox4x32-10 (Salmon et al., SC'11) ---------------------------------------
@@ -61,8 +63,10 @@ __device__ __forceinline__ void es_normal_pair(uint64_t seed, int g, uint32_t i,
   const double u1 = (double)(a + 1) * 0x1.0p-53, u2 = (double)b * 0x1.0p-53;
   const double rad = sqrt(-2.0 * log(u1));
   const double ang = 6.283185307179586 * u2;
-  z0 = rad * cos(ang);
-  z1 = rad * sin(ang);
+  double sn, cs;
+  sincos(ang, &sn, &cs);  // one shared argument reduction
+  z0 = rad * cs;
+  z1 = rad * sn;
 }
 
 __device__ __forceinline__ double es_eps(const EsDev& E, int g, uint32_t i, int d) {
@@ -142,7 +146,10 @@ __global__ void __launch_bounds__(TPB, 2) es_gen_kernel(const DTask* __restrict_
     uint64_t x = 0;
     for (int d = 0; d < E.dim; d += 2) {
       double z0 = 0.0, z1 = 0.0;
-      if (!start) es_normal_pair(E.seed, g, (uint32_t)i, d >> 1, z0, z1);
+      if (!start) {
+        es_normal_pair(E.seed, g, (uint32_t)i, d >> 1, z0, z1);
+        if (E.noise) reinterpret_cast<double2*>(E.noise)[(size_t)i * ((E.dim + 1) >> 1) + (d >> 1)] = make_double2(z0, z1);
+      }
       for (int q = d; q < d + 2 && q < E.dim; ++q) {
         const double pt = __dadd_rn(E.theta[q], __dmul_rn(E.sigma, q == d ? z0 : z1));
         const double m = (double)(E.n_ax[q] - 1);
@@ -174,23 +181,43 @@ __global__ void __launch_bounds__(TPB, 2) es_gen_kernel(const DTask* __restrict_
 //   rs_plan_kernel     the digits some keys differ in (the others are skipped), their global
 //                      digit bases, the in -> {tmp, out} chain so the last pass writes `out`;
 //   rs_pass_kernel     per active digit: tiles of RS_TILE keys taken in launch order (ticket),
-//                      stable in-tile ranks (sub-rounds of TPB keys: warp ranks by
-//                      __match_any_sync, prefix over warps), the tile's exclusive prefix per
-//                      digit by decoupled look-back over its predecessors' published counts,
-//                      scatter.  A predecessor tile always belongs to a block already running,
+//                      stable in-tile ranks (each warp ranks its contiguous run of the tile
+//                      by __match_any_sync with warp-private digit counters, then one
+//                      exclusive scan over the warps per digit), the tile's exclusive prefix per
+//                      digit by decoupled look-back over its predecessors' published counts
+//                      (RS_WIN words per round trip), scatter.  A predecessor tile always belongs to a block already running,
 //                      so the look-back never waits on an unscheduled block.
 // Every launch is fixed (inactive passes exit at once): a generation stays one CUDA graph.
-constexpr int RS_TILE = 2048;          // keys per tile
-constexpr int RS_SUB = RS_TILE / TPB;  // sub-rounds of TPB keys
+#ifndef LS_RS_TILE
+#define LS_RS_TILE 8192
+#endif
+#ifndef LS_RS_WIN
+#define LS_RS_WIN 8
+#endif
+constexpr int RS_TILE = LS_RS_TILE;    // keys per tile
+constexpr int RS_WIN = LS_RS_WIN;      // look-back window: predecessor words read per round trip
+#ifndef LS_RS_TPB
+#define LS_RS_TPB 512
+#endif
+constexpr int RS_TPB = LS_RS_TPB;      // pass-kernel threads
+constexpr int RS_SUB = RS_TILE / RS_TPB;  // keys per thread
 constexpr uint32_t RS_AGG = 1u << 30, RS_INC = 2u << 30, RS_MASK = (1u << 30) - 1u;
+// Per-sort control words, one allocation: everything before `epoch` is zeroed by ONE memset
+// per sort; the look-back status words carry the sort's epoch in their high half, so the
+// status array is never cleared (a word from an earlier sort reads as "not yet published").
+struct RsCtl {
+  unsigned long long nand, bor;  // OR of ~key (= ~AND of the keys), OR of the keys
+  uint32_t ticket[8];            // tile tickets per pass
+  uint32_t count[8 * 256];       // global digit counts, then (plan) digit bases
+  uint32_t epoch, pad[3];        // sort counter (plan kernel), never cleared
+};
+constexpr size_t RS_CTL_RESET = offsetof(RsCtl, epoch);
 struct RsBufs {
   unsigned long long* key[3];  // in, out, tmp
   uint32_t* idx[3];
-  uint32_t* count;             // [8][256] global digit counts, then (plan) digit bases
-  uint32_t* status;            // [8][nblk][256] look-back words (flag << 30 | count)
-  uint32_t* ticket;            // [8] tile tickets
+  RsCtl* ctl;
+  unsigned long long* status;  // [8][nblk][256] look-back words (epoch << 32 | flag << 30 | count)
   int32_t* plan;               // [8][4]: active, shift, src, dst
-  unsigned long long* andor;   // [2]
   int32_t n, nblk;
 };
 
@@ -211,21 +238,19 @@ __global__ void __launch_bounds__(TPB) rs_upsweep_kernel(RsBufs R) {
     o |= __shfl_xor_sync(0xffffffffu, o, off);
   }
   if ((threadIdx.x & 31) == 0) {
-    atomicAnd(&R.andor[0], a);
-    atomicOr(&R.andor[1], o);
+    atomicOr(&R.ctl->nand, ~a);
+    atomicOr(&R.ctl->bor, o);
   }
   __syncthreads();
   for (int c = threadIdx.x; c < 8 * 256; c += TPB)
-    if ((&h[0][0])[c]) atomicAdd(&R.count[c], (&h[0][0])[c]);
+    if ((&h[0][0])[c]) atomicAdd(&R.ctl->count[c], (&h[0][0])[c]);
 }
 
 __global__ void __launch_bounds__(256) rs_plan_kernel(RsBufs R) {
-  __shared__ int act[8];
-  __shared__ uint32_t sc[256];
   const int t = threadIdx.x;
   if (t == 0) {
-    const unsigned long long x = R.andor[0] ^ R.andor[1];
-    int m = 0;
+    const unsigned long long x = ~R.ctl->nand ^ R.ctl->bor;  // AND ^ OR: the bits that vary
+    int act[8], m = 0;
     for (int d = 0; d < 8; ++d) m += act[d] = ((x >> (8 * d)) & 0xFFull) != 0;
     if (!m) act[0] = 1, m = 1;  // every key equal: one stable copy in -> out
     int left = m, src = 0;
@@ -239,101 +264,132 @@ __global__ void __launch_bounds__(256) rs_plan_kernel(RsBufs R) {
       p[3] = dst;
       src = dst;
     }
+    R.ctl->epoch += 1u;
   }
-  __syncthreads();
-  for (int d = 0; d < 8; ++d) {  // digit bases: exclusive scan of each digit's global counts
-    const uint32_t c = R.count[d * 256 + t];
-    sc[t] = c;
-    __syncthreads();
-    for (int off = 1; off < 256; off <<= 1) {
-      const uint32_t v = t >= off ? sc[t - off] : 0u;
-      __syncthreads();
-      sc[t] += v;
-      __syncthreads();
-    }
-    R.count[d * 256 + t] = sc[t] - c;
-    __syncthreads();
+  // digit bases: warp d scans digit d's 256 global counts (8 per lane)
+  const int d = t >> 5, lane = t & 31;
+  uint4* row = reinterpret_cast<uint4*>(R.ctl->count + d * 256 + lane * 8);
+  uint4 c0 = row[0], c1 = row[1];
+  const uint32_t v[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+  uint32_t tot = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) tot += v[q];
+  uint32_t inc = tot;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, inc, off);
+    if (lane >= off) inc += u;
   }
+  uint32_t e[8], run = inc - tot;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) e[q] = run, run += v[q];
+  row[0] = make_uint4(e[0], e[1], e[2], e[3]);
+  row[1] = make_uint4(e[4], e[5], e[6], e[7]);
 }
 
-__global__ void __launch_bounds__(TPB) rs_pass_kernel(RsBufs R, int d) {
+__global__ void __launch_bounds__(RS_TPB) rs_pass_kernel(RsBufs R, int d) {
   const int32_t* p = R.plan + 4 * d;
   if (!p[0]) return;
-  __shared__ uint32_t lcount[256];       // the tile's keys per digit so far (stable in-tile ranks)
-  __shared__ uint32_t wcnt[TPB / 32][256];
+  __shared__ uint32_t lcount[256];       // the tile's keys per digit
+  __shared__ uint32_t wcnt[RS_TPB / 32][256];  // per warp: running digit counts, then the warp's digit offsets
   __shared__ uint32_t gbase[256];        // global position of the tile's first key of each digit
   __shared__ int s_tile;
   const int sh = p[1];
-  const unsigned long long* ks = R.key[p[2]];
-  const uint32_t* is = R.idx[p[2]];
-  unsigned long long* kd = R.key[p[3]];
-  uint32_t* id = R.idx[p[3]];
-  if (threadIdx.x == 0) s_tile = (int)atomicAdd(&R.ticket[d], 1u);
-  lcount[threadIdx.x] = 0;
+  const int src = p[2], dst = p[3];  // selects, not a dynamically indexed parameter array (no stack copy)
+  const unsigned long long* ks = src == 0 ? R.key[0] : src == 1 ? R.key[1] : R.key[2];
+  const uint32_t* is = src == 0 ? R.idx[0] : src == 1 ? R.idx[1] : R.idx[2];
+  unsigned long long* kd = dst == 1 ? R.key[1] : R.key[2];
+  uint32_t* id = dst == 1 ? R.idx[1] : R.idx[2];
+  if (threadIdx.x == 0) s_tile = (int)atomicAdd(&R.ctl->ticket[d], 1u);
+  for (int c = threadIdx.x; c < (RS_TPB / 32) * 256; c += RS_TPB) (&wcnt[0][0])[c] = 0;
   __syncthreads();
   const int tile = s_tile;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t t0 = (int64_t)tile * RS_TILE;
+  // warp w owns the tile's positions [w * 32 * RS_SUB, (w + 1) * 32 * RS_SUB): key q of a lane is
+  // position w * 32 * RS_SUB + 32 q + lane (coalesced loads; tile order = warp, then q, then lane)
+  const int64_t t0 = (int64_t)tile * RS_TILE + (int64_t)w * 32 * RS_SUB + lane;
   unsigned long long key[RS_SUB];
-  uint32_t val[RS_SUB], pos[RS_SUB];  // pos: in-tile rank among the digit's keys
+  uint32_t val[RS_SUB], pos[RS_SUB];  // pos: rank among the tile's keys of the same digit
 #pragma unroll
-  for (int q = 0; q < RS_SUB; ++q) {
-    for (int c = threadIdx.x; c < (TPB / 32) * 256; c += TPB) (&wcnt[0][0])[c] = 0;
-    __syncthreads();
-    const int64_t i = t0 + q * TPB + threadIdx.x;
-    const bool has = i < R.n;
-    uint32_t dig = 0x100u;
+  for (int q = 0; q < RS_SUB; ++q) {  // every load of the tile in flight before the ranking
+    const int64_t i = t0 + 32 * q;
     key[q] = 0;
     val[q] = 0;
-    if (has) {
+    if (i < R.n) {
       key[q] = ks[i];
       val[q] = is[i];
-      dig = (uint32_t)(key[q] >> sh) & 0xFFu;
     }
+  }
+  // warp-local stable ranks: no block barrier until the warps' digit counts are complete
+  uint32_t* wc = wcnt[w];
+#pragma unroll
+  for (int q = 0; q < RS_SUB; ++q) {
+    const bool has = t0 + 32 * q < R.n;
+    const uint32_t dig = has ? (uint32_t)(key[q] >> sh) & 0xFFu : 0x100u;
     const unsigned peers = __match_any_sync(0xffffffffu, dig);
     const int rank = __popc(peers & ((1u << lane) - 1u));
-    if (has && rank == 0) wcnt[w][dig] = __popc(peers);
-    __syncthreads();
-    if (has) {
-      uint32_t off = lcount[dig] + rank;
-      for (int u = 0; u < w; ++u) off += wcnt[u][dig];
-      pos[q] = off;
-    }
-    __syncthreads();
-    uint32_t add = 0;
-    for (int u = 0; u < TPB / 32; ++u) add += wcnt[u][threadIdx.x];
-    lcount[threadIdx.x] += add;
-    __syncthreads();
+    if (has) pos[q] = wc[dig] + rank;
+    __syncwarp();
+    if (has && rank == 0) wc[dig] += __popc(peers);
+    __syncwarp();
   }
-  // decoupled look-back: thread t owns digit t
-  {
+  __syncthreads();
+  if (threadIdx.x < 256) {  // per digit: exclusive scan over the warps, the tile's count
+    uint32_t run = 0;
+#pragma unroll
+    for (int u = 0; u < RS_TPB / 32; ++u) {
+      const uint32_t c = wcnt[u][threadIdx.x];
+      wcnt[u][threadIdx.x] = run;
+      run += c;
+    }
+    lcount[threadIdx.x] = run;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < RS_SUB; ++q)
+    if (t0 + 32 * q < R.n) pos[q] += wc[(uint32_t)(key[q] >> sh) & 0xFFu];
+  // decoupled look-back: thread t owns digit t and reads RS_WIN predecessor words per round trip
+  if (threadIdx.x < 256) {
     const int t = threadIdx.x;
-    uint32_t* st = R.status + (size_t)d * R.nblk * 256;
+    unsigned long long* st = R.status + (size_t)d * R.nblk * 256;
+    const unsigned long long ep = (unsigned long long)R.ctl->epoch << 32;
     const uint32_t mine = lcount[t];
-    volatile uint32_t* me = st + (size_t)tile * 256 + t;
+    volatile unsigned long long* me = st + (size_t)tile * 256 + t;
     if (tile == 0) {
-      *me = RS_INC | mine;
-      gbase[t] = R.count[d * 256 + t];
+      *me = ep | RS_INC | mine;
+      gbase[t] = R.ctl->count[d * 256 + t];
     } else {
-      *me = RS_AGG | mine;
+      *me = ep | RS_AGG | mine;
       uint32_t excl = 0;
-      for (int pt = tile - 1; pt >= 0; --pt) {
-        const volatile uint32_t* ps = st + (size_t)pt * 256 + t;
-        uint32_t v;
-        while (((v = *ps) >> 30) == 0u) __nanosleep(32);
-        excl += v & RS_MASK;
-        if ((v >> 30) == 2u) break;  // an inclusive prefix ends the walk
+      int pt = tile - 1;  // tile 0 always publishes an inclusive prefix: the walk ends there at the latest
+      for (;;) {
+        unsigned long long v[RS_WIN];
+#pragma unroll
+        for (int q = 0; q < RS_WIN; ++q)
+          v[q] = pt - q >= 0 ? *(const volatile unsigned long long*)(st + (size_t)(pt - q) * 256 + t) : 0ull;
+        int used = 0;
+        bool done = false;
+#pragma unroll
+        for (int q = 0; q < RS_WIN; ++q) {
+          if (done || used < q) continue;  // stopped at an inclusive prefix or an unpublished word
+          if ((v[q] & ~(unsigned long long)RS_MASK) < (ep | RS_AGG)) continue;
+          excl += (uint32_t)v[q] & RS_MASK;
+          used = q + 1;
+          done = ((uint32_t)v[q] >> 30) == 2u;
+        }
+        if (done) break;
+        pt -= used;
+        if (used < RS_WIN) __nanosleep(32);
       }
       __threadfence();
-      *me = RS_INC | (excl + mine);
-      gbase[t] = R.count[d * 256 + t] + excl;
+      *me = ep | RS_INC | (excl + mine);
+      gbase[t] = R.ctl->count[d * 256 + t] + excl;
     }
   }
   __syncthreads();
 #pragma unroll
   for (int q = 0; q < RS_SUB; ++q) {
-    const int64_t i = t0 + q * TPB + threadIdx.x;
-    if (i >= R.n) continue;
+    if (t0 + 32 * q >= R.n) continue;
     const uint32_t dig = (uint32_t)(key[q] >> sh) & 0xFFu;
     const uint32_t o = gbase[dig] + pos[q];
     kd[o] = key[q];
@@ -342,14 +398,16 @@ __global__ void __launch_bounds__(TPB) rs_pass_kernel(RsBufs R, int d) {
 }
 
 __global__ void __launch_bounds__(TPB) es_partial_kernel(EsDev* __restrict__ ges) {
-  __shared__ double red[TPB];
+  __shared__ double wred[TPB / 32][ES_MAXDIM];
   EsDev& E = *ges;
   const int n = E.pop, dim = E.dim, g = E.gen;
   const bool flat = E.rank_normalize && E.sort_out[0] == E.sort_out[n - 1];  // np.ptp(values) == 0
   const int chunk = E.c0 + blockIdx.x;
   const int j0 = chunk * ES_CHUNK;
-  double acc[ES_MAXDIM];
-  for (int d = 0; d < dim; ++d) acc[d] = 0.0;
+  const int pairs = (dim + 1) >> 1;
+  double acc[ES_MAXDIM];  // unrolled over ES_MAXDIM with dim guards: registers, not a stack array
+#pragma unroll
+  for (int d = 0; d < ES_MAXDIM; ++d) acc[d] = 0.0;
   for (int j = j0 + threadIdx.x; j < min(n, j0 + ES_CHUNK); j += TPB) {
     double w;
     if (E.rank_normalize)
@@ -357,33 +415,63 @@ __global__ void __launch_bounds__(TPB) es_partial_kernel(EsDev* __restrict__ ges
     else
       w = from_order_bits(E.sort_out[j]);
     const uint32_t i = E.idx_out[j];
-    for (int d = 0; d < dim; d += 2) {
+    const double2* kept = E.noise ? reinterpret_cast<const double2*>(E.noise) + (size_t)i * pairs : nullptr;
+#pragma unroll
+    for (int d = 0; d < ES_MAXDIM; d += 2) {
+      if (d >= dim) break;
       double z0, z1;
-      es_normal_pair(E.seed, g, i, d >> 1, z0, z1);
+      if (kept) {
+        const double2 z = kept[d >> 1];
+        z0 = z.x;
+        z1 = z.y;
+      } else {
+        es_normal_pair(E.seed, g, i, d >> 1, z0, z1);
+      }
       acc[d] = __dadd_rn(acc[d], __dmul_rn(w, z0));
       if (d + 1 < dim) acc[d + 1] = __dadd_rn(acc[d + 1], __dmul_rn(w, z1));
     }
   }
-  for (int d = 0; d < dim; ++d) {
-    red[threadIdx.x] = acc[d];
-    __syncthreads();
-    for (int w = TPB / 2; w > 0; w >>= 1) {
-      if (threadIdx.x < w) red[threadIdx.x] = __dadd_rn(red[threadIdx.x], red[threadIdx.x + w]);
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) E.partial[(size_t)chunk * dim + d] = red[0];
-    __syncthreads();
+  // fixed-shape reduction: butterfly within each warp, then the warps in order
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+#pragma unroll
+  for (int d = 0; d < ES_MAXDIM; ++d) {
+    if (d >= dim) break;
+    double v = acc[d];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
+    if (lane == 0) wred[wp][d] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < dim) {
+    double v = wred[0][threadIdx.x];
+#pragma unroll
+    for (int u = 1; u < TPB / 32; ++u) v = __dadd_rn(v, wred[u][threadIdx.x]);
+    E.partial[(size_t)chunk * dim + threadIdx.x] = v;
   }
 }
 
-__global__ void es_update_kernel(EsDev* __restrict__ ges) {
+// One block: the chunk partials are staged through shared memory in coalesced tiles (every
+// load of a tile in flight at once) and thread d adds its column in chunk order.
+constexpr int ES_UPD_TPB = 256, ES_UPD_TILE = 2048;  // doubles per staged tile
+__global__ void __launch_bounds__(ES_UPD_TPB) es_update_kernel(EsDev* __restrict__ ges) {
+  __shared__ double tile[ES_UPD_TILE];
   EsDev& E = *ges;
-  const int chunks = E.chunks;
+  const int chunks = E.chunks, dim = E.dim;
   const int d = threadIdx.x;
   const int g = E.gen;
-  if (d < E.dim) {
-    double sum = 0.0;
-    for (int b = 0; b < chunks; ++b) sum = __dadd_rn(sum, E.partial[(size_t)b * E.dim + d]);
+  const int per = ES_UPD_TILE / dim;  // chunks per tile
+  const double* __restrict__ part = E.partial;
+  double sum = 0.0;
+  for (int b0 = 0; b0 < chunks; b0 += per) {
+    const int nb = min(per, chunks - b0);
+    const double* src = part + (size_t)b0 * dim;
+    for (int q = threadIdx.x; q < nb * dim; q += ES_UPD_TPB) tile[q] = src[q];
+    __syncthreads();
+    if (d < dim)
+      for (int b = 0; b < nb; ++b) sum = __dadd_rn(sum, tile[b * dim + d]);
+    __syncthreads();
+  }
+  if (d < dim) {
     E.theta[d] = __dadd_rn(E.theta[d], __dmul_rn(E.coef, sum));
     E.theta_hist[(size_t)(g + 1) * E.dim + d] = E.theta[d];
   }
