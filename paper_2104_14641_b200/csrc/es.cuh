@@ -54,15 +54,35 @@ namespace {
 
 EsGenFn es_gen_fn(const DTask& T, int mode) { return k_es_gen_fn(T, mode); }
 
+#ifndef LS_ES_PDL
+#define LS_ES_PDL 1
+#endif
+// Programmatic dependent launch: the kernel's blocks are scheduled behind the previous kernel's
+// tail instead of after a full kernel boundary; every ES kernel starts with griddepcontrol.wait
+// (es_pdl_wait), so nothing upstream is read before the previous grid is complete and visible.
+template <typename... P, typename... A>
+int launch_pdl(void (*k)(P...), unsigned grid, unsigned block, size_t smem, cudaStream_t s, A&&... a) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = LS_ES_PDL;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, k, std::forward<A>(a)...));
+  return LS_E_OK;
+}
+
 int es_launch_gen(ls_es* es, int start, cudaStream_t s) {
   const ls_task* t = es->task;
   const EsGenFn fn = es_gen_fn(t->host, es->mode);
   const size_t sm = smem_score(t->host, es->mode);
   const int64_t n = start ? 1 : es->host.hi - es->host.lo;
   BPS_TRY(bps, fn, sm);
-  fn<<<grid_for(t, n, bps), TPB, sm, s>>>(t->d_task, es->dev, start);
-  CUDA_TRY(cudaGetLastError());
-  return LS_E_OK;
+  return launch_pdl(fn, (unsigned)grid_for(t, n, bps), TPB, sm, s, (const DTask*)t->d_task, es->dev, start);
 }
 
 // after the F keys of the whole population are present: global stable ranks and this
@@ -70,21 +90,18 @@ int es_launch_gen(ls_es* es, int start, cudaStream_t s) {
 int es_launch_rank(ls_es* es, cudaStream_t s) {
   const RsBufs& R = es->rs;
   CUDA_TRY(cudaMemsetAsync(R.ctl, 0, RS_CTL_RESET, s));  // status words are epoch-tagged: never cleared
-  rs_upsweep_kernel<<<std::min(R.nblk, 2 * es->task->num_sms), TPB, 0, s>>>(R);
-  rs_plan_kernel<<<1, 256, 0, s>>>(R);
-  for (int d = 0; d < 8; ++d) rs_pass_kernel<<<R.nblk, RS_TPB, 0, s>>>(R, d);
+  rs_upsweep_kernel<<<std::min(R.nblk, 2 * es->task->num_sms), TPB, 0, s>>>(R);  // behind a memset
   CUDA_TRY(cudaGetLastError());
-  if (es->host.c1 > es->host.c0) {
-    es_partial_kernel<<<es->host.c1 - es->host.c0, TPB, 0, s>>>(es->dev);
-    CUDA_TRY(cudaGetLastError());
-  }
+  if (int rc = launch_pdl(rs_plan_kernel, 1, 256, 0, s, R)) return rc;
+  for (int d = 0; d < 8; ++d)
+    if (int rc = launch_pdl(rs_pass_kernel, (unsigned)R.nblk, RS_TPB, 0, s, R, d)) return rc;
+  if (es->host.c1 > es->host.c0)
+    if (int rc = launch_pdl(es_partial_kernel, (unsigned)(es->host.c1 - es->host.c0), TPB, 0, s, es->dev)) return rc;
   return LS_E_OK;
 }
 
 int es_launch_update(ls_es* es, cudaStream_t s) {
-  es_update_kernel<<<1, ES_UPD_TPB, 0, s>>>(es->dev);
-  CUDA_TRY(cudaGetLastError());
-  return LS_E_OK;
+  return launch_pdl(es_update_kernel, 1, ES_UPD_TPB, 0, s, es->dev);
 }
 
 int es_enqueue_generation(ls_es* es, cudaStream_t s) {

@@ -36,6 +36,10 @@ struct EsDev {
                                        // es_gen for es_partial (single-rank runs), or null (regenerated)
 };
 
+// griddepcontrol.wait: a no-op unless the kernel was launched as a programmatic dependent
+// (launch_pdl, es.cuh); then it returns once the previous grid is complete and visible.
+__device__ __forceinline__ void es_pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ---- Philox4x32-10 (Salmon et al., SC'11) ---------------------------------------
 __host__ __device__ inline void philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {
   for (int r = 0; r < 10; ++r) {
@@ -134,11 +138,12 @@ __global__ void __launch_bounds__(TPB, 2) es_gen_kernel(const DTask* __restrict_
                                                        int start) {
   extern __shared__ __align__(16) unsigned char dyn[];
   DTask& T = *reinterpret_cast<DTask*>(dyn);
-  stage_task(T, gtask);
+  stage_task(T, gtask);  // the task's tables are constant over the run: staged before the wait
   unsigned char* p = dyn + T.task_bytes;
   const int32_t* tab = stage_tab<MODE>(p, T);
   p += tab_smem_bytes(MODE, T);
   Evaluator<TM, RM, MODE> ev(T, p, tab);
+  es_pdl_wait();
   EsDev& E = *ges;
   const int g = E.gen;
   const int lo = start ? 0 : E.lo, hi = start ? 1 : E.hi;
@@ -247,6 +252,7 @@ __global__ void __launch_bounds__(TPB) rs_upsweep_kernel(RsBufs R) {
 }
 
 __global__ void __launch_bounds__(256) rs_plan_kernel(RsBufs R) {
+  es_pdl_wait();
   const int t = threadIdx.x;
   if (t == 0) {
     const unsigned long long x = ~R.ctl->nand ^ R.ctl->bor;  // AND ^ OR: the bits that vary
@@ -288,6 +294,7 @@ __global__ void __launch_bounds__(256) rs_plan_kernel(RsBufs R) {
 }
 
 __global__ void __launch_bounds__(RS_TPB) rs_pass_kernel(RsBufs R, int d) {
+  es_pdl_wait();
   const int32_t* p = R.plan + 4 * d;
   if (!p[0]) return;
   __shared__ uint32_t lcount[256];       // the tile's keys per digit
@@ -398,6 +405,7 @@ __global__ void __launch_bounds__(RS_TPB) rs_pass_kernel(RsBufs R, int d) {
 }
 
 __global__ void __launch_bounds__(TPB) es_partial_kernel(EsDev* __restrict__ ges) {
+  es_pdl_wait();
   __shared__ double wred[TPB / 32][ES_MAXDIM];
   EsDev& E = *ges;
   const int n = E.pop, dim = E.dim, g = E.gen;
@@ -454,6 +462,7 @@ __global__ void __launch_bounds__(TPB) es_partial_kernel(EsDev* __restrict__ ges
 // load of a tile in flight at once) and thread d adds its column in chunk order.
 constexpr int ES_UPD_TPB = 256, ES_UPD_TILE = 2048;  // doubles per staged tile
 __global__ void __launch_bounds__(ES_UPD_TPB) es_update_kernel(EsDev* __restrict__ ges) {
+  es_pdl_wait();
   __shared__ double tile[ES_UPD_TILE];
   EsDev& E = *ges;
   const int chunks = E.chunks, dim = E.dim;
