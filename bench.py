@@ -647,7 +647,7 @@ def resnet_es_arm(args):
             "config": {"workload": f"ResNet-50 v1.5 conv/dense task set ({len(tasks)} tasks), "
                                    f"{args.generations}-generation ES per task, population {args.population}, "
                                    f"sigma {args.sigma}, every generation on device (Philox noise, decode, memo, "
-                                   "score, CUB rank sort, update; one CUDA graph per generation)",
+                                   "score, onesweep radix rank sort, update; one CUDA graph per generation)",
                        "config": "BASELINE.json configs[2]", "arch": args.arch,
                        "distinct_schedules_per_step": float(dt.item()), "points_paths": paths,
                        "l2": "flushed between timed steps (256 MiB write)"},

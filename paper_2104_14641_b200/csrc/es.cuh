@@ -2,7 +2,7 @@
 //
 // Included by engine.cu (same translation unit: the scoring kernels' task
 // table, evaluators and point decoding are reused).  One generation of the
-// reference's optimize loop (ls/es.py:130-204) is four launches with no host
+// reference's optimize loop (ls/es.py:130-204) is one memset and 13 launches with no host
 // round trip, captured once into a CUDA graph and replayed `iterations` times:
 //
 //   es_gen_kernel     member i: Gaussian noise from Philox4x32-10 keyed by
@@ -15,8 +15,8 @@
 //                     sort key of F = -score (ls/es.py:176)
 //   rs_* kernels      stable onesweep radix sort of (F bits, member index): stable ranks,
 //                     _shape_fitness's argsort(argsort(., stable), stable) (ls/es.py:65-71)
-//   es_partial_kernel fixed 1024-position chunks of sum_i w_i eps_i (noise
-//                     regenerated, not stored), fixed-order reductions
+//   es_partial_kernel fixed 1024-position chunks of sum_i w_i eps_i (noise kept by
+//                     es_gen on one rank, regenerated on a shard), fixed-order reductions
 //   es_update_kernel  theta += alpha / (population * sigma) * sum (ls/es.py:91-92),
 //                     incumbent trace (ls/es.py:189-190), generation counter
 //
