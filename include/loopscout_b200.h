@@ -432,6 +432,36 @@ int64_t ls_code_scratch_bytes(int64_t text_bytes);
 int ls_code_features(const ls_code_desc* desc, const char* d_texts, const int64_t* h_offsets, int32_t n_texts,
                      void* d_scratch, int64_t scratch_bytes, double* d_features, int32_t* d_status,
                      int64_t* d_err_info, void* stream);
+/* The diagnostics extract_features appends to its `diagnostics` list (ls/cost.py:134-148):
+ * CPU loop_map's unmatched blocks / bound mismatches / unmatched IR loops (ls/asm.py:
+ * 276-293), GPU _loop_trip's failures (ls/ptx.py:112-189), as events of
+ * LS_CODE_DIAG_WORDS int64 each: kind, block index, the block's label (offset, length in
+ * the text; -1 none), three integers, an auxiliary text span (offset, length; -1 none):
+ *   UNMATCHED_BLOCK  block
+ *   BOUND_MISMATCH   block, [has bound, bound, loop index]
+ *   LOOPS_MATCHED    [matched loop count] (the IR loops from there on are unmatched)
+ *   NO_SETP / NON_IMM_BOUND                   loop target block
+ *   NONLINEAR / NOT_DERIVABLE                 target, aux = the induction register
+ *   UNSUPPORTED_CMP                           target, aux = the comparison
+ *   INCONSISTENT     target, [init, delta, bound], aux = the comparison (-1: implicit "ne")
+ * in the reference's order; the host renders the reference's messages (the GPU family's
+ * list is produced twice by the reference: count_ptx, then thread_cycles).  Text i's
+ * events start at event ls_code_diag_offset = sum over j < i of ls_code_diag_cap(len_j);
+ * d_ndiag[i] = events written. */
+#define LS_CODE_DIAG_WORDS 10
+#define LS_CODE_D_UNMATCHED_BLOCK 1
+#define LS_CODE_D_BOUND_MISMATCH 2
+#define LS_CODE_D_LOOPS_MATCHED 3
+#define LS_CODE_D_NO_SETP 10
+#define LS_CODE_D_NON_IMM_BOUND 11
+#define LS_CODE_D_NONLINEAR 12
+#define LS_CODE_D_NOT_DERIVABLE 13
+#define LS_CODE_D_UNSUPPORTED_CMP 14
+#define LS_CODE_D_INCONSISTENT 15
+int64_t ls_code_diag_cap(int64_t text_bytes);
+int ls_code_features_diag(const ls_code_desc* desc, const char* d_texts, const int64_t* h_offsets, int32_t n_texts,
+                          void* d_scratch, int64_t scratch_bytes, double* d_features, int32_t* d_status,
+                          int64_t* d_err_info, int64_t* d_diag, int32_t* d_ndiag, void* stream);
 
 #ifdef __cplusplus
 }

@@ -574,7 +574,8 @@ def tree_rank_fixture(n_per=60, seed=77):
 
 
 def cli_fixture():
-    """Reference CLI outputs (rank --json with failures, search --json --trace) on files under golden/cli."""
+    """Reference CLI outputs (rank --json with failures, search --json --trace, analyze --code with
+    notes) on files under golden/cli."""
     import contextlib
     import io
     from loopscout import cli as ref_cli
@@ -591,6 +592,18 @@ def cli_fixture():
                     "--jobs", "1"] + (["--launch", str(d / "launch.json")] if arch == "nvidia-volta" else [])
             runs.append((f"rank_{pname}_{arch}", argv, None))
     (d / "launch.json").write_text(json.dumps(LAUNCH))
+    # analyze --code (f4): emitted texts and edited ones (changed loop bounds -> notes), text and JSON output
+    mrng = random.Random(5)
+    for pname in ("matmul48", "conv_small", "deep9"):
+        prog = L.parse_program(json.dumps(rc["programs"][pname]))
+        for arch, tgt in (("x86-avx2", "cpu-x86"), ("aarch64-neon", "cpu-aarch64"), ("nvidia-volta", "gpu-ptx")):
+            for kind in ("none", "bound"):
+                cf = d / f"{pname}_{tgt}_{kind}.s"
+                cf.write_text(_mutate(mrng, L.emit_mock_asm(prog, tgt), tgt, kind))
+                for js in ((["--json"], []) if kind == "bound" else (["--json"],)):
+                    argv = ["analyze", str(d / f"{pname}.json"), "--code", str(cf), "--arch", arch, *js] + \
+                        (["--launch", str(d / "launch.json")] if arch == "nvidia-volta" else [])
+                    runs.append((f"analyze_{pname}_{tgt}_{kind}{'_json' if js else ''}", argv, None))
     es_runs = json.loads((OUT / "es_runs.json").read_text())
     for r in es_runs:
         (d / f"es_{r['name']}.json").write_text(json.dumps(r["program"]))
@@ -717,8 +730,10 @@ def code_fixture():
                         entry = {"program": json.loads(serialize_program(q)), "arch": an, "kind": kind,
                                  "text": text}
                         try:
-                            fv = L.extract_features(q, text, arch, launch)
+                            diag = []
+                            fv = L.extract_features(q, text, arch, launch, diag)
                             entry["features"] = [[k, v] for k, v in fv.values]
+                            entry["diagnostics"] = diag
                             entry["score"] = L.score(fv, arch)
                         except Exception as e:  # noqa: BLE001
                             entry["error"] = [type(e).__name__, str(e)]
@@ -738,26 +753,34 @@ def code_fixture():
             "back:\n    add r1, r1, 1\n    setp.lt r1, 8\n    bra back\n", "    ret\n", "", "   // only a comment\n",
             "    mov r1, 0\nback:\n    add r1, r1, 1\n    setp.lt %p1, r1, 8\n    @%p1 bra back\n    ret\n",
             "    mov r1, 0\nL0: add r1, r1, 1\n    setp.ge r1, 8\n    @!%p1 bra L0\n",
-            "    jmp nowhere\n", "@p\n"]
+            "    jmp nowhere\n", "@p\n",
+            "    mov r1, 0\nback:\n    add r1, r1, 1\n    setp.lt r1, r2\n    bra back\n",  # non-immediate bound
+            countdown(10, 1, "lt", 4), countdown(0, 1, "gt", 8, body),  # inconsistent / consistent lt-gt
+            "    mov r1, 0\nback:\n    add r1, r1, 3\n    setp r1, 8\n    bra back\n"]  # implicit "ne"
     xhand = ["    movq $0, %r8\n.L1:\n    vmovups (%rax), %zmm0\n    vfmadd231ps %zmm0, %zmm1, %zmm2\n"
              "    vmovups %zmm2, (%rcx)\n    addq $1, %r8\n    cmpq $8, %r8\n    jne .L1\n    ret\n",
              "    mov x0, #0\n.L1:\n    ld1 {v0.4s}, [x1]\n    fmla v2.4s, v0.4s, v1.4s\n    st1 {v2.4s}, [x2]\n"
-             "    add x0, x0, #1\n    cmp x0, #8\n    b.ne .L1\n    ret\n"]
+             "    add x0, x0, #1\n    cmp x0, #8\n    b.ne .L1\n    ret\n",
+             "    movq $0, %r8\n.L1:\n    addq $1, %r8\n    cmpq %r9, %r8\n    jne .L1\n    ret\n"]  # no bound
     for text in hand:
         for an in ("nvidia-volta", "odd-gpu"):
             entry = {"program": json.loads(serialize_program(single)), "arch": an, "kind": "hand", "text": text}
             try:
-                fv = L.extract_features(single, text, ref_arch(an), launch)
+                diag = []
+                fv = L.extract_features(single, text, ref_arch(an), launch, diag)
                 entry["features"] = [[k, v] for k, v in fv.values]
+                entry["diagnostics"] = diag
                 entry["score"] = L.score(fv, ref_arch(an))
             except Exception as e:  # noqa: BLE001
                 entry["error"] = [type(e).__name__, str(e)]
             cases.append(entry)
-    for text, an in ((xhand[0], "x86-avx2"), (xhand[0], "odd-x86"), (xhand[1], "aarch64-neon")):
+    for text, an in ((xhand[0], "x86-avx2"), (xhand[0], "odd-x86"), (xhand[1], "aarch64-neon"), (xhand[2], "x86-avx2")):
         entry = {"program": json.loads(serialize_program(single)), "arch": an, "kind": "hand", "text": text}
         try:
-            fv = L.extract_features(single, text, ref_arch(an), launch)
+            diag = []
+            fv = L.extract_features(single, text, ref_arch(an), launch, diag)
             entry["features"] = [[k, v] for k, v in fv.values]
+            entry["diagnostics"] = diag
             entry["score"] = L.score(fv, ref_arch(an))
         except Exception as e:  # noqa: BLE001
             entry["error"] = [type(e).__name__, str(e)]

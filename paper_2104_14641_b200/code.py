@@ -24,6 +24,9 @@ from .arch import CPU_FEATURES, GPU_FEATURES, CostModelError, FeatureVector
 MAX_CLASSES = 32
 MAX_LOOPS = 64
 E_EMPTY, E_LABEL, E_VALUE, E_LIMIT = 1, 2, 3, 4
+DIAG_WORDS = 10
+(D_UNMATCHED_BLOCK, D_BOUND_MISMATCH, D_LOOPS_MATCHED, D_NO_SETP, D_NON_IMM_BOUND, D_NONLINEAR, D_NOT_DERIVABLE,
+ D_UNSUPPORTED_CMP, D_INCONSISTENT) = 1, 2, 3, 10, 11, 12, 13, 14, 15
 
 
 class AsmError(ValueError):
@@ -51,6 +54,9 @@ def _lib():
         L.ls_code_scratch_bytes.argtypes = [i64]
         L.ls_code_scratch_bytes.restype = i64
         L.ls_code_features.argtypes = [vp, vp, vp, i32, vp, i64, vp, vp, vp, vp]
+        L.ls_code_features_diag.argtypes = [vp, vp, vp, i32, vp, i64, vp, vp, vp, vp, vp, vp]
+        L.ls_code_diag_cap.argtypes = [i64]
+        L.ls_code_diag_cap.restype = i64
         L._code_bound = True
     return L
 
@@ -61,8 +67,8 @@ def _hash(L, name: str) -> int:
 
 
 def _branching_loops(program):
-    """(extent, step, weight) of the loops that lower to backward branches, in preorder, with
-    weight = the product of its and its branching ancestors' extents (ls/asm.py:245-262)."""
+    """(extent, step, weight, var) of the loops that lower to backward branches, in preorder,
+    with weight = the product of its and its branching ancestors' extents (ls/asm.py:245-262)."""
     from .ir import LoopNode
     out = []
 
@@ -72,7 +78,7 @@ def _branching_loops(program):
         here = prod
         if not n.unrolled and n.vector_width is None:
             here = prod * n.extent
-            out.append((n.extent, n.step, here))
+            out.append((n.extent, n.step, here, n.var))
         for c in n.children:
             walk(c, here)
 
@@ -103,7 +109,7 @@ def code_desc(program, arch) -> CodeDesc:
         if len(loops) > MAX_LOOPS:
             raise CostModelError(f"more than {MAX_LOOPS} branching loops")
         d.n_loops = len(loops)
-        for q, (e, s, w) in enumerate(loops):
+        for q, (e, s, w, _) in enumerate(loops):
             d.loop_extent[q], d.loop_step[q], d.loop_weight[q] = e, s, w
     else:
         d.issue_width = 1
@@ -127,9 +133,39 @@ def _ir_features(program, arch, launch, device):
     return res.features[0]
 
 
-def code_features(program, codes, arch, launch=None, device: int = 0) -> list:
+def _render(ev, blob: bytes, loops) -> list:
+    """The reference's diagnostic strings for one text's events (ls/asm.py:276-293,
+    ls/ptx.py:112-189)."""
+    out = []
+    for kind, blk, lo, ll, a, b, c, ao, al, _ in (tuple(int(x) for x in e) for e in ev):
+        where = blob[lo:lo + ll].decode() if lo >= 0 and ll > 0 else str(blk)  # block.label or block.index
+        aux = blob[ao:ao + al].decode() if ao >= 0 else "ne"
+        if kind == D_UNMATCHED_BLOCK:
+            out.append(f"unmatched loop block {where}")
+        elif kind == D_BOUND_MISMATCH:
+            ext, _, _, var = loops[c]
+            out.append(f"block {where} bound {b if a else None} does not match loop {var!r} extent {ext}")
+        elif kind == D_LOOPS_MATCHED:
+            out += [f"IR loop {lp[3]!r} not matched to any block" for lp in loops[a:]]
+        elif kind == D_NO_SETP:
+            out.append(f"loop at {where}: no setp/bra idiom")
+        elif kind == D_NON_IMM_BOUND:
+            out.append(f"loop at {where}: non-immediate bound")
+        elif kind == D_NONLINEAR:
+            out.append(f"loop at {where}: non-linear induction register {aux}")
+        elif kind == D_NOT_DERIVABLE:
+            out.append(f"loop at {where}: induction register {aux} not derivable")
+        elif kind == D_UNSUPPORTED_CMP:
+            out.append(f"loop at {where}: unsupported comparison {aux!r}")
+        elif kind == D_INCONSISTENT:
+            out.append(f"loop at {where}: inconsistent bounds (init {a}, delta {b}, {aux} {c})")
+    return out
+
+
+def code_features(program, codes, arch, launch=None, device: int = 0, diagnostics: list | None = None) -> list:
     """extract_features for every text in `codes` (one device launch): a FeatureVector or the
-    exception the reference raises, per text."""
+    exception the reference raises, per text.  `diagnostics`, if given, receives one list per
+    text: the notes the reference's extract_features appends for it."""
     import torch
 
     if arch.family == "gpu" and launch is None:  # ls/cost.py:137-138, before any parsing
@@ -148,22 +184,36 @@ def code_features(program, codes, arch, launch=None, device: int = 0) -> list:
     dev = torch.device("cuda", device)
     d_text = torch.from_numpy(np.frombuffer(b"".join(blobs) or b"\0", np.uint8).copy()).to(dev)
     scratch = sum(int(L.ls_code_scratch_bytes(int(offs[i + 1] - offs[i]))) + 256 for i in range(n)) + \
-        C.sizeof(CodeDesc) + 16 * (n + 2) + 4096
+        C.sizeof(CodeDesc) + 24 * (n + 2) + 4096
+    dstart = np.zeros(n + 1, np.int64)
+    for i in range(n):
+        dstart[i + 1] = dstart[i] + int(L.ls_code_diag_cap(int(offs[i + 1] - offs[i])))
     d_scratch = torch.empty(scratch, dtype=torch.uint8, device=dev)
     d_feat = torch.zeros((n, 4), dtype=torch.float64, device=dev)
     d_status = torch.zeros(n, dtype=torch.int32, device=dev)
     d_err = torch.zeros((n, 3), dtype=torch.int64, device=dev)
+    d_diag = torch.zeros((int(dstart[n]), DIAG_WORDS), dtype=torch.int64, device=dev)
+    d_ndiag = torch.zeros(n, dtype=torch.int32, device=dev)
     from .engine import _check
     with torch.cuda.device(device):
-        _check(L.ls_code_features(C.addressof(desc), d_text.data_ptr(), offs.ctypes.data, n, d_scratch.data_ptr(),
-                                  scratch, d_feat.data_ptr(), d_status.data_ptr(), d_err.data_ptr(),
-                                  torch.cuda.current_stream(dev).cuda_stream), "ls_code_features")
+        _check(L.ls_code_features_diag(C.addressof(desc), d_text.data_ptr(), offs.ctypes.data, n, d_scratch.data_ptr(),
+                                       scratch, d_feat.data_ptr(), d_status.data_ptr(), d_err.data_ptr(),
+                                       d_diag.data_ptr(), d_ndiag.data_ptr(),
+                                       torch.cuda.current_stream(dev).cuda_stream), "ls_code_features_diag")
         torch.cuda.synchronize(dev)
     feats, status, err = d_feat.cpu().numpy(), d_status.cpu().numpy(), d_err.cpu().numpy()
+    diag, ndiag = d_diag.cpu().numpy(), d_ndiag.cpu().numpy()
+    loops = _branching_loops(program) if arch.family == "cpu" else []
     ir = None
     out = []
     for i in range(n):
         st = int(status[i])
+        if diagnostics is not None:
+            k = int(ndiag[i]) if st == 0 else 0
+            if k > dstart[i + 1] - dstart[i]:
+                raise CostModelError("diagnostic events beyond the device buffer")
+            notes = _render(diag[dstart[i]:dstart[i] + k], blobs[i], loops)
+            diagnostics.append(notes + notes if arch.family == "gpu" else notes)  # count_ptx, thread_cycles
         if st == E_EMPTY:
             out.append(AsmError("empty assembly input"))
             continue
@@ -196,9 +246,12 @@ def code_features(program, codes, arch, launch=None, device: int = 0) -> list:
 
 
 def extract_features(program, code: str, arch, launch=None, diagnostics=None, device: int = 0) -> FeatureVector:
-    """Drop-in for ls/cost.py:132-152 (diagnostics are accepted and left empty: the device
-    parser does not produce the reference's free-text notes)."""
-    r = code_features(program, [code], arch, launch, device)[0]
+    """Drop-in for ls/cost.py:132-152: the features, and the reference's notes appended to
+    `diagnostics` (loop_map's unmatched blocks / loops, _loop_trip's failures)."""
+    notes: list = []
+    r = code_features(program, [code], arch, launch, device, notes)[0]
+    if diagnostics is not None and not isinstance(r, Exception):
+        diagnostics.extend(notes[0])
     if isinstance(r, Exception):
         raise r
     return r

@@ -330,7 +330,9 @@ __global__ void __launch_bounds__(CT_TPB) code_kernel(const unsigned char* __res
                                                       unsigned char* __restrict__ scratch,
                                                       const int64_t* __restrict__ scratch_off,
                                                       double* __restrict__ feats, int32_t* __restrict__ status,
-                                                      int64_t* __restrict__ err_info) {
+                                                      int64_t* __restrict__ err_info, int64_t* __restrict__ diag,
+                                                      const int64_t* __restrict__ diag_off,
+                                                      int32_t* __restrict__ ndiag) {
   const int t = blockIdx.x;
   if (t >= n_texts) return;
   const ls_code_desc& D = *gd;
@@ -338,6 +340,23 @@ __global__ void __launch_bounds__(CT_TPB) code_kernel(const unsigned char* __res
   const Str text{texts + a0, (int)(a1 - a0)};
   const int64_t cap = text.n + 2;
   Scratch S = carve(scratch + scratch_off[t], cap);
+  // diagnostics (thread 0 only): events in the reference's order, rendered by the host
+  int32_t n_note = 0;
+  int64_t* my_diag = diag ? diag + diag_off[t] * LS_CODE_DIAG_WORDS : nullptr;
+  auto note = [&](int kind, int blk, int64_t a, int64_t b, int64_t c, int64_t aux_off, int64_t aux_len) {
+    if (my_diag && n_note < cap) {  // cap = ls_code_diag_cap(text bytes) >= blocks, back edges + 1
+      int64_t* e = my_diag + (size_t)n_note * LS_CODE_DIAG_WORDS;
+      int64_t lo = -1, ll = 0;
+      if (blk >= 0 && S.blk[blk].label >= 0) {
+        const LineRec& r = S.rec[S.blk[blk].label];
+        lo = r.lab_off;
+        ll = r.lab_len;
+      }
+      e[0] = kind, e[1] = blk, e[2] = lo, e[3] = ll, e[4] = a, e[5] = b, e[6] = c, e[7] = aux_off, e[8] = aux_len;
+      e[9] = 0;
+    }
+    ++n_note;
+  };
   __shared__ int s_cnt[CT_TPB + 1];
   __shared__ int s_err, s_nlines, s_ninstr, s_nblk, s_nedge;
   if (threadIdx.x == 0) s_err = 0;
@@ -499,7 +518,10 @@ __global__ void __launch_bounds__(CT_TPB) code_kernel(const unsigned char* __res
         for (int e = 0; e < nedge && !is_t; ++e)
           is_t = S.edge[e].kind && S.edge[e].dst == b && S.edge[e].dst <= S.edge[e].src;
         if (!is_t) continue;
-        if (matched >= D.n_loops) continue;  // unmatched loop block (diagnostic only)
+        if (matched >= D.n_loops) {
+          note(LS_CODE_D_UNMATCHED_BLOCK, b, 0, 0, 0, -1, 0);
+          continue;
+        }
         // loop_bound_immediate: the first back edge's source block with a cmp/setp immediate
         bool have = false;
         int64_t bound = 0;
@@ -541,8 +563,11 @@ __global__ void __launch_bounds__(CT_TPB) code_kernel(const unsigned char* __res
             }
           }
           ++matched;
+        } else {
+          note(LS_CODE_D_BOUND_MISMATCH, b, have, bound, matched, -1, 0);
         }
       }
+      note(LS_CODE_D_LOOPS_MATCHED, -1, matched, 0, 0, -1, 0);
       F[0] = nfma;
       F[1] = nvl;
       F[2] = nvs;
@@ -754,6 +779,7 @@ __global__ void __launch_bounds__(CT_TPB) code_kernel(const unsigned char* __res
         if (S.blk[b].ni) total = __dadd_rn(total, (double)((int64_t)S.weight_i[S.blk[b].i0] * S.weight[b]));
       F[3] = total;
       status[t] = 0;
+      if (ndiag) ndiag[t] = n_note;
     }
     return;
   }
@@ -800,8 +826,12 @@ __global__ void __launch_bounds__(CT_TPB) code_kernel(const unsigned char* __res
               break;
             }
           Str reg = strip(op_of(text, sp, sp.nops >= 3 ? 1 : 0));
+          // the comparison's span in the text; -1: the implicit "ne" of a setp without a suffix
+          const int64_t reg_off = reg.p - text.p, op_off = op.p >= text.p && op.p <= text.p + text.n ? op.p - text.p : -1;
           int64_t bound;
-          if (parse_int(strip(op_of(text, sp, sp.nops >= 3 ? 2 : 1)), bound)) {
+          if (!parse_int(strip(op_of(text, sp, sp.nops >= 3 ? 2 : 1)), bound)) {
+            note(LS_CODE_D_NON_IMM_BOUND, E.dst, 0, 0, 0, -1, 0);
+          } else {
             bool have_init = false, nonlinear = false;
             int64_t init = 0, delta = 0;
             for (int q = 0; q < ninstr; ++q) {  // every instruction, block order == raw order
@@ -821,8 +851,13 @@ __global__ void __launch_bounds__(CT_TPB) code_kernel(const unsigned char* __res
                 }
               }
             }
-            if (!nonlinear && have_init && delta != 0) {
+            if (nonlinear) {
+              note(LS_CODE_D_NONLINEAR, E.dst, 0, 0, 0, reg_off, reg.n);
+            } else if (!have_init || delta == 0) {
+              note(LS_CODE_D_NOT_DERIVABLE, E.dst, 0, 0, 0, reg_off, reg.n);
+            } else {
               const double span = (double)(bound - init), dl = (double)delta;
+              bool known = true;
               if (seq(op, Str{reinterpret_cast<const unsigned char*>("lt"), 2}) ||
                   seq(op, Str{reinterpret_cast<const unsigned char*>("gt"), 2})) {
                 trip = (int64_t)ceil(span / dl);
@@ -832,10 +867,18 @@ __global__ void __launch_bounds__(CT_TPB) code_kernel(const unsigned char* __res
               } else if (seq(op, Str{reinterpret_cast<const unsigned char*>("ne"), 2})) {
                 const double q = span / dl;
                 trip = q == floor(q) ? (int64_t)q : -1;
+              } else {
+                known = false;
+                note(LS_CODE_D_UNSUPPORTED_CMP, E.dst, 0, 0, 0, op_off, op.n);
               }
-              if (trip <= 0) trip = -1;
+              if (trip <= 0) {
+                trip = -1;
+                if (known) note(LS_CODE_D_INCONSISTENT, E.dst, init, delta, bound, op_off, op.n);
+              }
             }
           }
+        } else {
+          note(LS_CODE_D_NO_SETP, E.dst, 0, 0, 0, -1, 0);
         }
         lst[nl] = start_line;
         lend[nl] = end_line;
@@ -870,6 +913,7 @@ __global__ void __launch_bounds__(CT_TPB) code_kernel(const unsigned char* __res
     F[2] = nld;
     F[3] = nst;
     status[t] = ovf ? LS_CODE_E_LIMIT : 0;
+    if (ndiag) ndiag[t] = n_note;
   }
 }
 
@@ -888,9 +932,19 @@ uint64_t ls_code_hash(const char* s, int32_t n) {  // the class / cost table key
 
 int64_t ls_code_scratch_bytes(int64_t text_bytes) { return (int64_t)scratch_bytes(text_bytes + 2); }
 
+int64_t ls_code_diag_cap(int64_t text_bytes) { return text_bytes + 2; }
+
 int ls_code_features(const ls_code_desc* desc, const char* d_texts, const int64_t* h_offsets, int32_t n_texts,
                      void* d_scratch, int64_t scratch_bytes_total, double* d_features, int32_t* d_status,
                      int64_t* d_err_info, void* stream) {
+  return ls_code_features_diag(desc, d_texts, h_offsets, n_texts, d_scratch, scratch_bytes_total, d_features, d_status,
+                               d_err_info, nullptr, nullptr, stream);
+}
+
+int ls_code_features_diag(const ls_code_desc* desc, const char* d_texts, const int64_t* h_offsets, int32_t n_texts,
+                          void* d_scratch, int64_t scratch_bytes_total, double* d_features, int32_t* d_status,
+                          int64_t* d_err_info, int64_t* d_diag, int32_t* d_ndiag, void* stream) {
+  if ((d_diag == nullptr) != (d_ndiag == nullptr)) return LS_E_ARG;
   if (!desc || n_texts < 0 || (n_texts && (!d_texts || !h_offsets || !d_features || !d_status || !d_err_info)))
     return LS_E_ARG;
   if (desc->n_classes > LS_CODE_MAX_CLASSES || desc->n_costs > LS_CODE_MAX_CLASSES || desc->n_loops > LS_CODE_MAX_LOOPS ||
@@ -901,14 +955,17 @@ int ls_code_features(const ls_code_desc* desc, const char* d_texts, const int64_
   // per-text scratch offsets (host) + the descriptor and offsets on the device
   std::string buf;
   int64_t need = 0;
-  std::vector<int64_t> soff((size_t)n_texts);
+  std::vector<int64_t> soff((size_t)n_texts * 2);  // scratch offsets, then diagnostic event offsets
+  int64_t ev = 0;
   for (int i = 0; i < n_texts; ++i) {
     const int64_t len = h_offsets[i + 1] - h_offsets[i];
     if (len < 0 || len > (1 << 26)) return LS_E_ARG;
     soff[i] = need;
     need += ((int64_t)scratch_bytes(len + 2) + 255) & ~(int64_t)255;
+    soff[n_texts + i] = ev;
+    ev += ls_code_diag_cap(len);
   }
-  const size_t meta = sizeof(ls_code_desc) + sizeof(int64_t) * (size_t)(n_texts + 1) + sizeof(int64_t) * n_texts;
+  const size_t meta = sizeof(ls_code_desc) + sizeof(int64_t) * (size_t)(n_texts + 1) + sizeof(int64_t) * 2 * n_texts;
   if (!d_scratch || scratch_bytes_total < need + (int64_t)meta + 256) return LS_E_ARG;
   unsigned char* sc = reinterpret_cast<unsigned char*>(d_scratch);
   unsigned char* md = sc + need;
@@ -919,12 +976,12 @@ int ls_code_features(const ls_code_desc* desc, const char* d_texts, const int64_
   std::vector<unsigned char> hm(meta);
   memcpy(hm.data(), desc, sizeof(ls_code_desc));
   memcpy(hm.data() + sizeof(ls_code_desc), h_offsets, sizeof(int64_t) * (n_texts + 1));
-  memcpy(hm.data() + sizeof(ls_code_desc) + sizeof(int64_t) * (n_texts + 1), soff.data(), sizeof(int64_t) * n_texts);
+  memcpy(hm.data() + sizeof(ls_code_desc) + sizeof(int64_t) * (n_texts + 1), soff.data(), sizeof(int64_t) * 2 * n_texts);
   cudaError_t e = cudaMemcpyAsync(md, hm.data(), meta, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // hm is a temporary
   if (e != cudaSuccess) return g_code_err = cudaGetErrorString(e), LS_E_CUDA;
   code_kernel<<<n_texts, CT_TPB, 0, s>>>(reinterpret_cast<const unsigned char*>(d_texts), doffs, n_texts, dd, sc, dsoff,
-                                         d_features, d_status, d_err_info);
+                                         d_features, d_status, d_err_info, d_diag, dsoff + n_texts, d_ndiag);
   e = cudaGetLastError();
   if (e != cudaSuccess) return g_code_err = cudaGetErrorString(e), LS_E_CUDA;
   return LS_E_OK;

@@ -38,3 +38,6 @@ def test_cli_user_errors(tmp_path):
     (tmp_path / "s.json").write_text("[]")
     assert cli.main(["rank", str(CLI / "matmul48.json"), str(tmp_path / "s.json"), "--arch", "x86-avx2"]) == 1
     assert cli.main(["rank", str(CLI / "matmul48.json"), str(CLI / "matmul48_scheds.json"), "--arch", "nope"]) == 1
+    # analyze: the mock emitter is not part of the backend; a missing --code file is a user error
+    assert cli.main(["analyze", str(CLI / "matmul48.json"), "--arch", "x86-avx2"]) == 1
+    assert cli.main(["analyze", str(CLI / "matmul48.json"), "--code", str(tmp_path / "no.s"), "--arch", "x86-avx2"]) == 1

@@ -1,5 +1,5 @@
 """f4: external code-text analysis on the device (csrc/code.cu) against the reference's own
-extract_features(program, code, arch, launch) on emitted texts, user-style edits of them and the
+extract_features(program, code, arch, launch, diagnostics) on emitted texts, user-style edits of them and the
 reference tests' hand-written texts (tests/golden/code_analysis.json, oracle/gen_golden.py)."""
 
 import json
@@ -24,13 +24,14 @@ def test_code_features_match_reference():
     groups = defaultdict(list)
     for i, c in enumerate(cases):
         groups[(json.dumps(c["program"], sort_keys=True), c["arch"])].append(i)
-    bad = []
-    checked = 0
+    bad, diag_bad = [], []
+    checked = n_notes = 0
     for (pj, an), idx in groups.items():
         prog = parse_program(pj)
         arch = arch_named(an)
-        res = K.code_features(prog, [cases[i]["text"] for i in idx], arch, launch())
-        for i, r in zip(idx, res):
+        notes: list = []
+        res = K.code_features(prog, [cases[i]["text"] for i in idx], arch, launch(), diagnostics=notes)
+        for i, r, nt in zip(idx, res, notes):
             c = cases[i]
             checked += 1
             if "error" in c:
@@ -44,8 +45,13 @@ def test_code_features_match_reference():
             got = [(k, v) for k, v in r.values]
             if got != want or score(r, arch) != c["score"]:
                 bad.append((i, c["kind"], an, got, want))
+            if nt != c["diagnostics"]:  # the notes extract_features appends, in order
+                bad.append((i, c["kind"], an, "diagnostics", nt[:4], c["diagnostics"][:4]))
+                diag_bad.append(i)
+            n_notes += len(nt)
     assert checked == len(cases)
-    assert not bad, (len(bad), bad[:5])
+    assert not bad, (len(bad), len(diag_bad), bad[:5])
+    assert n_notes > 1000  # the fixture exercises every kind of note
 
 
 def test_extract_features_drop_in_errors():
@@ -62,3 +68,7 @@ def test_extract_features_drop_in_errors():
     fv = K.extract_features(prog, "    mov r1, 0\nb:\n    add r1, r1, 1\n    setp.lt r1, 8\n    bra b\n",
                             arch_named("nvidia-volta"), launch())
     assert dict(fv.values)["workload_per_thread"] > 0
+    notes = ["kept"]
+    K.extract_features(prog, "    mov r1, 1\nb:\n    mul r1, r1, 2\n    setp.lt r1, 64\n    bra b\n",
+                       arch_named("nvidia-volta"), launch(), notes)
+    assert notes == ["kept"] + ["loop at b: non-linear induction register r1"] * 2  # count_ptx, thread_cycles
