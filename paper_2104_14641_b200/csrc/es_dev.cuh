@@ -157,8 +157,10 @@ __global__ void __launch_bounds__(TPB, 2) es_gen_kernel(const DTask* __restrict_
       }
       for (int q = d; q < d + 2 && q < E.dim; ++q) {
         const double pt = __dadd_rn(E.theta[q], __dmul_rn(E.sigma, q == d ? z0 : z1));
-        const double m = (double)(E.n_ax[q] - 1);
-        const double c = fmin(fmax(rint(pt), 0.0), m);  // np.clip(round(x), 0, n - 1)
+        // np.clip(round(x), 0, n - 1): round-half-even conversion, then an integer clamp (NaN
+        // converts to INT64_MIN and clamps to 0, +-inf saturate: the same as fmin/fmax on rint)
+        const long long r = __double2ll_rn(pt);
+        const long long c = r < 0 ? 0 : (r > (long long)E.n_ax[q] - 1 ? (long long)E.n_ax[q] - 1 : r);
         x = x * E.n_ax[q] + (uint64_t)c;
       }
     }

@@ -31,7 +31,7 @@ for n, k in [(1 << 14, 8), (1 << 14, 64), (3000, 4), (1 << 18, 64)]:  # bound K2
         task.score_topk(dr, k)
         task.score(dr)
     torch.cuda.synchronize()
-run = E.EsRun(task, 0.05, 2.0, 4096, 3, 7)
+run = E.EsRun(task, 0.05, 2.0, 40960, 3, 7)  # 5 sort tiles: the look-back walks
 run.run()
 run.result(st.dim)
 run.evaluated()
@@ -51,8 +51,11 @@ prog = parse_program(json.dumps({"tensors": [{"name": "A", "dims": [8]}], "body"
     {"loop": {"var": "i", "extent": 8, "body": [{"access": {"tensor": "A", "kind": "load", "idx": ["i"]}}]}}]}))
 x86 = ("    movq $0, %r8\n.L1:\n    vmovups (%rax), %zmm0\n    vfmadd231ps %zmm0, %zmm1, %zmm2\n"
        "    vmovups %zmm2, (%rcx)\n    addq $1, %r8\n    cmpq $8, %r8\n    jne .L1\n    ret\n")
-K.code_features(prog, [x86, "", "    jmp nowhere\n"], load_arch("x86-avx2"))
-K.code_features(prog, ["    mov r1, 0\nb:\n    add r1, r1, 1\n    setp.lt r1, 8\n    bra b\n"],
-                load_arch("nvidia-volta"), KernelLaunch.from_json(W.KERNEL_LAUNCH))
+notes: list = []
+K.code_features(prog, [x86, "", "    jmp nowhere\n", x86.replace("$8", "$9")], load_arch("x86-avx2"), diagnostics=notes)
+K.code_features(prog, ["    mov r1, 0\nb:\n    add r1, r1, 1\n    setp.lt r1, 8\n    bra b\n",
+                       "    mov r1, 1\nb:\n    mul r1, r1, 2\n    setp.lt r1, 64\n    bra b\n"],
+                load_arch("nvidia-volta"), KernelLaunch.from_json(W.KERNEL_LAUNCH), diagnostics=notes)
+assert any(notes), notes
 torch.cuda.synchronize()
 print("sanitize driver done")
