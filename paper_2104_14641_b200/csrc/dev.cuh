@@ -3658,16 +3658,18 @@ __global__ void __launch_bounds__(TPB, min_blocks(TM, RM, MODE)) score_topk_kern
   if (s_ticket != (unsigned)(gsize - 1)) return;
   __threadfence();
   int kept = merge_into(S, block_out + (int64_t)g * TK_GROUP * k, (int64_t)gsize * k, k, false);
-  write_keys(S, kept, k, group_out + (int64_t)g * k);
   trace_mark(g_trace, 4);
-  // ---- level 2: last group merger writes the final list
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_ticket = atomicAdd(&tickets[ngroups], 1u);
-  __syncthreads();
-  if (s_ticket != (unsigned)(ngroups - 1)) return;
-  __threadfence();
-  kept = merge_into(S, group_out, (int64_t)ngroups * k, k, false);
+  if (ngroups > 1) {  // one group (grid <= TK_GROUP): its merger already holds the final k
+    write_keys(S, kept, k, group_out + (int64_t)g * k);
+    // ---- level 2: last group merger writes the final list
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_ticket = atomicAdd(&tickets[ngroups], 1u);
+    __syncthreads();
+    if (s_ticket != (unsigned)(ngroups - 1)) return;
+    __threadfence();
+    kept = merge_into(S, group_out, (int64_t)ngroups * k, k, false);
+  }
   write_sorted(S, kept, k, out_s, out_i);
   if (threadIdx.x == 0) {  // the count out; every counter back to zero for the next launch
     const unsigned long long v = atomicExch(wvalid, 0ull);
