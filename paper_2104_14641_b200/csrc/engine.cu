@@ -6,6 +6,7 @@
 #include "dev.cuh"
 
 #include <dlfcn.h>
+#include <chrono>
 #include <nvtx3/nvToolsExt.h>
 
 // NVTX range over every public scoring / merge / ES entry point (header-only NVTX3: no cost
@@ -1648,10 +1649,19 @@ static int score_topk_mapped(ls_task* t, const void* d_alias, int pbytes, int64_
   }
   // cudaMallocHost memory is mapped at the same address under unified addressing (every 64-bit
   // platform CUDA supports): the kernel writes the results straight into the block
+  static const bool host_trace = getenv("LS_HOST_TRACE") != nullptr;  // host-side phase times (profiling aid)
+  const auto h0 = std::chrono::steady_clock::now();
   const int rc = topk_device(t, d_alias, pbytes, n, base_index, k, nullptr, nullptr, nullptr, s, S.p, S.p,
                              pbytes != 0);
   if (rc != LS_E_OK) return rc;
+  const auto h1 = std::chrono::steady_clock::now();
   CUDA_TRY(cudaStreamSynchronize(s));
+  if (host_trace) {
+    const auto h2 = std::chrono::steady_clock::now();
+    fprintf(stderr, "LS_HOST_TRACE enqueue %.1f us, synchronize %.1f us\n",
+            std::chrono::duration<double, std::micro>(h1 - h0).count(),
+            std::chrono::duration<double, std::micro>(h2 - h1).count());
+  }
   unsigned long long hv = 0;
   memcpy(&hv, S.p, 8);
   memcpy(h_top_scores, S.p + 16, sizeof(double) * k);

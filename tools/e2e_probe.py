@@ -47,6 +47,20 @@ for _ in range(20):
     L.ls_score_topk_points_host(*args)
     ts.append(time.perf_counter() - t0)
 print("raw C-ABI host call (3B) wall us median", round(1e6 * float(np.median(ts)), 1))
+# GPU-side span of the raw host call (events around it on the legacy stream) vs its wall time
+ts, gs = [], []
+for _ in range(30):
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record(torch.cuda.default_stream())
+    t0 = time.perf_counter()
+    L.ls_score_topk_points_host(*args)
+    t1 = time.perf_counter()
+    b.record(torch.cuda.default_stream())
+    torch.cuda.synchronize()
+    ts.append(t1 - t0)
+    gs.append(a.elapsed_time(b) * 1e-3)
+print("raw call wall us", round(1e6 * float(np.median(ts)), 1), "| GPU span event->event us", round(1e6 * float(np.median(gs)), 1))
 os.environ["LS_TRACE"] = "1"
 task.score_topk_points(dev, 64)
 task.score_topk_points_host(pin, 64, out=hout)

@@ -19,10 +19,11 @@ task = Task(st.template.desc(load_arch("x86-avx2"), KernelLaunch.from_json(W.KER
 task.set_space(st.space_desc())
 print("points path", task.points_path)
 n = int(os.environ.get("N", "4096"))
+K = int(os.environ.get("K", "64"))
 d = torch.from_numpy(st.points_from_indices(W.distinct_indices(st.sizes, n, 1024)).view(np.int32)).cuda()
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for _ in range(5):
-    task.score_topk_points(d, 64)
+    task.score_topk_points(d, K)
 for fl in (True, False):
     ts = []
     for _ in range(20):
@@ -30,14 +31,14 @@ for fl in (True, False):
             flush.fill_(1)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        task.score_topk_points(d, 64)
+        task.score_topk_points(d, K)
         b.record()
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b) * 1e3)
     print("flushed" if fl else "warm", "us median", round(float(np.median(ts)), 1))
 os.environ["LS_TRACE"] = "1"
 flush.fill_(1)
-task.score_topk_points(d, 64)
+task.score_topk_points(d, K)
 torch.cuda.synchronize()
-task.score_topk_points(d, 64)
+task.score_topk_points(d, K)
 torch.cuda.synchronize()
