@@ -2924,15 +2924,34 @@ static __device__ int topk_select(TopkState& S, int k) {
       mi |= 0xFFull << sh;
     }
     rank = S.sel_rank;
-    const bool done = S.sel_count == 1;
+    const int left = S.sel_count;
     __syncthreads();
-    if (done) break;
+    if (left == 1) break;
+    if (left <= 32) {  // few keys share the selected digits (ties): rank them in one warp
+      Key* const few = reinterpret_cast<Key*>(S.hist);  // the histogram is free: 1 KB = 64 keys
+      if (threadIdx.x == 0) S.cnt2 = 0;
+      __syncthreads();
+      for (int j = threadIdx.x; j < c; j += blockDim.x) {
+        const Key x = B[j];
+        if ((x.s & ms) == ps && ((unsigned long long)x.i & mi) == pi) few[atomicAdd(&S.cnt2, 1)] = x;
+      }
+      __syncthreads();
+      if (threadIdx.x < left) {  // keys are unique: exactly one has rank - 1 smaller ones
+        const Key x = few[threadIdx.x];
+        int r = 0;
+        for (int j = 0; j < left; ++j) r += kless(few[j], x) ? 1 : 0;
+        if (r == rank - 1) S.thr = x;
+      }
+      break;
+    }
   }
-  // the k-th key is the only one matching the selected digits
-  for (int j = threadIdx.x; j < c; j += blockDim.x) {
-    const Key x = B[j];
-    if ((x.s & ms) == ps && ((unsigned long long)x.i & mi) == pi) S.thr = x;
-  }
+  // the k-th key: the only one matching the selected digits (or ranked among the few above)
+  if (S.sel_count == 1)
+    for (int j = threadIdx.x; j < c; j += blockDim.x) {
+      const Key x = B[j];
+      if ((x.s & ms) == ps && ((unsigned long long)x.i & mi) == pi) S.thr = x;
+    }
+  __syncthreads();
   if (threadIdx.x == 0) S.cnt2 = 0;
   __syncthreads();
   const Key thr = S.thr;
