@@ -231,6 +231,11 @@ int ls_task_points_path(const ls_task* task);
  * (candidates needing an unprepared product report LS_ST_UNROLL_TABLE). */
 int ls_task_prepare_unroll(ls_task* task, const int64_t* u_values, int32_t n);
 
+/* The cache model's inexact-footprint flag per record (NodeCost.inexact of CacheModel.run, set
+ * where ls/cache.py:198-202 records "inexact footprint for tensor ... at loop ..."): 0 exact,
+ * 1 some visited footprint interval lost exactness, 255 the record fails apply_schedule.
+ * d_flags[n] on the device; stream-ordered.  Perfect chains (LS_E_UNSUPPORTED on a tree task). */
+int ls_inexact_footprints(ls_task* t, const ls_record* d_records, int64_t n, uint8_t* d_flags, void* stream);
 /* Distinct innermost-unroll products U needed by the structurally supported
  * records (device pass), sorted; feed them to ls_task_prepare_unroll before
  * scoring.  Only needed when the template or program marks loops `unroll`.

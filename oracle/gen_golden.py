@@ -790,12 +790,51 @@ def code_fixture():
           f"{sum('error' in c for c in cases)} raise in the reference")
 
 
+def inexact_fixture():
+    """The cache model's inexact-footprint flag (CacheModel.run -> NodeCost.inexact, set where
+    ls/cache.py:198-202 records its diagnostic) of the reference on every rank-fixture schedule
+    and on 160 schedules of each ResNet-50 task space (None: apply_schedule raises)."""
+    from loopscout import cache as ref_cache
+    from loopscout.ir import serialize_program
+    from paper_2104_14641_b200.pack import SpaceTemplate
+    rc = json.loads((OUT / "rank_cases.json").read_text())
+    programs, cases = {}, []
+
+    def flags(prog, scheds):
+        out = []
+        for s in scheds:
+            try:
+                q = L.apply_schedule(prog, L.Schedule.from_json(s))
+            except Exception:  # noqa: BLE001
+                out.append(None)
+                continue
+            out.append(bool(ref_cache.analyze(q, ref_cache.CacheSpec(4096)).node_costs["<root>"].inexact))
+        return out
+    for case in rc["cases"]:
+        name = case["program"]
+        programs[name] = rc["programs"][name]
+        prog = L.parse_program(json.dumps(programs[name]))
+        cases.append({"program": name, "schedules": case["schedules"], "inexact": flags(prog, case["schedules"])})
+    rng = np.random.default_rng(8)
+    for name, spec, space in W.resnet50_tasks():
+        prog = L.parse_program(json.dumps(spec))
+        st = SpaceTemplate(W.program(spec), space)
+        idx = np.stack([rng.integers(0, n, 160) for n in st.sizes], axis=1)
+        scheds = [st.schedule_of(row).to_json() for row in idx]
+        programs[f"resnet_{name}"] = json.loads(serialize_program(prog))
+        cases.append({"program": f"resnet_{name}", "schedules": scheds, "inexact": flags(prog, scheds)})
+    (OUT / "inexact.json").write_text(json.dumps({"programs": programs, "cases": cases}, separators=(",", ":")))
+    n = sum(len(c["inexact"]) for c in cases)
+    t = sum(sum(1 for f in c["inexact"] if f) for c in cases)
+    print(f"inexact: {n} schedules, {t} inexact in the reference")
+
+
 def main():
     OUT.mkdir(parents=True, exist_ok=True)
     for name in CUSTOM_ARCHS:  # write the TOMLs before the pool forks (no write races)
         ref_arch(name)
     which = set(sys.argv[1:]) or {"gemm", "conv", "bert", "rank", "trees", "emit", "es", "cli", "tree_rank",
-                                  "resnet", "bertbench", "code"}
+                                  "resnet", "bertbench", "code", "inexact"}
     if "gemm" in which:
         space_fixture("gemm1024", W.matmul_json(1024), W.gemm_space(1024), 4096, 0,
                       ["x86-avx2", "aarch64-neon", "nvidia-volta"])
@@ -835,6 +874,8 @@ def main():
         tree_rank_fixture()
     if "code" in which:
         code_fixture()
+    if "inexact" in which:
+        inexact_fixture()
 
 
 if __name__ == "__main__":

@@ -122,6 +122,27 @@ def score_batch(program, schedules, arch, launch=None, device: int = 0, features
     return BatchResult(scores, feats, status, names, messages)
 
 
+def inexact_footprints(program, schedules, arch, launch=None, device: int = 0) -> np.ndarray:
+    """Per schedule, the cache model's inexact-footprint flag of the scheduled program --
+    `analyze(apply_schedule(program, s), cache).node_costs["<root>"].inexact` (ls/cache.py:
+    198-202, 228-231) -- computed on the device: 1 inexact, 0 exact, -1 the schedule fails
+    apply_schedule (or its shape is outside the device class)."""
+    import torch
+
+    out = np.full(len(schedules), -1, np.int8)
+    for g in pack_schedules(program, schedules):
+        if g.template is None:
+            continue
+        task = _TASKS.get(g.template, arch, launch, device)
+        d_rec = to_device_records(g.records, device)
+        f = task.inexact_footprints(d_rec)
+        torch.cuda.synchronize(device)
+        f = f.cpu().numpy().astype(np.int16)
+        f = np.where((f == 255) | (g.host_status != 0), -1, f)
+        out[g.index] = f
+    return out
+
+
 def rank_schedules(program, schedules, arch, launch=None, device: int = 0):
     """cmd_rank's core: [(index, score, FeatureVector)] ascending by (score, index) + errors."""
     res = score_batch(program, schedules, arch, launch, device)

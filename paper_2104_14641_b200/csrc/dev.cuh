@@ -3788,6 +3788,43 @@ __global__ void __launch_bounds__(TPB) collect_unroll_kernel(const DTask* __rest
 }
 #endif  // LS_MAIN_TU
 
+// The cache model's inexact-footprint flag per record (CacheModel.run -> NodeCost.inexact; the
+// diagnostic of ls/cache.py:198-202): some tensor_footprint the walk evaluates has a dimension
+// whose strided-interval sums / unions (_si_sum / _si_union, ls/cache.py:47-77) lost exactness.
+// A dimension's interval changes only where the walk passes one of its variables, so the visited
+// intervals are the one with nothing expanded (the innermost loop's single set) and the one
+// after each of its variables (that loop's full set, held until the next): the same folds as the
+// generic walk's step (a).  out: 0 exact, 1 inexact, 255 the record fails apply_schedule.
+#ifdef LS_MAIN_TU
+__global__ void __launch_bounds__(TPB) inexact_kernel(const DTask* __restrict__ gtask, const ls_record* __restrict__ recs,
+                                                      int64_t n, uint8_t* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  DTask& T = *reinterpret_cast<DTask*>(dyn);
+  stage_task(T, gtask);
+  Cand c = carve(dyn + T.task_bytes, T);
+  for (int64_t i = (int64_t)blockIdx.x * TPB + threadIdx.x; i < n; i += (int64_t)gridDim.x * TPB) {
+    const ls_record r = load_record(recs, i);
+    if (apply_transforms(T, r, c)) {
+      out[i] = 255;
+      continue;
+    }
+    bool inexact = false;
+    for (int t = 0; t < T.n_tensors && !inexact; ++t)
+      for (int rr = 0; rr < T.t_rank[t] && !inexact; ++rr) {
+        const int D = t * T.layout_rm + rr;
+        for (int j = -1; j < (int)T.dim_nv[D] && !inexact; ++j) {  // j = -1: nothing expanded
+          const int thr = j < 0 ? (int)NOSLOT : (int)c.P(T.dim_var[D][j]);
+          if (j >= 0 && thr == NOSLOT) continue;
+          SI u = expr_range(T, T.expr[T.t_uacc[t][0]][rr], c, thr);
+          for (int a = 1; a < T.t_nu[t]; ++a) u = si_union(u, expr_range(T, T.expr[T.t_uacc[t][a]][rr], c, thr));
+          inexact = !u.exact;
+        }
+      }
+    out[i] = inexact ? 1 : 0;
+  }
+}
+#endif  // LS_MAIN_TU
+
 // ---------------------------------------------------------------------------
 // host: task construction
 // ---------------------------------------------------------------------------

@@ -1083,6 +1083,20 @@ int ls_task_prepare_unroll(ls_task* t, const int64_t* u, int32_t n) {
   return add_unroll(t, u, n);
 }
 
+int ls_inexact_footprints(ls_task* t, const ls_record* d_records, int64_t n, uint8_t* d_flags, void* stream) {
+  LS_NVTX("ls_inexact_footprints");
+  if (!t || n < 0 || (n && (!d_records || !d_flags))) return fail(LS_E_ARG, "bad argument");
+  if (t->host.tree) return fail(LS_E_UNSUPPORTED, "inexact-footprint flags cover perfect chains (not general trees)");
+  if (!n) return LS_E_OK;
+  CUDA_TRY(cudaSetDevice(t->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t sm = smem_score(t->host, 0);
+  BPS_TRY(bps, inexact_kernel, sm);
+  inexact_kernel<<<grid_for(t, n, bps), TPB, sm, s>>>(t->d_task, d_records, n, d_flags);
+  CUDA_TRY(cudaGetLastError());
+  return LS_E_OK;
+}
+
 int ls_collect_unroll(ls_task* t, const ls_record* d_records, int64_t n, int64_t* h_values, int32_t cap,
                       int32_t* h_count, void* stream) {
   LS_NVTX("ls_collect_unroll");

@@ -40,6 +40,7 @@ def lib():
     L.ls_task_num_features.argtypes = [vp]
     L.ls_task_prepare_unroll.argtypes = [vp, vp, i32]
     L.ls_collect_unroll.argtypes = [vp, vp, i64, vp, i32, vp, vp]
+    L.ls_inexact_footprints.argtypes = [vp, vp, i64, vp, vp]
     L.ls_score.argtypes = [vp, vp, i64, vp, vp, vp, vp]
     L.ls_score_topk.argtypes = [vp, vp, i64, i64, i32, vp, vp, vp, vp]
     L.ls_topk_merge.argtypes = [vp, vp, i32, i32, i32, vp, vp, vp]
@@ -175,6 +176,17 @@ class Task:
     def points_path(self) -> int:
         """Path of the points calls (LS_PATH_GENERIC / LS_PATH_TABULATED / LS_PATH_SPACE)."""
         return lib().ls_task_points_path(self._h)
+
+    def inexact_footprints(self, d_records, stream=None):
+        """Per record: 1 when the cache model's footprint intervals lose exactness (NodeCost.inexact,
+        ls/cache.py:198-202), 0 exact, 255 the record fails apply_schedule (uint8 device tensor)."""
+        torch = _torch()
+        n = int(d_records.shape[0])
+        out = torch.empty(n, dtype=torch.uint8, device=f"cuda:{self.device}")
+        with torch.cuda.device(self.device):
+            _check(lib().ls_inexact_footprints(self._h, _dptr(d_records), n, _dptr(out), _stream(torch, stream)),
+                   "ls_inexact_footprints")
+        return out
 
     # -- unroll table ---------------------------------------------------------------
     def prepare_unroll_for(self, d_records, stream=None):
