@@ -231,11 +231,15 @@ int ls_task_points_path(const ls_task* task);
  * (candidates needing an unprepared product report LS_ST_UNROLL_TABLE). */
 int ls_task_prepare_unroll(ls_task* task, const int64_t* u_values, int32_t n);
 
-/* The cache model's inexact-footprint flag per record (NodeCost.inexact of CacheModel.run, set
- * where ls/cache.py:198-202 records "inexact footprint for tensor ... at loop ..."): 0 exact,
- * 1 some visited footprint interval lost exactness, 255 the record fails apply_schedule.
- * d_flags[n] on the device; stream-ordered.  Perfect chains (LS_E_UNSUPPORTED on a tree task). */
-int ls_inexact_footprints(ls_task* t, const ls_record* d_records, int64_t n, uint8_t* d_flags, void* stream);
+/* The cache model's inexact-footprint flag per record (NodeCost.inexact of CacheModel.run) and
+ * the (loop, tensor) pairs of its diagnostic "inexact footprint for tensor T at loop L"
+ * (ls/cache.py:198-202): d_flags[n] 0 exact, 1 inexact, 255 the record fails apply_schedule;
+ * d_masks[2n] (optional) bit 8 * chain position + tensor index (position 0 = outermost loop;
+ * the notes run innermost first, tensors in first-access order); d_chains[16n] (optional) the
+ * loop slot (template variable id) at each chain position, 0xFF past the chain.  Device
+ * arrays; stream-ordered.  Perfect chains (LS_E_UNSUPPORTED on a tree task). */
+int ls_inexact_footprints(ls_task* t, const ls_record* d_records, int64_t n, uint8_t* d_flags,
+                          unsigned long long* d_masks, uint8_t* d_chains, void* stream);
 /* Distinct innermost-unroll products U needed by the structurally supported
  * records (device pass), sorted; feed them to ls_task_prepare_unroll before
  * scoring.  Only needed when the template or program marks loops `unroll`.

@@ -791,9 +791,9 @@ def code_fixture():
 
 
 def inexact_fixture():
-    """The cache model's inexact-footprint flag (CacheModel.run -> NodeCost.inexact, set where
-    ls/cache.py:198-202 records its diagnostic) of the reference on every rank-fixture schedule
-    and on 160 schedules of each ResNet-50 task space (None: apply_schedule raises)."""
+    """The cache model's inexact-footprint flag and notes (CacheModel.run -> NodeCost.inexact and
+    CacheModel.diagnostics, ls/cache.py:198-202) of the reference on every rank-fixture schedule
+    and on 160 schedules of each ResNet-50 task space ([flag, notes]; None: apply_schedule raises)."""
     from loopscout import cache as ref_cache
     from loopscout.ir import serialize_program
     from paper_2104_14641_b200.pack import SpaceTemplate
@@ -808,7 +808,8 @@ def inexact_fixture():
             except Exception:  # noqa: BLE001
                 out.append(None)
                 continue
-            out.append(bool(ref_cache.analyze(q, ref_cache.CacheSpec(4096)).node_costs["<root>"].inexact))
+            model = ref_cache.analyze(q, ref_cache.CacheSpec(4096))
+            out.append([bool(model.node_costs["<root>"].inexact), list(model.diagnostics)])
         return out
     for case in rc["cases"]:
         name = case["program"]
@@ -825,7 +826,7 @@ def inexact_fixture():
         cases.append({"program": f"resnet_{name}", "schedules": scheds, "inexact": flags(prog, scheds)})
     (OUT / "inexact.json").write_text(json.dumps({"programs": programs, "cases": cases}, separators=(",", ":")))
     n = sum(len(c["inexact"]) for c in cases)
-    t = sum(sum(1 for f in c["inexact"] if f) for c in cases)
+    t = sum(sum(1 for f in c["inexact"] if f and f[0]) for c in cases)
     print(f"inexact: {n} schedules, {t} inexact in the reference")
 
 

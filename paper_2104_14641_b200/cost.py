@@ -122,24 +122,56 @@ def score_batch(program, schedules, arch, launch=None, device: int = 0, features
     return BatchResult(scores, feats, status, names, messages)
 
 
-def inexact_footprints(program, schedules, arch, launch=None, device: int = 0) -> np.ndarray:
+def _access_order(program) -> list:
+    """Tensor names in first-access order (the order CacheModel merges tensor states)."""
+    order, stack = [], list(reversed(program.body))
+    while stack:
+        nd = stack.pop()
+        if hasattr(nd, "children"):
+            stack.extend(reversed(nd.children))
+        elif getattr(nd, "tensor", None) is not None and nd.tensor not in order:
+            order.append(nd.tensor)
+    return order
+
+
+def inexact_footprints(program, schedules, arch, launch=None, device: int = 0, diagnostics: "list | None" = None):
     """Per schedule, the cache model's inexact-footprint flag of the scheduled program --
     `analyze(apply_schedule(program, s), cache).node_costs["<root>"].inexact` (ls/cache.py:
     198-202, 228-231) -- computed on the device: 1 inexact, 0 exact, -1 the schedule fails
-    apply_schedule (or its shape is outside the device class)."""
+    apply_schedule (or its shape is outside the device class).  `diagnostics`, if given,
+    receives one list per schedule: the model's notes ("inexact footprint for tensor 'A' at
+    loop 'i'", innermost loop first)."""
     import torch
 
     out = np.full(len(schedules), -1, np.int8)
+    notes: list = [[] for _ in schedules]
+    tensors = [t.name for t in program.tensors]
+    rank_of = {nm: j for j, nm in enumerate(_access_order(program))}
     for g in pack_schedules(program, schedules):
         if g.template is None:
             continue
         task = _TASKS.get(g.template, arch, launch, device)
         d_rec = to_device_records(g.records, device)
-        f = task.inexact_footprints(d_rec)
+        f, m, ch = task.inexact_footprints(d_rec, notes=True)
         torch.cuda.synchronize(device)
         f = f.cpu().numpy().astype(np.int16)
         f = np.where((f == 255) | (g.host_status != 0), -1, f)
         out[g.index] = f
+        if diagnostics is None:
+            continue
+        m, ch = m.cpu().numpy().view(np.uint64), ch.cpu().numpy()
+        for row, gi in enumerate(g.index):
+            if f[row] != 1:
+                continue
+            chain = [int(x) for x in ch[row] if x != 0xFF]
+            for p in range(len(chain) - 1, -1, -1):
+                hit = [t for t in range(len(tensors))
+                       if (int(m[row, (8 * p + t) // 64]) >> ((8 * p + t) % 64)) & 1]
+                for t in sorted(hit, key=lambda t: rank_of.get(tensors[t], len(tensors))):
+                    notes[gi].append(f"inexact footprint for tensor {tensors[t]!r} at loop "
+                                     f"{g.template.names[chain[p]]!r}")
+    if diagnostics is not None:
+        diagnostics.extend(notes)
     return out
 
 

@@ -3788,39 +3788,70 @@ __global__ void __launch_bounds__(TPB) collect_unroll_kernel(const DTask* __rest
 }
 #endif  // LS_MAIN_TU
 
-// The cache model's inexact-footprint flag per record (CacheModel.run -> NodeCost.inexact; the
-// diagnostic of ls/cache.py:198-202): some tensor_footprint the walk evaluates has a dimension
-// whose strided-interval sums / unions (_si_sum / _si_union, ls/cache.py:47-77) lost exactness.
-// A dimension's interval changes only where the walk passes one of its variables, so the visited
-// intervals are the one with nothing expanded (the innermost loop's single set) and the one
-// after each of its variables (that loop's full set, held until the next): the same folds as the
-// generic walk's step (a).  out: 0 exact, 1 inexact, 255 the record fails apply_schedule.
+// The cache model's inexact-footprint flag per record (CacheModel.run -> NodeCost.inexact) and the
+// (loop, tensor) pairs of its diagnostic (ls/cache.py:198-202: "inexact footprint for tensor ...
+// at loop ..."): at each loop of the chain, innermost first, a tensor is inexact when one of its
+// dimensions' strided intervals (_si_sum / _si_union folds, ls/cache.py:47-77) lost exactness for
+// the loop's single set (the variables inside it) or its full set (those and its own).  A
+// dimension's interval changes only where the walk passes one of its variables, so each level
+// refolds only the dimensions of that variable (the generic walk's expr_range + _si_union).
+// flags: 0 exact, 1 inexact, 255 the record fails apply_schedule; masks (optional): bit
+// 8 * position + tensor, two words; chains (optional): the loop slot at each chain position
+// (position 0 outermost), 0xFF past the chain.
 #ifdef LS_MAIN_TU
 __global__ void __launch_bounds__(TPB) inexact_kernel(const DTask* __restrict__ gtask, const ls_record* __restrict__ recs,
-                                                      int64_t n, uint8_t* __restrict__ out) {
+                                                      int64_t n, uint8_t* __restrict__ out,
+                                                      unsigned long long* __restrict__ masks,
+                                                      uint8_t* __restrict__ chains) {
   extern __shared__ __align__(16) unsigned char dyn[];
   DTask& T = *reinterpret_cast<DTask*>(dyn);
   stage_task(T, gtask);
   Cand c = carve(dyn + T.task_bytes, T);
+  auto dim_exact = [&](int t, int rr, int thr) {
+    SI u = expr_range(T, T.expr[T.t_uacc[t][0]][rr], c, thr);
+    for (int a = 1; a < T.t_nu[t]; ++a) u = si_union(u, expr_range(T, T.expr[T.t_uacc[t][a]][rr], c, thr));
+    return u.exact != 0;
+  };
   for (int64_t i = (int64_t)blockIdx.x * TPB + threadIdx.x; i < n; i += (int64_t)gridDim.x * TPB) {
     const ls_record r = load_record(recs, i);
+    unsigned long long m0 = 0, m1 = 0;
     if (apply_transforms(T, r, c)) {
       out[i] = 255;
-      continue;
-    }
-    bool inexact = false;
-    for (int t = 0; t < T.n_tensors && !inexact; ++t)
-      for (int rr = 0; rr < T.t_rank[t] && !inexact; ++rr) {
-        const int D = t * T.layout_rm + rr;
-        for (int j = -1; j < (int)T.dim_nv[D] && !inexact; ++j) {  // j = -1: nothing expanded
-          const int thr = j < 0 ? (int)NOSLOT : (int)c.P(T.dim_var[D][j]);
-          if (j >= 0 && thr == NOSLOT) continue;
-          SI u = expr_range(T, T.expr[T.t_uacc[t][0]][rr], c, thr);
-          for (int a = 1; a < T.t_nu[t]; ++a) u = si_union(u, expr_range(T, T.expr[T.t_uacc[t][a]][rr], c, thr));
-          inexact = !u.exact;
+    } else {
+      unsigned long long ex = 0;  // bit t * MAXRANK + rr: the dimension's current interval is exact
+      for (int t = 0; t < T.n_tensors; ++t)
+        for (int rr = 0; rr < T.t_rank[t]; ++rr)
+          if (dim_exact(t, rr, (int)NOSLOT)) ex |= 1ull << (t * MAXRANK + rr);  // nothing expanded
+      for (int p = c.n - 1; p >= 0; --p) {  // innermost first
+        const int v = c.C(p);
+        for (int t = 0; t < T.n_tensors; ++t) {
+          bool bad = false;
+          for (int rr = 0; rr < T.t_rank[t]; ++rr) {
+            const int D = t * T.layout_rm + rr, b = t * MAXRANK + rr;
+            bool mine = false;
+            for (int x = 0; x < T.dim_nv[D]; ++x) mine |= T.dim_var[D][x] == v;
+            bad |= !((ex >> b) & 1ull);                       // the single set
+            if (mine) {
+              if (dim_exact(t, rr, p)) ex |= 1ull << b;
+              else ex &= ~(1ull << b);
+            }
+            bad |= !((ex >> b) & 1ull);                       // the full set
+          }
+          if (bad) {
+            const int bit = 8 * p + t;
+            if (bit < 64) m0 |= 1ull << bit;
+            else m1 |= 1ull << (bit - 64);
+          }
         }
       }
-    out[i] = inexact ? 1 : 0;
+      out[i] = (m0 | m1) ? 1 : 0;
+    }
+    if (masks) {
+      masks[2 * i] = m0;
+      masks[2 * i + 1] = m1;
+    }
+    if (chains)
+      for (int p = 0; p < 16; ++p) chains[16 * i + p] = out[i] != 255 && p < c.n ? c.C(p) : (uint8_t)0xFF;
   }
 }
 #endif  // LS_MAIN_TU

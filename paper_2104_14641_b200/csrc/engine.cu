@@ -1083,7 +1083,8 @@ int ls_task_prepare_unroll(ls_task* t, const int64_t* u, int32_t n) {
   return add_unroll(t, u, n);
 }
 
-int ls_inexact_footprints(ls_task* t, const ls_record* d_records, int64_t n, uint8_t* d_flags, void* stream) {
+int ls_inexact_footprints(ls_task* t, const ls_record* d_records, int64_t n, uint8_t* d_flags,
+                          unsigned long long* d_masks, uint8_t* d_chains, void* stream) {
   LS_NVTX("ls_inexact_footprints");
   if (!t || n < 0 || (n && (!d_records || !d_flags))) return fail(LS_E_ARG, "bad argument");
   if (t->host.tree) return fail(LS_E_UNSUPPORTED, "inexact-footprint flags cover perfect chains (not general trees)");
@@ -1092,7 +1093,7 @@ int ls_inexact_footprints(ls_task* t, const ls_record* d_records, int64_t n, uin
   cudaStream_t s = (cudaStream_t)stream;
   const size_t sm = smem_score(t->host, 0);
   BPS_TRY(bps, inexact_kernel, sm);
-  inexact_kernel<<<grid_for(t, n, bps), TPB, sm, s>>>(t->d_task, d_records, n, d_flags);
+  inexact_kernel<<<grid_for(t, n, bps), TPB, sm, s>>>(t->d_task, d_records, n, d_flags, d_masks, d_chains);
   CUDA_TRY(cudaGetLastError());
   return LS_E_OK;
 }

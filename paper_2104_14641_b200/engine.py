@@ -40,7 +40,7 @@ def lib():
     L.ls_task_num_features.argtypes = [vp]
     L.ls_task_prepare_unroll.argtypes = [vp, vp, i32]
     L.ls_collect_unroll.argtypes = [vp, vp, i64, vp, i32, vp, vp]
-    L.ls_inexact_footprints.argtypes = [vp, vp, i64, vp, vp]
+    L.ls_inexact_footprints.argtypes = [vp, vp, i64, vp, vp, vp, vp]
     L.ls_score.argtypes = [vp, vp, i64, vp, vp, vp, vp]
     L.ls_score_topk.argtypes = [vp, vp, i64, i64, i32, vp, vp, vp, vp]
     L.ls_topk_merge.argtypes = [vp, vp, i32, i32, i32, vp, vp, vp]
@@ -177,16 +177,21 @@ class Task:
         """Path of the points calls (LS_PATH_GENERIC / LS_PATH_TABULATED / LS_PATH_SPACE)."""
         return lib().ls_task_points_path(self._h)
 
-    def inexact_footprints(self, d_records, stream=None):
+    def inexact_footprints(self, d_records, stream=None, notes: bool = False):
         """Per record: 1 when the cache model's footprint intervals lose exactness (NodeCost.inexact,
-        ls/cache.py:198-202), 0 exact, 255 the record fails apply_schedule (uint8 device tensor)."""
+        ls/cache.py:198-202), 0 exact, 255 the record fails apply_schedule (uint8 device tensor);
+        with notes=True also the (loop, tensor) masks [n, 2] and the chains [n, 16] of the
+        diagnostic (ls_inexact_footprints)."""
         torch = _torch()
-        n = int(d_records.shape[0])
-        out = torch.empty(n, dtype=torch.uint8, device=f"cuda:{self.device}")
+        n, dev = int(d_records.shape[0]), f"cuda:{self.device}"
+        out = torch.empty(n, dtype=torch.uint8, device=dev)
+        masks = torch.empty((n, 2), dtype=torch.int64, device=dev) if notes else None
+        chains = torch.empty((n, 16), dtype=torch.uint8, device=dev) if notes else None
         with torch.cuda.device(self.device):
-            _check(lib().ls_inexact_footprints(self._h, _dptr(d_records), n, _dptr(out), _stream(torch, stream)),
-                   "ls_inexact_footprints")
-        return out
+            _check(lib().ls_inexact_footprints(self._h, _dptr(d_records), n, _dptr(out),
+                                               _dptr(masks) if notes else None, _dptr(chains) if notes else None,
+                                               _stream(torch, stream)), "ls_inexact_footprints")
+        return (out, masks, chains) if notes else out
 
     # -- unroll table ---------------------------------------------------------------
     def prepare_unroll_for(self, d_records, stream=None):

@@ -31,6 +31,7 @@ for n, k in [(1 << 14, 8), (1 << 14, 64), (3000, 4), (1 << 18, 64)]:  # bound K2
         task.score_topk(dr, k)
         task.score(dr)
         task.inexact_footprints(dr)
+        task.inexact_footprints(dr, notes=True)
     torch.cuda.synchronize()
 run = E.EsRun(task, 0.05, 2.0, 40960, 3, 7)  # 5 sort tiles: the look-back walks
 run.run()
