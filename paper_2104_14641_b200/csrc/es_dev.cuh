@@ -177,8 +177,6 @@ __global__ void __launch_bounds__(TPB, 2) es_gen_kernel(const DTask* __restrict_
   }
 }
 
-// sum over fixed chunks of sorted positions of w_j * eps[member_j]; w_j = the
-// centred rank j/(n-1) - 0.5 (rank_normalize) or F itself (ls/es.py:65-71, 90).
 #ifdef LS_MAIN_TU
 // ---- stable LSD radix sort of (F order bits, member) pairs: the ranks of _shape_fitness
 // (argsort(argsort(F, stable), stable), ls/es.py:65-71).  Single-pass-per-digit ("onesweep")
@@ -192,8 +190,9 @@ __global__ void __launch_bounds__(TPB, 2) es_gen_kernel(const DTask* __restrict_
 //                      by __match_any_sync with warp-private digit counters, then one
 //                      exclusive scan over the warps per digit), the tile's exclusive prefix per
 //                      digit by decoupled look-back over its predecessors' published counts
-//                      (RS_WIN words per round trip), scatter.  A predecessor tile always belongs to a block already running,
-//                      so the look-back never waits on an unscheduled block.
+//                      (RS_WIN words per round trip), scatter.  A predecessor tile always
+//                      belongs to a block already running, so the look-back never waits on an
+//                      unscheduled block.
 // Every launch is fixed (inactive passes exit at once): a generation stays one CUDA graph.
 #ifndef LS_RS_TILE
 #define LS_RS_TILE 8192
@@ -406,6 +405,8 @@ __global__ void __launch_bounds__(RS_TPB) rs_pass_kernel(RsBufs R, int d) {
   }
 }
 
+// sum over fixed chunks of sorted positions of w_j * eps[member_j]; w_j = the
+// centred rank j/(n-1) - 0.5 (rank_normalize) or F itself (ls/es.py:65-71, 90).
 __global__ void __launch_bounds__(TPB) es_partial_kernel(EsDev* __restrict__ ges) {
   es_pdl_wait();
   __shared__ double wred[TPB / 32][ES_MAXDIM];
