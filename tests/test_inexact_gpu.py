@@ -37,3 +37,28 @@ def test_inexact_flags_match_reference():
                 bad.append((case["program"], i, g, w, nt))
     assert checked > 5000 and inexact > 500 and n_notes > 4000
     assert not bad, (len(bad), bad[:3])
+
+
+def test_inexact_flags_tree_program_unsupported():
+    """General trees (sibling loops) are outside the flag kernel: the library says so (LS_E_UNSUPPORTED)."""
+    from paper_2104_14641_b200.cost import inexact_footprints
+    from paper_2104_14641_b200.engine import EngineError
+    from paper_2104_14641_b200.ir import Schedule, parse_program
+    fx = json.loads((GOLDEN / "tree_rank.json").read_text())
+    case = fx["cases"][0]
+    prog = parse_program(json.dumps(fx["programs"][case["program"]]))
+    with pytest.raises(EngineError, match="perfect chains"):
+        inexact_footprints(prog, [Schedule.from_json(s) for s in case["schedules"][:4]], arch_named("x86-avx2"))
+
+
+def test_inexact_flags_empty_and_failing():
+    """An empty list, and schedules that fail apply_schedule (-1, no notes)."""
+    from paper_2104_14641_b200 import workloads as W
+    from paper_2104_14641_b200.cost import inexact_footprints
+    from paper_2104_14641_b200.ir import Schedule
+    prog = W.program(W.matmul_json(32))
+    assert inexact_footprints(prog, [], arch_named("x86-avx2")).shape == (0,)
+    notes: list = []
+    bad = Schedule.from_json([{"tile": {"loop": "nope", "factor": 4}}])
+    got = inexact_footprints(prog, [bad, Schedule.from_json([])], arch_named("x86-avx2"), diagnostics=notes)
+    assert got.tolist() == [-1, 0] and notes == [[], []]
