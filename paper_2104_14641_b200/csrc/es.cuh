@@ -30,7 +30,7 @@
 // are all-gathered in place (every rank then holds the whole population's keys
 // and sorts them: global stable ranks, ls/es.py:65-71), rank r sums its share
 // of the fixed 1024-position chunks, the chunk partials are all-gathered in
-// place and every rank adds all of them in chunk order.  Chunk boundaries and
+// place and every rank adds all of them in one fixed tree (es_update_kernel).  Chunk boundaries and
 // the order of every float64 addition are independent of G, so theta, the
 // trace and the evaluated set are bit-identical for G = 1, 2, 4, 8.  The memo
 // is per rank; the distinct count is the size of the union of the ranks'

@@ -461,29 +461,41 @@ __global__ void __launch_bounds__(TPB) es_partial_kernel(EsDev* __restrict__ ges
   }
 }
 
-// One block: the chunk partials are staged through shared memory in coalesced tiles (every
-// load of a tile in flight at once) and thread d adds its column in chunk order.
-constexpr int ES_UPD_TPB = 256, ES_UPD_TILE = 2048;  // doubles per staged tile
+// One block: the chunk partials summed in a fixed-shape tree (thread t adds chunks t, t + TPB,
+// ... in order, a butterfly in each warp, then the warps in order) -- the same shape for every
+// rank count G, so theta stays bit-identical across G; every row load of a thread in flight.
+constexpr int ES_UPD_TPB = 256;
 __global__ void __launch_bounds__(ES_UPD_TPB) es_update_kernel(EsDev* __restrict__ ges) {
   es_pdl_wait();
-  __shared__ double tile[ES_UPD_TILE];
+  __shared__ double wred[ES_UPD_TPB / 32][ES_MAXDIM];
   EsDev& E = *ges;
   const int chunks = E.chunks, dim = E.dim;
-  const int d = threadIdx.x;
   const int g = E.gen;
-  const int per = ES_UPD_TILE / dim;  // chunks per tile
   const double* __restrict__ part = E.partial;
-  double sum = 0.0;
-  for (int b0 = 0; b0 < chunks; b0 += per) {
-    const int nb = min(per, chunks - b0);
-    const double* src = part + (size_t)b0 * dim;
-    for (int q = threadIdx.x; q < nb * dim; q += ES_UPD_TPB) tile[q] = src[q];
-    __syncthreads();
-    if (d < dim)
-      for (int b = 0; b < nb; ++b) sum = __dadd_rn(sum, tile[b * dim + d]);
-    __syncthreads();
+  double acc[ES_MAXDIM];
+#pragma unroll
+  for (int d = 0; d < ES_MAXDIM; ++d) acc[d] = 0.0;
+  for (int b = threadIdx.x; b < chunks; b += ES_UPD_TPB) {
+    const double* row = part + (size_t)b * dim;
+#pragma unroll
+    for (int d = 0; d < ES_MAXDIM; ++d)
+      if (d < dim) acc[d] = __dadd_rn(acc[d], row[d]);
   }
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+#pragma unroll
+  for (int d = 0; d < ES_MAXDIM; ++d) {
+    if (d >= dim) break;
+    double v = acc[d];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
+    if (lane == 0) wred[wp][d] = v;
+  }
+  __syncthreads();
+  const int d = threadIdx.x;
   if (d < dim) {
+    double sum = wred[0][d];
+#pragma unroll
+    for (int u = 1; u < ES_UPD_TPB / 32; ++u) sum = __dadd_rn(sum, wred[u][d]);
     E.theta[d] = __dadd_rn(E.theta[d], __dmul_rn(E.coef, sum));
     E.theta_hist[(size_t)(g + 1) * E.dim + d] = E.theta[d];
   }
