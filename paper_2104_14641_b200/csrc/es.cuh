@@ -15,8 +15,9 @@
 //                     sort key of F = -score (ls/es.py:176)
 //   rs_* kernels      stable onesweep radix sort of (F bits, member index): stable ranks,
 //                     _shape_fitness's argsort(argsort(., stable), stable) (ls/es.py:65-71)
-//   es_partial_kernel fixed 1024-position chunks of sum_i w_i eps_i (noise kept by
-//                     es_gen on one rank, regenerated on a shard), fixed-order reductions
+//   es_partial_kernel fixed 1024-member chunks of sum_i w_i eps_i in member order (w_i from
+//                     the member's sorted position, written by the sort's last pass; noise
+//                     kept by es_gen for this rank's members), fixed-shape reductions
 //   es_update_kernel  theta += alpha / (population * sigma) * sum (ls/es.py:91-92),
 //                     incumbent trace (ls/es.py:189-190), generation counter
 //
@@ -29,9 +30,9 @@
 // (r+1) P/G) (their noise depends on the global member index only), the F keys
 // are all-gathered in place (every rank then holds the whole population's keys
 // and sorts them: global stable ranks, ls/es.py:65-71), rank r sums its share
-// of the fixed 1024-position chunks, the chunk partials are all-gathered in
-// place and every rank adds all of them in one fixed tree (es_update_kernel).  Chunk boundaries and
-// the order of every float64 addition are independent of G, so theta, the
+// of the fixed 1024-member chunks, the chunk partials are all-gathered in
+// place and every rank adds all of them in one fixed tree (es_update_kernel).  Chunk
+// boundaries and the order of every float64 addition are independent of G, so theta, the
 // trace and the evaluated set are bit-identical for G = 1, 2, 4, 8.  The memo
 // is per rank; the distinct count is the size of the union of the ranks'
 // evaluated lists and the trace the per-generation minimum over ranks (both
@@ -190,12 +191,13 @@ int ls_es_create_shard(ls_task* t, const ls_es_params* p, const double* h_theta0
   rc = rc ? rc : alloc((void**)&H.partial, sizeof(double) * (size_t)es->cpr * world * H.dim);
   rc = rc ? rc : alloc((void**)&H.theta_hist, sizeof(double) * (H.iters + 1) * H.dim);
   rc = rc ? rc : alloc((void**)&H.trace, sizeof(double) * H.iters);
-  {  // single rank: es_gen keeps the noise for es_partial (a sharded rank's partials need every
-     // member's noise, so they regenerate it; the values are the same function either way)
-    const size_t nb = sizeof(double) * 2 * (size_t)((H.dim + 1) / 2) * (size_t)H.pop;
+  {  // es_gen keeps this rank's members' noise for es_partial (a partial over other ranks'
+     // members regenerates theirs: the values are the same function either way)
+    const size_t nb = sizeof(double) * 2 * (size_t)((H.dim + 1) / 2) * (size_t)(H.hi - H.lo);
     H.noise = nullptr;
-    if (world == 1 && nb <= ((size_t)1 << 31)) rc = rc ? rc : alloc((void**)&H.noise, nb);
+    if (nb <= ((size_t)1 << 31)) rc = rc ? rc : alloc((void**)&H.noise, nb);
   }
+  rc = rc ? rc : alloc((void**)&H.rank_of, sizeof(uint32_t) * H.pop);
   rc = rc ? rc : alloc((void**)&es->dev, sizeof(EsDev));
   if (rc == LS_E_OK) {  // the rank sort: ping-pong buffers, tile histograms, plan, AND / OR
     RsBufs& R = es->rs;
@@ -205,6 +207,7 @@ int ls_es_create_shard(ls_task* t, const ls_es_params* p, const double* h_theta0
     R.key[1] = H.sort_out;
     R.idx[0] = H.idx_in;
     R.idx[1] = H.idx_out;
+    R.rank = H.rank_of;
     rc = rc ? rc : alloc((void**)&R.key[2], sizeof(unsigned long long) * H.pop);
     rc = rc ? rc : alloc((void**)&R.idx[2], sizeof(uint32_t) * H.pop);
     const size_t st_bytes = sizeof(unsigned long long) * 8 * 256 * (size_t)R.nblk;

@@ -32,8 +32,9 @@ struct EsDev {
   double* partial;                     // [chunks][dim]
   double* theta_hist;                  // [iters + 1][dim]
   double* trace;                       // [iters]
-  double* noise;                       // [pop][dim rounded up to pairs]: the generation's noise kept by
-                                       // es_gen for es_partial (single-rank runs), or null (regenerated)
+  double* noise;                       // [hi - lo][dim rounded up to pairs]: this rank's members' noise kept
+                                       // by es_gen for es_partial, or null (regenerated)
+  uint32_t* rank_of;                   // [pop] member -> position in the stable sort (the last pass)
 };
 
 // griddepcontrol.wait: a no-op unless the kernel was launched as a programmatic dependent
@@ -153,7 +154,7 @@ __global__ void __launch_bounds__(TPB, 2) es_gen_kernel(const DTask* __restrict_
       double z0 = 0.0, z1 = 0.0;
       if (!start) {
         es_normal_pair(E.seed, g, (uint32_t)i, d >> 1, z0, z1);
-        if (E.noise) reinterpret_cast<double2*>(E.noise)[(size_t)i * ((E.dim + 1) >> 1) + (d >> 1)] = make_double2(z0, z1);
+        if (E.noise) reinterpret_cast<double2*>(E.noise)[(size_t)(i - lo) * ((E.dim + 1) >> 1) + (d >> 1)] = make_double2(z0, z1);
       }
       for (int q = d; q < d + 2 && q < E.dim; ++q) {
         const double pt = __dadd_rn(E.theta[q], __dmul_rn(E.sigma, q == d ? z0 : z1));
@@ -223,7 +224,8 @@ struct RsBufs {
   uint32_t* idx[3];
   RsCtl* ctl;
   unsigned long long* status;  // [8][nblk][256] look-back words (epoch << 32 | flag << 30 | count)
-  int32_t* plan;               // [8][4]: active, shift, src, dst
+  int32_t* plan;               // [8][4]: active (2: the last active pass), shift, src, dst
+  uint32_t* rank;              // [n] member -> sorted position, written by the last pass
   int32_t n, nblk;
 };
 
@@ -267,6 +269,7 @@ __global__ void __launch_bounds__(256) rs_plan_kernel(RsBufs R) {
       p[1] = 8 * d;
       if (!act[d]) continue;
       const int dst = (--left) % 2 == 0 ? 1 : 2;  // the last active pass writes `out`
+      p[0] = left == 0 ? 2 : 1;                     // 2: the last pass also writes the ranks
       p[2] = src;
       p[3] = dst;
       src = dst;
@@ -298,6 +301,7 @@ __global__ void __launch_bounds__(RS_TPB) rs_pass_kernel(RsBufs R, int d) {
   es_pdl_wait();
   const int32_t* p = R.plan + 4 * d;
   if (!p[0]) return;
+  const bool last = p[0] == 2;
   __shared__ uint32_t lcount[256];       // the tile's keys per digit
   __shared__ uint32_t wcnt[RS_TPB / 32][256];  // per warp: running digit counts, then the warp's digit offsets
   __shared__ uint32_t gbase[256];        // global position of the tile's first key of each digit
@@ -402,11 +406,13 @@ __global__ void __launch_bounds__(RS_TPB) rs_pass_kernel(RsBufs R, int d) {
     const uint32_t o = gbase[dig] + pos[q];
     kd[o] = key[q];
     id[o] = val[q];
+    if (last) R.rank[val[q]] = o;
   }
 }
 
-// sum over fixed chunks of sorted positions of w_j * eps[member_j]; w_j = the
-// centred rank j/(n-1) - 0.5 (rank_normalize) or F itself (ls/es.py:65-71, 90).
+// sum over fixed chunks of members of w_i * eps_i; w_i = the member's centred rank
+// rank_i/(n-1) - 0.5 (rank_normalize; rank_i from the sort's last pass) or F_i itself
+// (ls/es.py:65-71, 90).  Members in index order: the kept noise rows are read sequentially.
 __global__ void __launch_bounds__(TPB) es_partial_kernel(EsDev* __restrict__ ges) {
   es_pdl_wait();
   __shared__ double wred[TPB / 32][ES_MAXDIM];
@@ -414,19 +420,20 @@ __global__ void __launch_bounds__(TPB) es_partial_kernel(EsDev* __restrict__ ges
   const int n = E.pop, dim = E.dim, g = E.gen;
   const bool flat = E.rank_normalize && E.sort_out[0] == E.sort_out[n - 1];  // np.ptp(values) == 0
   const int chunk = E.c0 + blockIdx.x;
-  const int j0 = chunk * ES_CHUNK;
+  const int i0 = chunk * ES_CHUNK;
   const int pairs = (dim + 1) >> 1;
   double acc[ES_MAXDIM];  // unrolled over ES_MAXDIM with dim guards: registers, not a stack array
 #pragma unroll
   for (int d = 0; d < ES_MAXDIM; ++d) acc[d] = 0.0;
-  for (int j = j0 + threadIdx.x; j < min(n, j0 + ES_CHUNK); j += TPB) {
+  for (int i = i0 + threadIdx.x; i < min(n, i0 + ES_CHUNK); i += TPB) {  // members in index order
     double w;
-    if (E.rank_normalize)
-      w = flat ? 0.0 : __dadd_rn(__ddiv_rn((double)j, (double)(n - 1)), -0.5);
+    if (E.rank_normalize)  // the member's centred rank: its position in the stable sort
+      w = flat ? 0.0 : __dadd_rn(__ddiv_rn((double)E.rank_of[i], (double)(n - 1)), -0.5);
     else
-      w = from_order_bits(E.sort_out[j]);
-    const uint32_t i = E.idx_out[j];
-    const double2* kept = E.noise ? reinterpret_cast<const double2*>(E.noise) + (size_t)i * pairs : nullptr;
+      w = from_order_bits(E.sort_in[i]);  // F itself, in member order
+    const double2* kept = E.noise && i >= E.lo && i < E.hi
+                              ? reinterpret_cast<const double2*>(E.noise) + (size_t)(i - E.lo) * pairs
+                              : nullptr;
 #pragma unroll
     for (int d = 0; d < ES_MAXDIM; d += 2) {
       if (d >= dim) break;
@@ -436,7 +443,7 @@ __global__ void __launch_bounds__(TPB) es_partial_kernel(EsDev* __restrict__ ges
         z0 = z.x;
         z1 = z.y;
       } else {
-        es_normal_pair(E.seed, g, i, d >> 1, z0, z1);
+        es_normal_pair(E.seed, g, (uint32_t)i, d >> 1, z0, z1);
       }
       acc[d] = __dadd_rn(acc[d], __dmul_rn(w, z0));
       if (d + 1 < dim) acc[d + 1] = __dadd_rn(acc[d + 1], __dmul_rn(w, z1));
