@@ -390,9 +390,11 @@ int ls_es_evaluated(ls_es* es, uint64_t* h_points, double* h_scores, int64_t cap
 /* The Gaussian noise of a generation, [population][dim] float64 on the device (diagnostic). */
 int ls_es_noise(ls_es* es, int32_t generation, double* d_out, void* stream);
 /* The last generation's rank sort (diagnostic): the F order-bit keys as es_gen wrote them
- * (member order) and after the stable sort, with the member at each sorted position; device
- * arrays of `population` entries, stream-ordered copies. */
-int ls_es_sort_state(ls_es* es, uint64_t* d_keys_in, uint64_t* d_keys_out, uint32_t* d_members, void* stream);
+ * (member order) and after the stable sort, the member at each sorted position and (d_ranks,
+ * optional) each member's sorted position; device arrays of `population` entries,
+ * stream-ordered copies. */
+int ls_es_sort_state(ls_es* es, uint64_t* d_keys_in, uint64_t* d_keys_out, uint32_t* d_members, uint32_t* d_ranks,
+                     void* stream);
 int ls_es_destroy(ls_es* es);
 
 /* ---- external code-text analysis (`analyze --code`, ls/cli.py:86) ----

@@ -351,7 +351,8 @@ int ls_es_noise(ls_es* es, int32_t generation, double* d_out, void* stream) {
   return LS_E_OK;
 }
 
-int ls_es_sort_state(ls_es* es, uint64_t* d_keys_in, uint64_t* d_keys_out, uint32_t* d_members, void* stream) {
+int ls_es_sort_state(ls_es* es, uint64_t* d_keys_in, uint64_t* d_keys_out, uint32_t* d_members, uint32_t* d_ranks,
+                     void* stream) {
   if (!es || !d_keys_in || !d_keys_out || !d_members) return fail(LS_E_ARG, "bad argument");
   CUDA_TRY(cudaSetDevice(es->task->device));
   const cudaStream_t s = (cudaStream_t)stream;
@@ -359,6 +360,8 @@ int ls_es_sort_state(ls_es* es, uint64_t* d_keys_in, uint64_t* d_keys_out, uint3
   CUDA_TRY(cudaMemcpyAsync(d_keys_in, es->host.sort_in, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
   CUDA_TRY(cudaMemcpyAsync(d_keys_out, es->host.sort_out, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
   CUDA_TRY(cudaMemcpyAsync(d_members, es->host.idx_out, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+  if (d_ranks)
+    CUDA_TRY(cudaMemcpyAsync(d_ranks, es->host.rank_of, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
   return LS_E_OK;
 }
 

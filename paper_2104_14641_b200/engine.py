@@ -64,7 +64,7 @@ def lib():
     L.ls_es_result.argtypes = [vp, vp, vp, vp, vp, vp, vp]
     L.ls_es_evaluated.argtypes = [vp, vp, vp, i64, vp, vp]
     L.ls_es_noise.argtypes = [vp, i32, vp, vp]
-    L.ls_es_sort_state.argtypes = [vp, vp, vp, vp, vp]
+    L.ls_es_sort_state.argtypes = [vp, vp, vp, vp, vp, vp]
     L.ls_es_destroy.argtypes = [vp]
     if L.ls_abi_version() != abi.ABI_VERSION:
         raise EngineError("libloopscout_b200 ABI version mismatch")
@@ -475,16 +475,17 @@ class EsRun:
 
     def sort_state(self, stream=None):
         """The last generation's rank sort (diagnostic): (keys in member order, sorted keys,
-        member at each sorted position) as device tensors."""
+        member at each sorted position, each member's sorted position) as device tensors."""
         torch = _torch()
         n, dev = self.params.population, f"cuda:{self.task.device}"
         kin = torch.empty(n, dtype=torch.int64, device=dev)
         kout = torch.empty(n, dtype=torch.int64, device=dev)
         mem = torch.empty(n, dtype=torch.int32, device=dev)
+        rk = torch.empty(n, dtype=torch.int32, device=dev)
         with torch.cuda.device(self.task.device):
-            _check(lib().ls_es_sort_state(self._h, _dptr(kin), _dptr(kout), _dptr(mem), _stream(torch, stream)),
-                   "ls_es_sort_state")
-        return kin, kout, mem
+            _check(lib().ls_es_sort_state(self._h, _dptr(kin), _dptr(kout), _dptr(mem), _dptr(rk),
+                                          _stream(torch, stream)), "ls_es_sort_state")
+        return kin, kout, mem, rk
 
     def close(self):
         if getattr(self, "_h", None):

@@ -163,10 +163,13 @@ def test_rank_sort_is_stable_argsort(torch, name, pop, sigma):
     for iters in (1, 3):
         run = E.EsRun(task, 0.05, sigma, pop, iters, 99 + iters)
         run.run()
-        kin, kout, mem = (x.cpu().numpy() for x in run.sort_state())
+        kin, kout, mem, rk = (x.cpu().numpy() for x in run.sort_state())
         kin = kin.view(np.uint64)
         order = np.argsort(kin, kind="stable")
         assert np.array_equal(mem.astype(np.int64), order)
+        ranks = np.empty(pop, np.int64)
+        ranks[order] = np.arange(pop)  # argsort(argsort(F, stable), stable): each member's rank
+        assert np.array_equal(rk.astype(np.int64), ranks)
         assert np.array_equal(kout.view(np.uint64), kin[order])
         if name == "equal":
             assert (kin == kin[0]).all()
