@@ -2,7 +2,7 @@
 // state, Philox noise, the memoised scoring step and the generation kernels.
 #pragma once
 
-constexpr int ES_CHUNK = 1024;  // sorted positions per partial sum (independent of the grid)
+constexpr int ES_CHUNK = 1024;  // members per partial sum (independent of the grid; 512 and 4096 measured slower)
 constexpr int ES_MAXDIM = LS_MAX_AXES;
 
 struct EsDev {
